@@ -1,0 +1,277 @@
+/*
+ * itertrace_cuda.h — C-ABI of libitertrace_cuda.so, the B200 (sm_100a) hot path of
+ * DeepProf-style trace mining: intern -> suffix array -> LCP -> repeat/period ->
+ * iteration boundaries -> per-iteration aggregates.
+ *
+ * Every entry point replaces one function of the reference's header-only C++ API
+ * (paths relative to /root/reference/proj/include/itertrace/); the replaced function
+ * is cited beside each declaration.  The reference has no FFI of its own:
+ * this header is the contract a maintainer binds from the reference's C++ headers
+ * (see INTEGRATION.md).
+ *
+ * Conventions
+ *  - All entry points return 0 on success, otherwise an itt_status.  1..12 are
+ *    1 + (int)itertrace::ErrorKind (errors.hpp:8-21) so the C++ shim can rethrow
+ *    itertrace::Error with the same kind; the stage-prefixed message ("pattern-mining: ...")
+ *    is available from itt_last_error(ctx) until the next call on that context.
+ *  - Inputs are borrowed for the duration of the call.  Fixed-size outputs are
+ *    caller-allocated; variable-size outputs are allocated by the library and
+ *    released with itt_free().
+ *  - One context per host thread and device; it owns one cudaStream_t.  Calls are
+ *    synchronous with respect to the host (the reference API returns by value).
+ *  - There is no CPU fallback: without a usable sm_100 device itt_ctx_create fails
+ *    with ITT_E_CUDA.
+ */
+#ifndef ITERTRACE_CUDA_H
+#define ITERTRACE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ITT_ABI_VERSION 1
+
+typedef enum itt_status {
+  ITT_OK = 0,
+  /* 1 + itertrace::ErrorKind, errors.hpp:8-21 */
+  ITT_E_UNREADABLE_FILE = 1,
+  ITT_E_MISSING_COLUMN = 2,
+  ITT_E_TOO_MANY_BAD_ROWS = 3,
+  ITT_E_EMPTY_TRACE = 4,
+  ITT_E_NO_MAIN_STREAM = 5,
+  ITT_E_EMPTY_MAIN_STREAM = 6,
+  ITT_E_INVALID_ITERATION_COUNT = 7,
+  ITT_E_NO_PATTERN_FOUND = 8,
+  ITT_E_AMBIGUOUS_LOOPS = 9,
+  ITT_E_NO_ITERATIONS = 10,
+  ITT_E_INVALID_CONFIG = 11,
+  ITT_E_IO_ERROR = 12,
+  /* device / library failures: not an ErrorKind; the shim throws std::runtime_error (exit 1) */
+  ITT_E_CUDA = 100,
+  ITT_E_NCCL = 101,
+  ITT_E_INVALID_ARGUMENT = 102,
+} itt_status;
+
+/* OpKind, trace.hpp:17-24 */
+enum { ITT_KIND_KERNEL = 0, ITT_KIND_HTOD, ITT_KIND_DTOH, ITT_KIND_DTOD, ITT_KIND_MEMSET, ITT_KIND_OTHER };
+/* StreamClass, streams.hpp:34 */
+enum { ITT_CLASS_MAIN = 0, ITT_CLASS_COPY_HTOD, ITT_CLASS_COPY_DTOH, ITT_CLASS_COPY_MIXED, ITT_CLASS_ASSIST };
+
+/* itt_records.flags bits: presence of TraceRecord::size_bytes / throughput_bps (trace.hpp:46-47) */
+#define ITT_REC_HAS_SIZE 0x1u
+#define ITT_REC_HAS_THROUGHPUT 0x2u
+
+#define ITT_MEM_HOST 0
+#define ITT_MEM_DEVICE 1
+
+#define ITT_ORDER_UNKNOWN 0 /* rows in source order; the library stable-sorts by (start, row) */
+#define ITT_ORDER_SORTED 1  /* rows already in NormalizedTrace order (ingest.hpp:396-400) */
+
+/*
+ * Columnar trace records: the NormalizedTrace/TraceRecord AoS (trace.hpp:43-66) as
+ * structure-of-arrays.  Row i is record i in source order (its TraceRecord::row).
+ * Device labels are interned by the caller in byte-lexicographic order, so the
+ * reference's "ties to the lexicographically smallest label" (streams.hpp:187-194)
+ * becomes "ties to the smallest id".
+ */
+typedef struct itt_records {
+  uint64_t n;                 /* number of records */
+  const int64_t* start_ns;    /* [n] */
+  const int64_t* duration_ns; /* [n] */
+  const int64_t* size_bytes;  /* [n]; read only where flags & ITT_REC_HAS_SIZE */
+  const uint8_t* flags;       /* [n] */
+  const uint32_t* stream;     /* [n] */
+  const uint16_t* device;     /* [n] device-label rank; NULL = single device 0 */
+  const uint64_t* name_off;   /* [n+1]; name of row i = name_bytes[name_off[i] .. name_off[i+1]) */
+  const uint8_t* name_bytes;  /* [name_off[n]] */
+  int32_t mem;                /* ITT_MEM_HOST or ITT_MEM_DEVICE (all pointers alike) */
+  int32_t order;              /* ITT_ORDER_UNKNOWN or ITT_ORDER_SORTED */
+} itt_records;
+
+typedef struct itt_ctx itt_ctx;
+
+/* ---------------------------------------------------------------- context */
+int itt_abi_version(void);
+int itt_ctx_create(int device, itt_ctx** out);
+int itt_ctx_destroy(itt_ctx* ctx);
+const char* itt_last_error(itt_ctx* ctx);
+int itt_free(itt_ctx* ctx, void* p);
+
+/* profiling: per-kernel CUDA-event timing on the context stream (off by default) */
+typedef struct itt_kernel_stat {
+  char name[48];
+  uint64_t launches;
+  double total_ms;  /* sum of per-launch event durations */
+  double bytes;     /* sum of algorithmic bytes declared per launch */
+} itt_kernel_stat;
+int itt_ctx_set_profiling(itt_ctx* ctx, int enabled);
+int itt_ctx_reset_stats(itt_ctx* ctx);
+int itt_ctx_kernel_stats(itt_ctx* ctx, itt_kernel_stat* out, uint32_t cap, uint32_t* n_out);
+/* total kernel launches issued by the library on this context since creation */
+int itt_ctx_launch_count(itt_ctx* ctx, uint64_t* out);
+/* device memory helpers for callers that keep inputs resident in HBM */
+int itt_device_alloc(itt_ctx* ctx, uint64_t bytes, void** out);
+int itt_device_free(itt_ctx* ctx, void* p);
+int itt_memcpy_h2d(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes);
+int itt_host_unregister(itt_ctx* ctx, void* p);
+int itt_ctx_synchronize(itt_ctx* ctx);
+
+/* ------------------------------------------------------- L2 streams (a1, a2) */
+typedef struct itt_stream_summary { /* StreamSummary, streams.hpp:16-32 */
+  uint32_t stream;
+  int32_t cls;        /* ITT_CLASS_* from classify_streams (streams.hpp:85-103) */
+  int64_t counts[6];  /* indexed by ITT_KIND_* */
+  int64_t first_start;
+  int64_t last_end;
+} itt_stream_summary;
+
+typedef struct itt_census {
+  uint32_t n_streams;
+  itt_stream_summary* streams; /* sorted by stream id (std::map order, streams.hpp:64) */
+  uint32_t n_devices;          /* distinct device ids seen */
+  uint16_t majority_device;    /* filter_majority_device choice (streams.hpp:179-207) */
+  uint64_t dropped_records;    /* records of other devices */
+  uint64_t n_records;
+} itt_census;
+
+/* summarize_streams (streams.hpp:60-81) + classify_streams (:85-103) after
+ * filter_majority_device (:179-207) when filter_device != 0.  Frees with itt_free(census->streams). */
+int itt_summarize_streams(itt_ctx* ctx, const itt_records* recs, int filter_device, itt_census* out);
+
+/* select_main_stream (streams.hpp:113-145) over a census */
+int itt_select_main_stream(itt_ctx* ctx, const itt_census* census, uint32_t* main_stream, uint32_t* n_main_streams);
+
+typedef struct itt_tokens { /* TokenSequence, streams.hpp:49-58 */
+  uint64_t n;
+  int32_t* tokens;        /* [n] token ids, first-appearance order */
+  uint64_t* record_index; /* [n] position of the token's record in (start,row) order */
+  uint32_t n_names;       /* V; terminator() == V */
+  uint64_t* name_row;     /* [V] source row (itt_records index) of one record carrying name id v */
+} itt_tokens;
+
+/* build_token_sequence (streams.hpp:147-169).  Records are taken in (start,row)
+ * order; no device filter is applied (the reference applies it in analyze_trace). */
+int itt_build_token_sequence(itt_ctx* ctx, const itt_records* recs, uint32_t main_stream, itt_tokens** out);
+
+/* count_interval_overlaps (streams.hpp:212-221) */
+int itt_count_interval_overlaps(itt_ctx* ctx, const itt_records* recs, uint32_t stream, int64_t* out);
+
+/* ------------------------------------------------------- L3 mining (a3-a6) */
+/* Suffix array + LCP of tokens[0..n) followed by a unique terminator `term`:
+ * sa[k] = start of the k-th smallest suffix of tokens+[term] (n+1 entries), lcp[0] = 0,
+ * lcp[k] = lcp(sa[k-1], sa[k]).  Equals the leaf order of SuffixTree (suffix_tree.hpp:21-190)
+ * in ascending child-key order.  lcp may be NULL.  Host buffers of n+1 entries. */
+int itt_suffix_array(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, uint32_t* sa, uint32_t* lcp);
+
+typedef struct itt_repeat { /* RepeatCandidate, mine.hpp:31-35 */
+  int32_t start;
+  int32_t length;
+  int64_t count;
+} itt_repeat;
+/* enumerate_repeats (mine.hpp:46-60) over the suffix tree of tokens+[term] (any order). */
+int itt_enumerate_repeats(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, int64_t min_count,
+                          int64_t max_len, itt_repeat** out, uint64_t* n_out);
+
+typedef struct itt_mining_cfg { /* MiningConfig, mine.hpp:18-22 */
+  int64_t iterations;
+  int64_t epsilon0;
+  int64_t epsilon_cap; /* <= 0 means "defaults to iterations" (std::nullopt) */
+} itt_mining_cfg;
+
+typedef struct itt_pattern { /* PatternCandidate, mine.hpp:24-29 */
+  int64_t length;
+  int32_t* tokens; /* [length], library-allocated (freed with the itt_pattern array via itt_free_patterns) */
+  int64_t count;
+  int64_t first_token;
+  int64_t epsilon_used;
+} itt_pattern;
+
+/* mine_pattern (mine.hpp:119-122) when multi == 0 and n_loops == 1;
+ * mine_patterns_multi (mine.hpp:132-165) when multi != 0. */
+int itt_mine_patterns(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, const itt_mining_cfg* loops,
+                      uint32_t n_loops, int multi, itt_pattern** out);
+int itt_free_patterns(itt_ctx* ctx, itt_pattern* p, uint32_t n_loops);
+
+/* ------------------------------------------------------- L4 matching (a7) */
+typedef struct itt_span { /* MatchSpan, match.hpp:28-34 */
+  int64_t start_token;
+  int64_t end_token;
+  int64_t extra;
+} itt_span;
+/* approx_match (match.hpp:41-85) */
+int itt_approx_match(itt_ctx* ctx, const int32_t* tokens, uint64_t n, const int32_t* pattern, uint64_t m, int64_t k0,
+                     itt_span** out, uint64_t* n_out);
+
+/* ------------------------------------------------------- L5 aggregates (a8-a11) */
+typedef struct itt_iter_row { /* integer core of IterationMetrics, metrics.hpp:21-31 */
+  int64_t start_token, end_token, extra;
+  int64_t t_start, t_end;     /* partition_iterations (metrics.hpp:44-55) */
+  int64_t interval_ns;        /* valid when has_interval (k > 0), clamped at 0 (metrics.hpp:124-130) */
+  int64_t copy_ns;            /* clipped HtoD union in the gap; meaningful when interval_ns > 0 (:131-135, :76-100) */
+  int64_t htod_bytes;         /* (:138-143) */
+  int64_t gap_sum, gap_count; /* op_gap_mean = gap_sum / gap_count, 0 when gap_count == 0 (:145-160) */
+  int32_t has_interval;
+  int32_t pad_;
+} itt_iter_row;
+
+typedef struct itt_clamps {
+  int64_t negative_gap_clamps;      /* IterationAnalysis, metrics.hpp:68-72 */
+  int64_t negative_interval_clamps;
+} itt_clamps;
+
+/* partition_iterations + collect_htod_records + compute_iteration_metrics
+ * (metrics.hpp:44-164).  record_index indexes records in (start,row) order; HtoD records are
+ * all MemcpyHtoD records of `recs` (all streams).  rows: library-allocated [n_spans]. */
+int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t* record_index, uint64_t n_tokens,
+                          const itt_span* spans, uint64_t n_spans, itt_iter_row** rows, itt_clamps* clamps);
+
+/* ------------------------------------------------------- L7 orchestration */
+typedef struct itt_analyze_opts { /* AnalyzeOptions, pipeline.hpp:18-25 */
+  const int64_t* loops;
+  uint32_t n_loops;
+  int64_t epsilon0;
+  int64_t k0;           /* < 0: default_k0(pattern length) (match.hpp:19-21) */
+  int64_t main_stream;  /* < 0: select_main_stream */
+} itt_analyze_opts;
+
+typedef struct itt_loop_result { /* LoopReport (report.hpp:92-103) integer fields + details rows */
+  int64_t iterations_declared;
+  int64_t pattern_length;
+  int32_t* pattern_tokens; /* [pattern_length] token ids (names via itt_analysis.name_row) */
+  int64_t pattern_count;
+  int64_t epsilon_used;
+  int64_t first_token;
+  int64_t k0_used;
+  uint64_t n_iterations;
+  itt_iter_row* rows;      /* [n_iterations] */
+  itt_clamps clamps;
+} itt_loop_result;
+
+typedef struct itt_analysis {
+  itt_census census;          /* after the majority-device filter */
+  uint32_t main_stream;
+  uint32_t n_main_streams;    /* kernel-bearing streams (MultipleMainStreams warning when > 1) */
+  int32_t main_stream_override_non_main; /* MainStreamOverride warning (pipeline.hpp:62-67) */
+  int32_t pad_;
+  uint64_t n_tokens;
+  uint32_t n_names;
+  uint64_t* name_row;         /* [n_names] source row carrying each token id's name */
+  int64_t overlapping_kernels; /* count_interval_overlaps on the main stream */
+  uint32_t n_loops;
+  itt_loop_result* loops;
+} itt_analysis;
+
+/* analyze_trace (pipeline.hpp:34-134) up to the per-loop integer aggregates; the
+ * host finishes compute_summary / diagnose / warnings in reference order. */
+int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* opts, itt_analysis** out);
+int itt_free_analysis(itt_ctx* ctx, itt_analysis* a);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ITERTRACE_CUDA_H */
