@@ -1,0 +1,591 @@
+// capi.cu — extern "C" entry points of libitertrace_cuda.so (include/itertrace_cuda.h) and the
+// analyze_trace orchestration (pipeline.hpp:34-134) on the device.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <set>
+
+#include "pipeline.cuh"
+
+using namespace itt;
+
+struct itt_ctx {
+  Ctx c;
+};
+
+namespace {
+
+template <typename F>
+int guarded(itt_ctx* ctx, F&& f) {
+  if (!ctx) return ITT_E_INVALID_ARGUMENT;
+  Ctx* c = &ctx->c;
+  try {
+    ITT_CUDA(cudaSetDevice(c->device));
+    f(c);
+    c->sync();
+    c->last_error.clear();
+    return ITT_OK;
+  } catch (const Error& e) {
+    c->last_error = e.what();
+    cudaStreamSynchronize(c->stream);
+    c->pending.clear();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    c->last_error = "host allocation failed";
+    return ITT_E_CUDA;
+  } catch (const std::exception& e) {
+    c->last_error = e.what();
+    return ITT_E_CUDA;
+  }
+}
+
+template <typename T>
+T* host_alloc(size_t n) {
+  T* p = static_cast<T*>(std::calloc(n ? n : 1, sizeof(T)));
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+
+void check_records(const itt_records* r) {
+  if (!r) fail(ITT_E_INVALID_ARGUMENT, "records: null");
+  if (r->n && (!r->start_ns || !r->duration_ns || !r->size_bytes || !r->flags || !r->stream || !r->name_off || !r->name_bytes))
+    fail(ITT_E_INVALID_ARGUMENT, "records: missing column");
+  if (r->n >= 0xFFFFFFFFull) fail(ITT_E_INVALID_ARGUMENT, "records: more than 2^32-1 rows per trace");
+}
+
+// records -> dictionary -> census (optionally device-filtered)
+void prepare(Ctx* c, TraceState& t, const itt_records* r, bool device_filter) {
+  check_records(r);
+  t.c = c;
+  upload_records(c, r, t.rec);
+  order_records(t);
+  build_dictionary(t);
+  if (!device_filter) {
+    t.filtering = false;
+    t.kept = t.rec.n;
+  }
+  stream_census(t);
+}
+
+uint64_t stream_total(const itt_stream_summary& s) {
+  return s.counts[0] + s.counts[1] + s.counts[2] + s.counts[3] + s.counts[4] + s.counts[5];
+}
+
+void fill_census(const TraceState& t, itt_census* out) {
+  out->n_streams = static_cast<uint32_t>(t.streams.size());
+  out->streams = host_alloc<itt_stream_summary>(t.streams.size());
+  std::memcpy(out->streams, t.streams.data(), t.streams.size() * sizeof(itt_stream_summary));
+  out->n_devices = t.n_devices;
+  out->majority_device = t.majority;
+  out->dropped_records = t.filtering ? t.rec.n - t.kept : 0;
+  out->n_records = t.kept;
+}
+
+// select_main_stream (streams.hpp:113-145)
+uint32_t select_main(const std::vector<itt_stream_summary>& ss, uint32_t* n_main) {
+  const itt_stream_summary* best = nullptr;
+  uint32_t cnt = 0;
+  for (const auto& s : ss) {
+    if (s.cls != ITT_CLASS_MAIN) continue;
+    ++cnt;
+    if (!best || s.counts[0] > best->counts[0] || (s.counts[0] == best->counts[0] && s.stream < best->stream)) best = &s;
+  }
+  if (n_main) *n_main = cnt;
+  if (!best) fail(ITT_E_NO_MAIN_STREAM, "stream-classify: no stream contains kernel operations");
+  return best->stream;
+}
+
+void tokens_to_device(Ctx* c, const int32_t* tokens, uint64_t n, DBuf<int32_t>& d) {
+  d.alloc(c, n + 1);
+  h2d(c, d.p, tokens, n);
+}
+
+}  // namespace
+
+extern "C" {
+
+int itt_abi_version(void) { return ITT_ABI_VERSION; }
+
+int itt_ctx_create(int device, itt_ctx** out) {
+  if (!out) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) return ITT_E_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return ITT_E_CUDA;
+  if (prop.major < 10) return ITT_E_CUDA;  // sm_100a kernels only
+  itt_ctx* x = new (std::nothrow) itt_ctx;
+  if (!x) return ITT_E_CUDA;
+  Ctx* c = &x->c;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete x;
+    return ITT_E_CUDA;
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = x;
+  return ITT_OK;
+}
+
+int itt_ctx_destroy(itt_ctx* ctx) {
+  if (!ctx) return ITT_OK;
+  Ctx* c = &ctx->c;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  cudaStreamDestroy(c->stream);
+  delete ctx;
+  return ITT_OK;
+}
+
+const char* itt_last_error(itt_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
+
+int itt_free(itt_ctx*, void* p) {
+  std::free(p);
+  return ITT_OK;
+}
+
+int itt_ctx_set_profiling(itt_ctx* ctx, int enabled) {
+  return guarded(ctx, [&](Ctx* c) { c->profiling = enabled != 0; });
+}
+int itt_ctx_reset_stats(itt_ctx* ctx) {
+  return guarded(ctx, [&](Ctx* c) { c->stats.clear(); });
+}
+int itt_ctx_kernel_stats(itt_ctx* ctx, itt_kernel_stat* out, uint32_t cap, uint32_t* n_out) {
+  return guarded(ctx, [&](Ctx* c) {
+    uint32_t i = 0;
+    for (const auto& kv : c->stats) {
+      if (i < cap && out) {
+        std::memset(&out[i], 0, sizeof(out[i]));
+        std::strncpy(out[i].name, kv.first.c_str(), sizeof(out[i].name) - 1);
+        out[i].launches = kv.second.launches;
+        out[i].total_ms = kv.second.total_ms;
+        out[i].bytes = kv.second.bytes;
+      }
+      ++i;
+    }
+    if (n_out) *n_out = i;
+  });
+}
+int itt_ctx_launch_count(itt_ctx* ctx, uint64_t* out) {
+  if (!ctx || !out) return ITT_E_INVALID_ARGUMENT;
+  *out = ctx->c.launches;
+  return ITT_OK;
+}
+int itt_device_alloc(itt_ctx* ctx, uint64_t bytes, void** out) {
+  return guarded(ctx, [&](Ctx* c) {
+    ITT_CUDA(cudaMalloc(out, bytes + 16));
+    (void)c;
+  });
+}
+int itt_device_free(itt_ctx* ctx, void* p) {
+  return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaFree(p)); });
+}
+int itt_memcpy_h2d(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  return guarded(ctx, [&](Ctx* c) { ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream)); });
+}
+int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  return guarded(ctx, [&](Ctx* c) { ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream)); });
+}
+int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes) {
+  return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault)); });
+}
+int itt_host_unregister(itt_ctx* ctx, void* p) {
+  return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostUnregister(p)); });
+}
+int itt_ctx_synchronize(itt_ctx* ctx) {
+  return guarded(ctx, [&](Ctx*) {});
+}
+
+// ------------------------------------------------------------------ streams
+int itt_summarize_streams(itt_ctx* ctx, const itt_records* recs, int filter_device, itt_census* out) {
+  if (!out) return ITT_E_INVALID_ARGUMENT;
+  std::memset(out, 0, sizeof(*out));
+  return guarded(ctx, [&](Ctx* c) {
+    if (!recs || recs->n == 0) fail(ITT_E_EMPTY_TRACE, "stream-classify: trace has no records");
+    TraceState t;
+    prepare(c, t, recs, filter_device != 0);
+    fill_census(t, out);
+  });
+}
+
+int itt_select_main_stream(itt_ctx* ctx, const itt_census* census, uint32_t* main_stream, uint32_t* n_main_streams) {
+  return guarded(ctx, [&](Ctx*) {
+    if (!census || !main_stream) fail(ITT_E_INVALID_ARGUMENT, "select_main_stream: null argument");
+    std::vector<itt_stream_summary> ss(census->streams, census->streams + census->n_streams);
+    *main_stream = select_main(ss, n_main_streams);
+  });
+}
+
+int itt_build_token_sequence(itt_ctx* ctx, const itt_records* recs, uint32_t main_stream, itt_tokens** out) {
+  if (!out) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded(ctx, [&](Ctx* c) {
+    TraceState t;
+    if (!recs || recs->n == 0)
+      fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
+    prepare(c, t, recs, false);
+    uint64_t n_main = 0;
+    for (const auto& s : t.streams)
+      if (s.stream == main_stream) n_main = stream_total(s);
+    if (n_main == 0)
+      fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
+    compact_main(t, main_stream, true);
+    renumber_tokens(t);
+    itt_tokens* o = host_alloc<itt_tokens>(1);
+    o->n = t.n_tok;
+    o->tokens = host_alloc<int32_t>(t.n_tok);
+    o->record_index = host_alloc<uint64_t>(t.n_tok);
+    o->n_names = t.n_names;
+    o->name_row = host_alloc<uint64_t>(t.n_names);
+    d2h(c, o->tokens, t.tokens.p, t.n_tok);
+    d2h(c, o->record_index, t.tok_record.p, t.n_tok);
+    std::memcpy(o->name_row, t.name_row.data(), t.n_names * sizeof(uint64_t));
+    c->sync();
+    *out = o;
+  });
+}
+
+int itt_count_interval_overlaps(itt_ctx* ctx, const itt_records* recs, uint32_t stream, int64_t* out) {
+  if (!out) return ITT_E_INVALID_ARGUMENT;
+  *out = 0;
+  return guarded(ctx, [&](Ctx* c) {
+    if (!recs || recs->n == 0) return;
+    TraceState t;
+    prepare(c, t, recs, false);
+    compact_main(t, stream, false);
+    *out = count_overlaps(t);
+  });
+}
+
+// ------------------------------------------------------------------ mining
+int itt_suffix_array(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, uint32_t* sa, uint32_t* lcp) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (!sa || (n && !tokens)) fail(ITT_E_INVALID_ARGUMENT, "suffix_array: null argument");
+    DBuf<int32_t> dt;
+    tokens_to_device(c, tokens, n, dt);
+    SuffixState s;
+    radix::Scratch rs;
+    ScanScratch sc;
+    build_suffix_array(c, dt.p, n, term, s, lcp != nullptr, rs, sc);
+    d2h(c, sa, s.sa.p, n + 1);
+    if (lcp) d2h(c, lcp, s.lcp.p, n + 1);
+  });
+}
+
+namespace {
+__global__ void k_collect_repeats(const uint32_t* __restrict__ lcp, const uint32_t* __restrict__ cnt,
+                                  const uint32_t* __restrict__ par, const uint32_t* __restrict__ lb,
+                                  const uint32_t* __restrict__ sa, uint64_t np, int64_t min_count, int64_t max_len,
+                                  itt_repeat* out, unsigned int* n_out) {
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= np || cnt[k] == 0) return;
+  const int64_t c = cnt[k];
+  if (c < min_count) return;
+  const int64_t len = imin64(static_cast<int64_t>(lcp[k]), max_len);
+  if (len <= static_cast<int64_t>(par[k])) return;
+  uint32_t m = 0xFFFFFFFFu;
+  for (uint32_t q = 0; q < c; ++q) m = min(m, sa[lb[k] + q]);
+  const unsigned i = atomicAdd(n_out, 1u);
+  out[i].start = static_cast<int32_t>(m);
+  out[i].length = static_cast<int32_t>(len);
+  out[i].count = c;
+}
+}  // namespace
+
+int itt_enumerate_repeats(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, int64_t min_count, int64_t max_len,
+                          itt_repeat** out, uint64_t* n_out) {
+  if (!out || !n_out) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  *n_out = 0;
+  return guarded(ctx, [&](Ctx* c) {
+    itt_repeat* res = nullptr;
+    uint64_t cnt = 0;
+    if (max_len >= 1 && n > 0) {  // mine.hpp:50
+      DBuf<int32_t> dt;
+      tokens_to_device(c, tokens, n, dt);
+      SuffixState s;
+      radix::Scratch rs;
+      ScanScratch sc;
+      build_suffix_array(c, dt.p, n, term, s, true, rs, sc);
+      IntervalState iv;
+      lcp_intervals(c, s, iv);
+      DBuf<itt_repeat> dout(c, s.np);
+      DBuf<unsigned int> dn(c, 1);
+      dn.zero();
+      launch(c, "repeats_collect", s.np * 16.0, k_collect_repeats, dim3(grid_for(s.np, 256)), dim3(256), 0, s.lcp.p,
+             iv.cnt.p, iv.par.p, iv.lb.p, s.sa.p, s.np, min_count, max_len, dout.p, dn.p);
+      cnt = read1(c, dn.p);
+      res = host_alloc<itt_repeat>(cnt);
+      d2h(c, res, dout.p, cnt);
+      c->sync();
+    } else {
+      res = host_alloc<itt_repeat>(0);
+    }
+    *out = res;
+    *n_out = cnt;
+  });
+}
+
+int itt_mine_patterns(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, const itt_mining_cfg* loops,
+                      uint32_t n_loops, int multi, itt_pattern** out) {
+  if (!out) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded(ctx, [&](Ctx* c) {
+    std::vector<itt_mining_cfg> cfgs(loops, loops + n_loops);
+    if (multi) {  // mine.hpp:134-146
+      if (cfgs.empty()) fail(ITT_E_INVALID_CONFIG, "pattern-mining: no loop specs given");
+      std::set<int64_t> seen;
+      for (const auto& l : cfgs)
+        if (!seen.insert(l.iterations).second)
+          fail(ITT_E_INVALID_CONFIG, "pattern-mining: loop iteration counts must be pairwise distinct (duplicate " +
+                                         std::to_string(l.iterations) + ")");
+    } else {
+      if (cfgs.empty()) fail(ITT_E_INVALID_ARGUMENT, "mine_pattern: no config");
+      cfgs.resize(1);
+    }
+    DBuf<int32_t> dt;
+    tokens_to_device(c, tokens, n, dt);
+    SuffixState s;
+    radix::Scratch rs;
+    ScanScratch sc;
+    build_suffix_array(c, dt.p, n, term, s, true, rs, sc);
+    IntervalState iv;
+    lcp_intervals(c, s, iv);
+    const auto res = mine_loops(c, s, iv, cfgs, multi != 0);
+    for (const auto& r : res)
+      if (r.status) fail(r.status, r.error);
+    if (multi)  // mine.hpp:155-164
+      for (size_t a = 0; a < res.size(); ++a)
+        for (size_t b = a + 1; b < res.size(); ++b)
+          if (res[a].tokens == res[b].tokens)
+            fail(ITT_E_AMBIGUOUS_LOOPS, "pattern-mining: loops " + std::to_string(a + 1) + " and " + std::to_string(b + 1) +
+                                            " mined the same pattern; the loop specs are ambiguous");
+    itt_pattern* o = host_alloc<itt_pattern>(res.size());
+    for (size_t i = 0; i < res.size(); ++i) {
+      o[i].length = static_cast<int64_t>(res[i].tokens.size());
+      o[i].tokens = host_alloc<int32_t>(res[i].tokens.size());
+      std::memcpy(o[i].tokens, res[i].tokens.data(), res[i].tokens.size() * 4);
+      o[i].count = res[i].count;
+      o[i].first_token = res[i].first_token;
+      o[i].epsilon_used = res[i].epsilon_used;
+    }
+    *out = o;
+  });
+}
+
+int itt_free_patterns(itt_ctx*, itt_pattern* p, uint32_t n_loops) {
+  if (!p) return ITT_OK;
+  for (uint32_t i = 0; i < n_loops; ++i) std::free(p[i].tokens);
+  std::free(p);
+  return ITT_OK;
+}
+
+// ------------------------------------------------------------------ matching
+int itt_approx_match(itt_ctx* ctx, const int32_t* tokens, uint64_t n, const int32_t* pattern, uint64_t m, int64_t k0,
+                     itt_span** out, uint64_t* n_out) {
+  if (!out || !n_out) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  *n_out = 0;
+  return guarded(ctx, [&](Ctx* c) {
+    SpanState sp;
+    if (m > 0 && n >= m) {
+      DBuf<int32_t> dt, dp;
+      tokens_to_device(c, tokens, n, dt);
+      tokens_to_device(c, pattern, m, dp);
+      ScanScratch sc;
+      approx_match_dev(c, dt.p, n, dp.p, m, k0, sp, sc);
+    }
+    std::vector<uint32_t> s(sp.n), e(sp.n), x(sp.n);
+    d2h(c, s.data(), sp.start.p, sp.n);
+    d2h(c, e.data(), sp.end.p, sp.n);
+    d2h(c, x.data(), sp.extra.p, sp.n);
+    c->sync();
+    itt_span* o = host_alloc<itt_span>(sp.n);
+    for (uint64_t i = 0; i < sp.n; ++i) o[i] = itt_span{s[i], e[i], x[i]};
+    *out = o;
+    *n_out = sp.n;
+  });
+}
+
+// ------------------------------------------------------------------ aggregates
+namespace {
+__global__ void k_gather_tok_times(const uint64_t* __restrict__ ri, uint64_t n, const uint32_t* __restrict__ perm,
+                                   const int64_t* __restrict__ start, const int64_t* __restrict__ dur,
+                                   int64_t* __restrict__ ts, int64_t* __restrict__ te) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint64_t k = ri[j];
+  const uint64_t i = perm ? perm[k] : k;
+  ts[j] = start[i];
+  te[j] = start[i] + dur[i];
+}
+}  // namespace
+
+int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t* record_index, uint64_t n_tokens,
+                          const itt_span* spans, uint64_t n_spans, itt_iter_row** rows, itt_clamps* clamps) {
+  if (!rows || !clamps) return ITT_E_INVALID_ARGUMENT;
+  *rows = nullptr;
+  return guarded(ctx, [&](Ctx* c) {
+    std::vector<itt_iter_row> out;
+    itt_clamps cl{0, 0};
+    if (n_spans > 0) {
+      for (uint64_t i = 0; i < n_spans; ++i)
+        if (spans[i].start_token < 0 || spans[i].end_token < spans[i].start_token ||
+            static_cast<uint64_t>(spans[i].end_token) >= n_tokens)
+          fail(ITT_E_INVALID_ARGUMENT, "metrics: span outside the token sequence");
+      TraceState t;
+      prepare(c, t, recs, false);
+      compact_main(t, 0xFFFFFFFFu, false);  // HtoD list (all streams); the token columns come from record_index
+      DBuf<uint64_t> ri(c, n_tokens);
+      h2d(c, ri.p, record_index, n_tokens);
+      DBuf<int64_t> ts(c, n_tokens + 1), te(c, n_tokens + 1);
+      launch(c, "agg_gather", n_tokens * 40.0, k_gather_tok_times, dim3(grid_for(n_tokens, 256)), dim3(256), 0, ri.p, n_tokens,
+             t.sorted ? nullptr : t.perm.p, t.rec.start, t.rec.dur, ts.p, te.p);
+      SpanState sp;
+      sp.n = n_spans;
+      std::vector<uint32_t> s(n_spans), e(n_spans), x(n_spans);
+      for (uint64_t i = 0; i < n_spans; ++i) {
+        s[i] = static_cast<uint32_t>(spans[i].start_token);
+        e[i] = static_cast<uint32_t>(spans[i].end_token);
+        x[i] = static_cast<uint32_t>(spans[i].extra);
+      }
+      sp.start.alloc(c, n_spans);
+      sp.end.alloc(c, n_spans);
+      sp.extra.alloc(c, n_spans);
+      h2d(c, sp.start.p, s.data(), n_spans);
+      h2d(c, sp.end.p, e.data(), n_spans);
+      h2d(c, sp.extra.p, x.data(), n_spans);
+      iteration_aggregates(c, ts.p, te.p, n_tokens, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp, out, cl,
+                           t.scan);
+    }
+    itt_iter_row* o = host_alloc<itt_iter_row>(out.size());
+    std::memcpy(o, out.data(), out.size() * sizeof(itt_iter_row));
+    *rows = o;
+    *clamps = cl;
+  });
+}
+
+// ------------------------------------------------------------------ analyze
+int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* opts, itt_analysis** out) {
+  if (!out || !opts) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded(ctx, [&](Ctx* c) {
+    if (opts->n_loops == 0 || !opts->loops)
+      fail(ITT_E_INVALID_CONFIG, "analyze: at least one iteration count is required");
+    if (!recs || recs->n == 0) fail(ITT_E_EMPTY_TRACE, "stream-classify: trace has no records");
+    TraceState t;
+    prepare(c, t, recs, true);
+    // main stream: override or selection (pipeline.hpp:56-73)
+    uint32_t main_stream = 0, n_main_streams = 0;
+    int32_t override_non_main = 0;
+    for (const auto& s : t.streams) n_main_streams += s.cls == ITT_CLASS_MAIN;
+    if (opts->main_stream >= 0) {
+      main_stream = static_cast<uint32_t>(opts->main_stream);
+      const auto it = std::find_if(t.streams.begin(), t.streams.end(),
+                                   [&](const itt_stream_summary& s) { return s.stream == main_stream; });
+      if (it == t.streams.end())
+        fail(ITT_E_EMPTY_MAIN_STREAM,
+             "stream-classify: override stream " + std::to_string(main_stream) + " does not appear in the trace");
+      override_non_main = it->cls != ITT_CLASS_MAIN;
+    } else {
+      main_stream = select_main(t.streams, &n_main_streams);
+    }
+    compact_main(t, main_stream, false);
+    if (t.n_tok == 0)
+      fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
+    renumber_tokens(t);
+    const int64_t overlaps = count_overlaps(t);
+    // mining over one shared SA / LCP / interval set (pipeline.hpp:81-91)
+    std::vector<itt_mining_cfg> cfgs;
+    for (uint32_t k = 0; k < opts->n_loops; ++k) cfgs.push_back(itt_mining_cfg{opts->loops[k], opts->epsilon0, 0});
+    const bool multi = cfgs.size() > 1;
+    if (multi) {
+      std::set<int64_t> seen;
+      for (const auto& l : cfgs)
+        if (!seen.insert(l.iterations).second)
+          fail(ITT_E_INVALID_CONFIG, "pattern-mining: loop iteration counts must be pairwise distinct (duplicate " +
+                                         std::to_string(l.iterations) + ")");
+    }
+    SuffixState s;
+    build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan);
+    IntervalState iv;
+    lcp_intervals(c, s, iv);
+    const auto pats = mine_loops(c, s, iv, cfgs, multi);
+    for (const auto& p : pats)
+      if (p.status) fail(p.status, p.error);
+    if (multi)
+      for (size_t a = 0; a < pats.size(); ++a)
+        for (size_t b = a + 1; b < pats.size(); ++b)
+          if (pats[a].tokens == pats[b].tokens)
+            fail(ITT_E_AMBIGUOUS_LOOPS, "pattern-mining: loops " + std::to_string(a + 1) + " and " + std::to_string(b + 1) +
+                                            " mined the same pattern; the loop specs are ambiguous");
+    // per loop: match + aggregates (pipeline.hpp:96-132)
+    struct Holder {
+      itt_analysis* a = nullptr;
+      ~Holder() { itt_free_analysis(nullptr, a); }
+    } hold;
+    itt_analysis* a = hold.a = host_alloc<itt_analysis>(1);
+    fill_census(t, &a->census);
+    a->main_stream = main_stream;
+    a->n_main_streams = n_main_streams;
+    a->main_stream_override_non_main = override_non_main;
+    a->n_tokens = t.n_tok;
+    a->n_names = t.n_names;
+    a->name_row = host_alloc<uint64_t>(t.n_names);
+    std::memcpy(a->name_row, t.name_row.data(), t.n_names * sizeof(uint64_t));
+    a->overlapping_kernels = overlaps;
+    a->n_loops = static_cast<uint32_t>(pats.size());
+    a->loops = host_alloc<itt_loop_result>(pats.size());
+    for (size_t k = 0; k < pats.size(); ++k) {
+      const auto& p = pats[k];
+      itt_loop_result& L = a->loops[k];
+      L.iterations_declared = cfgs[k].iterations;
+      L.pattern_length = static_cast<int64_t>(p.tokens.size());
+      L.pattern_tokens = host_alloc<int32_t>(p.tokens.size());
+      std::memcpy(L.pattern_tokens, p.tokens.data(), p.tokens.size() * 4);
+      L.pattern_count = p.count;
+      L.epsilon_used = p.epsilon_used;
+      L.first_token = p.first_token;
+      L.k0_used = opts->k0 >= 0 ? opts->k0 : (L.pattern_length + 3) / 4;  // default_k0, match.hpp:19-21
+      DBuf<int32_t> dp;
+      tokens_to_device(c, p.tokens.data(), p.tokens.size(), dp);
+      SpanState sp;
+      approx_match_dev(c, t.tokens.p, t.n_tok, dp.p, p.tokens.size(), L.k0_used, sp, t.scan);
+      std::vector<itt_iter_row> rows;
+      iteration_aggregates(c, t.tok_start.p, t.tok_end.p, t.n_tok, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp,
+                           rows, L.clamps, t.scan);
+      L.n_iterations = rows.size();
+      L.rows = host_alloc<itt_iter_row>(rows.size());
+      std::memcpy(L.rows, rows.data(), rows.size() * sizeof(itt_iter_row));
+    }
+    *out = a;
+    hold.a = nullptr;
+  });
+}
+
+int itt_free_analysis(itt_ctx*, itt_analysis* a) {
+  if (!a) return ITT_OK;
+  std::free(a->census.streams);
+  std::free(a->name_row);
+  for (uint32_t k = 0; k < a->n_loops; ++k) {
+    std::free(a->loops[k].pattern_tokens);
+    std::free(a->loops[k].rows);
+  }
+  std::free(a->loops);
+  std::free(a);
+  return ITT_OK;
+}
+
+}  // extern "C"

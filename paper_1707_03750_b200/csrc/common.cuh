@@ -1,0 +1,239 @@
+// common.cuh — shared infrastructure of libitertrace_cuda.so: context, errors, device
+// buffers, profiled launches, small device helpers.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "itertrace_cuda.h"
+
+namespace itt {
+
+// ---------------------------------------------------------------- errors
+// Pipeline errors carry the reference's ErrorKind (as 1 + kind) and a stage-prefixed
+// message (errors.hpp:23-34); device failures carry ITT_E_CUDA.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+#define ITT_CUDA(call)                                                                                   \
+  do {                                                                                                   \
+    cudaError_t e_ = (call);                                                                             \
+    if (e_ != cudaSuccess)                                                                               \
+      ::itt::fail(ITT_E_CUDA, std::string("cuda: ") + cudaGetErrorString(e_) + " at " + __FILE__ + ":" + \
+                                  std::to_string(__LINE__));                                             \
+  } while (0)
+
+// ---------------------------------------------------------------- context
+struct KStat {
+  uint64_t launches = 0;
+  double total_ms = 0, bytes = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  uint64_t launches = 0;
+  bool profiling = false;
+  std::map<std::string, KStat> stats;
+  struct Pending {
+    std::string name;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  void* pinned = nullptr;  // small staging buffer for scalar readbacks
+  size_t pinned_bytes = 0;
+
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ITT_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  // resolve event pairs after a stream synchronize
+  void resolve_profile() {
+    for (auto& p : pending) {
+      float ms = 0;
+      ITT_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+      KStat& s = stats[p.name];
+      s.launches += 1;
+      s.total_ms += ms;
+      s.bytes += p.bytes;
+      event_pool.push_back(p.a);
+      event_pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+  void sync() {
+    ITT_CUDA(cudaStreamSynchronize(stream));
+    if (!pending.empty()) resolve_profile();
+  }
+  void* staging(size_t bytes) {
+    if (bytes > pinned_bytes) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned_bytes = bytes < 4096 ? 4096 : bytes;
+      ITT_CUDA(cudaMallocHost(&pinned, pinned_bytes));
+    }
+    return pinned;
+  }
+};
+
+// Profiled launch: records CUDA events on the context stream around the launch when
+// profiling is on; `bytes` is the launch's algorithmic HBM traffic.
+struct LaunchScope {
+  Ctx* c;
+  const char* name;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  LaunchScope(Ctx* c_, const char* n, double b) : c(c_), name(n), bytes(b) {
+    if (c->profiling) {
+      a = c->take_event();
+      ITT_CUDA(cudaEventRecord(a, c->stream));
+    }
+  }
+  ~LaunchScope() noexcept(false) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(ITT_E_CUDA, std::string("cuda launch ") + name + ": " + cudaGetErrorString(e));
+    c->launches += 1;
+    if (c->profiling) {
+      cudaEvent_t b = c->take_event();
+      ITT_CUDA(cudaEventRecord(b, c->stream));
+      c->pending.push_back({name, bytes, a, b});
+    }
+  }
+};
+
+// launch through a kernel pointer: <<<>>> on the context stream inside a LaunchScope
+template <typename... KArgs, typename... Args>
+inline void launch(Ctx* c, const char* name, double bytes, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   Args&&... args) {
+  LaunchScope ls(c, name, bytes);
+  k<<<grid, block, smem, c->stream>>>(static_cast<KArgs>(args)...);
+}
+
+// ---------------------------------------------------------------- device buffers
+// Stream-ordered allocations from the device's default pool (release threshold raised
+// at context creation so memory is recycled across calls instead of returned to the OS).
+template <typename T>
+struct DBuf {
+  Ctx* c = nullptr;
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(Ctx* ctx, size_t count) { alloc(ctx, count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : c(o.c), p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      c = o.c, p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(Ctx* ctx, size_t count) {
+    release();
+    c = ctx;
+    n = count;
+    if (count) ITT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->stream));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, c->stream);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+  void zero() {
+    if (n) ITT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), c->stream));
+  }
+  void fill_bytes(int v) {
+    if (n) ITT_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), c->stream));
+  }
+};
+
+template <typename T>
+inline void h2d(Ctx* c, T* dst, const T* src, size_t count) {
+  if (count) ITT_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+}
+template <typename T>
+inline void d2h(Ctx* c, T* dst, const T* src, size_t count) {
+  if (count) ITT_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+// read `count` values back through the pinned staging buffer (synchronizes)
+template <typename T>
+inline void readback(Ctx* c, T* dst, const T* src, size_t count) {
+  T* st = static_cast<T*>(c->staging(count * sizeof(T)));
+  d2h(c, st, src, count);
+  c->sync();
+  for (size_t i = 0; i < count; ++i) dst[i] = st[i];
+}
+template <typename T>
+inline T read1(Ctx* c, const T* src) {
+  T v;
+  readback(c, &v, src, 1);
+  return v;
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 1u << 30) {
+  uint64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+inline int bits_for(uint64_t maxval) {  // number of bits to represent values <= maxval (>= 1)
+  int b = 1;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return b;
+}
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace itt
+
+namespace itt {
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+}  // namespace itt

@@ -1,0 +1,832 @@
+// intern.cu — records -> (start,row) order -> GPU name dictionary -> census -> main-stream
+// token string in first-appearance order.
+//
+// Replaces, on the device:
+//   ingest.hpp:396-400      stable sort by (start, row)            (K1: radix sort of start)
+//   trace.hpp:103-113       classify_op_kind per record            (per distinct name, then a lookup)
+//   streams.hpp:60-81       summarize_streams                      (warp-aggregated census)
+//   streams.hpp:179-207     filter_majority_device                 (device census + keep mask)
+//   streams.hpp:147-169     build_token_sequence                   (hash dictionary + first appearance)
+//   streams.hpp:212-221     count_interval_overlaps
+// The dictionary is exact: a 64-bit hash only picks the slot; every record's name bytes are
+// then compared with the slot representative's bytes, and a mismatch (a true hash
+// collision) re-runs the dictionary with another seed.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "pipeline.cuh"
+
+namespace itt {
+
+namespace {
+
+constexpr int kHashBlock = 256;
+constexpr int kWarpBuf = 4096;  // staged name bytes per warp
+constexpr uint32_t kDevSmem = 64;
+constexpr uint32_t kStreamTableCap = 4096;
+constexpr uint32_t kBlockStreams = 64;
+
+// classify bits of a name (trace.hpp:103-113 needs memcpy+{htod,dtoh,dtod}, memset)
+enum : uint8_t { NB_MEMCPY = 1, NB_HTOD = 2, NB_DTOH = 4, NB_DTOD = 8, NB_MEMSET = 16 };
+
+__device__ __forceinline__ int kind_from(uint8_t nb, bool has_tp) {
+  if (nb & NB_MEMCPY) {
+    if (nb & NB_HTOD) return ITT_KIND_HTOD;
+    if (nb & NB_DTOH) return ITT_KIND_DTOH;
+    if (nb & NB_DTOD) return ITT_KIND_DTOD;
+  }
+  if (nb & NB_MEMSET) return ITT_KIND_MEMSET;
+  return has_tp ? ITT_KIND_OTHER : ITT_KIND_KERNEL;
+}
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+// 64-bit hash of a byte string read through `get(i)`
+template <typename Get>
+__device__ __forceinline__ uint64_t hash_name(Get get, uint32_t len, uint64_t seed) {
+  uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
+  uint32_t i = 0;
+  for (; i + 8 <= len; i += 8) {
+    uint64_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w |= static_cast<uint64_t>(get(i + j)) << (8 * j);
+    h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
+  }
+  uint64_t w = 0;
+  for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(get(i + j)) << (8 * j);
+  h = rotl64(h ^ (w * 0x87c37b91114253d5ull + len), 31) * 0x4cf5ad432745937full;
+  h = fmix64(h);
+  return h ? h : 1;  // 0 marks an empty slot
+}
+
+// Stage the name bytes of rows [g0, g1) into a per-warp shared buffer with 16-byte loads.
+// Returns false when they do not fit (the caller then reads global memory directly).
+__device__ __forceinline__ bool stage_names(const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes,
+                                            uint64_t total, uint64_t g0, uint64_t g1, uint8_t* buf, uint64_t& base) {
+  const uint64_t b0 = name_off[g0], b1 = name_off[g1];
+  const uint64_t a0 = b0 & ~15ull, a1 = (b1 + 15) & ~15ull;
+  if (a1 - a0 > static_cast<uint64_t>(kWarpBuf)) return false;
+  const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
+  for (uint64_t o = a0 + lane_id() * 16; o < a1; o += 512) {
+    if (aligned && o + 16 <= total) {
+      *reinterpret_cast<uint4*>(buf + (o - a0)) = __ldg(reinterpret_cast<const uint4*>(bytes + o));
+    } else {
+      for (int j = 0; j < 16; ++j) buf[o - a0 + j] = o + j < total ? bytes[o + j] : 0;
+    }
+  }
+  __syncwarp();
+  base = a0;
+  return true;
+}
+
+// ------------------------------------------------------------------ K1: order
+__global__ void k_order_stats(const int64_t* __restrict__ start, uint64_t n, unsigned long long* out /*min,max,desc*/) {
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  unsigned long long desc = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long s = start[i];
+    mn = s < mn ? s : mn;
+    mx = s > mx ? s : mx;
+    if (i > 0 && start[i - 1] > s) ++desc;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    desc += __shfl_xor_sync(0xffffffffu, desc, o);
+  }
+  if (lane_id() == 0) {
+    atomicMin(reinterpret_cast<long long*>(&out[0]), mn);
+    atomicMax(reinterpret_cast<long long*>(&out[1]), mx);
+    if (desc) atomicAdd(&out[2], desc);
+  }
+}
+
+__global__ void k_order_keys(const int64_t* __restrict__ start, uint64_t n, int64_t mn, uint64_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    keys[i] = static_cast<uint64_t>(start[i] - mn);
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// ------------------------------------------------------------------ K2: dictionary
+struct HashArgs {
+  const uint64_t* name_off;
+  const uint8_t* bytes;
+  uint64_t total;
+  uint64_t n;
+  const uint16_t* device;
+  uint64_t* tkey;
+  uint32_t* trep;
+  uint32_t mask;
+  uint64_t seed;
+  uint32_t* slot_out;
+  uint32_t* used;
+  uint32_t* used_count;  // [0] = count, [1] = overflow flag
+  unsigned long long* dev_counts;  // [65536]
+  uint32_t* dev_max;
+};
+
+__global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
+  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf];
+  __shared__ unsigned int s_dev[kDevSmem];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x) s_dev[i] = 0;
+  __syncthreads();
+  uint8_t* buf = s_buf[warp];
+  const uint64_t groups = (a.n + 31) / 32;
+  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp; g < groups; g += gstride) {
+    const uint64_t g0 = g * 32, g1 = min(g0 + 32, a.n);
+    const uint64_t row = g0 + lane;
+    const bool valid = row < a.n;
+    uint64_t base = 0;
+    const bool staged = stage_names(a.name_off, a.bytes, a.total, g0, g1, buf, base);
+    uint64_t h = 0;
+    if (valid) {
+      const uint64_t o = a.name_off[row];
+      const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
+      if (staged) {
+        const uint8_t* p = buf + (o - base);
+        h = hash_name([&](uint32_t i) { return p[i]; }, len, a.seed);
+      } else {
+        const uint8_t* p = a.bytes + o;
+        h = hash_name([&](uint32_t i) { return p[i]; }, len, a.seed);
+      }
+    }
+    // one insertion per distinct hash per warp; the lowest lane holds the smallest row
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? h : 0ull);
+    const int leader = __ffs(peers) - 1;
+    uint32_t s = 0;
+    if (valid && static_cast<int>(lane) == leader) {
+      s = static_cast<uint32_t>(h) & a.mask;
+      for (uint32_t probe = 0;; ++probe) {
+        if (probe > a.mask) {
+          atomicOr(&a.used_count[1], 1u);
+          break;
+        }
+        uint64_t k = ld_relaxed_u64(&a.tkey[s]);
+        if (k == 0) {
+          const unsigned long long old =
+              atomicCAS(reinterpret_cast<unsigned long long*>(&a.tkey[s]), 0ull, static_cast<unsigned long long>(h));
+          if (old == 0) {
+            const uint32_t u = atomicAdd(&a.used_count[0], 1u);
+            a.used[u] = s;
+            break;
+          }
+          k = old;
+        }
+        if (k == h) break;
+        s = (s + 1) & a.mask;
+      }
+      const uint32_t r = static_cast<uint32_t>(row);
+      if (__ldcg(&a.trep[s]) > r) atomicMin(&a.trep[s], r);
+    }
+    s = __shfl_sync(0xffffffffu, s, leader);
+    if (valid) a.slot_out[row] = s;
+    // device census (filter_majority_device), warp-aggregated
+    if (a.device) {
+      const uint32_t d = valid ? a.device[row] : 0xFFFFFu;
+      const unsigned dp = __match_any_sync(0xffffffffu, d);
+      if (valid && static_cast<int>(lane) == __ffs(dp) - 1) {
+        if (d < kDevSmem) atomicAdd(&s_dev[d], static_cast<unsigned>(__popc(dp)));
+        else atomicAdd(&a.dev_counts[d], static_cast<unsigned long long>(__popc(dp)));
+        atomicMax(a.dev_max, d);
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (a.device)
+    for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x)
+      if (s_dev[i]) atomicAdd(&a.dev_counts[i], static_cast<unsigned long long>(s_dev[i]));
+}
+
+__device__ __forceinline__ bool contains_ci(const uint8_t* h, uint32_t hl, const char* needle, uint32_t nl) {
+  if (hl < nl) return false;
+  for (uint32_t i = 0; i + nl <= hl; ++i) {
+    uint32_t j = 0;
+    while (j < nl) {
+      uint8_t ch = h[i + j];
+      if (ch >= 'A' && ch <= 'Z') ch += 32;
+      if (ch != static_cast<uint8_t>(needle[j])) break;
+      ++j;
+    }
+    if (j == nl) return true;
+  }
+  return false;
+}
+
+// classify each distinct name once (trace.hpp:103-113)
+__global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ trep,
+                                 const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes,
+                                 uint8_t* __restrict__ tflags) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n_used) return;
+  const uint32_t s = used[u];
+  const uint32_t r = trep[s];
+  const uint8_t* p = bytes + name_off[r];
+  const uint32_t len = static_cast<uint32_t>(name_off[r + 1] - name_off[r]);
+  uint8_t f = 0;
+  if (contains_ci(p, len, "memcpy", 6)) f |= NB_MEMCPY;
+  if (contains_ci(p, len, "htod", 4)) f |= NB_HTOD;
+  if (contains_ci(p, len, "dtoh", 4)) f |= NB_DTOH;
+  if (contains_ci(p, len, "dtod", 4)) f |= NB_DTOD;
+  if (contains_ci(p, len, "memset", 6)) f |= NB_MEMSET;
+  tflags[s] = f;
+}
+
+// exactness check: every record's bytes equal its slot representative's bytes; also the
+// per-record kind (classified names + throughput presence)
+struct VerifyArgs {
+  const uint64_t* name_off;
+  const uint8_t* bytes;
+  uint64_t total;
+  uint64_t n;
+  const uint32_t* slot;
+  const uint32_t* trep;
+  const uint8_t* tflags;
+  const uint8_t* rflags;
+  uint8_t* kind;
+  uint32_t* collision;
+};
+
+__global__ void __launch_bounds__(kHashBlock) k_verify(VerifyArgs a) {
+  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  uint8_t* buf = s_buf[warp];
+  const uint64_t groups = (a.n + 31) / 32;
+  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  bool bad = false;
+  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp; g < groups; g += gstride) {
+    const uint64_t g0 = g * 32, g1 = min(g0 + 32, a.n);
+    const uint64_t row = g0 + lane;
+    uint64_t base = 0;
+    const bool staged = stage_names(a.name_off, a.bytes, a.total, g0, g1, buf, base);
+    if (row < a.n) {
+      const uint32_t s = a.slot[row];
+      const uint32_t rep = a.trep[s];
+      if (rep != row) {
+        const uint64_t o = a.name_off[row];
+        const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
+        const uint64_t ro = a.name_off[rep];
+        const uint32_t rlen = static_cast<uint32_t>(a.name_off[rep + 1] - ro);
+        if (len != rlen) {
+          bad = true;
+        } else {
+          const uint8_t* p = staged ? buf + (o - base) : a.bytes + o;
+          const uint8_t* q = a.bytes + ro;
+          for (uint32_t i = 0; i < len; ++i)
+            if (p[i] != q[i]) {
+              bad = true;
+              break;
+            }
+        }
+      }
+      a.kind[row] = static_cast<uint8_t>(kind_from(a.tflags[s], (a.rflags[row] & ITT_REC_HAS_THROUGHPUT) != 0));
+    }
+    __syncwarp();
+  }
+  if (bad) atomicOr(a.collision, 1u);
+}
+
+// ------------------------------------------------------------------ stream census
+struct StreamEntry {
+  unsigned long long key;  // stream + 1 (0 = empty)
+  unsigned long long counts[6];
+  unsigned long long min_start;  // order-preserving u64 of int64
+  unsigned long long max_end;
+};
+__device__ __forceinline__ unsigned long long ord64(int64_t v) {
+  return static_cast<unsigned long long>(v) ^ 0x8000000000000000ull;
+}
+__host__ __device__ inline int64_t unord64(unsigned long long u) { return static_cast<int64_t>(u ^ 0x8000000000000000ull); }
+
+__device__ uint32_t global_stream_slot(StreamEntry* table, uint32_t* list, uint32_t* count, unsigned long long key) {
+  uint32_t s = static_cast<uint32_t>(key * 0x9E3779B1u) & (kStreamTableCap - 1);
+  for (uint32_t probe = 0; probe < kStreamTableCap; ++probe) {
+    unsigned long long k = atomicAdd(&table[s].key, 0ull);
+    if (k == 0) {
+      k = atomicCAS(&table[s].key, 0ull, key);
+      if (k == 0) {
+        list[atomicAdd(count, 1u)] = s;
+        return s;
+      }
+    }
+    if (k == key) return s;
+    s = (s + 1) & (kStreamTableCap - 1);
+  }
+  return kNone;
+}
+
+struct CensusArgs {
+  uint64_t n;
+  const uint32_t* stream;
+  const uint16_t* device;
+  int filter;  // keep only device == majority
+  uint16_t majority;
+  const uint8_t* kind;
+  const int64_t* start;
+  const int64_t* dur;
+  StreamEntry* table;
+  uint32_t* list;
+  uint32_t* count;
+};
+
+__global__ void __launch_bounds__(256) k_stream_census(CensusArgs a) {
+  __shared__ unsigned long long s_key[kBlockStreams];
+  __shared__ unsigned int s_cnt[kBlockStreams][6];
+  __shared__ unsigned long long s_min[kBlockStreams], s_max[kBlockStreams];
+  for (unsigned i = threadIdx.x; i < kBlockStreams; i += blockDim.x) {
+    s_key[i] = 0;
+    s_min[i] = ~0ull;
+    s_max[i] = 0;
+    for (int k = 0; k < 6; ++k) s_cnt[i][k] = 0;
+  }
+  __syncthreads();
+  const unsigned lane = lane_id();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x; b < a.n; b += stride) {
+    const uint64_t i = b + threadIdx.x;
+    bool valid = i < a.n;
+    if (valid && a.filter && a.device[i] != a.majority) valid = false;
+    const uint32_t st = valid ? a.stream[i] : 0u;
+    const unsigned long long key = static_cast<unsigned long long>(st) + 1ull;
+    // per-block slot of this stream
+    uint32_t bs = kNone;
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : 0ull);
+    const int leader = __ffs(peers) - 1;
+    if (valid && static_cast<int>(lane) == leader) {
+      uint32_t s = static_cast<uint32_t>(key * 0x9E3779B1u) & (kBlockStreams - 1);
+      for (uint32_t probe = 0; probe < kBlockStreams; ++probe) {
+        unsigned long long k = s_key[s];
+        if (k == 0) {
+          k = atomicCAS(&s_key[s], 0ull, key);
+          if (k == 0) k = key;
+        }
+        if (k == key) {
+          bs = s;
+          break;
+        }
+        s = (s + 1) & (kBlockStreams - 1);
+      }
+    }
+    bs = __shfl_sync(0xffffffffu, bs, leader);
+    if (valid) {
+      const int kd = a.kind[i];
+      const int64_t s0 = a.start[i];
+      const int64_t e0 = s0 + a.dur[i];
+      if (bs == kNone) {  // block table overflow: update the global table directly
+        const uint32_t gs = global_stream_slot(a.table, a.list, a.count, key);
+        if (gs != kNone) {
+          atomicAdd(&a.table[gs].counts[kd], 1ull);
+          atomicMin(&a.table[gs].min_start, ord64(s0));
+          atomicMax(&a.table[gs].max_end, ord64(e0));
+        }
+      } else {
+        const unsigned kp = __match_any_sync(peers, static_cast<unsigned>(kd));
+        if (static_cast<int>(lane) == __ffs(kp) - 1) atomicAdd(&s_cnt[bs][kd], static_cast<unsigned>(__popc(kp)));
+        // min start / max end over the stream's lanes: reduce 32-bit halves
+        const unsigned long long us = ord64(s0), ue = ord64(e0);
+        const unsigned hs = __reduce_min_sync(peers, static_cast<unsigned>(us >> 32));
+        const unsigned ls = __reduce_min_sync(peers, static_cast<unsigned>(us >> 32) == hs ? static_cast<unsigned>(us) : ~0u);
+        const unsigned he = __reduce_max_sync(peers, static_cast<unsigned>(ue >> 32));
+        const unsigned le = __reduce_max_sync(peers, static_cast<unsigned>(ue >> 32) == he ? static_cast<unsigned>(ue) : 0u);
+        if (static_cast<int>(lane) == leader) {
+          atomicMin(&s_min[bs], (static_cast<unsigned long long>(hs) << 32) | ls);
+          atomicMax(&s_max[bs], (static_cast<unsigned long long>(he) << 32) | le);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < kBlockStreams; i += blockDim.x) {
+    if (!s_key[i]) continue;
+    const uint32_t gs = global_stream_slot(a.table, a.list, a.count, s_key[i]);
+    if (gs == kNone) continue;
+    for (int k = 0; k < 6; ++k)
+      if (s_cnt[i][k]) atomicAdd(&a.table[gs].counts[k], static_cast<unsigned long long>(s_cnt[i][k]));
+    atomicMin(&a.table[gs].min_start, s_min[i]);
+    atomicMax(&a.table[gs].max_end, s_max[i]);
+  }
+}
+
+__global__ void k_init_stream_table(StreamEntry* t) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < kStreamTableCap) {
+    t[i].key = 0;
+    for (int k = 0; k < 6; ++k) t[i].counts[k] = 0;
+    t[i].min_start = ~0ull;
+    t[i].max_end = 0;
+  }
+}
+
+// ------------------------------------------------------------------ K3: compaction
+struct CompactF {
+  uint64_t n;
+  const uint32_t* perm;  // sorted position -> row (null: identity)
+  const uint32_t* stream;
+  const uint16_t* device;
+  int filter;
+  uint16_t majority;
+  uint32_t main_stream;
+  const uint8_t* kind;
+  const uint32_t* slot;
+  const int64_t* start;
+  const int64_t* dur;
+  const int64_t* size;
+  const uint8_t* rflags;
+  uint32_t* tok_slot;
+  int64_t* tok_start;
+  int64_t* tok_end;
+  uint64_t* tok_record;  // optional
+  uint32_t* tfirst;
+  int64_t* htod_start;
+  int64_t* htod_end;
+  int64_t* htod_size;
+  __device__ __forceinline__ uint32_t row(uint64_t k) const { return perm ? perm[k] : static_cast<uint32_t>(k); }
+  __device__ __forceinline__ uint64_t load(uint64_t k) const {
+    const uint32_t i = row(k);
+    if (filter && device[i] != majority) return 0;
+    const uint64_t m = stream[i] == main_stream ? 1ull : 0ull;
+    const uint64_t h = kind[i] == ITT_KIND_HTOD ? (1ull << 31) : 0ull;
+    return m | h;
+  }
+  __device__ __forceinline__ void store(uint64_t k, uint64_t excl, uint64_t v) const {
+    if (!v) return;
+    const uint32_t i = row(k);
+    const int64_t s = start[i];
+    const int64_t e = s + dur[i];
+    if (v & 1ull) {
+      const uint32_t j = static_cast<uint32_t>(excl & 0x7FFFFFFFull);
+      const uint32_t sl = slot[i];
+      tok_slot[j] = sl;
+      tok_start[j] = s;
+      tok_end[j] = e;
+      if (tok_record) tok_record[j] = k;
+      if (__ldcg(&tfirst[sl]) > j) atomicMin(&tfirst[sl], j);
+    }
+    if (v >> 31) {
+      const uint64_t h = excl >> 31;
+      htod_start[h] = s;
+      htod_end[h] = e;
+      htod_size[h] = (rflags[i] & ITT_REC_HAS_SIZE) ? size[i] : 0;
+    }
+  }
+};
+
+// ------------------------------------------------------------------ renumber
+// rank of each used slot among slots with a main-stream first position (first-appearance id)
+__global__ void k_rank_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ tfirst,
+                             uint32_t* __restrict__ id_of_slot, uint32_t* __restrict__ name_count) {
+  __shared__ uint32_t s_first[1024];
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t my = u < n_used ? tfirst[used[u]] : kNone;
+  uint32_t less = 0;
+  for (uint32_t t0 = 0; t0 < n_used; t0 += 1024) {
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < 1024; q += blockDim.x)
+      s_first[q] = t0 + q < n_used ? tfirst[used[t0 + q]] : kNone;
+    __syncthreads();
+    const uint32_t lim = min(1024u, n_used - t0);
+    if (my != kNone)
+      for (uint32_t q = 0; q < lim; ++q) less += s_first[q] < my;
+  }
+  if (u < n_used) {
+    id_of_slot[used[u]] = my == kNone ? kNone : less;
+    if (my != kNone) atomicAdd(name_count, 1u);
+  }
+}
+
+__global__ void k_slot_ids_from_sorted(const uint32_t* __restrict__ sorted_slots, uint32_t m,
+                                       uint32_t* __restrict__ id_of_slot) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) id_of_slot[sorted_slots[r]] = r;
+}
+
+__global__ void k_first_pairs(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ tfirst,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < n_used) {
+    keys[u] = tfirst[used[u]];
+    vals[u] = used[u];
+  }
+}
+
+__global__ void k_map_tokens(const uint32_t* __restrict__ tok_slot, uint64_t n, const uint32_t* __restrict__ id_of_slot,
+                             int32_t* __restrict__ tokens) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < n) tokens[j] = static_cast<int32_t>(id_of_slot[tok_slot[j]]);
+}
+
+__global__ void k_name_rows(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ id_of_slot,
+                            const uint32_t* __restrict__ trep, uint64_t* __restrict__ name_row) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < n_used) {
+    const uint32_t id = id_of_slot[used[u]];
+    if (id != kNone) name_row[id] = trep[used[u]];
+  }
+}
+
+__global__ void k_overlaps(const int64_t* __restrict__ ts, const int64_t* __restrict__ te, uint64_t n,
+                           unsigned long long* out) {
+  unsigned long long c = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j + 1 < n; j += stride)
+    c += te[j] > ts[j + 1];
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
+  d.n = r->n;
+  d.order = r->order;
+  const uint64_t n = r->n;
+  if (r->mem == ITT_MEM_DEVICE) {
+    d.start = r->start_ns;
+    d.dur = r->duration_ns;
+    d.size = r->size_bytes;
+    d.flags = r->flags;
+    d.stream = r->stream;
+    d.device = r->device;
+    d.name_off = r->name_off;
+    d.name_bytes = r->name_bytes;
+    return;
+  }
+  uint64_t nb = 0;
+  if (n) std::memcpy(&nb, &r->name_off[n], sizeof(nb));
+  d.o_start.alloc(c, n);
+  d.o_dur.alloc(c, n);
+  d.o_size.alloc(c, n);
+  d.o_flags.alloc(c, n);
+  d.o_stream.alloc(c, n);
+  d.o_off.alloc(c, n + 1);
+  d.o_names.alloc(c, nb + 16);
+  h2d(c, d.o_start.p, r->start_ns, n);
+  h2d(c, d.o_dur.p, r->duration_ns, n);
+  h2d(c, d.o_size.p, r->size_bytes, n);
+  h2d(c, d.o_flags.p, r->flags, n);
+  h2d(c, d.o_stream.p, r->stream, n);
+  h2d(c, d.o_off.p, r->name_off, n + 1);
+  h2d(c, d.o_names.p, r->name_bytes, nb);
+  d.start = d.o_start.p;
+  d.dur = d.o_dur.p;
+  d.size = d.o_size.p;
+  d.flags = d.o_flags.p;
+  d.stream = d.o_stream.p;
+  d.name_off = d.o_off.p;
+  d.name_bytes = d.o_names.p;
+  if (r->device) {
+    d.o_device.alloc(c, n);
+    h2d(c, d.o_device.p, r->device, n);
+    d.device = d.o_device.p;
+  }
+}
+
+void order_records(TraceState& t) {
+  Ctx* c = t.c;
+  const uint64_t n = t.rec.n;
+  t.sorted = true;
+  if (n <= 1 || t.rec.order == ITT_ORDER_SORTED) return;
+  DBuf<unsigned long long> st(c, 3);
+  unsigned long long init[3] = {static_cast<unsigned long long>(LLONG_MAX), static_cast<unsigned long long>(LLONG_MIN), 0};
+  h2d(c, st.p, init, 3);
+  const unsigned grid = std::min<unsigned>(grid_for(n, 256), c->sm_count * 8);
+  launch(c, "order_stats", n * 8.0, k_order_stats, dim3(grid), dim3(256), 0, t.rec.start, n, st.p);
+  unsigned long long h[3];
+  readback(c, h, st.p, 3);
+  if (h[2] == 0) return;  // already in (start,row) order
+  t.sorted = false;
+  const int64_t mn = static_cast<int64_t>(h[0]), mx = static_cast<int64_t>(h[1]);
+  const int bits = bits_for(static_cast<uint64_t>(mx - mn));
+  DBuf<uint64_t> k0(c, n), k1(c, n);
+  DBuf<uint32_t> v0(c, n), v1(c, n);
+  launch(c, "order_keys", n * 20.0, k_order_keys, dim3(grid_for(n, 256)), dim3(256), 0, t.rec.start, n, mn, k0.p, v0.p);
+  // LSD radix sort is stable, so equal starts keep source-row order (ingest.hpp:396-400)
+  const bool alt = radix_sort_pairs<uint64_t>(c, k0.p, v0.p, k1.p, v1.p, n, 0, bits, t.rs);
+  t.perm = alt ? std::move(v1) : std::move(v0);
+}
+
+void build_dictionary(TraceState& t) {
+  Ctx* c = t.c;
+  const uint64_t n = t.rec.n;
+  uint64_t total = 0;
+  if (n) total = read1(c, t.rec.name_off + n);
+  t.slot.alloc(c, n);
+  t.kind.alloc(c, n);
+  DBuf<uint32_t> counters(c, 4);
+  DBuf<unsigned long long> dev_counts;
+  DBuf<uint32_t> dev_max(c, 1);
+  if (t.rec.device) {
+    dev_counts.alloc(c, 65536);
+    dev_counts.zero();
+  }
+  DBuf<uint32_t> collision(c, 1);
+  uint32_t bits = 14;
+  uint64_t seed = 0x243F6A8885A308D3ull;
+  const unsigned groups = static_cast<unsigned>(std::min<uint64_t>((n + 31) / 32, 1ull << 30));
+  const unsigned grid = std::max(1u, std::min<unsigned>((groups + 7) / 8, c->sm_count * 8));
+  for (int attempt = 0;; ++attempt) {
+    const uint32_t cap = 1u << bits;
+    t.tkey.alloc(c, cap);
+    t.trep.alloc(c, cap);
+    t.tflags.alloc(c, cap);
+    t.used.alloc(c, cap);
+    t.tkey.zero();
+    t.trep.fill_bytes(0xFF);
+    counters.zero();
+    dev_max.zero();
+    collision.zero();
+    if (t.rec.device) dev_counts.zero();
+    HashArgs ha{t.rec.name_off, t.rec.name_bytes, total, n, t.rec.device, t.tkey.p, t.trep.p, cap - 1, seed,
+                t.slot.p,       t.used.p,         counters.p, dev_counts.p, dev_max.p};
+    launch(c, "intern_hash", static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0, ha);
+    uint32_t cnt[2];
+    readback(c, cnt, counters.p, 2);
+    if (cnt[1] || cnt[0] > cap / 2) {  // table too full: grow and redo
+      if (bits >= 30) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: name dictionary overflow");
+      bits += 2;
+      continue;
+    }
+    t.n_used = cnt[0];
+    t.table_bits = bits;
+    if (t.n_used)
+      launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(t.n_used, 128)), dim3(128), 0, t.used.p,
+             t.n_used, t.trep.p, t.rec.name_off, t.rec.name_bytes, t.tflags.p);
+    VerifyArgs va{t.rec.name_off, t.rec.name_bytes, total, n, t.slot.p, t.trep.p, t.tflags.p, t.rec.flags, t.kind.p,
+                  collision.p};
+    launch(c, "intern_verify", static_cast<double>(total) + n * 6.0, k_verify, dim3(grid), dim3(kHashBlock), 0, va);
+    if (read1(c, collision.p) == 0) break;
+    if (attempt >= 3) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: unresolvable name hash collision");
+    seed = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;  // a true 64-bit collision: new seed
+  }
+  // device census -> majority (ties to the smallest label rank, streams.hpp:187-194)
+  t.n_devices = 1;
+  t.majority = 0;
+  t.filtering = false;
+  t.kept = n;
+  if (t.rec.device && n) {
+    const uint32_t mx = read1(c, dev_max.p);
+    t.dev_counts.assign(mx + 1, 0);
+    readback(c, reinterpret_cast<unsigned long long*>(t.dev_counts.data()), dev_counts.p, mx + 1);
+    uint64_t best = 0;
+    t.n_devices = 0;
+    for (uint32_t d = 0; d <= mx; ++d) {
+      if (t.dev_counts[d]) ++t.n_devices;
+      if (t.dev_counts[d] > best) best = t.dev_counts[d], t.majority = static_cast<uint16_t>(d);
+    }
+    if (t.n_devices > 1) {
+      t.filtering = true;
+      t.kept = best;
+    }
+  }
+}
+
+void stream_census(TraceState& t) {
+  Ctx* c = t.c;
+  const uint64_t n = t.rec.n;
+  DBuf<StreamEntry> table(c, kStreamTableCap);
+  DBuf<uint32_t> list(c, kStreamTableCap + 1);
+  list.zero();
+  launch(c, "census_init", 0.0, k_init_stream_table, dim3(kStreamTableCap / 256), dim3(256), 0, table.p);
+  CensusArgs ca{n, t.rec.stream, t.rec.device, t.filtering ? 1 : 0, t.majority, t.kind.p, t.rec.start, t.rec.dur,
+                table.p, list.p + 1, list.p};
+  if (n) {
+    const unsigned grid = std::min<unsigned>(grid_for(n, 256), c->sm_count * 8);
+    launch(c, "census", n * 23.0, k_stream_census, dim3(grid), dim3(256), 0, ca);
+  }
+  const uint32_t ns = read1(c, list.p);
+  std::vector<uint32_t> slots(ns);
+  readback(c, slots.data(), list.p + 1, ns);
+  std::vector<StreamEntry> all(kStreamTableCap);
+  readback(c, all.data(), table.p, kStreamTableCap);
+  t.streams.clear();
+  for (uint32_t s : slots) {
+    const StreamEntry& e = all[s];
+    itt_stream_summary o{};
+    o.stream = static_cast<uint32_t>(e.key - 1);
+    for (int k = 0; k < 6; ++k) o.counts[k] = static_cast<int64_t>(e.counts[k]);
+    o.first_start = unord64(e.min_start);
+    o.last_end = unord64(e.max_end);
+    // classify_streams (streams.hpp:85-103)
+    const int64_t total = o.counts[0] + o.counts[1] + o.counts[2] + o.counts[3] + o.counts[4] + o.counts[5];
+    const int64_t mem = o.counts[ITT_KIND_HTOD] + o.counts[ITT_KIND_DTOH] + o.counts[ITT_KIND_DTOD];
+    o.cls = ITT_CLASS_ASSIST;
+    if (o.counts[ITT_KIND_KERNEL] > 0) {
+      o.cls = ITT_CLASS_MAIN;
+    } else if (total > 0 && mem == total) {
+      const bool h = o.counts[ITT_KIND_HTOD] > 0, d = o.counts[ITT_KIND_DTOH] > 0, dd = o.counts[ITT_KIND_DTOD] > 0;
+      o.cls = (h && !d && !dd) ? ITT_CLASS_COPY_HTOD : (d && !h && !dd) ? ITT_CLASS_COPY_DTOH : ITT_CLASS_COPY_MIXED;
+    }
+    t.streams.push_back(o);
+  }
+  std::sort(t.streams.begin(), t.streams.end(),
+            [](const itt_stream_summary& a, const itt_stream_summary& b) { return a.stream < b.stream; });
+}
+
+void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
+  Ctx* c = t.c;
+  const uint64_t n = t.rec.n;
+  t.tfirst.alloc(c, t.tkey.n);
+  t.tfirst.fill_bytes(0xFF);
+  // capacities: count first (cheap readback of the census would do, but the scan itself is exact)
+  uint64_t n_main = 0, n_htod = 0;
+  for (const auto& s : t.streams) {
+    if (s.stream == main_stream) n_main = s.counts[0] + s.counts[1] + s.counts[2] + s.counts[3] + s.counts[4] + s.counts[5];
+    n_htod += s.counts[ITT_KIND_HTOD];
+  }
+  t.tok_slot.alloc(c, n_main + 1);
+  t.tok_start.alloc(c, n_main + 1);
+  t.tok_end.alloc(c, n_main + 1);
+  t.tokens.alloc(c, n_main + 1);
+  if (want_record_index) t.tok_record.alloc(c, n_main + 1);
+  t.htod_start.alloc(c, n_htod + 1);
+  t.htod_end.alloc(c, n_htod + 1);
+  t.htod_size.alloc(c, n_htod + 1);
+  DBuf<uint64_t> tot(c, 1);
+  CompactF f{n,
+             t.sorted ? nullptr : t.perm.p,
+             t.rec.stream,
+             t.rec.device,
+             t.filtering ? 1 : 0,
+             t.majority,
+             main_stream,
+             t.kind.p,
+             t.slot.p,
+             t.rec.start,
+             t.rec.dur,
+             t.rec.size,
+             t.rec.flags,
+             t.tok_slot.p,
+             t.tok_start.p,
+             t.tok_end.p,
+             want_record_index ? t.tok_record.p : nullptr,
+             t.tfirst.p,
+             t.htod_start.p,
+             t.htod_end.p,
+             t.htod_size.p};
+  device_scan<uint64_t, SumOp<uint64_t>>(c, "compact", n * (t.sorted ? 14.0 : 18.0) + n_main * 28.0 + n_htod * 24.0, f, n,
+                                         t.scan);
+  if (t.streams.empty()) fail(ITT_E_INVALID_ARGUMENT, "internal: compact_main needs the stream census");
+  t.n_tok = n_main;
+  t.n_htod = n_htod;
+}
+
+void renumber_tokens(TraceState& t) {
+  Ctx* c = t.c;
+  DBuf<uint32_t> id_of_slot(c, t.tkey.n);
+  DBuf<uint32_t> cnt(c, 1);
+  cnt.zero();
+  const uint32_t nu = t.n_used;
+  if (nu <= 16384) {
+    launch(c, "intern_rank", nu * 4.0, k_rank_slots, dim3(grid_for(nu, 256)), dim3(256), 0, t.used.p, nu, t.tfirst.p,
+           id_of_slot.p, cnt.p);
+    t.n_names = read1(c, cnt.p);
+  } else {
+    DBuf<uint32_t> k0(c, nu), k1(c, nu), v0(c, nu), v1(c, nu);
+    launch(c, "intern_pairs", nu * 16.0, k_first_pairs, dim3(grid_for(nu, 256)), dim3(256), 0, t.used.p, nu, t.tfirst.p,
+           k0.p, v0.p);
+    const bool alt = radix_sort_pairs<uint32_t>(c, k0.p, v0.p, k1.p, v1.p, nu, 0, 32, t.rs);
+    std::vector<uint32_t> keys(nu);
+    readback(c, keys.data(), alt ? k1.p : k0.p, nu);
+    uint32_t m = 0;
+    while (m < nu && keys[m] != kNone) ++m;
+    id_of_slot.fill_bytes(0xFF);
+    launch(c, "intern_ids", m * 8.0, k_slot_ids_from_sorted, dim3(grid_for(m, 256)), dim3(256), 0, alt ? v1.p : v0.p, m,
+           id_of_slot.p);
+    t.n_names = m;
+  }
+  if (t.n_tok)
+    launch(c, "intern_map", t.n_tok * 8.0, k_map_tokens, dim3(grid_for(t.n_tok, 256)), dim3(256), 0, t.tok_slot.p, t.n_tok,
+           id_of_slot.p, t.tokens.p);
+  DBuf<uint64_t> rows(c, t.n_names + 1);
+  launch(c, "intern_names", nu * 8.0, k_name_rows, dim3(grid_for(nu, 256)), dim3(256), 0, t.used.p, nu, id_of_slot.p,
+         t.trep.p, rows.p);
+  t.name_row.resize(t.n_names);
+  readback(c, t.name_row.data(), rows.p, t.n_names);
+}
+
+int64_t count_overlaps(TraceState& t) {
+  Ctx* c = t.c;
+  if (t.n_tok < 2) return 0;
+  DBuf<unsigned long long> out(c, 1);
+  out.zero();
+  const unsigned grid = std::min<unsigned>(grid_for(t.n_tok, 256), c->sm_count * 8);
+  launch(c, "overlaps", t.n_tok * 16.0, k_overlaps, dim3(grid), dim3(256), 0, t.tok_start.p, t.tok_end.p, t.n_tok, out.p);
+  return static_cast<int64_t>(read1(c, out.p));
+}
+
+}  // namespace itt

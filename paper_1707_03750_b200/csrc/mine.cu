@@ -1,0 +1,383 @@
+// mine.cu — LCP-interval enumeration (all nearest smaller values) and the repeat mining
+// reduction, sm_100a.
+//
+// enumerate_repeats (mine.hpp:46-60) visits every internal suffix-tree node; here a node is
+// the LCP interval represented by its leftmost position k with value l = LCP[k] > 0:
+//   lb  = previous j < k with LCP[j] <= l     (if LCP[lb] == l, k is not leftmost: skip)
+//   nsv = next j > k with LCP[j] < l          (n' past the end)
+//   count = nsv - lb, parent depth = max(LCP[lb], LCP[nsv]), first_leaf = min SA[lb, nsv).
+// Searches run in two levels: inside a 1024-wide tile through a shared-memory sparse table
+// (binary lifting), across tiles through a sparse table of tile minima plus a binary search
+// over the target tile's prefix/suffix minima.
+//
+// mine_pattern_impl (mine.hpp:75-111) tries epsilon = eps0 * 2^p for p = 0, 1, ... and
+// returns the preferred candidate (mine.hpp:69-73) of the first pass that has one.  A
+// candidate (count c) first qualifies at pass p(c) = min{p : iters - eps_p + 1 <= c}, so the
+// answer is the max over all candidates of (-p(c), len, count, -first_leaf): one reduction
+// plus a min-SA pass over the (disjoint) intervals tied on (p, len, count).
+#include <algorithm>
+#include <cstring>
+
+#include "pipeline.cuh"
+
+namespace itt {
+
+namespace {
+
+constexpr int kTileA = 1024;
+constexpr int kLogTileA = 10;
+constexpr int kAnsvBlock = 256;
+
+// per tile: prefix minima, suffix minima (within the tile) and the tile minimum
+__global__ void __launch_bounds__(kTileA) k_tile_minima(const uint32_t* __restrict__ lcp, uint64_t np,
+                                                        uint32_t* __restrict__ premin, uint32_t* __restrict__ sufmin,
+                                                        uint32_t* __restrict__ tmin) {
+  __shared__ uint32_t s[kTileA];
+  __shared__ uint32_t sw[32];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTileA;
+  const uint64_t j = base + threadIdx.x;
+  const uint32_t v = j < np ? lcp[j] : 0xFFFFFFFFu;
+  // inclusive prefix min (warp scan + warp totals)
+  uint32_t p = v;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, p, o);
+    if (static_cast<int>(lane) >= o) p = min(p, u);
+  }
+  if (lane == 31) sw[warp] = p;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = sw[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
+      if (static_cast<int>(lane) >= o) w = min(w, u);
+    }
+    sw[lane] = w;
+  }
+  __syncthreads();
+  if (warp > 0) p = min(p, sw[warp - 1]);
+  if (j < np) premin[j] = p;
+  if (threadIdx.x == kTileA - 1) tmin[blockIdx.x] = p;
+  __syncthreads();
+  // inclusive suffix min
+  uint32_t q = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_down_sync(0xffffffffu, q, o);
+    if (static_cast<int>(lane) + o < 32) q = min(q, u);
+  }
+  if (lane == 0) sw[warp] = q;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = sw[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_down_sync(0xffffffffu, w, o);
+      if (static_cast<int>(lane) + o < 32) w = min(w, u);
+    }
+    sw[lane] = w;
+  }
+  __syncthreads();
+  if (warp < 31) q = min(q, sw[warp + 1]);
+  if (j < np) sufmin[j] = q;
+  (void)s;
+}
+
+// sparse table over tile minima: st[l * nt + t] = min(tmin[t, t + 2^l))
+__global__ void k_sparse_level(uint32_t* st, uint32_t nt, int l) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const uint32_t half = 1u << (l - 1);
+  const uint32_t* prev = st + static_cast<uint64_t>(l - 1) * nt;
+  uint32_t v = prev[t];
+  if (t + half < nt) v = min(v, prev[t + half]);
+  st[static_cast<uint64_t>(l) * nt + t] = v;
+}
+
+struct AnsvArgs {
+  const uint32_t* lcp;
+  const uint32_t* premin;
+  const uint32_t* sufmin;
+  const uint32_t* tst;  // tile sparse table
+  uint32_t nt;
+  int tlevels;
+  uint64_t np;
+  uint32_t* cnt;
+  uint32_t* par;
+  uint32_t* lb;
+};
+
+// last j in tile t with LCP[j] <= thr (the tile's min is known to be <= thr)
+__device__ __forceinline__ uint64_t last_le_in_tile(const AnsvArgs& a, uint32_t t, uint32_t thr) {
+  uint64_t lo = static_cast<uint64_t>(t) * kTileA, hi = min(lo + kTileA, a.np) - 1;  // sufmin non-decreasing in j
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi + 1) >> 1;
+    if (a.sufmin[mid] <= thr) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+// first j in tile t with LCP[j] < thr (the tile's min is known to be < thr)
+__device__ __forceinline__ uint64_t first_lt_in_tile(const AnsvArgs& a, uint32_t t, uint32_t thr) {
+  uint64_t lo = static_cast<uint64_t>(t) * kTileA, hi = min(lo + kTileA, a.np) - 1;  // premin non-increasing in j
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a.premin[mid] < thr) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
+  __shared__ uint32_t st[kLogTileA][kTileA];  // st[l][x] = min(LCP[x, x + 2^l)) within the tile
+  const uint32_t t = blockIdx.x;
+  const uint64_t base = static_cast<uint64_t>(t) * kTileA;
+  const uint32_t len = static_cast<uint32_t>(umin64(kTileA, a.np - base));
+  for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock) st[0][x] = x < len ? a.lcp[base + x] : 0xFFFFFFFFu;
+  __syncthreads();
+  for (int l = 1; l < kLogTileA; ++l) {
+    const uint32_t half = 1u << (l - 1);
+    for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock)
+      st[l][x] = x + half < kTileA ? min(st[l - 1][x], st[l - 1][x + half]) : st[l - 1][x];
+    __syncthreads();
+  }
+  for (uint32_t x = threadIdx.x; x < len; x += kAnsvBlock) {
+    const uint64_t k = base + x;
+    const uint32_t l = st[0][x];
+    uint32_t cnt = 0, par = 0, lbv = 0;
+    if (k > 0 && l > 0) {
+      // ---- previous j < k with LCP[j] <= l
+      uint32_t pos = x;
+#pragma unroll
+      for (int lv = kLogTileA - 1; lv >= 0; --lv) {
+        const uint32_t w = 1u << lv;
+        if (pos >= w && st[lv][pos - w] > l) pos -= w;
+      }
+      uint64_t pse;
+      if (pos > 0) {
+        pse = base + pos - 1;
+      } else {  // cross-tile: last tile before t whose min <= l (tile 0 holds LCP[0] = 0)
+        uint32_t tp = t;
+        for (int lv = a.tlevels - 1; lv >= 0; --lv) {
+          const uint32_t w = 1u << lv;
+          if (tp >= w && a.tst[static_cast<uint64_t>(lv) * a.nt + tp - w] > l) tp -= w;
+        }
+        pse = last_le_in_tile(a, tp - 1, l);
+      }
+      const uint32_t lp = pse - base < kTileA && pse >= base ? st[0][pse - base] : a.lcp[pse];
+      if (lp < l) {  // k is the leftmost position of its interval
+        // ---- next j > k with LCP[j] < l
+        uint32_t q = x + 1;
+#pragma unroll
+        for (int lv = kLogTileA - 1; lv >= 0; --lv) {
+          const uint32_t w = 1u << lv;
+          if (q + w <= len && st[lv][q] >= l) q += w;
+        }
+        uint64_t nsv;
+        uint32_t ln = 0;
+        if (q < len) {
+          nsv = base + q;
+          ln = st[0][q];
+        } else {
+          uint32_t tn = t + 1;
+          for (int lv = a.tlevels - 1; lv >= 0; --lv) {
+            const uint32_t w = 1u << lv;
+            if (tn + w <= a.nt && a.tst[static_cast<uint64_t>(lv) * a.nt + tn] >= l) tn += w;
+          }
+          if (tn < a.nt) {
+            nsv = first_lt_in_tile(a, tn, l);
+            ln = a.lcp[nsv];
+          } else {
+            nsv = a.np;
+            ln = 0;
+          }
+        }
+        cnt = static_cast<uint32_t>(nsv - pse);
+        par = max(lp, ln);
+        lbv = static_cast<uint32_t>(pse);
+      }
+    }
+    a.cnt[k] = cnt;
+    a.par[k] = par;
+    a.lb[k] = lbv;
+  }
+}
+
+// ---------------------------------------------------------------- mining reduction
+struct MineArgs {
+  const uint32_t* lcp;
+  const uint32_t* cnt;
+  const uint32_t* par;
+  uint64_t np;
+  int64_t iters;
+  int64_t max_len;
+  int npass;
+  int64_t min_count[64];  // iters - eps_p + 1 per pass
+};
+struct Best {
+  unsigned long long hi;  // (63 - pass) << 32 | len
+  unsigned long long lo;  // count
+};
+__device__ __forceinline__ bool better(const Best& a, const Best& b) { return a.hi != b.hi ? a.hi > b.hi : a.lo > b.lo; }
+
+__device__ __forceinline__ bool candidate_key(const MineArgs& a, uint64_t k, Best& out) {
+  const uint32_t c = a.cnt[k];
+  if (c == 0) return false;
+  const uint32_t l = a.lcp[k];
+  const int64_t len = imin64(static_cast<int64_t>(l), a.max_len);
+  if (len <= static_cast<int64_t>(a.par[k])) return false;  // mid-edge truncation stays below the node
+  if (static_cast<int64_t>(c) > a.iters) return false;
+  int p = 0;
+  while (p < a.npass && static_cast<int64_t>(c) < a.min_count[p]) ++p;
+  if (p == a.npass) return false;
+  out.hi = (static_cast<unsigned long long>(63 - p) << 32) | static_cast<unsigned long long>(len);
+  out.lo = c;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_mine_reduce(MineArgs a, Best* block_best) {
+  Best b{0, 0};
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < a.np; k += stride) {
+    Best x;
+    if (candidate_key(a, k, x) && better(x, b)) b = x;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    Best y{__shfl_xor_sync(0xffffffffu, b.hi, o), __shfl_xor_sync(0xffffffffu, b.lo, o)};
+    if (better(y, b)) b = y;
+  }
+  __shared__ Best sw[8];
+  if (lane_id() == 0) sw[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (better(sw[w], b)) b = sw[w];
+    block_best[blockIdx.x] = b;
+  }
+}
+
+__global__ void k_best_final(const Best* bb, uint32_t nb, Best* out) {
+  Best b{0, 0};
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+    if (better(bb[i], b)) b = bb[i];
+  for (int o = 16; o > 0; o >>= 1) {
+    Best y{__shfl_xor_sync(0xffffffffu, b.hi, o), __shfl_xor_sync(0xffffffffu, b.lo, o)};
+    if (better(y, b)) b = y;
+  }
+  if (threadIdx.x == 0) *out = b;
+}
+
+// min SA over the intervals tied on the winning (pass, len, count): they are disjoint
+__global__ void __launch_bounds__(256) k_tied_min_sa(MineArgs a, const uint32_t* __restrict__ lb,
+                                                     const uint32_t* __restrict__ sa, const Best* best,
+                                                     unsigned int* __restrict__ result) {
+  const Best w = *best;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < a.np; k += stride) {
+    Best x;
+    if (!candidate_key(a, k, x) || x.hi != w.hi || x.lo != w.lo) continue;
+    const uint32_t l0 = lb[k], c = a.cnt[k];
+    uint32_t m = 0xFFFFFFFFu;
+    for (uint32_t q = 0; q < c; ++q) m = min(m, sa[l0 + q]);
+    atomicMin(result, m);
+  }
+}
+
+}  // namespace
+
+void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv) {
+  const uint64_t np = s.np;
+  const uint32_t nt = static_cast<uint32_t>((np + kTileA - 1) / kTileA);
+  DBuf<uint32_t> premin(c, np), sufmin(c, np);
+  int tlevels = 1;
+  while ((1u << tlevels) <= nt) ++tlevels;
+  DBuf<uint32_t> tst(c, static_cast<size_t>(tlevels) * nt);
+  launch(c, "ansv_tile_minima", np * 12.0, k_tile_minima, dim3(nt), dim3(kTileA), 0, s.lcp.p, np, premin.p, sufmin.p, tst.p);
+  for (int l = 1; l < tlevels; ++l)
+    launch(c, "ansv_sparse", nt * 12.0, k_sparse_level, dim3(grid_for(nt, 256)), dim3(256), 0, tst.p, nt, l);
+  iv.cnt.alloc(c, np);
+  iv.par.alloc(c, np);
+  iv.lb.alloc(c, np);
+  AnsvArgs a{s.lcp.p, premin.p, sufmin.p, tst.p, nt, tlevels, np, iv.cnt.p, iv.par.p, iv.lb.p};
+  launch(c, "ansv_intervals", np * 16.0, k_ansv, dim3(nt), dim3(kAnsvBlock), 0, a);
+  c->sync();
+}
+
+MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, const itt_mining_cfg& cfg,
+                      const std::string& label) {
+  MinedPattern r;
+  const int64_t iters = cfg.iterations, eps0 = cfg.epsilon0;
+  const int64_t n = static_cast<int64_t>(s.n);
+  if (iters < 2 || eps0 < 1 || eps0 >= iters) {
+    r.status = ITT_E_INVALID_ITERATION_COUNT;
+    r.error = "pattern-mining" + label + ": need iterations >= 2 and 1 <= epsilon0 < iterations (got iterations=" +
+              std::to_string(iters) + ", epsilon0=" + std::to_string(eps0) + ")";
+    return r;
+  }
+  if (n < iters) {
+    r.status = ITT_E_INVALID_ITERATION_COUNT;
+    r.error = "pattern-mining" + label + ": sequence of " + std::to_string(n) + " operations cannot contain " +
+              std::to_string(iters) + " iterations";
+    return r;
+  }
+  const int64_t cap = cfg.epsilon_cap > 0 ? cfg.epsilon_cap : iters;
+  const int64_t max_len = (n - 1) / iters;  // mine.hpp:64-67
+  MineArgs a{};
+  a.lcp = s.lcp.p;
+  a.cnt = iv.cnt.p;
+  a.par = iv.par.p;
+  a.np = s.np;
+  a.iters = iters;
+  a.max_len = max_len;
+  std::vector<int64_t> eps;
+  for (int64_t e = eps0; e < cap && eps.size() < 63; e *= 2) eps.push_back(e);
+  a.npass = static_cast<int>(eps.size());
+  for (size_t p = 0; p < eps.size(); ++p) a.min_count[p] = iters - eps[p] + 1;
+  auto no_pattern = [&]() {
+    r.status = ITT_E_NO_PATTERN_FOUND;
+    r.error = "pattern-mining" + label +
+              ": no repeated substring satisfies the repetition and length criteria for iterations=" +
+              std::to_string(iters) + " (epsilon exhausted at cap " + std::to_string(cap) +
+              "); the trace may not be iterative at the declared count";
+  };
+  if (max_len < 1 || a.npass == 0) {  // enumerate_repeats is empty (mine.hpp:50)
+    no_pattern();
+    return r;
+  }
+  const unsigned grid = std::min<unsigned>(grid_for(s.np, 256), c->sm_count * 4);
+  DBuf<Best> bb(c, grid + 1);
+  launch(c, "mine_reduce", s.np * 12.0, k_mine_reduce, dim3(grid), dim3(256), 0, a, bb.p);
+  launch(c, "mine_final", grid * 16.0, k_best_final, dim3(1), dim3(32), 0, bb.p, grid, bb.p + grid);
+  const Best best = read1(c, bb.p + grid);
+  if (best.hi == 0 && best.lo == 0) {
+    no_pattern();
+    return r;
+  }
+  DBuf<unsigned int> start(c, 1);
+  start.fill_bytes(0xFF);
+  launch(c, "mine_tied_min_sa", s.np * 12.0, k_tied_min_sa, dim3(grid), dim3(256), 0, a, iv.lb.p, s.sa.p, bb.p + grid, start.p);
+  const uint32_t st = read1(c, start.p);
+  const int64_t len = static_cast<int64_t>(best.hi & 0xFFFFFFFFull);
+  const int pass = 63 - static_cast<int>(best.hi >> 32);
+  r.tokens.resize(static_cast<size_t>(len));
+  r.count = static_cast<int64_t>(best.lo);
+  r.first_token = st;
+  r.epsilon_used = eps[static_cast<size_t>(pass)];
+  // pattern = text[start, start+len) as codes; the caller maps codes back to token values
+  std::vector<int32_t> codes(static_cast<size_t>(len));
+  readback(c, codes.data(), s.text.p + st, static_cast<size_t>(len));
+  for (auto& v : codes) v += s.lo;
+  r.tokens = codes;
+  return r;
+}
+
+std::vector<MinedPattern> mine_loops(Ctx* c, const SuffixState& s, const IntervalState& iv,
+                                     const std::vector<itt_mining_cfg>& loops, bool multi) {
+  std::vector<MinedPattern> out;
+  for (size_t k = 0; k < loops.size(); ++k) {
+    const std::string label = multi ? " (loop " + std::to_string(k + 1) + ")" : "";
+    out.push_back(mine_one(c, s, iv, loops[k], label));
+    if (out.back().status) return out;
+  }
+  return out;
+}
+
+}  // namespace itt

@@ -1,0 +1,130 @@
+// pipeline.cuh — device-side state of one trace flowing through the hot path, and the
+// stage entry points implemented across intern.cu / sa.cu / mine.cu / match.cu / metrics.cu.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "radix.cuh"
+#include "scan.cuh"
+
+namespace itt {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// ------------------------------------------------------------------ records (intern.cu)
+struct DevRecords {
+  uint64_t n = 0;
+  const int64_t* start = nullptr;
+  const int64_t* dur = nullptr;
+  const int64_t* size = nullptr;
+  const uint8_t* flags = nullptr;
+  const uint32_t* stream = nullptr;
+  const uint16_t* device = nullptr;  // may be null
+  const uint64_t* name_off = nullptr;
+  const uint8_t* name_bytes = nullptr;
+  int order = ITT_ORDER_UNKNOWN;
+  // owned copies when the caller passed host memory
+  DBuf<int64_t> o_start, o_dur, o_size;
+  DBuf<uint8_t> o_flags, o_names;
+  DBuf<uint32_t> o_stream;
+  DBuf<uint16_t> o_device;
+  DBuf<uint64_t> o_off;
+};
+
+// Records flowing through intern: (start,row) order, the name dictionary, the census.
+struct TraceState {
+  Ctx* c = nullptr;
+  DevRecords rec;
+  // ordering (K1)
+  bool sorted = true;
+  DBuf<uint32_t> perm;  // sorted position -> source row (only when !sorted)
+  // name dictionary (K2)
+  uint32_t table_bits = 0;
+  DBuf<uint64_t> tkey;     // 64-bit name hash per slot (0 = empty)
+  DBuf<uint32_t> trep;     // smallest source row carrying the slot's name
+  DBuf<uint32_t> tfirst;   // first main-stream token index with this name
+  DBuf<uint8_t> tflags;    // classify bits of the slot's name
+  DBuf<uint32_t> used;     // claimed slots
+  uint32_t n_used = 0;
+  DBuf<uint32_t> slot;     // per source row
+  DBuf<uint8_t> kind;      // per source row (ITT_KIND_*)
+  // device census
+  std::vector<uint64_t> dev_counts;
+  uint32_t n_devices = 1;
+  uint16_t majority = 0;
+  bool filtering = false;  // more than one device: drop non-majority records
+  uint64_t kept = 0;
+  // stream census
+  std::vector<itt_stream_summary> streams;
+  // compaction outputs (K3)
+  uint64_t n_tok = 0, n_htod = 0;
+  DBuf<uint32_t> tok_slot;
+  DBuf<int32_t> tokens;
+  DBuf<int64_t> tok_start, tok_end;
+  DBuf<uint64_t> tok_record;  // sorted-order record index (only for build_token_sequence)
+  DBuf<int64_t> htod_start, htod_end, htod_size;
+  uint32_t n_names = 0;
+  std::vector<uint64_t> name_row;  // token id -> source row
+  ScanScratch scan;
+  radix::Scratch rs;
+};
+
+void upload_records(Ctx* c, const itt_records* r, DevRecords& d);
+void order_records(TraceState& t);
+void build_dictionary(TraceState& t);          // hash + verify + classify + device census
+void stream_census(TraceState& t);             // summaries over the kept records (classified)
+void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index);
+void renumber_tokens(TraceState& t);           // first-appearance ids + token map
+int64_t count_overlaps(TraceState& t);         // count_interval_overlaps on the compacted main stream
+
+// ------------------------------------------------------------------ suffix array (sa.cu)
+struct SuffixState {
+  uint64_t n = 0;   // tokens
+  uint64_t np = 0;  // n + 1 suffixes
+  DBuf<int32_t> text;         // tokens + [terminator] (codes)
+  DBuf<uint32_t> sa;          // [np]
+  DBuf<uint32_t> lcp;         // [np]
+  std::vector<DBuf<uint32_t>> levels;  // rank (group head) after each doubling round
+  uint32_t h0 = 1;            // prefix length of levels[0]
+  int32_t lo = 0;             // text code = token - lo
+  int rounds = 0;
+};
+// tokens: device int32[n]; term: unique terminator
+void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
+                        radix::Scratch& rs, ScanScratch& scan);
+
+// ------------------------------------------------------------------ mining (mine.cu)
+struct IntervalState {
+  DBuf<uint32_t> cnt;  // count of the interval represented at k (0 = not a representative)
+  DBuf<uint32_t> par;  // parent depth
+  DBuf<uint32_t> lb;   // left boundary
+};
+void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv);
+
+struct MinedPattern {
+  int status = 0;
+  std::string error;
+  std::vector<int32_t> tokens;
+  int64_t count = 0, first_token = 0, epsilon_used = 0;
+};
+// mine_pattern_impl (mine.hpp:75-111) over shared SA/LCP/intervals
+MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, const itt_mining_cfg& cfg,
+                      const std::string& label);
+std::vector<MinedPattern> mine_loops(Ctx* c, const SuffixState& s, const IntervalState& iv,
+                                     const std::vector<itt_mining_cfg>& loops, bool multi);
+
+// ------------------------------------------------------------------ matching (match.cu)
+struct SpanState {
+  uint64_t n = 0;
+  DBuf<uint32_t> start, end, extra;
+};
+void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* pattern_dev, uint64_t m, int64_t k0,
+                      SpanState& out, ScanScratch& scan);
+
+// ------------------------------------------------------------------ aggregates (metrics.cu)
+void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_end, uint64_t n_tok,
+                          const int64_t* htod_start, const int64_t* htod_end, const int64_t* htod_size, uint64_t n_htod,
+                          const SpanState& spans, std::vector<itt_iter_row>& rows, itt_clamps& clamps,
+                          ScanScratch& scan);
+
+}  // namespace itt

@@ -1,0 +1,313 @@
+"""ctypes binding of libitertrace_cuda.so (include/itertrace_cuda.h).
+
+There is no CPU fallback: loading fails loudly when the in-tree library is missing, and
+creating a context fails without an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libitertrace_cuda.so")
+P = C.POINTER
+_lib = None
+
+
+class IttError(Exception):
+    """A failed C-ABI call.  ``kind`` is the reference ErrorKind name for statuses 1..12."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+        self.kind = abi.ERROR_KINDS[status - 1] if 1 <= status <= 12 else {
+            abi.ITT_E_CUDA: "Cuda", abi.ITT_E_NCCL: "Nccl", abi.ITT_E_INVALID_ARGUMENT: "InvalidArgument"}.get(
+                status, f"status{status}")
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    sig = {
+        "itt_abi_version": ([], C.c_int),
+        "itt_ctx_create": ([C.c_int, P(vp)], C.c_int),
+        "itt_ctx_destroy": ([vp], C.c_int),
+        "itt_last_error": ([vp], C.c_char_p),
+        "itt_free": ([vp, vp], C.c_int),
+        "itt_ctx_set_profiling": ([vp, C.c_int], C.c_int),
+        "itt_ctx_reset_stats": ([vp], C.c_int),
+        "itt_ctx_kernel_stats": ([vp, P(abi.itt_kernel_stat), C.c_uint32, P(C.c_uint32)], C.c_int),
+        "itt_ctx_launch_count": ([vp, P(C.c_uint64)], C.c_int),
+        "itt_device_alloc": ([vp, C.c_uint64, P(vp)], C.c_int),
+        "itt_device_free": ([vp, vp], C.c_int),
+        "itt_memcpy_h2d": ([vp, vp, vp, C.c_uint64], C.c_int),
+        "itt_memcpy_d2h": ([vp, vp, vp, C.c_uint64], C.c_int),
+        "itt_host_register": ([vp, vp, C.c_uint64], C.c_int),
+        "itt_host_unregister": ([vp, vp], C.c_int),
+        "itt_ctx_synchronize": ([vp], C.c_int),
+        "itt_summarize_streams": ([vp, P(abi.itt_records), C.c_int, P(abi.itt_census)], C.c_int),
+        "itt_select_main_stream": ([vp, P(abi.itt_census), P(C.c_uint32), P(C.c_uint32)], C.c_int),
+        "itt_build_token_sequence": ([vp, P(abi.itt_records), C.c_uint32, P(P(abi.itt_tokens))], C.c_int),
+        "itt_count_interval_overlaps": ([vp, P(abi.itt_records), C.c_uint32, P(C.c_int64)], C.c_int),
+        "itt_suffix_array": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, P(C.c_uint32), P(C.c_uint32)], C.c_int),
+        "itt_enumerate_repeats": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, C.c_int64, C.c_int64,
+                                   P(P(abi.itt_repeat)), P(C.c_uint64)], C.c_int),
+        "itt_mine_patterns": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, P(abi.itt_mining_cfg), C.c_uint32, C.c_int,
+                               P(P(abi.itt_pattern))], C.c_int),
+        "itt_free_patterns": ([vp, P(abi.itt_pattern), C.c_uint32], C.c_int),
+        "itt_approx_match": ([vp, P(C.c_int32), C.c_uint64, P(C.c_int32), C.c_uint64, C.c_int64, P(P(abi.itt_span)),
+                              P(C.c_uint64)], C.c_int),
+        "itt_iteration_metrics": ([vp, P(abi.itt_records), P(C.c_uint64), C.c_uint64, P(abi.itt_span), C.c_uint64,
+                                   P(P(abi.itt_iter_row)), P(abi.itt_clamps)], C.c_int),
+        "itt_analyze": ([vp, P(abi.itt_records), P(abi.itt_analyze_opts), P(P(abi.itt_analysis))], C.c_int),
+        "itt_free_analysis": ([vp, P(abi.itt_analysis)], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    if L.itt_abi_version() != abi.ABI_VERSION:
+        raise RuntimeError("libitertrace_cuda.so ABI version mismatch")
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    """Entry points declared in include/itertrace_cuda.h (checked by the CPU test suite)."""
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "itertrace_cuda.h")
+    import re
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(itt_\w+)\s*\(", open(hdr).read(), re.M)))
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(P(t))
+
+
+class DeviceRecords:
+    """Trace columns resident in HBM (allocated through the context)."""
+
+    def __init__(self, ctx: "Context", recs: abi.Records):
+        self.ctx = ctx
+        self.n = recs.n
+        self.order = recs.order
+        self.bufs = {}
+        cols = dict(start_ns=recs.start_ns, duration_ns=recs.duration_ns, size_bytes=recs.size_bytes, flags=recs.flags,
+                    stream=recs.stream, name_off=recs.name_off, name_bytes=recs.name_bytes)
+        if recs.device is not None:
+            cols["device"] = recs.device
+        for k, a in cols.items():
+            p = C.c_void_p()
+            ctx._check(lib().itt_device_alloc(ctx.h, max(1, a.nbytes), C.byref(p)))
+            ctx._check(lib().itt_memcpy_h2d(ctx.h, p, a.ctypes.data, a.nbytes))
+            self.bufs[k] = p
+        self.nbytes = sum(a.nbytes for a in cols.values())
+
+    def c(self) -> abi.itt_records:
+        b = self.bufs
+        return abi.itt_records(self.n, b["start_ns"], b["duration_ns"], b["size_bytes"], b["flags"], b["stream"],
+                               b.get("device"), b["name_off"], b["name_bytes"], abi.MEM_DEVICE, self.order)
+
+    def free(self):
+        for p in self.bufs.values():
+            lib().itt_device_free(self.ctx.h, p)
+        self.bufs = {}
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        rc = L.itt_ctx_create(device, C.byref(h))
+        if rc != 0:
+            raise IttError(rc, f"itt_ctx_create({device}) failed: no usable sm_100 device")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().itt_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            raise IttError(rc, lib().itt_last_error(self.h).decode(errors="replace"))
+
+    # ---------------------------------------------------------------- profiling
+    def set_profiling(self, on: bool):
+        self._check(lib().itt_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def reset_stats(self):
+        self._check(lib().itt_ctx_reset_stats(self.h))
+
+    def kernel_stats(self) -> dict:
+        arr = (abi.itt_kernel_stat * 256)()
+        n = C.c_uint32()
+        self._check(lib().itt_ctx_kernel_stats(self.h, arr, 256, C.byref(n)))
+        return {arr[i].name.decode(): dict(launches=arr[i].launches, total_ms=arr[i].total_ms, bytes=arr[i].bytes)
+                for i in range(min(n.value, 256))}
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        self._check(lib().itt_ctx_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    def synchronize(self):
+        self._check(lib().itt_ctx_synchronize(self.h))
+
+    def upload(self, recs: abi.Records) -> DeviceRecords:
+        return DeviceRecords(self, recs)
+
+    def register_host(self, arr: np.ndarray):
+        self._check(lib().itt_host_register(self.h, arr.ctypes.data, arr.nbytes))
+
+    def unregister_host(self, arr: np.ndarray):
+        self._check(lib().itt_host_unregister(self.h, arr.ctypes.data))
+
+    # ---------------------------------------------------------------- hot path
+    def suffix_array(self, tokens, term: int, want_lcp: bool = True):
+        t = _i32(tokens)
+        n = t.shape[0]
+        sa = np.zeros(n + 1, np.uint32)
+        lcp = np.zeros(n + 1, np.uint32) if want_lcp else None
+        self._check(lib().itt_suffix_array(self.h, _ptr(t, C.c_int32), n, term, _ptr(sa, C.c_uint32),
+                                           _ptr(lcp, C.c_uint32) if want_lcp else None))
+        return sa, lcp
+
+    def enumerate_repeats(self, tokens, term, min_count, max_len):
+        t = _i32(tokens)
+        out = P(abi.itt_repeat)()
+        cnt = C.c_uint64()
+        self._check(lib().itt_enumerate_repeats(self.h, _ptr(t, C.c_int32), t.shape[0], term, min_count, max_len,
+                                                C.byref(out), C.byref(cnt)))
+        res = [(out[i].start, out[i].length, out[i].count) for i in range(cnt.value)]
+        lib().itt_free(self.h, C.cast(out, C.c_void_p))
+        return res
+
+    def mine_patterns(self, tokens, term, loops, multi=False):
+        t = _i32(tokens)
+        cfgs = (abi.itt_mining_cfg * max(1, len(loops)))()
+        for i, lp in enumerate(loops):
+            cfgs[i].iterations = lp[0]
+            cfgs[i].epsilon0 = lp[1] if len(lp) > 1 else 1
+            cfgs[i].epsilon_cap = lp[2] if len(lp) > 2 else 0
+        out = P(abi.itt_pattern)()
+        self._check(lib().itt_mine_patterns(self.h, _ptr(t, C.c_int32), t.shape[0], term, cfgs, len(loops),
+                                            1 if multi else 0, C.byref(out)))
+        k = len(loops) if multi else 1
+        res = [dict(tokens=[out[i].tokens[j] for j in range(out[i].length)], count=out[i].count,
+                    first_token=out[i].first_token, epsilon_used=out[i].epsilon_used) for i in range(k)]
+        lib().itt_free_patterns(self.h, out, k)
+        return res
+
+    def approx_match(self, tokens, pattern, k0):
+        t = _i32(tokens)
+        p = _i32(pattern)
+        out = P(abi.itt_span)()
+        cnt = C.c_uint64()
+        self._check(lib().itt_approx_match(self.h, _ptr(t, C.c_int32), t.shape[0], _ptr(p, C.c_int32), p.shape[0], k0,
+                                           C.byref(out), C.byref(cnt)))
+        res = np.array([(out[i].start_token, out[i].end_token, out[i].extra) for i in range(cnt.value)],
+                       dtype=np.int64).reshape(-1, 3)
+        lib().itt_free(self.h, C.cast(out, C.c_void_p))
+        return res
+
+    def build_token_sequence(self, recs, main_stream):
+        c = recs.c()
+        out = P(abi.itt_tokens)()
+        self._check(lib().itt_build_token_sequence(self.h, C.byref(c), main_stream, C.byref(out)))
+        o = out[0]
+        n = o.n
+        tok = np.ctypeslib.as_array(o.tokens, shape=(n,)).copy() if n else np.zeros(0, np.int32)
+        ri = np.ctypeslib.as_array(o.record_index, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+        names = (np.ctypeslib.as_array(o.name_row, shape=(o.n_names,)).copy() if o.n_names
+                 else np.zeros(0, np.uint64))
+        for p in (o.tokens, o.record_index, o.name_row):
+            lib().itt_free(self.h, C.cast(p, C.c_void_p))
+        lib().itt_free(self.h, C.cast(out, C.c_void_p))
+        return tok, ri, names
+
+    def count_interval_overlaps(self, recs, stream):
+        c = recs.c()
+        v = C.c_int64()
+        self._check(lib().itt_count_interval_overlaps(self.h, C.byref(c), stream, C.byref(v)))
+        return v.value
+
+    def summarize_streams(self, recs, filter_device=False):
+        c = recs.c()
+        out = abi.itt_census()
+        self._check(lib().itt_summarize_streams(self.h, C.byref(c), 1 if filter_device else 0, C.byref(out)))
+        from_c = [(s.stream, s.cls, tuple(s.counts[k] for k in range(6)), s.first_start, s.last_end)
+                  for s in (out.streams[i] for i in range(out.n_streams))]
+        info = dict(n_devices=out.n_devices, majority_device=out.majority_device, dropped=out.dropped_records,
+                    n_records=out.n_records)
+        lib().itt_free(self.h, C.cast(out.streams, C.c_void_p))
+        return from_c, info
+
+    def iteration_metrics(self, recs, record_index, spans):
+        c = recs.c()
+        ri = np.ascontiguousarray(record_index, dtype=np.uint64)
+        sp = (abi.itt_span * max(1, len(spans)))()
+        for i, s in enumerate(spans):
+            sp[i].start_token, sp[i].end_token, sp[i].extra = int(s[0]), int(s[1]), int(s[2])
+        rows = P(abi.itt_iter_row)()
+        cl = abi.itt_clamps()
+        self._check(lib().itt_iteration_metrics(self.h, C.byref(c), _ptr(ri, C.c_uint64), ri.shape[0], sp, len(spans),
+                                                C.byref(rows), C.byref(cl)))
+        out = [abi.itt_iter_row.from_buffer_copy(rows[i]) for i in range(len(spans))]
+        lib().itt_free(self.h, C.cast(rows, C.c_void_p))
+        return out, (cl.negative_gap_clamps, cl.negative_interval_clamps)
+
+    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1) -> dict:
+        """itt_analyze: device pipeline up to the per-loop integer aggregates."""
+        c = recs.c()
+        lp = (C.c_int64 * max(1, len(loops)))(*loops)
+        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream)
+        out = P(abi.itt_analysis)()
+        self._check(lib().itt_analyze(self.h, C.byref(c), C.byref(opts), C.byref(out)))
+        try:
+            a = out[0]
+            res = dict(
+                streams=[(s.stream, s.cls, tuple(s.counts[k] for k in range(6)), s.first_start, s.last_end)
+                         for s in (a.census.streams[i] for i in range(a.census.n_streams))],
+                n_devices=a.census.n_devices, majority_device=a.census.majority_device,
+                dropped=a.census.dropped_records, main_stream=a.main_stream, n_main_streams=a.n_main_streams,
+                override_non_main=bool(a.main_stream_override_non_main), n_tokens=a.n_tokens, n_names=a.n_names,
+                name_row=[a.name_row[i] for i in range(a.n_names)], overlapping_kernels=a.overlapping_kernels,
+                loops=[])
+            for k in range(a.n_loops):
+                L = a.loops[k]
+                rows = np.ctypeslib.as_array(C.cast(L.rows, P(C.c_int64)), shape=(L.n_iterations, 11)).copy() \
+                    if L.n_iterations else np.zeros((0, 11), np.int64)
+                res["loops"].append(dict(
+                    iterations_declared=L.iterations_declared, pattern_length=L.pattern_length,
+                    pattern_tokens=[L.pattern_tokens[j] for j in range(L.pattern_length)],
+                    pattern_count=L.pattern_count, epsilon_used=L.epsilon_used, first_token=L.first_token,
+                    k0_used=L.k0_used, rows=rows,
+                    clamps=(L.clamps.negative_gap_clamps, L.clamps.negative_interval_clamps)))
+            return res
+        finally:
+            lib().itt_free_analysis(self.h, out)
+
+
+# column order of analyze_raw()["loops"][k]["rows"] (itt_iter_row as int64 words; the last word
+# packs has_interval | pad)
+ROW_FIELDS = ["start_token", "end_token", "extra", "t_start", "t_end", "interval_ns", "copy_ns", "htod_bytes",
+              "gap_sum", "gap_count", "has_interval"]
