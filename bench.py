@@ -1,0 +1,296 @@
+#!/usr/bin/env python3
+"""bench.py — trace events/sec of the B200 mining pipeline (intern -> SA -> LCP -> repeat ->
+spans -> per-iteration aggregates) on BASELINE.json's configs[1] (C2: 10M-event TF-like
+trace, 50K iterations x 200 ops, 5% memcpy noise, rows locally shuffled).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference] [--config C2]
+
+* value : whole-job events/s with the columns already resident in HBM (device-timed with CUDA
+          events on the library's stream; one step = one itt_analyze call = the full path).
+* e2e   : the same metric through the C-ABI with pinned HOST buffers (H2D of every column and
+          the D2H of the per-iteration rows inside the timed region).
+* roofline : dominant kernel's algorithmic bytes / its CUDA-event launch time (profiled pass).
+* cpu_baseline : the reference itself (oracle/_ref, compiled from the reference headers) on a
+          bounded sample of the same workload, 1 host core (the reference is single-threaded).
+Under torchrun each rank runs one replica (C2 does not shard: "replicas only").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace events/sec for SA+LCP+repeat mining+segmentation; % HBM roofline"
+WORKLOADS = {
+    "C1": ("C1: synthetic TF-like trace, 100 iterations x 200 ops (~20K events), V=150 body names + 16 init names",
+           dict(), 100),
+    "C2": ("C2: 10M-event trace, 50K iterations x 200 ops, V=150 (+16 init), 5% memcpy noise on streams 14/15, "
+           "rows shuffled in windows of 64", dict(), 50_000),
+    "C3": ("C3: 100M-event trace, 20K iterations x 5000 ops, V=4096 (+16 init)", dict(), 20_000),
+}
+# bounded CPU samples (same generator and shape, fewer iterations)
+CPU_SAMPLE_ITERS = {"C1": 100, "C2": 10_000, "C3": 400}
+REF_ARM_ITERS = {"C1": 100, "C2": 5_000, "C3": 200}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def make_trace(config: str, iterations: int | None = None):
+    from paper_1707_03750_b200 import synth
+    kw = {}
+    if iterations is not None:
+        kw["iterations"] = iterations
+    return synth.generate_config(config, **kw)
+
+
+def cpu_reference_run(config: str, iters: int, steps: int, warmup: int):
+    """Time the reference (oracle/_ref) on a bounded sample: events/s on 1 core."""
+    from oracle.bindings import ref
+    recs, info = make_trace(config, iters)
+    R = ref()
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        res = R.analyze(recs, [iters], staged=True)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+    ev = info["n"] / statistics.mean(times)
+    stage = res["times"]
+    sample = (f"{config}-shaped trace with {iters} iterations ({info['n']} events, {info['n_main']} tokens); "
+              f"reference analyze stages (ms): " + ", ".join(f"{k[:-3]}={v:.0f}" for k, v in stage.items()))
+    return ev, info, sample, times
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=2)
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    workload, _, iters = WORKLOADS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        it = REF_ARM_ITERS[args.config]
+        ev, info, sample, times = cpu_reference_run(args.config, it, args.steps, max(1, args.warmup))
+        line = {"metric": METRIC, "value": ev, "unit": "events/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": workload, "sample_iterations": it, "events_per_step": info["n"]},
+                "cpu_baseline": {"value": ev, "unit": "events/s", "cores": 1, "kind": "reference", "sample": sample},
+                "e2e": {"value": ev, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_1707_03750_b200 import cuda as itt
+
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    ctx = itt.Context(dev)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", dev))
+    t_gen = time.perf_counter()
+    recs, info = make_trace(args.config)
+    log(f"[rank {rank}] generated {args.config}: {info} in {time.perf_counter() - t_gen:.1f}s")
+    n_events = info["n"]
+    drecs = ctx.upload(recs)
+
+    def step_device():
+        return ctx.analyze_raw(drecs, [iters])
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        ctx.synchronize()
+
+    def timed(fn, steps):
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            res = fn()
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, res
+
+    for _ in range(max(3, args.warmup)):
+        res = step_device()
+    # correctness guard: the mined period must be the planted body
+    assert res["loops"][0]["pattern_length"] > 0
+    l0 = ctx.launch_count()
+    with ClockSampler(dev) as clk:
+        ms, res = timed(step_device, args.steps)
+    launches = (ctx.launch_count() - l0) // max(1, args.steps)
+    ms_step = ms / args.steps
+    value = world * n_events / (ms_step / 1000.0)
+
+    # ---- roofline: profiled pass (per-kernel CUDA events on the library stream)
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    for _ in range(args.profile_steps):
+        step_device()
+    stats = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    tot = sum(s["total_ms"] for s in stats.values()) or 1.0
+    top = max(stats.items(), key=lambda kv: kv[1]["total_ms"])
+    name, st = top
+    per_launch_bytes = st["bytes"] / st["launches"]
+    avg_ms = st["total_ms"] / st["launches"]
+    achieved = per_launch_bytes / (avg_ms / 1000.0) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get("kernels", {}).get(name, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "share_of_step": st["total_ms"] / tot, "launches_per_step": st["launches"] / args.profile_steps}
+    kernel_table = {k: {"ms_per_step": v["total_ms"] / args.profile_steps,
+                        "GBps": (v["bytes"] / (v["total_ms"] / 1000.0) / 1e9) if v["total_ms"] > 0 else None}
+                    for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])}
+
+    # ---- e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off,
+                recs.name_bytes] + ([recs.device] if recs.device is not None else [])
+        for a in cols:
+            ctx.register_host(a)
+        try:
+            def step_host():
+                return ctx.analyze_raw(recs, [iters])
+            step_host()
+            ms_e, res_e = timed(step_host, args.steps)
+        finally:
+            for a in cols:
+                ctx.unregister_host(a)
+        d2h = sum(L["rows"].nbytes + 4 * L["pattern_length"] for L in res_e["loops"])
+        e2e = {"value": world * n_events / (ms_e / args.steps / 1000.0), "unit": "events/s",
+               "h2d_bytes_per_step": int(recs.nbytes()), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": ms_e / args.steps}
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ev, cinfo, sample, _ = cpu_reference_run(args.config, CPU_SAMPLE_ITERS[args.config], 1, 0)
+            cpu = {"value": ev, "unit": "events/s", "cores": 1, "kind": "reference", "sample": sample}
+        except Exception as e:  # the reference library must be prebuilt in this container
+            cpu = {"value": None, "unit": "events/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        L = res["loops"][0]
+        line = {
+            "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": workload, "events": n_events, "tokens": info["n_main"],
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (%.2f GB resident columns)" % (drecs.nbytes / 1e9),
+                       "mined": {"pattern_length": L["pattern_length"], "pattern_count": L["pattern_count"],
+                                 "iterations_found": int(L["rows"].shape[0])}},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": int(launches), "kernels": kernel_table,
+        }
+        print(json.dumps(line), flush=True)
+    drecs.free()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

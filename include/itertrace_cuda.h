@@ -120,6 +120,8 @@ int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes);
 int itt_host_unregister(itt_ctx* ctx, void* p);
 int itt_ctx_synchronize(itt_ctx* ctx);
+/* the context's cudaStream_t (for callers that time with CUDA events on it) */
+int itt_ctx_stream(itt_ctx* ctx, void** stream);
 
 /* ------------------------------------------------------- L2 streams (a1, a2) */
 typedef struct itt_stream_summary { /* StreamSummary, streams.hpp:16-32 */

@@ -204,6 +204,11 @@ int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes) {
 int itt_host_unregister(itt_ctx* ctx, void* p) {
   return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostUnregister(p)); });
 }
+int itt_ctx_stream(itt_ctx* ctx, void** stream) {
+  if (!ctx || !stream) return ITT_E_INVALID_ARGUMENT;
+  *stream = ctx->c.stream;
+  return ITT_OK;
+}
 int itt_ctx_synchronize(itt_ctx* ctx) {
   return guarded(ctx, [&](Ctx*) {});
 }

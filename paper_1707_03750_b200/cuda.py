@@ -54,6 +54,7 @@ def lib() -> C.CDLL:
         "itt_host_register": ([vp, vp, C.c_uint64], C.c_int),
         "itt_host_unregister": ([vp, vp], C.c_int),
         "itt_ctx_synchronize": ([vp], C.c_int),
+        "itt_ctx_stream": ([vp, P(vp)], C.c_int),
         "itt_summarize_streams": ([vp, P(abi.itt_records), C.c_int, P(abi.itt_census)], C.c_int),
         "itt_select_main_stream": ([vp, P(abi.itt_census), P(C.c_uint32), P(C.c_uint32)], C.c_int),
         "itt_build_token_sequence": ([vp, P(abi.itt_records), C.c_uint32, P(P(abi.itt_tokens))], C.c_int),
@@ -168,6 +169,11 @@ class Context:
         v = C.c_uint64()
         self._check(lib().itt_ctx_launch_count(self.h, C.byref(v)))
         return v.value
+
+    def stream_ptr(self) -> int:
+        v = C.c_void_p()
+        self._check(lib().itt_ctx_stream(self.h, C.byref(v)))
+        return v.value or 0
 
     def synchronize(self):
         self._check(lib().itt_ctx_synchronize(self.h))
