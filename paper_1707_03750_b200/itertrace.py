@@ -1,0 +1,338 @@
+"""Host-side mirror of the reference's analyze_trace (pipeline.hpp:34-134) over the C-ABI.
+
+The device (``itt_analyze``) does every O(n) stage and returns integer per-iteration rows;
+this module finishes what the reference does on the host, in the reference's order, so the
+doubles are bit-identical:
+  * IterationMetrics doubles: overlap = copy / interval (metrics.hpp:131-135),
+    op_gap_mean = gap_sum / gap_count (metrics.hpp:158-160);
+  * compute_summary ordered sums (metrics.hpp:166-202), diagnose (report.hpp:61-90);
+  * warnings text and order (pipeline.hpp:51-52, 62-67, 72, 76-79, 117-125);
+  * rendering: summary_to_json(...).dump(2) (report.hpp:121-185, 304) and details_to_csv
+    (report.hpp:191-220), byte for byte.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+from . import abi
+from .cuda import Context, IttError
+
+TOOL = "itertrace"
+VERSION = "0.1.0"  # version.hpp:5-6
+DIAG = ["COPY_BOUND", "CPU_BOUND", "NONE", "INSUFFICIENT_DATA"]  # report.hpp:24
+DETAILS_HEADER = ("iteration,token_start,token_end,t_start_ns,t_end_ns,interval_ns,overlap_ratio,"
+                  "htod_bytes,op_gap_mean_ns,extra_ops")
+
+
+@dataclass
+class IterationMetrics:  # metrics.hpp:21-31
+    index: int
+    start_token: int
+    end_token: int
+    t_start: int
+    t_end: int
+    interval_ns: Optional[int]
+    overlap_ratio: Optional[float]
+    htod_bytes: int
+    op_gap_mean_ns: float
+    extra_ops: int
+
+
+@dataclass
+class SummaryMetrics:  # metrics.hpp:33-42
+    avg_interval_ns: float = 0.0
+    max_interval_ns: int = 0
+    avg_overlap: float = 0.0
+    avg_operation_ns: float = 0.0
+    avg_size_bytes: float = 0.0
+    iterations_found: int = 0
+    iterations_declared: int = 0
+    insufficient_intervals: bool = False
+
+
+@dataclass
+class Diagnosis:  # report.hpp:36-40
+    code: str = "NONE"
+    evidence: list = field(default_factory=list)
+    message: str = ""
+
+
+@dataclass
+class LoopReport:  # report.hpp:92-103
+    iterations_declared: int
+    pattern_names: list
+    pattern_tokens: list
+    pattern_length: int
+    pattern_count: int
+    epsilon_used: int
+    first_occurrence_token: int
+    k0_used: int
+    iterations_found: int
+    summary: SummaryMetrics
+    diagnosis: Diagnosis
+
+
+@dataclass
+class AnalysisResult:  # pipeline.hpp:27-30 (+ the rendered outputs)
+    trace_path: str
+    epsilon0: int
+    theta_copy: float
+    theta_cpu: float
+    k0_override: Optional[int]
+    main_stream_override: Optional[int]
+    streams: list
+    main_stream: int
+    loops: list
+    details: list
+    warnings: list
+
+    def summary_json(self) -> str:
+        return render_summary(self)
+
+    def details_csv(self, k: int = 0) -> str:
+        return details_to_csv(self.details[k])
+
+
+class AnalyzeError(Exception):
+    def __init__(self, kind: str, message: str):
+        super().__init__(message)
+        self.kind = kind
+
+
+def fmt6(v: float) -> str:  # detail::format_double, report.hpp:49-53
+    return "%.6f" % v
+
+
+def compute_summary(items: list, iterations_declared: int) -> SummaryMetrics:
+    """compute_summary, metrics.hpp:166-202 (same accumulation order)."""
+    if not items:
+        raise AnalyzeError("NoIterations", "metrics: no iterations to summarize")
+    s = SummaryMetrics(iterations_found=len(items), iterations_declared=iterations_declared)
+    isum = icnt = ocnt = btot = 0
+    osum = 0.0
+    gsum = 0.0
+    for m in items:
+        if m.interval_ns is not None:
+            isum += m.interval_ns
+            icnt += 1
+            s.max_interval_ns = max(s.max_interval_ns, m.interval_ns)
+        if m.overlap_ratio is not None:
+            osum += m.overlap_ratio
+            ocnt += 1
+        gsum += m.op_gap_mean_ns
+        btot += m.htod_bytes
+    if icnt > 0:
+        s.avg_interval_ns = float(isum) / float(icnt)
+    else:
+        s.insufficient_intervals = True
+    if ocnt > 0:
+        s.avg_overlap = osum / float(ocnt)
+    s.avg_operation_ns = gsum / float(len(items))
+    s.avg_size_bytes = float(btot) / float(len(items))
+    return s
+
+
+def diagnose(s: SummaryMetrics, theta_copy: float = 0.10, theta_cpu: float = 10.0) -> Diagnosis:
+    """diagnose, report.hpp:61-90."""
+    d = Diagnosis()
+    if s.iterations_found < 2 or s.insufficient_intervals:
+        d.code = "INSUFFICIENT_DATA"
+        d.message = ("fewer than two recovered iterations; interval metrics are undefined, rerun with a longer trace "
+                     "or check the declared iteration count")
+        return d
+    if s.avg_overlap >= theta_copy:
+        d.code = "COPY_BOUND"
+        d.evidence = ["avg_overlap=" + fmt6(s.avg_overlap) + " >= theta_copy=" + fmt6(theta_copy),
+                      "avg_interval_ns=" + fmt6(s.avg_interval_ns)]
+        d.message = ("host-to-device copies occupy a large share of the gap between iterations; data transfer is the "
+                     "likely bottleneck. A smaller batch reduces per-step copy volume, at the cost of more steps; weigh "
+                     "that against what the algorithm needs per batch.")
+        return d
+    if s.avg_interval_ns > 0 and s.avg_interval_ns >= theta_cpu * s.avg_operation_ns:
+        d.code = "CPU_BOUND"
+        d.evidence = ["avg_interval_ns=" + fmt6(s.avg_interval_ns) + " >= theta_cpu=" + fmt6(theta_cpu) +
+                      " * avg_operation_ns=" + fmt6(s.avg_operation_ns),
+                      "avg_overlap=" + fmt6(s.avg_overlap) + " below theta_copy=" + fmt6(theta_copy)]
+        d.message = ("iteration gaps dwarf the in-iteration dispatch cadence while copy activity is low; host-side "
+                     "work between steps is the likely bottleneck. Inspect the training loop for per-step work such as "
+                     "operations that keep growing or re-initializing the computation graph.")
+        return d
+    d.code = "NONE"
+    d.message = "no bottleneck indicated by the interval and copy-overlap heuristics"
+    return d
+
+
+def rows_to_metrics(rows) -> list:
+    """itt_iter_row integers -> IterationMetrics with the reference's two divisions."""
+    out = []
+    for k, r in enumerate(rows):
+        start, end, extra, t0, t1, interval, copy, htod, gsum, gcnt, has_int = (int(x) for x in r[:11])
+        has_int = has_int & 0xFFFFFFFF
+        iv = interval if has_int else None
+        ov = (float(copy) / float(interval)) if (has_int and interval > 0) else None
+        gap = float(gsum) / float(gcnt) if gcnt > 0 else 0.0
+        out.append(IterationMetrics(k + 1, start, end, t0, t1, iv, ov, htod, gap, extra))
+    return out
+
+
+def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Optional[int] = None,
+                  theta_copy: float = 0.10, theta_cpu: float = 10.0, main_stream: Optional[int] = None,
+                  trace_label: str = "trace.csv", device_labels=None, names=None) -> AnalysisResult:
+    """analyze_trace (pipeline.hpp:34-134): device pipeline + host finish in reference order."""
+    try:
+        raw = ctx.analyze_raw(recs, list(loops), epsilon0, -1 if k0 is None else k0,
+                              -1 if main_stream is None else main_stream)
+    except IttError as e:
+        raise AnalyzeError(e.kind, str(e)) from e
+    label = (lambda d: device_labels[d]) if device_labels is not None else (lambda d: "dev%05u" % d)
+    warnings = []
+    if raw["n_devices"] > 1:  # streams.hpp:198-203
+        warnings.append("MultiDeviceTrace: kept majority device '%s', dropped %d records from other devices"
+                        % (label(raw["majority_device"]), raw["dropped"]))
+    if main_stream is not None:
+        if raw["override_non_main"]:
+            warnings.append("MainStreamOverride: stream %d carries no kernels but was selected by override" % main_stream)
+    elif raw["n_main_streams"] > 1:  # streams.hpp:130-143
+        others = ", ".join(str(s[0]) for s in raw["streams"] if s[1] == 0 and s[0] != raw["main_stream"])
+        warnings.append("MultipleMainStreams: analyzing stream %d (most kernels); other kernel-bearing streams: %s"
+                        % (raw["main_stream"], others))
+    if raw["overlapping_kernels"] > 0:
+        warnings.append("OverlappingKernels: %d consecutive main-stream records report overlapping intervals "
+                        "(timer granularity)" % raw["overlapping_kernels"])
+    name_of = None
+    if names is not None:
+        name_of = names
+    elif hasattr(recs, "name"):
+        name_of = [recs.name(r).decode("utf-8", "surrogateescape") for r in raw["name_row"]]
+    loop_reports, details = [], []
+    for k, L in enumerate(raw["loops"]):
+        items = rows_to_metrics(L["rows"])
+        ng, ni = L["clamps"]
+        if ng > 0:
+            warnings.append("NegativeGaps: %d negative dispatch gaps clamped to zero" % ng)
+        if ni > 0:
+            warnings.append("NegativeIntervals: %d negative iteration intervals clamped to zero" % ni)
+        summ = compute_summary(items, loops[k])
+        pnames = [name_of[t] for t in L["pattern_tokens"]] if name_of is not None else [str(t) for t in L["pattern_tokens"]]
+        loop_reports.append(LoopReport(loops[k], pnames, L["pattern_tokens"], L["pattern_length"], L["pattern_count"],
+                                       L["epsilon_used"], L["first_token"], L["k0_used"], len(items), summ,
+                                       diagnose(summ, theta_copy, theta_cpu)))
+        details.append(items)
+    return AnalysisResult(trace_label, epsilon0, theta_copy, theta_cpu, k0, main_stream, raw["streams"],
+                          raw["main_stream"], loop_reports, details, warnings)
+
+
+# ---------------------------------------------------------------- rendering (report.hpp)
+def _json_str(s: str) -> str:
+    out = ['"']
+    for ch in s:
+        o = ord(ch)
+        if ch == '"':
+            out.append('\\"')
+        elif ch == "\\":
+            out.append("\\\\")
+        elif ch == "\b":
+            out.append("\\b")
+        elif ch == "\f":
+            out.append("\\f")
+        elif ch == "\n":
+            out.append("\\n")
+        elif ch == "\r":
+            out.append("\\r")
+        elif ch == "\t":
+            out.append("\\t")
+        elif o < 0x20:
+            out.append("\\u%04x" % o)
+        else:
+            out.append(ch)
+    out.append('"')
+    return "".join(out)
+
+
+def _json_float(v: float) -> str:
+    """nlohmann::json number_float dump: shortest round-trip digits, '.0' for integral values,
+    exponent form outside (1e-5, 1e15]."""
+    if math.isnan(v) or math.isinf(v):
+        return "null"
+    r = repr(float(v))
+    a = abs(v)
+    if a != 0.0 and 1e15 <= a < 1e16:  # nlohmann switches to exponent one decade earlier than Python
+        m, e = ("%.17e" % v).split("e")
+        digits = repr(v).rstrip("0").rstrip(".").replace("-", "").replace(".", "")
+        mant = digits[0] + ("." + digits[1:] if len(digits) > 1 else "")
+        return ("-" if v < 0 else "") + mant + "e+" + "%02d" % int(e)
+    return r
+
+
+def _dump(v, indent: int, level: int) -> str:
+    pad = " " * (indent * (level + 1))
+    end = " " * (indent * level)
+    if v is None:
+        return "null"
+    if v is True:
+        return "true"
+    if v is False:
+        return "false"
+    if isinstance(v, int):
+        return str(v)
+    if isinstance(v, float):
+        return _json_float(v)
+    if isinstance(v, str):
+        return _json_str(v)
+    if isinstance(v, list):
+        if not v:
+            return "[]"
+        return "[\n" + ",\n".join(pad + _dump(x, indent, level + 1) for x in v) + "\n" + end + "]"
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        return "{\n" + ",\n".join(pad + _json_str(k) + ": " + _dump(x, indent, level + 1) for k, x in v.items()) + \
+            "\n" + end + "}"
+    raise TypeError(type(v))
+
+
+def summary_object(r: AnalysisResult) -> dict:
+    """summary_to_json, report.hpp:121-185 (key order preserved)."""
+    streams = []
+    for (sid, cls, counts, first, last) in r.streams:
+        streams.append({"stream": sid, "class": abi.CLASS_NAMES[cls], "kernel": counts[0], "memcpy_htod": counts[1],
+                        "memcpy_dtoh": counts[2], "memcpy_dtod": counts[3], "memset": counts[4], "other": counts[5],
+                        "first_start_ns": first, "last_end_ns": last})
+    loops = []
+    for L in r.loops:
+        s = L.summary
+        loops.append({
+            "iterations_declared": L.iterations_declared, "pattern": list(L.pattern_names),
+            "pattern_length": L.pattern_length, "pattern_count": L.pattern_count, "epsilon_used": L.epsilon_used,
+            "first_occurrence_token": L.first_occurrence_token, "k0": L.k0_used, "iterations_found": L.iterations_found,
+            "metrics": {"avg_interval_ns": float(s.avg_interval_ns), "max_interval_ns": s.max_interval_ns,
+                        "avg_overlap": float(s.avg_overlap), "avg_operation_ns": float(s.avg_operation_ns),
+                        "avg_size_bytes": float(s.avg_size_bytes), "insufficient_intervals": s.insufficient_intervals},
+            "diagnosis": {"code": L.diagnosis.code, "evidence": list(L.diagnosis.evidence),
+                          "message": L.diagnosis.message}})
+    return {"tool": TOOL, "version": VERSION, "trace": r.trace_path,
+            "config": {"epsilon0": r.epsilon0, "theta_copy": float(r.theta_copy), "theta_cpu": float(r.theta_cpu),
+                       "k0_override": r.k0_override, "main_stream_override": r.main_stream_override},
+            "streams": streams, "main_stream": r.main_stream, "loops": loops, "warnings": list(r.warnings)}
+
+
+def render_summary(r: AnalysisResult) -> str:
+    return _dump(summary_object(r), 2, 0) + "\n"
+
+
+def details_to_csv(items: list) -> str:
+    """details_to_csv, report.hpp:191-220."""
+    out = [DETAILS_HEADER]
+    for m in items:
+        cells = [str(m.index), str(m.start_token), str(m.end_token), str(m.t_start), str(m.t_end),
+                 "" if m.interval_ns is None else str(m.interval_ns),
+                 "" if m.overlap_ratio is None else fmt6(m.overlap_ratio), str(m.htod_bytes),
+                 str(_llround(m.op_gap_mean_ns)), str(m.extra_ops)]
+        out.append(",".join(cells))
+    return "\n".join(out) + "\n"
+
+
+def _llround(x: float) -> int:  # std::llround: half away from zero
+    return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
