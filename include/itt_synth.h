@@ -33,6 +33,7 @@ typedef struct itt_synth_cfg {
   int64_t htod_lo, htod_hi;            /* HtoD bytes per gap [lo, hi] (1024, 9216) */
   int64_t body_inserts;   /* >0: per iteration, with prob insert_prob, insert 1..body_inserts foreign kernels inside the body */
   double insert_prob;
+  double extra_stream_frac; /* fraction of main kernels duplicated onto kernel stream 21 */
 } itt_synth_cfg;
 
 typedef struct itt_synth_trace {

@@ -94,6 +94,7 @@ extern "C" void itt_synth_default(itt_synth_cfg* c) {
   c->htod_hi = 9216;
   c->body_inserts = 0;
   c->insert_prob = 0.0;
+  c->extra_stream_frac = 0.0;
 }
 
 extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out) {
@@ -179,6 +180,18 @@ extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out
         for (int64_t x = 0; x < n_ins; ++x) emit_kernel(foreign0 + static_cast<int32_t>(rng.range(0, n_foreign)));
     }
     push(prev_end + 200, copy_dur(512), 512, SZ | TP, kDtoHStream, kDtoH);  // result drain
+  }
+  // a second kernel-bearing stream (exercise select_main_stream's MultipleMainStreams warning)
+  if (cfg->extra_stream_frac > 0.0) {
+    const size_t base = recs.size();
+    for (size_t i = 0; i < base; ++i) {
+      if (recs[i].stream != kMain || !rng.coin(cfg->extra_stream_frac)) continue;
+      Rec r = recs[i];
+      r.stream = 21;
+      r.start += 7;
+      r.seq = seq++;
+      recs.push_back(r);
+    }
   }
   // minority device records (exercise filter_majority_device): copies of random main records
   if (cfg->minority_frac > 0.0) {

@@ -259,10 +259,9 @@ def _json_float(v: float) -> str:
     r = repr(float(v))
     a = abs(v)
     if a != 0.0 and 1e15 <= a < 1e16:  # nlohmann switches to exponent one decade earlier than Python
-        m, e = ("%.17e" % v).split("e")
-        digits = repr(v).rstrip("0").rstrip(".").replace("-", "").replace(".", "")
+        digits = repr(a)[:-2].replace(".", "").rstrip("0")  # repr(a) == "dddddddddddddddd.0" here
         mant = digits[0] + ("." + digits[1:] if len(digits) > 1 else "")
-        return ("-" if v < 0 else "") + mant + "e+" + "%02d" % int(e)
+        return ("-" if v < 0 else "") + mant + "e+15"
     return r
 
 

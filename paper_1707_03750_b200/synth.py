@@ -22,7 +22,7 @@ class itt_synth_cfg(C.Structure):
         ("minority_frac", C.c_double), ("name_min", C.c_int64), ("name_max", C.c_int64),
         ("kdur_lo", C.c_int64), ("kdur_hi", C.c_int64), ("intra_lo", C.c_int64), ("intra_hi", C.c_int64),
         ("inter_lo", C.c_int64), ("inter_hi", C.c_int64), ("htod_lo", C.c_int64), ("htod_hi", C.c_int64),
-        ("body_inserts", C.c_int64), ("insert_prob", C.c_double),
+        ("body_inserts", C.c_int64), ("insert_prob", C.c_double), ("extra_stream_frac", C.c_double),
     ]
 
 

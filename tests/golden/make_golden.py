@@ -103,6 +103,12 @@ TRACE_CASES = [
     ("C1_invalid_iters", dict(seed=18, iterations=40), [1], {}),
     ("C1_main_override_copy", dict(seed=19, iterations=30), [30], {"main_stream": 14}),
     ("C1_main_override_absent", dict(seed=19, iterations=30), [30], {"main_stream": 99}),
+    ("C1_overlapping_kernels", dict(seed=20, intra_lo=-300, intra_hi=400), [100], {}),
+    ("C1_negative_intervals", dict(seed=21, inter_lo=-6000, inter_hi=3000), [100], {}),
+    ("C1_two_kernel_streams", dict(seed=22, extra_stream_frac=0.02), [100], {}),
+    ("C1_multi_loop", dict(seed=23, iterations=40), [40, 20], {}),
+    ("C1_multi_loop_dup", dict(seed=23, iterations=40), [40, 40], {}),
+    ("C1_eps0_4", dict(seed=24, iterations=50), [64], {"epsilon0": 4}),
 ]
 
 
@@ -114,7 +120,8 @@ def trace_cases(R):
         recs, info = synth.generate(**kw)
         case = {"name": name, "generator": kw, "loops": loops, "opts": opts, "info": info}
         try:
-            r = R.analyze(recs, loops, k0=opts.get("k0", -1), main_stream=opts.get("main_stream", -1))
+            r = R.analyze(recs, loops, epsilon0=opts.get("epsilon0", 1), k0=opts.get("k0", -1),
+                          main_stream=opts.get("main_stream", -1))
             case["streams"] = [list(s[:2]) + [list(s[2])] + list(s[3:]) for s in r["streams"]]
             case["main_stream"] = r["main_stream"]
             case["warnings"] = r["warnings"]
@@ -145,7 +152,19 @@ def trace_cases(R):
     return out
 
 
+def reference_render_goldens():
+    """The reference's own rendering goldens (tests/golden/*, report.hpp byte format), kept as
+    fixtures so the CPU suite can pin the host renderer without the reference sources."""
+    src = "/root/reference/proj/tests/golden"
+    for name in ("summary_golden.json", "details_golden.csv"):
+        p = os.path.join(src, name)
+        if os.path.exists(p):
+            with open(p, "rb") as f, open(os.path.join(HERE, "reference_" + name), "wb") as g:
+                g.write(f.read())
+
+
 def main():
+    reference_render_goldens()
     R = ref()
     with open(os.path.join(HERE, "token_cases.json"), "w") as f:
         json.dump(token_cases(R), f, separators=(",", ":"))
