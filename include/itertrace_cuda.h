@@ -163,6 +163,13 @@ int itt_build_token_sequence(itt_ctx* ctx, const itt_records* recs, uint32_t mai
 /* count_interval_overlaps (streams.hpp:212-221) */
 int itt_count_interval_overlaps(itt_ctx* ctx, const itt_records* recs, uint32_t stream, int64_t* out);
 
+/* ------------------------------------------------------- primitives */
+/* Stable LSD onesweep radix sort of (u32 key, u32 value) pairs on key bits [begin_bit, end_bit),
+ * in place.  mem selects host (copied in and out) or device pointers.  The sort behind the
+ * suffix array (K4/K5) and the (start,row) ingest order (K1, ingest.hpp:396-400). */
+int itt_radix_sort_pairs_u32(itt_ctx* ctx, uint32_t* keys, uint32_t* vals, uint64_t n, int begin_bit, int end_bit,
+                             int mem);
+
 /* ------------------------------------------------------- L3 mining (a3-a6) */
 /* Suffix array + LCP of tokens[0..n) followed by a unique terminator `term`:
  * sa[k] = start of the k-th smallest suffix of tokens+[term] (n+1 entries), lcp[0] = 0,

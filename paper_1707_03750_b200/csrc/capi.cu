@@ -10,6 +10,16 @@
 
 using namespace itt;
 
+// onesweep tile shape (radix.cuh kCfgBlock/kCfgItems); ITT_RADIX_CFG overrides for tuning sweeps
+int itt::radix::config_index() {
+  static int cfg = [] {
+    const char* e = std::getenv("ITT_RADIX_CFG");
+    const int v = e ? std::atoi(e) : 0;
+    return (v >= 0 && v < 5) ? v : 0;
+  }();
+  return cfg;
+}
+
 struct itt_ctx {
   Ctx c;
 };
@@ -271,6 +281,34 @@ int itt_count_interval_overlaps(itt_ctx* ctx, const itt_records* recs, uint32_t 
     prepare(c, t, recs, false);
     compact_main(t, stream, false);
     *out = count_overlaps(t);
+  });
+}
+
+// ------------------------------------------------------------------ primitives
+int itt_radix_sort_pairs_u32(itt_ctx* ctx, uint32_t* keys, uint32_t* vals, uint64_t n, int begin_bit, int end_bit,
+                             int mem) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (n == 0) return;
+    if (!keys || !vals || begin_bit < 0 || end_bit > 32 || begin_bit >= end_bit)
+      fail(ITT_E_INVALID_ARGUMENT, "radix_sort: bad arguments");
+    DBuf<uint32_t> k0, v0, k1(c, n), v1(c, n);
+    uint32_t* kp = keys;
+    uint32_t* vp = vals;
+    if (mem != ITT_MEM_DEVICE) {
+      k0.alloc(c, n);
+      v0.alloc(c, n);
+      h2d(c, k0.p, keys, n);
+      h2d(c, v0.p, vals, n);
+      kp = k0.p;
+      vp = v0.p;
+    }
+    radix::Scratch rs;
+    const bool alt = radix_sort_pairs<uint32_t>(c, kp, vp, k1.p, v1.p, n, begin_bit, end_bit, rs);
+    const uint32_t* rk = alt ? k1.p : kp;
+    const uint32_t* rv = alt ? v1.p : vp;
+    const cudaMemcpyKind kind = mem == ITT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (rk != keys) ITT_CUDA(cudaMemcpyAsync(keys, rk, n * 4, kind, c->stream));
+    if (rv != vals) ITT_CUDA(cudaMemcpyAsync(vals, rv, n * 4, kind, c->stream));
   });
 }
 

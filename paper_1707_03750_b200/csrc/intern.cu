@@ -120,6 +120,22 @@ __global__ void k_order_keys(const int64_t* __restrict__ start, uint64_t n, int6
 }
 
 // ------------------------------------------------------------------ K2: dictionary
+// 4 bytes at an arbitrary address from two aligned words (callers keep the read in bounds)
+__device__ __forceinline__ uint32_t load4(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~static_cast<uintptr_t>(3));
+  return __funnelshift_r(w[0], w[1], static_cast<uint32_t>(a & 3) * 8);
+}
+// byte equality of two names (shared or global memory); words while 8 bytes remain, then bytes
+__device__ __forceinline__ bool same_bytes(const uint8_t* p, const uint8_t* q, uint32_t len) {
+  uint32_t i = 0;
+  for (; i + 8 <= len; i += 4)
+    if (load4(p + i) != load4(q + i)) return false;
+  for (; i < len; ++i)
+    if (p[i] != q[i]) return false;
+  return true;
+}
+
 struct HashArgs {
   const uint64_t* name_off;
   const uint8_t* bytes;
@@ -127,18 +143,22 @@ struct HashArgs {
   uint64_t n;
   const uint16_t* device;
   uint64_t* tkey;
-  uint32_t* trep;
+  uint32_t* tfirst_row;  // row of the slot's first inserter (verification representative)
   uint32_t mask;
   uint64_t seed;
   uint32_t* slot_out;
   uint32_t* used;
-  uint32_t* used_count;  // [0] = count, [1] = overflow flag
+  uint32_t* used_count;  // [0] = count, [1] = overflow flag, [2] = collision flag
   unsigned long long* dev_counts;  // [65536]
   uint32_t* dev_max;
 };
 
+// Hash every name (bytes staged per warp in shared memory), insert one key per distinct hash per
+// warp into the open-addressing table, then compare every record's bytes with its slot's first
+// inserter: a mismatch is a true 64-bit collision and raises the collision flag (the host then
+// re-runs with another seed), so a hash never decides equality on its own.
 __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
-  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf];
+  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf + 16];
   __shared__ unsigned int s_dev[kDevSmem];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x) s_dev[i] = 0;
@@ -146,54 +166,66 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
   uint8_t* buf = s_buf[warp];
   const uint64_t groups = (a.n + 31) / 32;
   const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  bool bad = false;
   for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp; g < groups; g += gstride) {
     const uint64_t g0 = g * 32, g1 = min(g0 + 32, a.n);
     const uint64_t row = g0 + lane;
     const bool valid = row < a.n;
     uint64_t base = 0;
     const bool staged = stage_names(a.name_off, a.bytes, a.total, g0, g1, buf, base);
-    uint64_t h = 0;
+    uint64_t h = 0, o = 0;
+    uint32_t len = 0;
+    const uint8_t* mine = nullptr;
     if (valid) {
-      const uint64_t o = a.name_off[row];
-      const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
-      if (staged) {
-        const uint8_t* p = buf + (o - base);
-        h = hash_name([&](uint32_t i) { return p[i]; }, len, a.seed);
-      } else {
-        const uint8_t* p = a.bytes + o;
-        h = hash_name([&](uint32_t i) { return p[i]; }, len, a.seed);
-      }
+      o = a.name_off[row];
+      len = static_cast<uint32_t>(a.name_off[row + 1] - o);
+      mine = staged ? buf + (o - base) : a.bytes + o;
+      h = hash_name([&](uint32_t i) { return mine[i]; }, len, a.seed);
     }
     // one insertion per distinct hash per warp; the lowest lane holds the smallest row
     const unsigned peers = __match_any_sync(0xffffffffu, valid ? h : 0ull);
     const int leader = __ffs(peers) - 1;
-    uint32_t s = 0;
+    uint32_t s = 0, rep = kNone;
     if (valid && static_cast<int>(lane) == leader) {
       s = static_cast<uint32_t>(h) & a.mask;
       for (uint32_t probe = 0;; ++probe) {
         if (probe > a.mask) {
           atomicOr(&a.used_count[1], 1u);
+          rep = static_cast<uint32_t>(row);
           break;
         }
         uint64_t k = ld_relaxed_u64(&a.tkey[s]);
         if (k == 0) {
           const unsigned long long old =
               atomicCAS(reinterpret_cast<unsigned long long*>(&a.tkey[s]), 0ull, static_cast<unsigned long long>(h));
-          if (old == 0) {
-            const uint32_t u = atomicAdd(&a.used_count[0], 1u);
-            a.used[u] = s;
+          if (old == 0) {  // claimed: this row represents the slot
+            rep = static_cast<uint32_t>(row);
+            st_relaxed_u32(&a.tfirst_row[s], rep);
+            a.used[atomicAdd(&a.used_count[0], 1u)] = s;
             break;
           }
           k = old;
         }
-        if (k == h) break;
+        if (k == h) {  // another warp claimed it: wait for its representative row
+          do {
+            rep = ld_relaxed_u32(&a.tfirst_row[s]);
+          } while (rep == kNone);
+          break;
+        }
         s = (s + 1) & a.mask;
       }
-      const uint32_t r = static_cast<uint32_t>(row);
-      if (__ldcg(&a.trep[s]) > r) atomicMin(&a.trep[s], r);
     }
     s = __shfl_sync(0xffffffffu, s, leader);
-    if (valid) a.slot_out[row] = s;
+    rep = __shfl_sync(0xffffffffu, rep, leader);
+    if (valid) {
+      a.slot_out[row] = s;
+      if (rep != row) {
+        const uint64_t ro = a.name_off[rep];
+        const uint32_t rlen = static_cast<uint32_t>(a.name_off[rep + 1] - ro);
+        const uint8_t* theirs = (staged && rep >= g0 && rep < g1) ? buf + (ro - base) : a.bytes + ro;
+        if (rlen != len || !same_bytes(mine, theirs, len)) bad = true;
+      }
+    }
     // device census (filter_majority_device), warp-aggregated
     if (a.device) {
       const uint32_t d = valid ? a.device[row] : 0xFFFFFu;
@@ -206,6 +238,7 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
     }
     __syncwarp();
   }
+  if (bad) atomicOr(&a.used_count[2], 1u);
   __syncthreads();
   if (a.device)
     for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x)
@@ -246,58 +279,16 @@ __global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_u
   tflags[s] = f;
 }
 
-// exactness check: every record's bytes equal its slot representative's bytes; also the
-// per-record kind (classified names + throughput presence)
-struct VerifyArgs {
-  const uint64_t* name_off;
-  const uint8_t* bytes;
-  uint64_t total;
-  uint64_t n;
-  const uint32_t* slot;
-  const uint32_t* trep;
-  const uint8_t* tflags;
-  const uint8_t* rflags;
-  uint8_t* kind;
-  uint32_t* collision;
-};
-
-__global__ void __launch_bounds__(kHashBlock) k_verify(VerifyArgs a) {
-  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf];
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  uint8_t* buf = s_buf[warp];
-  const uint64_t groups = (a.n + 31) / 32;
-  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
-  bool bad = false;
-  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp; g < groups; g += gstride) {
-    const uint64_t g0 = g * 32, g1 = min(g0 + 32, a.n);
-    const uint64_t row = g0 + lane;
-    uint64_t base = 0;
-    const bool staged = stage_names(a.name_off, a.bytes, a.total, g0, g1, buf, base);
-    if (row < a.n) {
-      const uint32_t s = a.slot[row];
-      const uint32_t rep = a.trep[s];
-      if (rep != row) {
-        const uint64_t o = a.name_off[row];
-        const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
-        const uint64_t ro = a.name_off[rep];
-        const uint32_t rlen = static_cast<uint32_t>(a.name_off[rep + 1] - ro);
-        if (len != rlen) {
-          bad = true;
-        } else {
-          const uint8_t* p = staged ? buf + (o - base) : a.bytes + o;
-          const uint8_t* q = a.bytes + ro;
-          for (uint32_t i = 0; i < len; ++i)
-            if (p[i] != q[i]) {
-              bad = true;
-              break;
-            }
-        }
-      }
-      a.kind[row] = static_cast<uint8_t>(kind_from(a.tflags[s], (a.rflags[row] & ITT_REC_HAS_THROUGHPUT) != 0));
-    }
-    __syncwarp();
+// per record: kind from the slot's classify bits and throughput presence; per slot: the smallest
+// row carrying the name (deterministic name_row, whichever warp inserted first)
+__global__ void k_kinds_minrow(const uint32_t* __restrict__ slot, const uint8_t* __restrict__ rflags, uint64_t n,
+                               const uint8_t* __restrict__ tflags, uint8_t* __restrict__ kind, uint32_t* __restrict__ trep) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t s = slot[i];
+    kind[i] = static_cast<uint8_t>(kind_from(__ldg(&tflags[s]), (rflags[i] & ITT_REC_HAS_THROUGHPUT) != 0));
+    if (__ldcg(&trep[s]) > i) atomicMin(&trep[s], static_cast<uint32_t>(i));
   }
-  if (bad) atomicOr(a.collision, 1u);
 }
 
 // ------------------------------------------------------------------ stream census
@@ -627,14 +618,14 @@ void build_dictionary(TraceState& t) {
   if (n) total = read1(c, t.rec.name_off + n);
   t.slot.alloc(c, n);
   t.kind.alloc(c, n);
-  DBuf<uint32_t> counters(c, 4);
+  DBuf<uint32_t> counters(c, 4);  // used count, overflow, collision
   DBuf<unsigned long long> dev_counts;
   DBuf<uint32_t> dev_max(c, 1);
   if (t.rec.device) {
     dev_counts.alloc(c, 65536);
     dev_counts.zero();
   }
-  DBuf<uint32_t> collision(c, 1);
+  DBuf<uint32_t> first_row;
   uint32_t bits = 14;
   uint64_t seed = 0x243F6A8885A308D3ull;
   const unsigned groups = static_cast<unsigned>(std::min<uint64_t>((n + 31) / 32, 1ull << 30));
@@ -643,35 +634,42 @@ void build_dictionary(TraceState& t) {
     const uint32_t cap = 1u << bits;
     t.tkey.alloc(c, cap);
     t.trep.alloc(c, cap);
+    first_row.alloc(c, cap);
     t.tflags.alloc(c, cap);
     t.used.alloc(c, cap);
     t.tkey.zero();
     t.trep.fill_bytes(0xFF);
+    first_row.fill_bytes(0xFF);
     counters.zero();
     dev_max.zero();
-    collision.zero();
     if (t.rec.device) dev_counts.zero();
-    HashArgs ha{t.rec.name_off, t.rec.name_bytes, total, n, t.rec.device, t.tkey.p, t.trep.p, cap - 1, seed,
+    HashArgs ha{t.rec.name_off, t.rec.name_bytes, total, n, t.rec.device, t.tkey.p, first_row.p, cap - 1, seed,
                 t.slot.p,       t.used.p,         counters.p, dev_counts.p, dev_max.p};
-    launch(c, "intern_hash", static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0, ha);
-    uint32_t cnt[2];
-    readback(c, cnt, counters.p, 2);
+    launch(c, "intern_hash", 2.0 * static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0,
+           ha);
+    uint32_t cnt[3];
+    readback(c, cnt, counters.p, 3);
     if (cnt[1] || cnt[0] > cap / 2) {  // table too full: grow and redo
       if (bits >= 30) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: name dictionary overflow");
       bits += 2;
       continue;
     }
+    if (cnt[2]) {  // a true 64-bit collision between different names: new seed
+      if (attempt >= 3) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: unresolvable name hash collision");
+      seed = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+      continue;
+    }
     t.n_used = cnt[0];
     t.table_bits = bits;
-    if (t.n_used)
-      launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(t.n_used, 128)), dim3(128), 0, t.used.p,
-             t.n_used, t.trep.p, t.rec.name_off, t.rec.name_bytes, t.tflags.p);
-    VerifyArgs va{t.rec.name_off, t.rec.name_bytes, total, n, t.slot.p, t.trep.p, t.tflags.p, t.rec.flags, t.kind.p,
-                  collision.p};
-    launch(c, "intern_verify", static_cast<double>(total) + n * 6.0, k_verify, dim3(grid), dim3(kHashBlock), 0, va);
-    if (read1(c, collision.p) == 0) break;
-    if (attempt >= 3) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: unresolvable name hash collision");
-    seed = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;  // a true 64-bit collision: new seed
+    break;
+  }
+  if (t.n_used)
+    launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(t.n_used, 128)), dim3(128), 0, t.used.p,
+           t.n_used, first_row.p, t.rec.name_off, t.rec.name_bytes, t.tflags.p);
+  if (n) {
+    const unsigned g2 = std::min<unsigned>(grid_for(n, 256), c->sm_count * 16);
+    launch(c, "intern_kinds", n * 6.0, k_kinds_minrow, dim3(g2), dim3(256), 0, t.slot.p, t.rec.flags, n, t.tflags.p,
+           t.kind.p, t.trep.p);
   }
   // device census -> majority (ties to the smallest label rank, streams.hpp:187-194)
   t.n_devices = 1;

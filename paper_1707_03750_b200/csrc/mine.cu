@@ -265,20 +265,50 @@ __global__ void k_best_final(const Best* bb, uint32_t nb, Best* out) {
   if (threadIdx.x == 0) *out = b;
 }
 
-// min SA over the intervals tied on the winning (pass, len, count): they are disjoint
+// min SA over the intervals tied on the winning (pass, len, count): they are disjoint.  Small
+// intervals are reduced by the thread that finds them; wide ones are listed for k_tied_wide.
+constexpr uint32_t kTiedSerial = 256;
+constexpr uint32_t kTiedChunk = 4096;
 __global__ void __launch_bounds__(256) k_tied_min_sa(MineArgs a, const uint32_t* __restrict__ lb,
                                                      const uint32_t* __restrict__ sa, const Best* best,
-                                                     unsigned int* __restrict__ result) {
+                                                     unsigned int* __restrict__ result, uint32_t* __restrict__ wide,
+                                                     unsigned int* __restrict__ n_wide) {
   const Best w = *best;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < a.np; k += stride) {
     Best x;
     if (!candidate_key(a, k, x) || x.hi != w.hi || x.lo != w.lo) continue;
     const uint32_t l0 = lb[k], c = a.cnt[k];
+    if (c > kTiedSerial) {
+      const unsigned q = atomicAdd(n_wide, 1u);
+      wide[2 * q] = l0;
+      wide[2 * q + 1] = c;
+      continue;
+    }
     uint32_t m = 0xFFFFFFFFu;
     for (uint32_t q = 0; q < c; ++q) m = min(m, sa[l0 + q]);
     atomicMin(result, m);
   }
+}
+
+// wide tied intervals in kTiedChunk pieces spread over all blocks
+__global__ void __launch_bounds__(256) k_tied_wide(const uint32_t* __restrict__ wide, const unsigned int* __restrict__ n_wide,
+                                                   const uint32_t* __restrict__ sa, unsigned int* __restrict__ result) {
+  const unsigned nw = *n_wide;
+  uint32_t m = 0xFFFFFFFFu;
+  uint64_t chunk0 = 0;  // global chunk numbering across the listed intervals
+  for (unsigned e = 0; e < nw; ++e) {
+    const uint32_t l0 = wide[2 * e], c = wide[2 * e + 1];
+    const uint64_t nch = (c + kTiedChunk - 1) / kTiedChunk;
+    for (uint64_t ch = (blockIdx.x + gridDim.x - chunk0 % gridDim.x) % gridDim.x; ch < nch; ch += gridDim.x) {
+      const uint32_t b = l0 + static_cast<uint32_t>(ch * kTiedChunk);
+      const uint32_t end = l0 + min(c, static_cast<uint32_t>((ch + 1) * kTiedChunk));
+      for (uint32_t q = b + threadIdx.x; q < end; q += blockDim.x) m = min(m, sa[q]);
+    }
+    chunk0 += nch;
+  }
+  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m != 0xFFFFFFFFu) atomicMin(result, m);
 }
 
 }  // namespace
@@ -351,9 +381,15 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
     no_pattern();
     return r;
   }
-  DBuf<unsigned int> start(c, 1);
+  DBuf<unsigned int> start(c, 2);
   start.fill_bytes(0xFF);
-  launch(c, "mine_tied_min_sa", s.np * 12.0, k_tied_min_sa, dim3(grid), dim3(256), 0, a, iv.lb.p, s.sa.p, bb.p + grid, start.p);
+  ITT_CUDA(cudaMemsetAsync(start.p + 1, 0, 4, c->stream));
+  const size_t wide_cap = s.np / (kTiedSerial + 1) + 2;  // disjoint intervals wider than kTiedSerial
+  DBuf<uint32_t> wide(c, 2 * wide_cap);
+  launch(c, "mine_tied_min_sa", s.np * 12.0, k_tied_min_sa, dim3(grid), dim3(256), 0, a, iv.lb.p, s.sa.p, bb.p + grid, start.p,
+         wide.p, start.p + 1);
+  launch(c, "mine_tied_wide", 0.0, k_tied_wide, dim3(static_cast<unsigned>(c->sm_count) * 4), dim3(256), 0, wide.p, start.p + 1,
+         s.sa.p, start.p);
   const uint32_t st = read1(c, start.p);
   const int64_t len = static_cast<int64_t>(best.hi & 0xFFFFFFFFull);
   const int pass = 63 - static_cast<int>(best.hi >> 32);

@@ -1,26 +1,31 @@
 // sa.cu — suffix array by prefix doubling + LCP by phi / chunked Kasai, sm_100a.
 //
 // Replaces the Ukkonen suffix tree (suffix_tree.hpp:21-190, built by mine.hpp:38-40): the
-// tree's leaves in child-key order are the suffixes of tokens+[terminator] in sorted
-// order (SA), internal nodes are the LCP intervals, depth = LCP value, leaf_count =
-// interval width, first_leaf = min SA over the interval.
+// tree's leaves in child-key order are the suffixes of tokens+[terminator] in sorted order
+// (SA); internal nodes are the LCP intervals, depth = LCP value, leaf_count = interval width,
+// first_leaf = min SA over the interval.
 //
-// Doubling (h -> 2h) with group-head ranks:
-//   1. init: key_i = the first k symbols of suffix i packed into 32 bits (k = 32 / bits per
-//      symbol), one onesweep sort, ranks = index of the first suffix of each key group.
-//   2. round h: the sequence E_j = SA_j - h (or SA_j + n' - h for SA_j < h, which are
-//      singletons) lists every suffix i ordered by the rank of i + h.  A STABLE sort of E
-//      by rank_i (b = log2 n' bits, ceil(b/8) passes instead of 2b/8) yields SA ordered by
-//      (rank_i, rank_{i+h}).  New ranks = max-scan of group-start flags (decoupled look-back).
-//   3. stop when every group is a singleton.
-// Every round's rank array is kept: level r identifies equal (k * 2^r)-prefixes, so
-// lcp(i, j) = sum of the levels where the ranks agree (binary lifting) + < k direct compares.
+// Doubling with dense group ids (rank_i = index of i's group among groups in SA order):
+//   init   key_i = the first k symbols of suffix i packed into 32 bits (k = 32 / bits per
+//          symbol); one onesweep sort; ids = inclusive count of group starts - 1.
+//   round  the sequence E_j = SA_j - h (SA_j + n' - h for SA_j < h: those suffixes are
+//          singletons) lists every suffix i in the order of rank_{i+h}.  A STABLE sort of E by
+//          rank_i yields SA ordered by (rank_i, rank_{i+h}).  E is never stored: the first radix
+//          pass gathers rank[E_j] itself (EmitLoader).  Keys need only bits(G-1) bits (G = group
+//          count), so early rounds take 1-2 passes.
+//   update one kernel per round: flags from (rank_i, rank_{i+h}) of adjacent suffixes (the
+//          second key is gathered here), ids by a decoupled look-back sum scan, scatter
+//          rank_new[SA_j], group count, and the digit histograms of the NEXT round's keys
+//          (the ids themselves: a non-decreasing run per thread, so one shared atomic per run).
+//   stop   when G == n'.
+// Every round's id array is kept: level r identifies equal (k * 2^r)-prefixes, so
+// lcp(i, j) = sum of the levels where the ids agree (binary lifting) + < k direct compares.
 //
-// LCP: phi[SA_j] = SA_{j-1}; PLCP by Kasai in chunks of kChunk text positions per thread
-// (each chunk restarts at l = 0); any direct comparison longer than kLiftAfter symbols
-// switches to lifting, so periodic traces (Sum LCP ~ n^2/2) cost O(n log n) at worst;
-// LCP_j = PLCP[SA_j].
+// LCP: phi[SA_j] = SA_{j-1}; PLCP by Kasai in chunks of kChunk text positions per thread (each
+// chunk restarts at l = 0); a direct comparison longer than kLiftAfter symbols switches to
+// lifting, so periodic traces (Sum LCP ~ n^2/2) stay O(n log n); LCP_j = PLCP[SA_j].
 #include <algorithm>
+#include <climits>
 
 #include "pipeline.cuh"
 
@@ -32,6 +37,7 @@ constexpr int kChunk = 64;
 constexpr int kLiftAfter = 24;
 constexpr int kRankBlock = 256;
 constexpr int kRankItems = 8;
+constexpr int kMaxPasses = 4;  // ids < 2^32
 
 __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int* out /*min,max,termhits*/) {
   int mn = INT_MAX, mx = INT_MIN, hits = 0;
@@ -74,83 +80,101 @@ __global__ void k_init_keys(const int32_t* __restrict__ text, uint64_t np, int b
   vals[i] = static_cast<uint32_t>(i);
 }
 
-// E_j: suffix whose (i + h) is SA_j; the h suffixes with i + h >= n' (already singletons) take
-// the slots of SA_j < h.  key = rank_i.
-__global__ void k_emit(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ rank, uint64_t np, uint32_t h,
-                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= np) return;
-  const uint32_t x = sa[j];
-  const uint32_t i = x >= h ? x - h : static_cast<uint32_t>(x + np - h);
-  keys[j] = rank[i];
-  vals[j] = i;
-}
+// first radix pass input of a doubling round: E_j and its key rank_{E_j}
+struct EmitLoader {
+  const uint32_t* sa;
+  const uint32_t* rank;
+  uint64_t np;
+  uint32_t h;
+  __device__ __forceinline__ void operator()(uint64_t j, uint32_t& k, uint32_t& v) const {
+    const uint32_t x = sa[j];
+    const uint32_t i = x >= h ? x - h : static_cast<uint32_t>(x + np - h);
+    k = __ldg(&rank[i]);
+    v = i;
+  }
+};
 
-__global__ void k_second_key(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ rank, uint64_t np, uint32_t h,
-                             uint32_t* __restrict__ r2) {
-  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= np) return;
-  const uint64_t x = static_cast<uint64_t>(sa[j]) + h;
-  r2[j] = x < np ? rank[x] : kNone;
-}
-
-// New group-head ranks: flag_j = (key, r2) differs from j-1; head_j = max-scan(flag ? j : 0);
-// rank_new[SA_j] = head_j.  r2 may be null (init round).  groups += number of flags.
-__global__ void __launch_bounds__(kRankBlock) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ r2,
-                                                            const uint32_t* __restrict__ sa, uint64_t np,
-                                                            uint32_t* __restrict__ rank_new, uint64_t* status, uint32_t* counter,
-                                                            unsigned long long* groups) {
+// New dense ids.  flag_j = (key_j, r2_j) != (key_{j-1}, r2_{j-1}) with key = old id of SA_j (the
+// sorted keys) and r2 = old id of SA_j + h (gathered here; none when SA_j + h >= n' or when
+// rank_old is null in the init round).  id_j = inclusive count of flags - 1 (decoupled look-back
+// sum scan); rank_new[SA_j] = id_j; hist_next[p][digit_p(id_j)] += 1.
+__global__ void __launch_bounds__(kRankBlock) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
+                                                            const uint32_t* __restrict__ rank_old, uint32_t h, uint64_t np,
+                                                            uint32_t* __restrict__ rank_new, uint32_t* __restrict__ hist_next,
+                                                            int passes, uint64_t* status, uint32_t* counter) {
   __shared__ uint32_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile, s_prefix;
-  __shared__ uint32_t s_cnt;
-  if (threadIdx.x == 0) {
-    s_tile = atomicAdd(counter, 1u);
-    s_cnt = 0;
-  }
+  __shared__ uint32_t s_hist[kMaxPasses][256];
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += kRankBlock) (&s_hist[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t base = static_cast<uint64_t>(tile) * (kRankBlock * kRankItems) + static_cast<uint64_t>(threadIdx.x) * kRankItems;
-  uint32_t head[kRankItems];
-  uint32_t run = 0, flags = 0;
-  uint32_t pk = 0, pr = 0;
+  auto second = [&](uint32_t x) -> uint32_t {
+    if (!rank_old) return 0u;
+    const uint64_t y = static_cast<uint64_t>(x) + h;
+    return y < np ? __ldg(&rank_old[y]) : kNone;
+  };
+  uint32_t s_idx[kRankItems];
+  uint32_t cnt[kRankItems];
+  uint32_t pk = 0, pr = 0, run = 0;
   if (base < np && base > 0) {
     pk = keys[base - 1];
-    pr = r2 ? r2[base - 1] : 0;
+    pr = second(sa[base - 1]);
   }
 #pragma unroll
   for (int q = 0; q < kRankItems; ++q) {
     const uint64_t j = base + q;
-    uint32_t v = 0;
     if (j < np) {
+      const uint32_t x = sa[j];
+      s_idx[q] = x;
       const uint32_t k = keys[j];
-      const uint32_t r = r2 ? r2[j] : 0;
-      const bool f = j == 0 || k != pk || r != pr;
-      flags += f;
-      v = f ? static_cast<uint32_t>(j) : 0u;
+      const uint32_t r = second(x);
+      run += (j == 0 || k != pk || r != pr) ? 1u : 0u;
       pk = k;
       pr = r;
     }
-    run = max(run, v);
-    head[q] = run;
+    cnt[q] = run;  // inclusive count within the thread
   }
   uint32_t total;
-  const uint32_t texcl = block_exclusive_scan<uint32_t, MaxOp<uint32_t>, kRankBlock>(run, MaxOp<uint32_t>(), &total, s_warp);
+  const uint32_t texcl = block_exclusive_scan<uint32_t, SumOp<uint32_t>, kRankBlock>(run, SumOp<uint32_t>(), &total, s_warp);
   if (threadIdx.x < 32) {
-    const uint32_t p = tile_lookback<uint32_t, MaxOp<uint32_t>>(status, tile, total, MaxOp<uint32_t>());
+    const uint32_t p = tile_lookback<uint32_t, SumOp<uint32_t>>(status, tile, total, SumOp<uint32_t>());
     if (threadIdx.x == 0) s_prefix = p;
   }
-  // flags count: warp reduce then one shared atomic per warp
-  uint32_t fc = flags;
-  for (int o = 16; o > 0; o >>= 1) fc += __shfl_xor_sync(0xffffffffu, fc, o);
-  if (lane_id() == 0 && fc) atomicAdd(&s_cnt, fc);
   __syncthreads();
-  const uint32_t pre = max(s_prefix, texcl);
+  const uint32_t pre = s_prefix + texcl;
+  // ids are non-decreasing across the thread's items: one shared atomic per run of equal digits
+  uint32_t cur[kMaxPasses], len[kMaxPasses];
+#pragma unroll
+  for (int p = 0; p < kMaxPasses; ++p) cur[p] = kNone, len[p] = 0;
 #pragma unroll
   for (int q = 0; q < kRankItems; ++q) {
     const uint64_t j = base + q;
-    if (j < np) rank_new[sa[j]] = max(pre, head[q]);
+    if (j < np) {
+      const uint32_t id = pre + cnt[q] - 1;
+      rank_new[s_idx[q]] = id;
+#pragma unroll
+      for (int p = 0; p < kMaxPasses; ++p) {
+        if (p >= passes) break;
+        const uint32_t d = (id >> (8 * p)) & 0xFFu;
+        if (d != cur[p]) {
+          if (len[p]) atomicAdd(&s_hist[p][cur[p]], len[p]);
+          cur[p] = d;
+          len[p] = 0;
+        }
+        ++len[p];
+      }
+    }
   }
-  if (threadIdx.x == 0 && s_cnt) atomicAdd(groups, static_cast<unsigned long long>(s_cnt));
+#pragma unroll
+  for (int p = 0; p < kMaxPasses; ++p)
+    if (p < passes && len[p]) atomicAdd(&s_hist[p][cur[p]], len[p]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kRankBlock) {
+    const uint32_t v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(&hist_next[i], v);
+  }
 }
 
 // ---------------------------------------------------------------- LCP
@@ -167,7 +191,7 @@ struct LiftArgs {
   uint32_t h0;
 };
 
-// lcp of suffixes a != b (both < np) by binary lifting over the doubling levels
+// lcp of suffixes a != b by binary lifting over the doubling levels
 __device__ __forceinline__ uint32_t lcp_lift(const LiftArgs& L, uint64_t a, uint64_t b) {
   uint32_t acc = 0;
   for (int r = L.nlev - 1; r >= 0; --r) {
@@ -196,16 +220,13 @@ __global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* _
       continue;
     }
     int steps = 0;
-    bool lifted = false;
     while (i + l < L.np && p + l < L.np && __ldg(&L.text[i + l]) == __ldg(&L.text[p + l])) {
       ++l;
       if (++steps == kLiftAfter) {
         l += lcp_lift(L, i + l, static_cast<uint64_t>(p) + l);
-        lifted = true;
         break;
       }
     }
-    (void)lifted;
     plcp[i] = l;
     if (l > 0) --l;
   }
@@ -249,48 +270,64 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   s.text.alloc(c, np);
   launch(c, "sa_text", np * 8.0, k_text_codes, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, s.text.p);
 
-  DBuf<uint32_t> ka(c, np), kb(c, np), va(c, np), vb(c, np);
+  // five rotating buffers: the current SA plus the sort's (keys, vals) double buffer
+  DBuf<uint32_t> bufs[5];
+  for (auto& b : bufs) b.alloc(c, np);
+  uint32_t* ka = bufs[0].p;
+  uint32_t* va = bufs[1].p;
+  uint32_t* kb = bufs[2].p;
+  uint32_t* vb = bufs[3].p;
+  uint32_t* spare = bufs[4].p;
   launch(c, "sa_init_keys", np * (4.0 * k + 8.0), k_init_keys, dim3(grid_for(np, 256)), dim3(256), 0, s.text.p, np, cbits, k,
-         ka.p, va.p);
+         ka, va);
   const int init_bits = std::min(32, cbits * k);
-  bool alt = radix_sort_pairs<uint32_t>(c, ka.p, va.p, kb.p, vb.p, np, 0, init_bits, rs);
-  uint32_t* keys = alt ? kb.p : ka.p;
-  uint32_t* sa = alt ? vb.p : va.p;
-  uint32_t* keys_o = alt ? ka.p : kb.p;  // the other buffer pair is scratch for the next sort
-  uint32_t* sa_o = alt ? va.p : vb.p;
+  const bool a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs);
+  uint32_t* keys = a0 ? kb : ka;
+  uint32_t* sa = a0 ? vb : va;
+  uint32_t* f1 = a0 ? ka : kb;  // free buffers
+  uint32_t* f2 = a0 ? va : vb;
 
-  DBuf<unsigned long long> groups(c, 1);
+  const int max_passes = (bits_for(np - 1) + 7) / 8;
+  DBuf<uint32_t> hist(c, static_cast<size_t>(kMaxPasses) * 256);
   const uint64_t rtiles = (np + kRankBlock * kRankItems - 1) / (kRankBlock * kRankItems);
-  auto rank_update = [&](const uint32_t* kk, const uint32_t* r2, const uint32_t* ss, uint32_t* rank_new) -> uint64_t {
-    groups.zero();
+  auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, const uint32_t* rank_old, uint32_t h,
+                         uint32_t* rank_new) -> uint64_t {
+    hist.zero();
     scan.prepare(c, rtiles);
-    launch(c, "sa_rank_update", np * (r2 ? 16.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock),
-           0, kk, r2, ss, np, rank_new, scan.buf.p + 1, reinterpret_cast<uint32_t*>(scan.buf.p), groups.p);
-    return read1(c, groups.p);
+    launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
+           dim3(kRankBlock), 0, kk, ss, rank_old, h, np, rank_new, hist.p, max_passes, scan.buf.p + 1,
+           reinterpret_cast<uint32_t*>(scan.buf.p));
+    return scan.total(c);  // group count G (synchronizes)
   };
   s.levels.emplace_back(c, np);
-  uint64_t g = rank_update(keys, nullptr, sa, s.levels.back().p);
-  const int b = bits_for(np - 1);
-  DBuf<uint32_t> r2(c, np);
+  uint64_t g = rank_update(keys, sa, nullptr, 0, s.levels.back().p);
   uint32_t h = s.h0;
   while (g < np) {
     const uint32_t* rank = s.levels.back().p;
-    // E sorted stably by rank_i
-    launch(c, "sa_emit", np * 16.0, k_emit, dim3(grid_for(np, 256)), dim3(256), 0, sa, rank, np, h, keys_o, sa_o);
-    const bool a2 = radix_sort_pairs<uint32_t>(c, keys_o, sa_o, keys, sa, np, 0, b, rs);
-    if (!a2) {  // result landed in (keys_o, sa_o)
-      std::swap(keys, keys_o);
-      std::swap(sa, sa_o);
-    }
-    launch(c, "sa_second_key", np * 12.0, k_second_key, dim3(grid_for(np, 256)), dim3(256), 0, sa, rank, np, h, r2.p);
+    const int b = bits_for(g - 1);
+    const EmitLoader ld{sa, rank, np, h};
+    // the SA buffer is read by the first pass, so the sort only writes the other buffers:
+    // pass 1: loader(sa) -> (f1, f2); pass 2: (f1, f2) -> (kx, vx); pass 3: -> (f1, f2) ...
+    uint32_t* kx = keys;  // the previous round's sorted keys are dead now
+    uint32_t* vx = spare;
+    const bool alt = radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist.p, &ld, false);
+    uint32_t* nkeys = alt ? f1 : kx;
+    uint32_t* nsa = alt ? f2 : vx;
+    uint32_t* other_k = alt ? kx : f1;
+    uint32_t* other_v = alt ? vx : f2;
     s.levels.emplace_back(c, np);
-    g = rank_update(keys, r2.p, sa, s.levels.back().p);
+    g = rank_update(nkeys, nsa, rank, h, s.levels.back().p);
     ++s.rounds;
+    // rotate: new SA / keys; the old SA and the unused pair become free
+    spare = sa;
+    sa = nsa;
+    keys = nkeys;
+    f1 = other_k;
+    f2 = other_v;
     if (static_cast<uint64_t>(h) * 2 > 0xFFFFFFFFull) break;
     h *= 2;
   }
   if (g != np) fail(ITT_E_CUDA, "internal: prefix doubling did not converge");
-  // SA into its own buffer
   s.sa.alloc(c, np);
   ITT_CUDA(cudaMemcpyAsync(s.sa.p, sa, np * 4, cudaMemcpyDeviceToDevice, c->stream));
   if (!want_lcp) return;

@@ -59,6 +59,7 @@ def lib() -> C.CDLL:
         "itt_select_main_stream": ([vp, P(abi.itt_census), P(C.c_uint32), P(C.c_uint32)], C.c_int),
         "itt_build_token_sequence": ([vp, P(abi.itt_records), C.c_uint32, P(P(abi.itt_tokens))], C.c_int),
         "itt_count_interval_overlaps": ([vp, P(abi.itt_records), C.c_uint32, P(C.c_int64)], C.c_int),
+        "itt_radix_sort_pairs_u32": ([vp, vp, vp, C.c_uint64, C.c_int, C.c_int, C.c_int], C.c_int),
         "itt_suffix_array": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, P(C.c_uint32), P(C.c_uint32)], C.c_int),
         "itt_enumerate_repeats": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, C.c_int64, C.c_int64,
                                    P(P(abi.itt_repeat)), P(C.c_uint64)], C.c_int),
@@ -186,6 +187,18 @@ class Context:
 
     def unregister_host(self, arr: np.ndarray):
         self._check(lib().itt_host_unregister(self.h, arr.ctypes.data))
+
+    # ---------------------------------------------------------------- primitives
+    def radix_sort_pairs(self, keys, vals, begin_bit=0, end_bit=32):
+        """Stable sort of (u32 key, u32 value) host arrays; returns sorted copies."""
+        k = np.array(keys, dtype=np.uint32, copy=True)
+        v = np.array(vals, dtype=np.uint32, copy=True)
+        self._check(lib().itt_radix_sort_pairs_u32(self.h, k.ctypes.data, v.ctypes.data, k.shape[0], begin_bit, end_bit,
+                                                   abi.MEM_HOST))
+        return k, v
+
+    def radix_sort_device(self, keys_ptr, vals_ptr, n, begin_bit=0, end_bit=32):
+        self._check(lib().itt_radix_sort_pairs_u32(self.h, keys_ptr, vals_ptr, n, begin_bit, end_bit, abi.MEM_DEVICE))
 
     # ---------------------------------------------------------------- hot path
     def suffix_array(self, tokens, term: int, want_lcp: bool = True):
