@@ -56,6 +56,13 @@ T* host_alloc(size_t n) {
   if (!p) throw std::bad_alloc();
   return p;
 }
+// for outputs the device overwrites completely: no zeroing, so recycled heap pages stay warm
+template <typename T>
+T* host_alloc_uninit(size_t n) {
+  T* p = static_cast<T*>(std::malloc((n ? n : 1) * sizeof(T)));
+  if (!p) throw std::bad_alloc();
+  return p;
+}
 
 void check_records(const itt_records* r) {
   if (!r) fail(ITT_E_INVALID_ARGUMENT, "records: null");
@@ -68,13 +75,23 @@ void check_records(const itt_records* r) {
 void prepare(Ctx* c, TraceState& t, const itt_records* r, bool device_filter) {
   check_records(r);
   t.c = c;
-  upload_records(c, r, t.rec);
-  order_records(t);
-  build_dictionary(t);
+  {
+    StageTimer st(c, "upload");
+    upload_records(c, r, t.rec);
+  }
+  {
+    StageTimer st(c, "order");
+    order_records(t);
+  }
+  {
+    StageTimer st(c, "dictionary");
+    build_dictionary(t);
+  }
   if (!device_filter) {
     t.filtering = false;
     t.kept = t.rec.n;
   }
+  StageTimer st(c, "census");
   stream_census(t);
 }
 
@@ -104,6 +121,15 @@ uint32_t select_main(const std::vector<itt_stream_summary>& ss, uint32_t* n_main
   if (n_main) *n_main = cnt;
   if (!best) fail(ITT_E_NO_MAIN_STREAM, "stream-classify: no stream contains kernel operations");
   return best->stream;
+}
+
+// Mining reads repeats of length <= L_max = (n-1)/iterations only (mine.hpp:64-67), so suffixes need
+// ordering by their first max(L_max) + 1 symbols (sa.cu: capped suffix array / LCP).
+uint32_t mining_cap(uint64_t n, const std::vector<itt_mining_cfg>& cfgs) {
+  int64_t lmax = 0;
+  for (const auto& l : cfgs)
+    if (l.iterations >= 1 && n >= 1) lmax = std::max<int64_t>(lmax, (static_cast<int64_t>(n) - 1) / l.iterations);
+  return static_cast<uint32_t>(std::min<int64_t>(lmax, 0xFFFFFFFEll) + 1);
 }
 
 void tokens_to_device(Ctx* c, const int32_t* tokens, uint64_t n, DBuf<int32_t>& d) {
@@ -361,7 +387,9 @@ int itt_enumerate_repeats(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32
       SuffixState s;
       radix::Scratch rs;
       ScanScratch sc;
-      build_suffix_array(c, dt.p, n, term, s, true, rs, sc);
+      // repeats longer than max_len are cut to max_len: groups by max_len + 1 symbols suffice
+      const uint32_t cap = static_cast<uint32_t>(std::min<int64_t>(max_len, 0xFFFFFFFEll) + 1);
+      build_suffix_array(c, dt.p, n, term, s, true, rs, sc, cap);
       IntervalState iv;
       lcp_intervals(c, s, iv);
       DBuf<itt_repeat> dout(c, s.np);
@@ -403,7 +431,7 @@ int itt_mine_patterns(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t t
     SuffixState s;
     radix::Scratch rs;
     ScanScratch sc;
-    build_suffix_array(c, dt.p, n, term, s, true, rs, sc);
+    build_suffix_array(c, dt.p, n, term, s, true, rs, sc, mining_cap(n, cfgs));
     IntervalState iv;
     lcp_intervals(c, s, iv);
     const auto res = mine_loops(c, s, iv, cfgs, multi != 0);
@@ -481,7 +509,11 @@ int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t*
   if (!rows || !clamps) return ITT_E_INVALID_ARGUMENT;
   *rows = nullptr;
   return guarded(ctx, [&](Ctx* c) {
-    std::vector<itt_iter_row> out;
+    itt_iter_row* o = host_alloc<itt_iter_row>(n_spans);
+    struct Free {
+      itt_iter_row*& p;
+      ~Free() { std::free(p); }
+    } guard{o};
     itt_clamps cl{0, 0};
     if (n_spans > 0) {
       for (uint64_t i = 0; i < n_spans; ++i)
@@ -510,12 +542,11 @@ int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t*
       h2d(c, sp.start.p, s.data(), n_spans);
       h2d(c, sp.end.p, e.data(), n_spans);
       h2d(c, sp.extra.p, x.data(), n_spans);
-      iteration_aggregates(c, ts.p, te.p, n_tokens, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp, out, cl,
+      iteration_aggregates(c, ts.p, te.p, n_tokens, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp, o, cl,
                            t.scan);
     }
-    itt_iter_row* o = host_alloc<itt_iter_row>(out.size());
-    std::memcpy(o, out.data(), out.size() * sizeof(itt_iter_row));
     *rows = o;
+    o = nullptr;  // ownership passes to the caller
     *clamps = cl;
   });
 }
@@ -545,11 +576,15 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
     } else {
       main_stream = select_main(t.streams, &n_main_streams);
     }
-    compact_main(t, main_stream, false);
-    if (t.n_tok == 0)
-      fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
-    renumber_tokens(t);
-    const int64_t overlaps = count_overlaps(t);
+    int64_t overlaps = 0;
+    {
+      StageTimer st(c, "tokens");
+      compact_main(t, main_stream, false);
+      if (t.n_tok == 0)
+        fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
+      renumber_tokens(t);
+      overlaps = count_overlaps(t);
+    }
     // mining over one shared SA / LCP / interval set (pipeline.hpp:81-91)
     std::vector<itt_mining_cfg> cfgs;
     for (uint32_t k = 0; k < opts->n_loops; ++k) cfgs.push_back(itt_mining_cfg{opts->loops[k], opts->epsilon0, 0});
@@ -562,10 +597,18 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
                                          std::to_string(l.iterations) + ")");
     }
     SuffixState s;
-    build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan);
+    {
+      StageTimer st(c, "sa+lcp");
+      build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan,
+                         mining_cap(t.n_tok, cfgs));
+    }
     IntervalState iv;
-    lcp_intervals(c, s, iv);
-    const auto pats = mine_loops(c, s, iv, cfgs, multi);
+    std::vector<MinedPattern> pats;
+    {
+      StageTimer st(c, "mine");
+      lcp_intervals(c, s, iv);
+      pats = mine_loops(c, s, iv, cfgs, multi);
+    }
     for (const auto& p : pats)
       if (p.status) fail(p.status, p.error);
     if (multi)
@@ -605,13 +648,15 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       DBuf<int32_t> dp;
       tokens_to_device(c, p.tokens.data(), p.tokens.size(), dp);
       SpanState sp;
-      approx_match_dev(c, t.tokens.p, t.n_tok, dp.p, p.tokens.size(), L.k0_used, sp, t.scan);
-      std::vector<itt_iter_row> rows;
+      {
+        StageTimer st(c, "match");
+        approx_match_dev(c, t.tokens.p, t.n_tok, dp.p, p.tokens.size(), L.k0_used, sp, t.scan);
+      }
+      StageTimer st(c, "aggregates");
+      L.n_iterations = sp.n;
+      L.rows = host_alloc_uninit<itt_iter_row>(sp.n);
       iteration_aggregates(c, t.tok_start.p, t.tok_end.p, t.n_tok, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp,
-                           rows, L.clamps, t.scan);
-      L.n_iterations = rows.size();
-      L.rows = host_alloc<itt_iter_row>(rows.size());
-      std::memcpy(L.rows, rows.data(), rows.size() * sizeof(itt_iter_row));
+                           L.rows, L.clamps, t.scan);
     }
     *out = a;
     hold.a = nullptr;

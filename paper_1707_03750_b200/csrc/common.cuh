@@ -6,6 +6,9 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <ctime>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -179,13 +182,52 @@ template <typename T>
 inline void d2h(Ctx* c, T* dst, const T* src, size_t count) {
   if (count) ITT_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
 }
+// ITT_TRACE=1: per-stage wall time (synchronizing) and host round-trip counts on stderr
+struct StageTimer {
+  Ctx* c;
+  const char* name;
+  double t0;
+  uint64_t l0;
+  static bool on() {
+    static const bool v = [] {
+      const char* e = std::getenv("ITT_TRACE");
+      return e && *e == '1';
+    }();
+    return v;
+  }
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  static uint64_t& syncs() {
+    static uint64_t s = 0;
+    return s;
+  }
+  StageTimer(Ctx* c_, const char* n) : c(c_), name(n), t0(0), l0(0) {
+    if (on()) {
+      cudaStreamSynchronize(c->stream);
+      t0 = now();
+      l0 = syncs();
+    }
+  }
+  ~StageTimer() {
+    if (on()) {
+      cudaStreamSynchronize(c->stream);
+      std::fprintf(stderr, "[itt] %-14s %8.3f ms  host syncs %llu\n", name, now() - t0,
+                   static_cast<unsigned long long>(syncs() - l0));
+    }
+  }
+};
+
 // read `count` values back through the pinned staging buffer (synchronizes)
 template <typename T>
 inline void readback(Ctx* c, T* dst, const T* src, size_t count) {
+  ++StageTimer::syncs();
   T* st = static_cast<T*>(c->staging(count * sizeof(T)));
   d2h(c, st, src, count);
   c->sync();
-  for (size_t i = 0; i < count; ++i) dst[i] = st[i];
+  std::memcpy(static_cast<void*>(dst), st, count * sizeof(T));
 }
 template <typename T>
 inline T read1(Ctx* c, const T* src) {

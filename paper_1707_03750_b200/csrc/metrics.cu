@@ -167,10 +167,9 @@ __global__ void k_span_aggregates(AggArgs a) {
 
 void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_end, uint64_t n_tok,
                           const int64_t* htod_start, const int64_t* htod_end, const int64_t* htod_size, uint64_t n_htod,
-                          const SpanState& spans, std::vector<itt_iter_row>& rows, itt_clamps& clamps,
+                          const SpanState& spans, itt_iter_row* rows, itt_clamps& clamps,
                           ScanScratch& scan) {
   (void)n_tok;
-  rows.resize(spans.n);
   clamps = itt_clamps{0, 0};
   if (spans.n == 0) return;
   DBuf<int64_t> pmax(c, n_htod + 1);
@@ -194,7 +193,7 @@ void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_e
   const uint64_t threads = spans.n * 32;
   launch(c, "agg_spans", static_cast<double>(n_tok) * 16.0 + spans.n * 96.0, k_span_aggregates, dim3(grid_for(threads, 256)),
          dim3(256), 0, a);
-  d2h(c, rows.data(), drows.p, spans.n);
+  readback(c, rows, drows.p, spans.n);  // one copy: device -> pinned staging -> caller's buffer
   unsigned long long cl[2];
   readback(c, cl, dcl.p, 2);
   clamps.negative_gap_clamps = static_cast<int64_t>(cl[0]);

@@ -88,10 +88,13 @@ struct SuffixState {
   uint32_t h0 = 1;            // prefix length of levels[0]
   int32_t lo = 0;             // text code = token - lo
   int rounds = 0;
+  uint32_t h_final = 0;       // prefix length the last level separates
+  uint32_t cap = 0xFFFFFFFFu; // LCP values are min(lcp, cap); SA exact up to ties of h_final-prefixes
 };
-// tokens: device int32[n]; term: unique terminator
+// tokens: device int32[n]; term: unique terminator.  cap: only the first `cap` symbols matter
+// (mining with max length L_max needs cap = L_max + 1); 0xFFFFFFFF = full suffix array.
 void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
-                        radix::Scratch& rs, ScanScratch& scan);
+                        radix::Scratch& rs, ScanScratch& scan, uint32_t cap = 0xFFFFFFFFu);
 
 // ------------------------------------------------------------------ mining (mine.cu)
 struct IntervalState {
@@ -124,7 +127,7 @@ void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* 
 // ------------------------------------------------------------------ aggregates (metrics.cu)
 void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_end, uint64_t n_tok,
                           const int64_t* htod_start, const int64_t* htod_end, const int64_t* htod_size, uint64_t n_htod,
-                          const SpanState& spans, std::vector<itt_iter_row>& rows, itt_clamps& clamps,
+                          const SpanState& spans, itt_iter_row* rows /* host, spans.n */, itt_clamps& clamps,
                           ScanScratch& scan);
 
 }  // namespace itt

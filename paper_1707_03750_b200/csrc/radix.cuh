@@ -35,8 +35,8 @@ struct ArrayLoader {
   const K* keys;
   const uint32_t* vals;
   __device__ __forceinline__ void operator()(uint64_t i, K& k, uint32_t& v) const {
-    k = keys[i];
-    v = vals[i];
+    k = __ldcs(&keys[i]);  // streaming: evict-first, keeps L2 for the random-access arrays
+    v = __ldcs(&vals[i]);
   }
 };
 
@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep(Loader ld, K* __restrict__ k
     const K k = S.keys[p];
     const uint32_t d = digit_of(k, shift);
     const uint32_t o = S.global_base[d] + (p - S.local_off[d]);
-    keys_out[o] = k;
-    vals_out[o] = S.vals[p];
+    __stcs(&keys_out[o], k);
+    __stcs(&vals_out[o], S.vals[p]);
   }
 }
 

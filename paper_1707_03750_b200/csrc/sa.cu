@@ -36,7 +36,7 @@ namespace {
 constexpr int kChunk = 64;
 constexpr int kLiftAfter = 24;
 constexpr int kRankBlock = 256;
-constexpr int kRankItems = 8;
+constexpr int kRankItems = 16;
 constexpr int kMaxPasses = 4;  // ids < 2^32
 
 __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int* out /*min,max,termhits*/) {
@@ -87,7 +87,7 @@ struct EmitLoader {
   uint64_t np;
   uint32_t h;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t& k, uint32_t& v) const {
-    const uint32_t x = sa[j];
+    const uint32_t x = __ldcs(&sa[j]);
     const uint32_t i = x >= h ? x - h : static_cast<uint32_t>(x + np - h);
     k = __ldg(&rank[i]);
     v = i;
@@ -115,27 +115,44 @@ __global__ void __launch_bounds__(kRankBlock) k_rank_update(const uint32_t* __re
     const uint64_t y = static_cast<uint64_t>(x) + h;
     return y < np ? __ldg(&rank_old[y]) : kNone;
   };
-  uint32_t s_idx[kRankItems];
-  uint32_t cnt[kRankItems];
-  uint32_t pk = 0, pr = 0, run = 0;
+  // phase 1: this thread's SA entries and sorted keys (16-byte loads when the run is whole)
+  uint32_t s_idx[kRankItems], kv[kRankItems], r2[kRankItems];
+  const bool whole = base + kRankItems <= np;
+  if (whole) {
+#pragma unroll
+    for (int q = 0; q < kRankItems; q += 4) {
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(sa + base + q));
+      const uint4 b = __ldcs(reinterpret_cast<const uint4*>(keys + base + q));
+      s_idx[q] = a.x, s_idx[q + 1] = a.y, s_idx[q + 2] = a.z, s_idx[q + 3] = a.w;
+      kv[q] = b.x, kv[q + 1] = b.y, kv[q + 2] = b.z, kv[q + 3] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRankItems; ++q) {
+      s_idx[q] = base + q < np ? sa[base + q] : 0u;
+      kv[q] = base + q < np ? keys[base + q] : 0u;
+    }
+  }
+  // phase 2: every second-key gather in flight before any compare
+  uint32_t pk = 0, pr = 0;
   if (base < np && base > 0) {
     pk = keys[base - 1];
     pr = second(sa[base - 1]);
   }
 #pragma unroll
+  for (int q = 0; q < kRankItems; ++q) r2[q] = base + q < np ? second(s_idx[q]) : 0u;
+  // phase 3: group-start flags as a bit mask (keeps the register footprint to s_idx + mask)
+  uint32_t fmask = 0;
+#pragma unroll
   for (int q = 0; q < kRankItems; ++q) {
     const uint64_t j = base + q;
     if (j < np) {
-      const uint32_t x = sa[j];
-      s_idx[q] = x;
-      const uint32_t k = keys[j];
-      const uint32_t r = second(x);
-      run += (j == 0 || k != pk || r != pr) ? 1u : 0u;
-      pk = k;
-      pr = r;
+      if (j == 0 || kv[q] != pk || r2[q] != pr) fmask |= 1u << q;
+      pk = kv[q];
+      pr = r2[q];
     }
-    cnt[q] = run;  // inclusive count within the thread
   }
+  const uint32_t run = __popc(fmask);
   uint32_t total;
   const uint32_t texcl = block_exclusive_scan<uint32_t, SumOp<uint32_t>, kRankBlock>(run, SumOp<uint32_t>(), &total, s_warp);
   if (threadIdx.x < 32) {
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(kRankBlock) k_rank_update(const uint32_t* __re
   for (int q = 0; q < kRankItems; ++q) {
     const uint64_t j = base + q;
     if (j < np) {
-      const uint32_t id = pre + cnt[q] - 1;
+      const uint32_t id = pre + __popc(fmask & ((2u << q) - 1u)) - 1;
       rank_new[s_idx[q]] = id;
 #pragma unroll
       for (int p = 0; p < kMaxPasses; ++p) {
@@ -207,27 +224,47 @@ __device__ __forceinline__ uint32_t lcp_lift(const LiftArgs& L, uint64_t a, uint
   return acc;
 }
 
-__global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* __restrict__ plcp) {
+// PLCP capped at `cap` over a SA sorted by the first h_final >= cap symbols (a full SA when every
+// group is a singleton).  Suffixes in the same final group share >= h_final symbols: plcp = cap.
+// Kasai's carried bound lcp(i-1, phi) - 1 holds across groups (their order is exact) EXCEPT when it
+// was capped and i opens its group: then the predecessor lies in another group and the scan
+// restarts at 0.  Anything below h_final is exact (direct compares, then lifting).  Proof sketch:
+// the carry needs suffix p+1 (p = phi(i-1)) to precede i with every suffix in between sharing
+// >= lcp(p+1, i) symbols with i; group order is exact, so this can only fail when p+1 and i share
+// a group, i.e. lcp(p, i-1) >= h_final + 1, i.e. i-1 itself took the same-group shortcut.
+__global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* __restrict__ plcp, uint32_t cap) {
   const uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kChunk;
   if (i0 >= L.np) return;
   const uint64_t i1 = min(i0 + kChunk, L.np);
+  const uint32_t* top = L.levels[L.nlev - 1];
   uint32_t l = 0;
+  bool capped = false;
   for (uint64_t i = i0; i < i1; ++i) {
     const uint32_t p = phi[i];
     if (p == kNone) {
       plcp[i] = 0;
       l = 0;
+      capped = false;
       continue;
     }
+    if (__ldg(&top[i]) == __ldg(&top[p])) {  // same final group: lcp >= h_final >= cap
+      plcp[i] = cap;
+      l = cap - 1;
+      capped = true;
+      continue;
+    }
+    if (capped) l = 0;
     int steps = 0;
-    while (i + l < L.np && p + l < L.np && __ldg(&L.text[i + l]) == __ldg(&L.text[p + l])) {
+    while (l < cap && i + l < L.np && p + l < L.np && __ldg(&L.text[i + l]) == __ldg(&L.text[p + l])) {
       ++l;
       if (++steps == kLiftAfter) {
         l += lcp_lift(L, i + l, static_cast<uint64_t>(p) + l);
         break;
       }
     }
+    if (l > cap) l = cap;
     plcp[i] = l;
+    capped = false;  // i-1 and phi(i-1) were in different groups: the carry below stays a valid bound
     if (l > 0) --l;
   }
 }
@@ -241,7 +278,7 @@ __global__ void k_lcp_gather(const uint32_t* __restrict__ sa, const uint32_t* __
 }  // namespace
 
 void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
-                        radix::Scratch& rs, ScanScratch& scan) {
+                        radix::Scratch& rs, ScanScratch& scan, uint32_t cap) {
   const uint64_t np = n + 1;
   if (np >= 0xFFFFFFFFull) fail(ITT_E_INVALID_ARGUMENT, "pattern-mining: sequence too long for 32-bit suffix indices");
   s.n = n;
@@ -301,8 +338,10 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   };
   s.levels.emplace_back(c, np);
   uint64_t g = rank_update(keys, sa, nullptr, 0, s.levels.back().p);
-  uint32_t h = s.h0;
-  while (g < np) {
+  uint32_t h = s.h0;  // prefix length the newest level separates
+  // stop when every suffix is alone, or when the groups already separate `cap` symbols (mining
+  // never looks deeper than its L_max; see k_plcp for why the capped LCP stays exact below cap)
+  while (g < np && h < cap) {
     const uint32_t* rank = s.levels.back().p;
     const int b = bits_for(g - 1);
     const EmitLoader ld{sa, rank, np, h};
@@ -327,7 +366,9 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     if (static_cast<uint64_t>(h) * 2 > 0xFFFFFFFFull) break;
     h *= 2;
   }
-  if (g != np) fail(ITT_E_CUDA, "internal: prefix doubling did not converge");
+  if (g != np && h < cap) fail(ITT_E_CUDA, "internal: prefix doubling did not converge");
+  s.h_final = h;
+  s.cap = g == np ? 0xFFFFFFFFu : cap;
   s.sa.alloc(c, np);
   ITT_CUDA(cudaMemcpyAsync(s.sa.p, sa, np * 4, cudaMemcpyDeviceToDevice, c->stream));
   if (!want_lcp) return;
@@ -341,7 +382,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   h2d(c, dlv.p, lv.data(), lv.size());
   LiftArgs L{s.text.p, np, dlv.p, static_cast<int>(lv.size()), s.h0};
   const uint64_t chunks = (np + kChunk - 1) / kChunk;
-  launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p);
+  launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p, s.cap);
   s.lcp.alloc(c, np);
   launch(c, "lcp_gather", np * 12.0, k_lcp_gather, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, plcp.p, np, s.lcp.p);
   c->sync();  // dlv must outlive the kernels
