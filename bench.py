@@ -40,7 +40,7 @@ WORKLOADS = {
 }
 # bounded CPU samples (same generator and shape, fewer iterations)
 CPU_SAMPLE_ITERS = {"C1": 100, "C2": 10_000, "C3": 400}
-REF_ARM_ITERS = {"C1": 100, "C2": 5_000, "C3": 200}
+REF_ARM_ITERS = {"C1": 100, "C2": 2_000, "C3": 100}  # ~2 s per reference step on one core
 
 
 def log(*a):
@@ -57,9 +57,11 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons every 20 ms; only samples stamped inside the timed
+    window (mark_start/mark_end) are summarised.  The sampler starts before the warm-up so it is
+    producing rows by the time the timed region begins."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -67,11 +69,12 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -80,8 +83,21 @@ class ClockSampler:
         return self
 
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except Exception:
+                ts = time.time()
+            self.rows.append((ts, r[1:]))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(0.05)  # let the last in-window rows arrive
 
     def __exit__(self, *a):
         if self.proc:
@@ -92,12 +108,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        rows = [r for ts, r in self.rows if self.t0 is None or (self.t0 - 0.02 <= ts <= (self.t1 or ts) + 0.02)]
+        ok = [r for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in ok]
+        mx = [float(r[1]) for r in ok if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in ok for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(ok)}
 
 
 def dist_env():
@@ -135,7 +153,7 @@ def cpu_reference_run(config: str, iters: int, steps: int, warmup: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
@@ -203,13 +221,16 @@ def main():
             ms = float(t.item())
         return ms, res
 
+    clk = ClockSampler(dev).__enter__()
     for _ in range(max(3, args.warmup)):
         res = step_device()
     # correctness guard: the mined period must be the planted body
     assert res["loops"][0]["pattern_length"] > 0
     l0 = ctx.launch_count()
-    with ClockSampler(dev) as clk:
-        ms, res = timed(step_device, args.steps)
+    clk.mark_start()
+    ms, res = timed(step_device, args.steps)
+    clk.mark_end()
+    clk.__exit__()
     launches = (ctx.launch_count() - l0) // max(1, args.steps)
     ms_step = ms / args.steps
     value = world * n_events / (ms_step / 1000.0)
