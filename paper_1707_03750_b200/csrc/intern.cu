@@ -142,8 +142,7 @@ struct HashArgs {
   uint64_t total;
   uint64_t n;
   const uint16_t* device;
-  uint64_t* tkey;
-  uint32_t* tfirst_row;  // row of the slot's first inserter (verification representative)
+  uint64_t* tkey;  // (32-bit hash fragment | 1) << 32 | row of the slot's first inserter; 0 = empty
   uint32_t mask;
   uint64_t seed;
   uint32_t* slot_out;
@@ -153,10 +152,27 @@ struct HashArgs {
   uint32_t* dev_max;
 };
 
-// Hash every name (bytes staged per warp in shared memory), insert one key per distinct hash per
-// warp into the open-addressing table, then compare every record's bytes with its slot's first
-// inserter: a mismatch is a true 64-bit collision and raises the collision flag (the host then
-// re-runs with another seed), so a hash never decides equality on its own.
+// 64-bit hash of a name staged in shared memory: 8-byte words from two funnel-shifted aligned
+// loads (the staging buffer is padded, so the word reads stay in bounds)
+__device__ __forceinline__ uint64_t hash_staged(const uint8_t* p, uint32_t len, uint64_t seed) {
+  uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
+  uint32_t i = 0;
+  for (; i + 8 <= len; i += 8) {
+    const uint64_t w = static_cast<uint64_t>(load4(p + i)) | (static_cast<uint64_t>(load4(p + i + 4)) << 32);
+    h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
+  }
+  uint64_t w = 0;
+  for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(p[i + j]) << (8 * j);
+  h = rotl64(h ^ (w * 0x87c37b91114253d5ull + len), 31) * 0x4cf5ad432745937full;
+  h = fmix64(h);
+  return h ? h : 1;  // bit-identical to hash_name (the unstaged path): one name, one hash
+}
+
+// Hash every name (bytes staged per warp in shared memory), find or claim its slot with one 64-bit
+// CAS of (hash fragment, row) — the first inserter's row is the slot representative — then compare
+// every record's bytes with that representative: a mismatch means two different names landed in
+// one slot and raises the collision flag (the host re-runs with another seed), so a hash never
+// decides equality on its own.  Device census: one ballot round per distinct device id in the warp.
 __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
   __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf + 16];
   __shared__ unsigned int s_dev[kDevSmem];
@@ -173,51 +189,34 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
     const bool valid = row < a.n;
     uint64_t base = 0;
     const bool staged = stage_names(a.name_off, a.bytes, a.total, g0, g1, buf, base);
-    uint64_t h = 0, o = 0;
-    uint32_t len = 0;
-    const uint8_t* mine = nullptr;
     if (valid) {
-      o = a.name_off[row];
-      len = static_cast<uint32_t>(a.name_off[row + 1] - o);
-      mine = staged ? buf + (o - base) : a.bytes + o;
-      h = hash_name([&](uint32_t i) { return mine[i]; }, len, a.seed);
-    }
-    // one insertion per distinct hash per warp; the lowest lane holds the smallest row
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? h : 0ull);
-    const int leader = __ffs(peers) - 1;
-    uint32_t s = 0, rep = kNone;
-    if (valid && static_cast<int>(lane) == leader) {
-      s = static_cast<uint32_t>(h) & a.mask;
+      const uint64_t o = a.name_off[row];
+      const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
+      const uint8_t* mine = staged ? buf + (o - base) : a.bytes + o;
+      const uint64_t h = staged ? hash_staged(mine, len, a.seed)
+                                : hash_name([&](uint32_t i) { return mine[i]; }, len, a.seed);
+      const uint64_t frag = ((h >> 32) | 1ull) << 32;  // nonzero: 0 marks an empty slot
+      uint32_t s = static_cast<uint32_t>(h) & a.mask, rep = static_cast<uint32_t>(row);
       for (uint32_t probe = 0;; ++probe) {
         if (probe > a.mask) {
           atomicOr(&a.used_count[1], 1u);
-          rep = static_cast<uint32_t>(row);
           break;
         }
         uint64_t k = ld_relaxed_u64(&a.tkey[s]);
         if (k == 0) {
-          const unsigned long long old =
-              atomicCAS(reinterpret_cast<unsigned long long*>(&a.tkey[s]), 0ull, static_cast<unsigned long long>(h));
-          if (old == 0) {  // claimed: this row represents the slot
-            rep = static_cast<uint32_t>(row);
-            st_relaxed_u32(&a.tfirst_row[s], rep);
+          const unsigned long long mine_key = frag | row;
+          k = atomicCAS(reinterpret_cast<unsigned long long*>(&a.tkey[s]), 0ull, mine_key);
+          if (k == 0) {  // claimed: this row represents the slot
             a.used[atomicAdd(&a.used_count[0], 1u)] = s;
             break;
           }
-          k = old;
         }
-        if (k == h) {  // another warp claimed it: wait for its representative row
-          do {
-            rep = ld_relaxed_u32(&a.tfirst_row[s]);
-          } while (rep == kNone);
+        if ((k & 0xFFFFFFFF00000000ull) == frag) {
+          rep = static_cast<uint32_t>(k);
           break;
         }
         s = (s + 1) & a.mask;
       }
-    }
-    s = __shfl_sync(0xffffffffu, s, leader);
-    rep = __shfl_sync(0xffffffffu, rep, leader);
-    if (valid) {
       a.slot_out[row] = s;
       if (rep != row) {
         const uint64_t ro = a.name_off[rep];
@@ -226,14 +225,19 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
         if (rlen != len || !same_bytes(mine, theirs, len)) bad = true;
       }
     }
-    // device census (filter_majority_device), warp-aggregated
+    // device census (filter_majority_device): one ballot round per distinct id in the warp
     if (a.device) {
-      const uint32_t d = valid ? a.device[row] : 0xFFFFFu;
-      const unsigned dp = __match_any_sync(0xffffffffu, d);
-      if (valid && static_cast<int>(lane) == __ffs(dp) - 1) {
-        if (d < kDevSmem) atomicAdd(&s_dev[d], static_cast<unsigned>(__popc(dp)));
-        else atomicAdd(&a.dev_counts[d], static_cast<unsigned long long>(__popc(dp)));
-        atomicMax(a.dev_max, d);
+      uint32_t d = valid ? a.device[row] : 0xFFFFFu;
+      unsigned todo = __ballot_sync(0xffffffffu, valid);
+      while (todo) {
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(todo) - 1);
+        const unsigned m = __ballot_sync(0xffffffffu, valid && d == d0) & todo;
+        if (lane == static_cast<unsigned>(__ffs(m) - 1)) {
+          if (d0 < kDevSmem) atomicAdd(&s_dev[d0], static_cast<unsigned>(__popc(m)));
+          else atomicAdd(&a.dev_counts[d0], static_cast<unsigned long long>(__popc(m)));
+          atomicMax(a.dev_max, d0);
+        }
+        todo &= ~m;
       }
     }
     __syncwarp();
@@ -261,13 +265,13 @@ __device__ __forceinline__ bool contains_ci(const uint8_t* h, uint32_t hl, const
 }
 
 // classify each distinct name once (trace.hpp:103-113)
-__global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ trep,
+__global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint64_t* __restrict__ tkey,
                                  const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes,
                                  uint8_t* __restrict__ tflags) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n_used) return;
   const uint32_t s = used[u];
-  const uint32_t r = trep[s];
+  const uint32_t r = static_cast<uint32_t>(tkey[s]);  // first inserter's row
   const uint8_t* p = bytes + name_off[r];
   const uint32_t len = static_cast<uint32_t>(name_off[r + 1] - name_off[r]);
   uint8_t f = 0;
@@ -625,7 +629,6 @@ void build_dictionary(TraceState& t) {
     dev_counts.alloc(c, 65536);
     dev_counts.zero();
   }
-  DBuf<uint32_t> first_row;
   uint32_t bits = 14;
   uint64_t seed = 0x243F6A8885A308D3ull;
   const unsigned groups = static_cast<unsigned>(std::min<uint64_t>((n + 31) / 32, 1ull << 30));
@@ -634,17 +637,15 @@ void build_dictionary(TraceState& t) {
     const uint32_t cap = 1u << bits;
     t.tkey.alloc(c, cap);
     t.trep.alloc(c, cap);
-    first_row.alloc(c, cap);
     t.tflags.alloc(c, cap);
     t.used.alloc(c, cap);
     t.tkey.zero();
     t.trep.fill_bytes(0xFF);
-    first_row.fill_bytes(0xFF);
     counters.zero();
     dev_max.zero();
     if (t.rec.device) dev_counts.zero();
-    HashArgs ha{t.rec.name_off, t.rec.name_bytes, total, n, t.rec.device, t.tkey.p, first_row.p, cap - 1, seed,
-                t.slot.p,       t.used.p,         counters.p, dev_counts.p, dev_max.p};
+    HashArgs ha{t.rec.name_off, t.rec.name_bytes, total, n,          t.rec.device, t.tkey.p,  cap - 1,
+                seed,           t.slot.p,         t.used.p, counters.p, dev_counts.p, dev_max.p};
     launch(c, "intern_hash", 2.0 * static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0,
            ha);
     uint32_t cnt[3];
@@ -665,7 +666,7 @@ void build_dictionary(TraceState& t) {
   }
   if (t.n_used)
     launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(t.n_used, 128)), dim3(128), 0, t.used.p,
-           t.n_used, first_row.p, t.rec.name_off, t.rec.name_bytes, t.tflags.p);
+           t.n_used, t.tkey.p, t.rec.name_off, t.rec.name_bytes, t.tflags.p);
   if (n) {
     const unsigned g2 = std::min<unsigned>(grid_for(n, 256), c->sm_count * 16);
     launch(c, "intern_kinds", n * 6.0, k_kinds_minrow, dim3(g2), dim3(256), 0, t.slot.p, t.rec.flags, n, t.tflags.p,

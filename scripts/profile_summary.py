@@ -1,0 +1,61 @@
+"""Turn a round's ncu launch list + full capture into the committed summaries under profiles/.
+Usage: python scripts/profile_summary.py <launches.csv> <prof.ncu-rep> <tag>"""
+import collections, csv, io, json, re, subprocess, sys
+launches, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+rows = list(csv.reader(open(launches)))
+hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+h = rows[hi]
+ki, vi, mi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name"), h.index("Metric Unit")
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows[hi + 1:]:
+    if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+        continue
+    name = re.sub(r"\(.*", "", r[ki]).replace("void ", "")
+    name = re.sub(r"<.*", "", name).split("::")[-1]
+    v = float(r[vi].replace(",", "")) * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3}.get(r[ui], 1e-3)
+    agg[name][0] += 1
+    agg[name][1] += v
+tot = sum(v[1] for v in agg.values())
+out = [f"# {tag}: ncu launch list of `python bench.py --steps 1 --warmup 3` (C2), gpu__time_duration.sum,",
+       "# --clock-control none; cold-cache and serialised per launch: compare SHARES, not absolutes",
+       "kernel,launches,total_us,share"]
+for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    out.append(f"{k},{c},{t:.1f},{t / tot:.4f}")
+open(f"profiles/{tag}_launches_summary.csv", "w").write("\n".join(out) + "\n")
+print("\n".join(out[:16]))
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rr = list(csv.reader(io.StringIO(raw)))
+hdr = rr[0]
+def g(r, k):
+    return float(r[hdr.index(k)]) if k in hdr and r[hdr.index(k)] not in ("", "n/a") else None
+keys = {"duration_us": "gpu__time_duration.sum", "dram_read_MB": "dram__bytes_read.sum", "dram_write_MB": "dram__bytes_write.sum",
+        "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active", "registers": "launch__registers_per_thread",
+        "l2_hit_pct": "lts__t_sector_hit_rate.pct", "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active"}
+names = {"k_onesweep": "radix_onesweep", "k_rank_update": "sa_rank_update", "k_hash_insert": "intern_hash", "k_plcp": "lcp_plcp",
+         "k_ansv": "ansv_intervals", "k_scan": "compact"}
+per = collections.defaultdict(list)
+for r in rr[2:]:
+    full = r[hdr.index("Kernel Name")]
+    base = re.sub(r"<.*", "", re.sub(r"\(.*", "", full).replace("void ", "")).split("::")[-1]
+    nm = names.get(base, base)
+    if "EmitLoader" in full:
+        nm = "radix_onesweep(emit)"
+    d = {k: g(r, m) for k, m in keys.items()}
+    st = sorted(((k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""), g(r, k))
+                 for k in hdr if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")),
+                key=lambda x: -(x[1] or 0))[:4]
+    d["top_stalls"] = {a: b for a, b in st}
+    per[nm].append(d)
+summ = {"source": f"{tag}: ncu --set full --clock-control none --import-source on, bench.py C2 (n'=10,000,017)",
+        "kernels": {}}
+for nm, lst in per.items():
+    avg = {k: sum(x[k] for x in lst) / len(lst) for k in keys if all(x[k] is not None for x in lst)}
+    avg["dram_bytes_per_launch"] = (avg["dram_read_MB"] + avg["dram_write_MB"]) * 1e6
+    avg["launches_profiled"] = len(lst)
+    avg["top_stalls"] = lst[0]["top_stalls"]
+    summ["kernels"][nm] = avg
+json.dump(summ, open("profiles/ncu_summary.json", "w"), indent=1)
+for k, v in summ["kernels"].items():
+    print(f"{k:24s} {v['duration_us']:7.1f}us dram {v['dram_bytes_per_launch']/1e6:6.1f}MB {v['dram_throughput_pct']:4.0f}% warps {v['warps_active_pct']:3.0f}% regs {v['registers']:.0f}")

@@ -116,6 +116,25 @@ def test_build_token_sequence_vs_reference(ctx, R):
     assert e.value.kind == "EmptyMainStream"
 
 
+def test_long_names_staged_and_unstaged_intern_identically(ctx, R):
+    """Warp groups whose names exceed the 4 KiB staging buffer hash from global memory; the same
+    name must get the same id whichever path a record takes (and hash prefixes must not merge)."""
+    rng = np.random.default_rng(5)
+    long = ["L" * 300 + "#%d" % i for i in range(6)]
+    short = ["k%d" % i for i in range(6)]
+    prefix = ["L" * 300 + "#%d" % i + "x" for i in range(3)]  # share 303 bytes with long names
+    ops, t = [], 0
+    for blk in range(400):
+        pool = long + prefix if blk % 3 == 0 else short + long[:2]
+        for _ in range(32):
+            ops.append((13, pool[int(rng.integers(0, len(pool)))], t, 5))
+            t += 7
+    recs = records_from_ops(ops)
+    gt, gri, gn = ctx.build_token_sequence(recs, 13)
+    rt, rri, rn = R.build_token_sequence(recs, 13)
+    assert np.array_equal(gt, rt) and len(gn) == len(rn) == 15
+
+
 def test_token_replay_100k(ctx):
     # test_streams.cpp:204-225
     rng = np.random.default_rng(33)
