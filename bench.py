@@ -37,6 +37,8 @@ WORKLOADS = {
     "C2": ("C2: 10M-event trace, 50K iterations x 200 ops, V=150 (+16 init), 5% memcpy noise on streams 14/15, "
            "rows shuffled in windows of 64", dict(), 50_000),
     "C3": ("C3: 100M-event trace, 20K iterations x 5000 ops, V=4096 (+16 init)", dict(), 20_000),
+    "C4": ("C4: batch of 8192 independent 100K-event traces (500 iterations x 200 ops, V=150 + 16 init), "
+           "sharded across ranks", dict(), 500),
 }
 # bounded CPU samples (same generator and shape, fewer iterations)
 CPU_SAMPLE_ITERS = {"C1": 100, "C2": 10_000, "C3": 400}
@@ -150,6 +152,83 @@ def cpu_reference_run(config: str, iters: int, steps: int, warmup: int):
     return ev, info, sample, times
 
 
+def bench_batch(args, world, rank, local, workload):
+    """C4: every rank analyzes its contiguous shard of the batch; no collective on the data path
+    (a barrier + max-over-ranks time bracket the timed region).  Strong scaling: the batch size is
+    fixed, so per-rank work shrinks as N grows."""
+    import concurrent.futures as cf
+
+    import torch
+    from paper_1707_03750_b200 import batch, cuda as itt, synth
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl")
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    lo, hi = batch.shard_bounds(args.traces, world, rank)
+    pool_ids = sorted({t % args.distinct for t in range(lo, hi)})
+    kw = dict(synth.CONFIGS["C4"])
+
+    def gen(t):
+        return t, synth.generate(**dict(kw, seed=1000 + t))
+    with cf.ThreadPoolExecutor(8) as ex:
+        pool = dict(ex.map(gen, pool_ids))
+    up_ctx = itt.Context(dev)
+    dev_pool = {t: (up_ctx.upload(recs), info) for t, (recs, info) in pool.items()}
+    traces = [dev_pool[t % args.distinct][0] for t in range(args.traces)]  # global index -> resident trace
+    events = sum(dev_pool[t % args.distinct][1]["n"] for t in range(lo, hi))
+    process = batch.cuda_processor(dev)
+    loops_of = lambda i: [500]  # noqa: E731
+
+    def one_pass():
+        return batch.run_shard(traces, loops_of, lo, hi, process, workers=args.workers)
+
+    for _ in range(max(1, args.warmup)):
+        res = one_pass()
+    l0 = sum(c.launch_count() for c in process.contexts)
+
+    def bar():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+    clk = ClockSampler(dev).__enter__()
+    time.sleep(0.3)
+    bar()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.mark_start()
+    e0.record()
+    for _ in range(args.steps):
+        res = one_pass()
+    torch.cuda.synchronize(dev)
+    e1.record()
+    e1.synchronize()
+    clk.mark_end()
+    clk.__exit__()
+    bar()
+    ms = e0.elapsed_time(e1)
+    ev_total = torch.tensor([float(events), ms], device=f"cuda:{dev}")
+    if world > 1:
+        t = ev_total.clone()
+        torch.distributed.all_reduce(ev_total[0:1], op=torch.distributed.ReduceOp.SUM)
+        torch.distributed.all_reduce(t[1:2], op=torch.distributed.ReduceOp.MAX)
+        ev_total[1] = t[1]
+    total_events, ms = float(ev_total[0].item()), float(ev_total[1].item())
+    launches = (sum(c.launch_count() for c in process.contexts) - l0) // max(1, args.steps)
+    ok = all(r["loops"][0]["pattern_length"] == 200 and r["loops"][0]["iterations"] == 500 for r in res)
+    if rank == 0:
+        line = {"metric": METRIC, "value": total_events / (ms / args.steps / 1000.0), "unit": "events/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "config": {"workload": workload, "traces": args.traces, "distinct_traces": args.distinct,
+                           "events_per_step": int(total_events), "workers_per_gpu": args.workers,
+                           "parallelism": f"shard{world}", "mined_ok": bool(ok)},
+                "clocks": clk.summary(), "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -160,6 +239,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
+    ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
+    ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
+    ap.add_argument("--workers", type=int, default=8, help="C4: concurrent streams (host threads) per GPU")
     args = ap.parse_args()
     world, rank, local = dist_env()
     workload, _, iters = WORKLOADS[args.config]
@@ -177,6 +259,9 @@ def main():
                 "e2e": {"value": ev, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
+
+    if args.config == "C4":
+        return bench_batch(args, world, rank, local, workload)
 
     import torch
     if world > 1:

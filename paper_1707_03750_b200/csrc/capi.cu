@@ -160,11 +160,17 @@ int itt_ctx_create(int device, itt_ctx** out) {
     delete x;
     return ITT_E_CUDA;
   }
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  if (cudaMemPoolCreate(&c->pool, &props) != cudaSuccess) {
+    cudaStreamDestroy(c->stream);
+    delete x;
+    return ITT_E_CUDA;
   }
+  uint64_t thr = UINT64_MAX;  // keep freed blocks for reuse across calls
+  cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   *out = x;
   return ITT_OK;
 }
@@ -180,6 +186,7 @@ int itt_ctx_destroy(itt_ctx* ctx) {
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   cudaStreamDestroy(c->stream);
   delete ctx;
   return ITT_OK;

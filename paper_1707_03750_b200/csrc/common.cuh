@@ -57,6 +57,7 @@ struct Ctx {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  cudaMemPool_t pool = nullptr;  // per-context stream-ordered pool (no cross-context lock contention)
   void* pinned = nullptr;  // small staging buffer for scalar readbacks
   size_t pinned_bytes = 0;
 
@@ -156,7 +157,7 @@ struct DBuf {
     release();
     c = ctx;
     n = count;
-    if (count) ITT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->stream));
+    if (count) ITT_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->pool, ctx->stream));
   }
   void release() {
     if (p) cudaFreeAsync(p, c->stream);
