@@ -250,7 +250,11 @@ inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& tr
   o.main_stream = opt.main_stream ? static_cast<int64_t>(*opt.main_stream) : -1;
   itt_analysis* a = nullptr;
   ctx.check(itt_analyze(ctx.get(), &rv, &o, &a));
-  std::unique_ptr<itt_analysis, void (*)(itt_analysis*)> hold(a, [](itt_analysis* x) { itt_free_analysis(nullptr, x); });
+  struct FreeAnalysis {
+    itt_ctx* c;
+    void operator()(itt_analysis* x) const { itt_free_analysis(c, x); }  // rows return to the context's pool
+  };
+  std::unique_ptr<itt_analysis, FreeAnalysis> hold(a, FreeAnalysis{ctx.get()});
 
   AnalysisResult result;
   Report& report = result.report;

@@ -185,6 +185,8 @@ int itt_ctx_destroy(itt_ctx* ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  for (auto& kv : c->out_live) cudaFreeHost(kv.first);  // outputs must be released before this
+  for (auto& kv : c->out_free) cudaFreeHost(kv.second);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->pool) cudaMemPoolDestroy(c->pool);
   cudaStreamDestroy(c->stream);
@@ -194,7 +196,9 @@ int itt_ctx_destroy(itt_ctx* ctx) {
 
 const char* itt_last_error(itt_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
 
-int itt_free(itt_ctx*, void* p) {
+int itt_free(itt_ctx* ctx, void* p) {
+  if (!p) return ITT_OK;
+  if (ctx && ctx->c.out_release(p)) return ITT_OK;  // pinned output block: back to the context
   std::free(p);
   return ITT_OK;
 }
@@ -627,8 +631,10 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
     // per loop: match + aggregates (pipeline.hpp:96-132)
     struct Holder {
       itt_analysis* a = nullptr;
-      ~Holder() { itt_free_analysis(nullptr, a); }
+      itt_ctx* ctx = nullptr;
+      ~Holder() { itt_free_analysis(ctx, a); }
     } hold;
+    hold.ctx = ctx;
     itt_analysis* a = hold.a = host_alloc<itt_analysis>(1);
     fill_census(t, &a->census);
     a->main_stream = main_stream;
@@ -661,7 +667,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       }
       StageTimer st(c, "aggregates");
       L.n_iterations = sp.n;
-      L.rows = host_alloc_uninit<itt_iter_row>(sp.n);
+      L.rows = static_cast<itt_iter_row*>(c->out_alloc(sp.n * sizeof(itt_iter_row)));  // pinned: DMA target
       iteration_aggregates(c, t.tok_start.p, t.tok_end.p, t.n_tok, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp,
                            L.rows, L.clamps, t.scan);
     }
@@ -670,13 +676,13 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
   });
 }
 
-int itt_free_analysis(itt_ctx*, itt_analysis* a) {
+int itt_free_analysis(itt_ctx* ctx, itt_analysis* a) {
   if (!a) return ITT_OK;
   std::free(a->census.streams);
   std::free(a->name_row);
   for (uint32_t k = 0; k < a->n_loops; ++k) {
     std::free(a->loops[k].pattern_tokens);
-    std::free(a->loops[k].rows);
+    itt_free(ctx, a->loops[k].rows);
   }
   std::free(a->loops);
   std::free(a);

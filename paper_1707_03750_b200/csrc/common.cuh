@@ -89,6 +89,31 @@ struct Ctx {
     ITT_CUDA(cudaStreamSynchronize(stream));
     if (!pending.empty()) resolve_profile();
   }
+  // Pinned host blocks for large variable-size outputs (per-iteration rows): the device writes them
+  // directly, and itt_free returns them here for reuse instead of paying cudaMallocHost again.
+  std::map<void*, size_t> out_live;
+  std::multimap<size_t, void*> out_free;
+  void* out_alloc(size_t bytes) {
+    bytes = bytes < 256 ? 256 : bytes;
+    auto it = out_free.lower_bound(bytes);
+    if (it != out_free.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      out_live[p] = it->first;
+      out_free.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    ITT_CUDA(cudaMallocHost(&p, bytes));
+    out_live[p] = bytes;
+    return p;
+  }
+  bool out_release(void* p) {
+    auto it = out_live.find(p);
+    if (it == out_live.end()) return false;
+    out_free.emplace(it->second, p);
+    out_live.erase(it);
+    return true;
+  }
   void* staging(size_t bytes) {
     if (bytes > pinned_bytes) {
       if (pinned) cudaFreeHost(pinned);

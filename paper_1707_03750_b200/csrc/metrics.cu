@@ -193,9 +193,9 @@ void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_e
   const uint64_t threads = spans.n * 32;
   launch(c, "agg_spans", static_cast<double>(n_tok) * 16.0 + spans.n * 96.0, k_span_aggregates, dim3(grid_for(threads, 256)),
          dim3(256), 0, a);
-  readback(c, rows, drows.p, spans.n);  // one copy: device -> pinned staging -> caller's buffer
+  d2h(c, rows, drows.p, spans.n);  // straight into the caller's (pinned) buffer
   unsigned long long cl[2];
-  readback(c, cl, dcl.p, 2);
+  readback(c, cl, dcl.p, 2);  // synchronizes
   clamps.negative_gap_clamps = static_cast<int64_t>(cl[0]);
   clamps.negative_interval_clamps = static_cast<int64_t>(cl[1]);
 }

@@ -295,35 +295,52 @@ class Context:
         return out, (cl.negative_gap_clamps, cl.negative_interval_clamps)
 
     def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1) -> dict:
-        """itt_analyze: device pipeline up to the per-loop integer aggregates."""
+        """itt_analyze: device pipeline up to the per-loop integer aggregates.  The per-iteration
+        rows are zero-copy numpy views of the library's pinned output blocks; the analysis is
+        released (blocks back to the context) when the last view is dropped."""
         c = recs.c()
         lp = (C.c_int64 * max(1, len(loops)))(*loops)
         opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream)
         out = P(abi.itt_analysis)()
         self._check(lib().itt_analyze(self.h, C.byref(c), C.byref(opts), C.byref(out)))
+        owner = _AnalysisOwner(self, out)
+        a = out[0]
+        res = dict(
+            streams=[(s.stream, s.cls, tuple(s.counts[k] for k in range(6)), s.first_start, s.last_end)
+                     for s in (a.census.streams[i] for i in range(a.census.n_streams))],
+            n_devices=a.census.n_devices, majority_device=a.census.majority_device,
+            dropped=a.census.dropped_records, main_stream=a.main_stream, n_main_streams=a.n_main_streams,
+            override_non_main=bool(a.main_stream_override_non_main), n_tokens=a.n_tokens, n_names=a.n_names,
+            name_row=[a.name_row[i] for i in range(a.n_names)], overlapping_kernels=a.overlapping_kernels,
+            loops=[])
+        for k in range(a.n_loops):
+            L = a.loops[k]
+            if L.n_iterations:
+                buf = (C.c_int64 * (L.n_iterations * 11)).from_address(C.cast(L.rows, C.c_void_p).value)
+                buf._owner = owner  # keeps the analysis (and the context) alive while views exist
+                rows = np.frombuffer(buf, dtype=np.int64).reshape(L.n_iterations, 11)
+            else:
+                rows = np.zeros((0, 11), np.int64)
+            res["loops"].append(dict(
+                iterations_declared=L.iterations_declared, pattern_length=L.pattern_length,
+                pattern_tokens=[L.pattern_tokens[j] for j in range(L.pattern_length)],
+                pattern_count=L.pattern_count, epsilon_used=L.epsilon_used, first_token=L.first_token,
+                k0_used=L.k0_used, rows=rows,
+                clamps=(L.clamps.negative_gap_clamps, L.clamps.negative_interval_clamps)))
+        return res
+
+
+class _AnalysisOwner:
+    def __init__(self, ctx: Context, ptr):
+        self.ctx = ctx
+        self.ptr = ptr
+
+    def __del__(self):
         try:
-            a = out[0]
-            res = dict(
-                streams=[(s.stream, s.cls, tuple(s.counts[k] for k in range(6)), s.first_start, s.last_end)
-                         for s in (a.census.streams[i] for i in range(a.census.n_streams))],
-                n_devices=a.census.n_devices, majority_device=a.census.majority_device,
-                dropped=a.census.dropped_records, main_stream=a.main_stream, n_main_streams=a.n_main_streams,
-                override_non_main=bool(a.main_stream_override_non_main), n_tokens=a.n_tokens, n_names=a.n_names,
-                name_row=[a.name_row[i] for i in range(a.n_names)], overlapping_kernels=a.overlapping_kernels,
-                loops=[])
-            for k in range(a.n_loops):
-                L = a.loops[k]
-                rows = np.ctypeslib.as_array(C.cast(L.rows, P(C.c_int64)), shape=(L.n_iterations, 11)).copy() \
-                    if L.n_iterations else np.zeros((0, 11), np.int64)
-                res["loops"].append(dict(
-                    iterations_declared=L.iterations_declared, pattern_length=L.pattern_length,
-                    pattern_tokens=[L.pattern_tokens[j] for j in range(L.pattern_length)],
-                    pattern_count=L.pattern_count, epsilon_used=L.epsilon_used, first_token=L.first_token,
-                    k0_used=L.k0_used, rows=rows,
-                    clamps=(L.clamps.negative_gap_clamps, L.clamps.negative_interval_clamps)))
-            return res
-        finally:
-            lib().itt_free_analysis(self.h, out)
+            if self.ctx.h:  # after close() the context already released its pinned blocks
+                lib().itt_free_analysis(self.ctx.h, self.ptr)
+        except Exception:
+            pass
 
 
 # column order of analyze_raw()["loops"][k]["rows"] (itt_iter_row as int64 words; the last word
