@@ -110,6 +110,73 @@ __global__ void k_order_stats(const int64_t* __restrict__ start, uint64_t n, uns
   }
 }
 
+// Sort each 256-row block by (start, row) — rank = number of block rows ordered before this one,
+// unique because the row breaks ties, so the result is the stable order — and record the block's
+// start range, the descent count of the source order and the global min/max start.
+constexpr int kOrderBlock = 256;
+__global__ void __launch_bounds__(kOrderBlock) k_order_block_sort(const int64_t* __restrict__ start, uint64_t n,
+                                                                  uint32_t* __restrict__ perm, int64_t* __restrict__ bmin,
+                                                                  int64_t* __restrict__ bmax, unsigned long long* stats) {
+  __shared__ long long s[kOrderBlock];
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kOrderBlock;
+  const uint32_t len = static_cast<uint32_t>(umin64(kOrderBlock, n - base));
+  const uint32_t t = threadIdx.x;
+  const long long me = t < len ? start[base + t] : LLONG_MAX;
+  s[t] = me;
+  __shared__ uint32_t r[kOrderBlock];  // row offsets; padding rows (t >= len) sort last
+  r[t] = t;
+  __syncthreads();
+  unsigned desc = 0;
+  if (t < len) {
+    desc = t > 0 && s[t - 1] > me;
+    if (t == 0 && base > 0 && start[base - 1] > me) desc = 1;
+  }
+  __syncthreads();
+  // bitonic network on (start, row): keys are unique, so the result is the stable order
+  for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t p = t ^ j;
+      if (p > t) {
+        const long long a = s[t], b = s[p];
+        const uint32_t ra = r[t], rb = r[p];
+        const bool a_gt_b = a > b || (a == b && ra > rb);
+        if (((t & k) == 0) == a_gt_b) {  // ascending in the lower half of each k-run, descending above
+          s[t] = b, s[p] = a;
+          r[t] = rb, r[p] = ra;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (t < len) perm[base + t] = static_cast<uint32_t>(base + r[t]);
+  long long mn = me, mx = t < len ? me : LLONG_MIN;
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const unsigned d = __reduce_add_sync(0xffffffffu, desc);
+  __shared__ long long wmn[kOrderBlock / 32], wmx[kOrderBlock / 32];
+  __shared__ unsigned wd[kOrderBlock / 32];
+  if (lane_id() == 0) wmn[t >> 5] = mn, wmx[t >> 5] = mx, wd[t >> 5] = d;
+  __syncthreads();
+  if (t == 0) {
+    unsigned dd = 0;
+    for (int w = 0; w < kOrderBlock / 32; ++w) mn = min(mn, wmn[w]), mx = max(mx, wmx[w]), dd += wd[w];
+    bmin[blockIdx.x] = mn;
+    bmax[blockIdx.x] = mx;
+    atomicMin(reinterpret_cast<long long*>(&stats[0]), mn);
+    atomicMax(reinterpret_cast<long long*>(&stats[1]), mx);
+    if (dd) atomicAdd(&stats[2], static_cast<unsigned long long>(dd));
+  }
+}
+
+// block b's largest start must not exceed block b+1's smallest (equal starts stay in row order)
+__global__ void k_order_check(const int64_t* __restrict__ bmin, const int64_t* __restrict__ bmax, uint64_t nb,
+                              unsigned long long* bad) {
+  const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b + 1 < nb && bmax[b] > bmin[b + 1]) atomicAdd(bad, 1ull);
+}
+
 __global__ void k_order_keys(const int64_t* __restrict__ start, uint64_t n, int64_t mn, uint64_t* __restrict__ keys,
                              uint32_t* __restrict__ vals) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -596,15 +663,25 @@ void order_records(TraceState& t) {
   const uint64_t n = t.rec.n;
   t.sorted = true;
   if (n <= 1 || t.rec.order == ITT_ORDER_SORTED) return;
-  DBuf<unsigned long long> st(c, 3);
-  unsigned long long init[3] = {static_cast<unsigned long long>(LLONG_MAX), static_cast<unsigned long long>(LLONG_MIN), 0};
-  h2d(c, st.p, init, 3);
-  const unsigned grid = std::min<unsigned>(grid_for(n, 256), c->sm_count * 8);
-  launch(c, "order_stats", n * 8.0, k_order_stats, dim3(grid), dim3(256), 0, t.rec.start, n, st.p);
-  unsigned long long h[3];
-  readback(c, h, st.p, 3);
+  // fast path: sort 256-row blocks locally; if block ranges do not overlap the result is global
+  const uint64_t nb = (n + kOrderBlock - 1) / kOrderBlock;
+  DBuf<unsigned long long> st(c, 4);  // min, max, descents, overlapping block boundaries
+  unsigned long long init[4] = {static_cast<unsigned long long>(LLONG_MAX), static_cast<unsigned long long>(LLONG_MIN), 0, 0};
+  h2d(c, st.p, init, 4);
+  DBuf<uint32_t> perm(c, n);
+  DBuf<int64_t> bmin(c, nb), bmax(c, nb);
+  launch(c, "order_blocks", n * 12.0, k_order_block_sort, dim3(static_cast<unsigned>(nb)), dim3(kOrderBlock), 0, t.rec.start, n,
+         perm.p, bmin.p, bmax.p, st.p);
+  launch(c, "order_check", nb * 16.0, k_order_check, dim3(grid_for(nb, 256)), dim3(256), 0, bmin.p, bmax.p, nb, st.p + 3);
+  unsigned long long h[4];
+  readback(c, h, st.p, 4);
   if (h[2] == 0) return;  // already in (start,row) order
   t.sorted = false;
+  if (h[3] == 0) {  // locally shuffled rows (the usual profiler export): the block sort is the order
+    t.perm = std::move(perm);
+    return;
+  }
+  perm.release();
   const int64_t mn = static_cast<int64_t>(h[0]), mx = static_cast<int64_t>(h[1]);
   const int bits = bits_for(static_cast<uint64_t>(mx - mn));
   DBuf<uint64_t> k0(c, n), k1(c, n);

@@ -102,6 +102,33 @@ def test_match_greedy_skip_semantics(ctx, R):
 
 
 # ---------------------------------------------------------------- records level
+def test_row_order_fast_path_and_fallback(ctx, R):
+    """(start,row) ordering: already sorted, locally shuffled (block fast path), globally shuffled
+    (radix fallback), and heavy start ties across block boundaries (stability)."""
+    rng = np.random.default_rng(21)
+    n = 5000
+    base = np.sort(rng.integers(0, 4000, n))  # many equal starts
+    variants = {"sorted": base.copy()}
+    loc = base.copy()
+    for b in range(0, n, 64):
+        seg = loc[b:b + 64].copy()
+        rng.shuffle(seg)
+        loc[b:b + 64] = seg
+    variants["local"] = loc
+    glob = base.copy()
+    rng.shuffle(glob)
+    variants["global"] = glob
+    variants["ties"] = np.repeat(np.arange(n // 500), 500)[::-1].copy()
+    for name, starts in variants.items():
+        ops = [(13 if i % 3 else 14, "op%d" % (i % 17) if i % 3 else "[CUDA memcpy HtoD]", int(s), 3, 64, 1e9)
+               for i, s in enumerate(starts)]
+        recs = records_from_ops(ops)
+        gt, gri, _ = ctx.build_token_sequence(recs, 13)
+        rt, rri, _ = R.build_token_sequence(recs, 13)
+        assert np.array_equal(gt, rt) and np.array_equal(gri, rri), name
+        assert ctx.summarize_streams(recs)[0] == R.summarize_streams(recs)[0], name
+
+
 def test_build_token_sequence_vs_reference(ctx, R):
     for kw in (dict(), dict(noise_frac=0.05, shuffle_window=64, seed=11), dict(minority_frac=0.1, seed=12),
                dict(vocab=2000, body_len=3000, iterations=20, seed=5)):
