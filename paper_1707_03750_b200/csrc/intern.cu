@@ -21,7 +21,8 @@ namespace itt {
 
 namespace {
 
-constexpr int kHashBlock = 256;
+constexpr int kHashBlock = 128;
+constexpr int kRepScratch = 128;  // per-lane staging of the slot representative's name
 constexpr int kWarpBuf = 4096;  // staged name bytes per warp
 constexpr uint32_t kDevSmem = 64;
 constexpr uint32_t kStreamTableCap = 4096;
@@ -75,13 +76,16 @@ __device__ __forceinline__ bool stage_names(const uint64_t* __restrict__ name_of
   const uint64_t a0 = b0 & ~15ull, a1 = (b1 + 15) & ~15ull;
   if (a1 - a0 > static_cast<uint64_t>(kWarpBuf)) return false;
   const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
+  // all 16-byte chunks in flight at once (cp.async, L2-only: the names are streamed once)
   for (uint64_t o = a0 + lane_id() * 16; o < a1; o += 512) {
     if (aligned && o + 16 <= total) {
-      *reinterpret_cast<uint4*>(buf + (o - a0)) = __ldg(reinterpret_cast<const uint4*>(bytes + o));
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + (o - a0)));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(bytes + o) : "memory");
     } else {
       for (int j = 0; j < 16; ++j) buf[o - a0 + j] = o + j < total ? bytes[o + j] : 0;
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
   base = a0;
   return true;
@@ -188,18 +192,46 @@ __global__ void k_order_keys(const int64_t* __restrict__ start, uint64_t n, int6
 
 // ------------------------------------------------------------------ K2: dictionary
 // 4 bytes at an arbitrary address from two aligned words (callers keep the read in bounds)
-__device__ __forceinline__ uint32_t load4(const uint8_t* p) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~static_cast<uintptr_t>(3));
-  return __funnelshift_r(w[0], w[1], static_cast<uint32_t>(a & 3) * 8);
-}
-// byte equality of two names (shared or global memory); words while 8 bytes remain, then bytes
-__device__ __forceinline__ bool same_bytes(const uint8_t* p, const uint8_t* q, uint32_t len) {
+// explicit address spaces: an address rebuilt from an integer would otherwise compile to a
+// generic LD (long-scoreboard, LSU path) even when it points into shared memory
+struct SharedBytes {
+  uint32_t base;  // shared-window address
+  __device__ __forceinline__ explicit SharedBytes(const uint8_t* p)
+      : base(static_cast<uint32_t>(__cvta_generic_to_shared(p))) {}
+  __device__ __forceinline__ uint32_t word(uint32_t a) const {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  __device__ __forceinline__ uint32_t load4(uint32_t i) const {
+    const uint32_t a = base + i;
+    return __funnelshift_r(word(a & ~3u), word((a & ~3u) + 4), (a & 3) * 8);
+  }
+  __device__ __forceinline__ uint8_t byte(uint32_t i) const {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(base + i));
+    return static_cast<uint8_t>(v);
+  }
+};
+struct GlobalBytes {
+  const uint8_t* p;
+  __device__ __forceinline__ explicit GlobalBytes(const uint8_t* q) : p(q) {}
+  __device__ __forceinline__ uint32_t load4(uint32_t i) const {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p + i);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~static_cast<uintptr_t>(3));
+    return __funnelshift_r(__ldg(w), __ldg(w + 1), static_cast<uint32_t>(a & 3) * 8);
+  }
+  __device__ __forceinline__ uint8_t byte(uint32_t i) const { return __ldg(p + i); }
+};
+// byte equality of two names; words while 8 bytes remain (keeps the aligned-word reads inside
+// the name's buffer), then bytes
+template <typename A, typename B>
+__device__ __forceinline__ bool same_bytes(const A& p, const B& q, uint32_t len) {
   uint32_t i = 0;
   for (; i + 8 <= len; i += 4)
-    if (load4(p + i) != load4(q + i)) return false;
+    if (p.load4(i) != q.load4(i)) return false;
   for (; i < len; ++i)
-    if (p[i] != q[i]) return false;
+    if (p.byte(i) != q.byte(i)) return false;
   return true;
 }
 
@@ -221,15 +253,15 @@ struct HashArgs {
 
 // 64-bit hash of a name staged in shared memory: 8-byte words from two funnel-shifted aligned
 // loads (the staging buffer is padded, so the word reads stay in bounds)
-__device__ __forceinline__ uint64_t hash_staged(const uint8_t* p, uint32_t len, uint64_t seed) {
+__device__ __forceinline__ uint64_t hash_staged(const SharedBytes& p, uint32_t len, uint64_t seed) {
   uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
   uint32_t i = 0;
   for (; i + 8 <= len; i += 8) {
-    const uint64_t w = static_cast<uint64_t>(load4(p + i)) | (static_cast<uint64_t>(load4(p + i + 4)) << 32);
+    const uint64_t w = static_cast<uint64_t>(p.load4(i)) | (static_cast<uint64_t>(p.load4(i + 4)) << 32);
     h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
   }
   uint64_t w = 0;
-  for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(p[i + j]) << (8 * j);
+  for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(p.byte(i + j)) << (8 * j);
   h = rotl64(h ^ (w * 0x87c37b91114253d5ull + len), 31) * 0x4cf5ad432745937full;
   h = fmix64(h);
   return h ? h : 1;  // bit-identical to hash_name (the unstaged path): one name, one hash
@@ -242,6 +274,7 @@ __device__ __forceinline__ uint64_t hash_staged(const uint8_t* p, uint32_t len, 
 // decides equality on its own.  Device census: one ballot round per distinct device id in the warp.
 __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
   __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf + 16];
+  __shared__ __align__(16) uint8_t s_rep[kHashBlock / 32][32][kRepScratch + 16];
   __shared__ unsigned int s_dev[kDevSmem];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x) s_dev[i] = 0;
@@ -259,9 +292,9 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
     if (valid) {
       const uint64_t o = a.name_off[row];
       const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
-      const uint8_t* mine = staged ? buf + (o - base) : a.bytes + o;
-      const uint64_t h = staged ? hash_staged(mine, len, a.seed)
-                                : hash_name([&](uint32_t i) { return mine[i]; }, len, a.seed);
+      // separate shared / global paths so the staged case compiles to LDS, not generic loads
+      const uint64_t h = staged ? hash_staged(SharedBytes(buf + (o - base)), len, a.seed)
+                                : hash_name([&](uint32_t i) { return a.bytes[o + i]; }, len, a.seed);
       const uint64_t frag = ((h >> 32) | 1ull) << 32;  // nonzero: 0 marks an empty slot
       uint32_t s = static_cast<uint32_t>(h) & a.mask, rep = static_cast<uint32_t>(row);
       for (uint32_t probe = 0;; ++probe) {
@@ -288,8 +321,29 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
       if (rep != row) {
         const uint64_t ro = a.name_off[rep];
         const uint32_t rlen = static_cast<uint32_t>(a.name_off[rep + 1] - ro);
-        const uint8_t* theirs = (staged && rep >= g0 && rep < g1) ? buf + (ro - base) : a.bytes + ro;
-        if (rlen != len || !same_bytes(mine, theirs, len)) bad = true;
+        bool same = rlen == len;
+        if (same) {
+          const uint64_t q0 = ro & ~15ull, q1 = (ro + len + 15) & ~15ull;
+          const bool aligned = (reinterpret_cast<uintptr_t>(a.bytes) & 15) == 0;
+          if (staged && rep >= g0 && rep < g1) {
+            same = same_bytes(SharedBytes(buf + (o - base)), SharedBytes(buf + (ro - base)), len);
+          } else if (staged && aligned && q1 - q0 <= kRepScratch && q1 <= a.total) {
+            // the representative's bytes into this lane's scratch in one round trip (cp.async),
+            // then a shared-to-shared compare instead of a chain of dependent global loads
+            uint8_t* scr = s_rep[warp][lane];
+            for (uint64_t q = q0; q < q1; q += 16) {
+              const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(scr + (q - q0)));
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.bytes + q) : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            same = same_bytes(SharedBytes(buf + (o - base)), SharedBytes(scr + (ro - q0)), len);
+          } else if (staged) {
+            same = same_bytes(SharedBytes(buf + (o - base)), GlobalBytes(a.bytes + ro), len);
+          } else {
+            same = same_bytes(GlobalBytes(a.bytes + o), GlobalBytes(a.bytes + ro), len);
+          }
+        }
+        if (!same) bad = true;
       }
     }
     // device census (filter_majority_device): one ballot round per distinct id in the warp
@@ -709,7 +763,9 @@ void build_dictionary(TraceState& t) {
   uint32_t bits = 14;
   uint64_t seed = 0x243F6A8885A308D3ull;
   const unsigned groups = static_cast<unsigned>(std::min<uint64_t>((n + 31) / 32, 1ull << 30));
-  const unsigned grid = std::max(1u, std::min<unsigned>((groups + 7) / 8, c->sm_count * 8));
+  constexpr unsigned kWarpsPerBlock = kHashBlock / 32;
+  const unsigned grid =
+      std::max(1u, std::min<unsigned>((groups + kWarpsPerBlock - 1) / kWarpsPerBlock, c->sm_count * 12));
   for (int attempt = 0;; ++attempt) {
     const uint32_t cap = 1u << bits;
     t.tkey.alloc(c, cap);
