@@ -338,7 +338,10 @@ def main():
     prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_json):
         try:
-            traffic = json.load(open(prof_json)).get("kernels", {}).get(name, {}).get("dram_bytes_per_launch")
+            pj = json.load(open(prof_json))
+            # ncu bytes only describe the workload they were captured on
+            if pj.get("workload") == args.config:
+                traffic = pj.get("kernels", {}).get(name, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,

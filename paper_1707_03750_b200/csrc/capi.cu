@@ -487,7 +487,7 @@ int itt_approx_match(itt_ctx* ctx, const int32_t* tokens, uint64_t n, const int3
       tokens_to_device(c, tokens, n, dt);
       tokens_to_device(c, pattern, m, dp);
       ScanScratch sc;
-      approx_match_dev(c, dt.p, n, dp.p, m, k0, sp, sc);
+      approx_match_dev(c, dt.p, n, dp.p, pattern[0], m, k0, sp, sc);
     }
     std::vector<uint32_t> s(sp.n), e(sp.n), x(sp.n);
     d2h(c, s.data(), sp.start.p, sp.n);
@@ -553,7 +553,8 @@ int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t*
       h2d(c, sp.start.p, s.data(), n_spans);
       h2d(c, sp.end.p, e.data(), n_spans);
       h2d(c, sp.extra.p, x.data(), n_spans);
-      iteration_aggregates(c, ts.p, te.p, n_tokens, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp, o, cl,
+      iteration_aggregates(c, ts.p, te.p, n_tokens, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod,
+                           t.htod_range.p, sp, o, cl,
                            t.scan);
     }
     *rows = o;
@@ -611,7 +612,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
     {
       StageTimer st(c, "sa+lcp");
       build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan,
-                         mining_cap(t.n_tok, cfgs));
+                         mining_cap(t.n_tok, cfgs), /*known_alphabet=*/true);
     }
     IntervalState iv;
     std::vector<MinedPattern> pats;
@@ -663,12 +664,14 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       SpanState sp;
       {
         StageTimer st(c, "match");
-        approx_match_dev(c, t.tokens.p, t.n_tok, dp.p, p.tokens.size(), L.k0_used, sp, t.scan);
+        approx_match_dev(c, t.tokens.p, t.n_tok, dp.p, p.tokens.empty() ? 0 : p.tokens[0], p.tokens.size(), L.k0_used, sp,
+                         t.scan);
       }
       StageTimer st(c, "aggregates");
       L.n_iterations = sp.n;
       L.rows = static_cast<itt_iter_row*>(c->out_alloc(sp.n * sizeof(itt_iter_row)));  // pinned: DMA target
-      iteration_aggregates(c, t.tok_start.p, t.tok_end.p, t.n_tok, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod, sp,
+      iteration_aggregates(c, t.tok_start.p, t.tok_end.p, t.n_tok, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod,
+                           t.htod_range.p, sp,
                            L.rows, L.clamps, t.scan);
     }
     *out = a;

@@ -114,71 +114,96 @@ __global__ void k_order_stats(const int64_t* __restrict__ start, uint64_t n, uns
   }
 }
 
-// Sort each 256-row block by (start, row) — rank = number of block rows ordered before this one,
-// unique because the row breaks ties, so the result is the stable order — and record the block's
-// start range, the descent count of the source order and the global min/max start.
+// Sort each 256-row block by (start, row) — unique keys because the row breaks ties, so the
+// result is the stable order — and record the block's start range and whether the source order
+// has a descent.  Bitonic network with one row per thread: the 30 stages whose partner is in the
+// same warp exchange through shuffles; only the 6 cross-warp stages (j >= 32) go through shared
+// memory.  Global min/max and the descent flag are folded in k_order_check (no same-address
+// atomics per block).
 constexpr int kOrderBlock = 256;
 __global__ void __launch_bounds__(kOrderBlock) k_order_block_sort(const int64_t* __restrict__ start, uint64_t n,
                                                                   uint32_t* __restrict__ perm, int64_t* __restrict__ bmin,
-                                                                  int64_t* __restrict__ bmax, unsigned long long* stats) {
+                                                                  int64_t* __restrict__ bmax, uint8_t* __restrict__ bdesc) {
   __shared__ long long s[kOrderBlock];
+  __shared__ uint32_t r[kOrderBlock];
+  __shared__ long long wmn[kOrderBlock / 32], wmx[kOrderBlock / 32];
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kOrderBlock;
   const uint32_t len = static_cast<uint32_t>(umin64(kOrderBlock, n - base));
   const uint32_t t = threadIdx.x;
-  const long long me = t < len ? start[base + t] : LLONG_MAX;
-  s[t] = me;
-  __shared__ uint32_t r[kOrderBlock];  // row offsets; padding rows (t >= len) sort last
-  r[t] = t;
-  __syncthreads();
-  unsigned desc = 0;
-  if (t < len) {
-    desc = t > 0 && s[t - 1] > me;
-    if (t == 0 && base > 0 && start[base - 1] > me) desc = 1;
-  }
-  __syncthreads();
-  // bitonic network on (start, row): keys are unique, so the result is the stable order
-  for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t p = t ^ j;
-      if (p > t) {
-        const long long a = s[t], b = s[p];
-        const uint32_t ra = r[t], rb = r[p];
-        const bool a_gt_b = a > b || (a == b && ra > rb);
-        if (((t & k) == 0) == a_gt_b) {  // ascending in the lower half of each k-run, descending above
-          s[t] = b, s[p] = a;
-          r[t] = rb, r[p] = ra;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (t < len) perm[base + t] = static_cast<uint32_t>(base + r[t]);
-  long long mn = me, mx = t < len ? me : LLONG_MIN;
+  long long a = t < len ? __ldcs(&start[base + t]) : LLONG_MAX;  // padding rows sort last
+  uint32_t ra = t;
+  s[t] = a;
+  long long mn = a, mx = t < len ? a : LLONG_MIN;
   for (int o = 16; o > 0; o >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  const unsigned d = __reduce_add_sync(0xffffffffu, desc);
-  __shared__ long long wmn[kOrderBlock / 32], wmx[kOrderBlock / 32];
-  __shared__ unsigned wd[kOrderBlock / 32];
-  if (lane_id() == 0) wmn[t >> 5] = mn, wmx[t >> 5] = mx, wd[t >> 5] = d;
+  if (lane_id() == 0) wmn[t >> 5] = mn, wmx[t >> 5] = mx;
   __syncthreads();
+  // descent in the source order: against the previous row of the block / of the previous block
+  const long long prev = t > 0 ? s[t - 1] : (base > 0 ? start[base - 1] : LLONG_MIN);
+  const int any_desc = __syncthreads_or(t < len && prev > a);
   if (t == 0) {
-    unsigned dd = 0;
-    for (int w = 0; w < kOrderBlock / 32; ++w) mn = min(mn, wmn[w]), mx = max(mx, wmx[w]), dd += wd[w];
+    for (int w = 0; w < kOrderBlock / 32; ++w) mn = min(mn, wmn[w]), mx = max(mx, wmx[w]);
     bmin[blockIdx.x] = mn;
     bmax[blockIdx.x] = mx;
-    atomicMin(reinterpret_cast<long long*>(&stats[0]), mn);
-    atomicMax(reinterpret_cast<long long*>(&stats[1]), mx);
-    if (dd) atomicAdd(&stats[2], static_cast<unsigned long long>(dd));
+    bdesc[blockIdx.x] = any_desc ? 1 : 0;
   }
+  for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      long long b;
+      uint32_t rb;
+      if (j >= 32) {
+        __syncthreads();
+        s[t] = a;
+        r[t] = ra;
+        __syncthreads();
+        b = s[t ^ j];
+        rb = r[t ^ j];
+      } else {
+        b = __shfl_xor_sync(0xffffffffu, a, j);
+        rb = __shfl_xor_sync(0xffffffffu, ra, j);
+      }
+      const bool a_gt_b = a > b || (a == b && ra > rb);
+      const bool lower = (t & j) == 0, ascending = (t & k) == 0;
+      if ((lower == ascending) == a_gt_b) a = b, ra = rb;  // lower keeps the min when ascending
+    }
+  }
+  if (t < len) perm[base + t] = static_cast<uint32_t>(base + ra);
 }
 
-// block b's largest start must not exceed block b+1's smallest (equal starts stay in row order)
-__global__ void k_order_check(const int64_t* __restrict__ bmin, const int64_t* __restrict__ bmax, uint64_t nb,
-                              unsigned long long* bad) {
+// Fold the per-block results: stats = [min start, max start, any descent, overlapping block
+// boundaries]; block b's largest start must not exceed block b+1's smallest (equal starts stay in
+// row order).  One set of atomics per CTA.
+__global__ void __launch_bounds__(256) k_order_check(const int64_t* __restrict__ bmin, const int64_t* __restrict__ bmax,
+                                                     const uint8_t* __restrict__ bdesc, uint64_t nb,
+                                                     unsigned long long* stats) {
   const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (b + 1 < nb && bmax[b] > bmin[b + 1]) atomicAdd(bad, 1ull);
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  unsigned desc = 0, bad = 0;
+  if (b < nb) {
+    mn = bmin[b];
+    mx = bmax[b];
+    desc = bdesc[b];
+    bad = b + 1 < nb && mx > bmin[b + 1];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  desc = __reduce_or_sync(0xffffffffu, desc);
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  __shared__ long long smn[8], smx[8];
+  __shared__ unsigned sd[8], sb[8];
+  if (lane_id() == 0) smn[threadIdx.x >> 5] = mn, smx[threadIdx.x >> 5] = mx, sd[threadIdx.x >> 5] = desc, sb[threadIdx.x >> 5] = bad;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mn = min(mn, smn[w]), mx = max(mx, smx[w]), desc |= sd[w], bad += sb[w];
+    atomicMin(reinterpret_cast<long long*>(&stats[0]), mn);
+    atomicMax(reinterpret_cast<long long*>(&stats[1]), mx);
+    if (desc) atomicAdd(&stats[2], 1ull);
+    if (bad) atomicAdd(&stats[3], static_cast<unsigned long long>(bad));
+  }
 }
 
 __global__ void k_order_keys(const int64_t* __restrict__ start, uint64_t n, int64_t mn, uint64_t* __restrict__ keys,
@@ -570,6 +595,7 @@ struct CompactF {
   int64_t* htod_start;
   int64_t* htod_end;
   int64_t* htod_size;
+  unsigned long long* htod_range;
   __device__ __forceinline__ uint32_t row(uint64_t k) const { return perm ? perm[k] : static_cast<uint32_t>(k); }
   __device__ __forceinline__ uint64_t load(uint64_t k) const {
     const uint32_t i = row(k);
@@ -597,6 +623,9 @@ struct CompactF {
       htod_start[h] = s;
       htod_end[h] = e;
       htod_size[h] = (rflags[i] & ITT_REC_HAS_SIZE) ? size[i] : 0;
+      const unsigned long long fe = static_cast<unsigned long long>(e) ^ (1ull << 63);
+      atomicMin(&htod_range[0], fe);
+      atomicMax(&htod_range[1], fe);
     }
   }
 };
@@ -724,9 +753,11 @@ void order_records(TraceState& t) {
   h2d(c, st.p, init, 4);
   DBuf<uint32_t> perm(c, n);
   DBuf<int64_t> bmin(c, nb), bmax(c, nb);
+  DBuf<uint8_t> bdesc(c, nb);
   launch(c, "order_blocks", n * 12.0, k_order_block_sort, dim3(static_cast<unsigned>(nb)), dim3(kOrderBlock), 0, t.rec.start, n,
-         perm.p, bmin.p, bmax.p, st.p);
-  launch(c, "order_check", nb * 16.0, k_order_check, dim3(grid_for(nb, 256)), dim3(256), 0, bmin.p, bmax.p, nb, st.p + 3);
+         perm.p, bmin.p, bmax.p, bdesc.p);
+  launch(c, "order_check", nb * 17.0, k_order_check, dim3(grid_for(nb, 256)), dim3(256), 0, bmin.p, bmax.p, bdesc.p, nb,
+         st.p);
   unsigned long long h[4];
   readback(c, h, st.p, 4);
   if (h[2] == 0) return;  // already in (start,row) order
@@ -888,6 +919,9 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
   t.htod_start.alloc(c, n_htod + 1);
   t.htod_end.alloc(c, n_htod + 1);
   t.htod_size.alloc(c, n_htod + 1);
+  t.htod_range.alloc(c, 2);
+  ITT_CUDA(cudaMemsetAsync(t.htod_range.p, 0xFF, 8, c->stream));
+  ITT_CUDA(cudaMemsetAsync(t.htod_range.p + 1, 0, 8, c->stream));
   DBuf<uint64_t> tot(c, 1);
   CompactF f{n,
              t.sorted ? nullptr : t.perm.p,
@@ -909,7 +943,8 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
              t.tfirst.p,
              t.htod_start.p,
              t.htod_end.p,
-             t.htod_size.p};
+             t.htod_size.p,
+             t.htod_range.p};
   device_scan<uint64_t, SumOp<uint64_t>>(c, "compact", n * (t.sorted ? 14.0 : 18.0) + n_main * 28.0 + n_htod * 24.0, f, n,
                                          t.scan);
   if (t.streams.empty()) fail(ITT_E_INVALID_ARGUMENT, "internal: compact_main needs the stream census");

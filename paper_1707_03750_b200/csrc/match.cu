@@ -141,12 +141,10 @@ __global__ void k_chain_nodes(const uint32_t* const* __restrict__ levels, int nl
 
 }  // namespace
 
-void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* pattern_dev, uint64_t m, int64_t k0,
-                      SpanState& out, ScanScratch& scan) {
+void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* pattern_dev, int32_t head, uint64_t m,
+                      int64_t k0, SpanState& out, ScanScratch& scan) {
   out.n = 0;
   if (m == 0 || n < m) return;  // match.hpp:47
-  int32_t head;
-  readback(c, &head, pattern_dev, 1);
   DBuf<uint32_t> anchors(c, n);
   DBuf<uint32_t> cnt(c, 1);
   device_scan<uint32_t, SumOp<uint32_t>>(c, "match_anchors", n * 4.0, AnchorF{tokens, head, anchors.p}, n, scan);

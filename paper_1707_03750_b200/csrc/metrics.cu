@@ -19,30 +19,20 @@ namespace itt {
 
 namespace {
 
-__global__ void k_minmax64(const int64_t* __restrict__ v, uint64_t n, long long* out /*min,max*/) {
-  long long mn = LLONG_MAX, mx = LLONG_MIN;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    mn = min(mn, static_cast<long long>(v[i]));
-    mx = max(mx, static_cast<long long>(v[i]));
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  }
-  if (lane_id() == 0) {
-    atomicMin(&out[0], mn);
-    atomicMax(&out[1], mx);
-  }
-}
+constexpr unsigned long long kFlip = 1ull << 63;  // int64 order -> uint64 order
+__device__ __forceinline__ int64_t unflip(unsigned long long v) { return static_cast<int64_t>(v ^ kFlip); }
 
-struct PrefMaxF {  // inclusive prefix max of HtoD ends, relative to the minimum end
+// inclusive prefix max of HtoD ends relative to their minimum (the look-back words carry 62-bit
+// values); the minimum comes from compact_main's atomics, so no range pass or host sync is needed
+struct PrefMaxF {
   const int64_t* end;
-  int64_t base;
+  const unsigned long long* range;
   int64_t* out;
-  __device__ __forceinline__ uint64_t load(uint64_t i) const { return static_cast<uint64_t>(end[i] - base); }
+  __device__ __forceinline__ uint64_t load(uint64_t i) const {
+    return static_cast<uint64_t>(end[i] - unflip(__ldg(&range[0]))) & ((1ull << 62) - 1);
+  }
   __device__ __forceinline__ void store(uint64_t i, uint64_t excl, uint64_t v) const {
-    out[i] = static_cast<int64_t>(excl > v ? excl : v) + base;
+    out[i] = static_cast<int64_t>(excl > v ? excl : v) + unflip(__ldg(&range[0]));
   }
 };
 
@@ -59,7 +49,8 @@ struct AggArgs {
   const uint32_t* sp_extra;
   uint64_t I;
   itt_iter_row* rows;
-  unsigned long long* clamps;  // [0] negative gaps, [1] negative intervals
+  const unsigned long long* htod_range;
+  unsigned long long* clamps;  // [0] negative gaps, [1] negative intervals, [2] HtoD range overflow
 };
 
 __device__ __forceinline__ uint64_t lower_bound64(const int64_t* a, uint64_t n, int64_t x) {  // first a[i] >= x
@@ -83,6 +74,9 @@ __device__ __forceinline__ uint64_t upper_bound64(const int64_t* a, uint64_t n, 
 
 __global__ void k_span_aggregates(AggArgs a) {
   const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (k == 0 && threadIdx.x == 0 && a.H &&
+      static_cast<unsigned long long>(unflip(a.htod_range[1]) - unflip(a.htod_range[0])) >= (1ull << 62))
+    a.clamps[2] = 1;
   if (k >= a.I) return;
   const unsigned lane = lane_id();
   const uint64_t s = a.sp_start[k], e = a.sp_end[k];
@@ -167,35 +161,27 @@ __global__ void k_span_aggregates(AggArgs a) {
 
 void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_end, uint64_t n_tok,
                           const int64_t* htod_start, const int64_t* htod_end, const int64_t* htod_size, uint64_t n_htod,
-                          const SpanState& spans, itt_iter_row* rows, itt_clamps& clamps,
+                          const unsigned long long* htod_range, const SpanState& spans, itt_iter_row* rows,
+                          itt_clamps& clamps,
                           ScanScratch& scan) {
   (void)n_tok;
   clamps = itt_clamps{0, 0};
   if (spans.n == 0) return;
   DBuf<int64_t> pmax(c, n_htod + 1);
-  if (n_htod) {
-    DBuf<long long> mm(c, 2);
-    long long init[2] = {LLONG_MAX, LLONG_MIN};
-    h2d(c, mm.p, init, 2);
-    launch(c, "agg_htod_minmax", n_htod * 8.0, k_minmax64, dim3(std::min<unsigned>(grid_for(n_htod, 256), 1024)), dim3(256), 0,
-           htod_end, n_htod, mm.p);
-    long long h[2];
-    readback(c, h, mm.p, 2);
-    if (static_cast<unsigned long long>(h[1] - h[0]) >= (1ull << 62))
-      fail(ITT_E_INVALID_ARGUMENT, "metrics: HtoD time range exceeds 2^62 ns");
-    device_scan<uint64_t, MaxOp<uint64_t>>(c, "agg_htod_prefmax", n_htod * 16.0, PrefMaxF{htod_end, h[0], pmax.p}, n_htod, scan);
-  }
+  if (n_htod)
+    device_scan<uint64_t, MaxOp<uint64_t>>(c, "agg_htod_prefmax", n_htod * 16.0, PrefMaxF{htod_end, htod_range, pmax.p}, n_htod, scan);
   DBuf<itt_iter_row> drows(c, spans.n);
-  DBuf<unsigned long long> dcl(c, 2);
+  DBuf<unsigned long long> dcl(c, 3);
   dcl.zero();
-  AggArgs a{tok_start,  tok_end,   htod_start, htod_end,       htod_size,      pmax.p, n_htod,
-            spans.start.p, spans.end.p, spans.extra.p, spans.n, drows.p, dcl.p};
+  AggArgs a{tok_start,     tok_end,     htod_start,    htod_end, htod_size, pmax.p,     n_htod,
+            spans.start.p, spans.end.p, spans.extra.p, spans.n,  drows.p,   htod_range, dcl.p};
   const uint64_t threads = spans.n * 32;
   launch(c, "agg_spans", static_cast<double>(n_tok) * 16.0 + spans.n * 96.0, k_span_aggregates, dim3(grid_for(threads, 256)),
          dim3(256), 0, a);
   d2h(c, rows, drows.p, spans.n);  // straight into the caller's (pinned) buffer
-  unsigned long long cl[2];
-  readback(c, cl, dcl.p, 2);  // synchronizes
+  unsigned long long cl[3];
+  readback(c, cl, dcl.p, 3);  // synchronizes
+  if (cl[2]) fail(ITT_E_INVALID_ARGUMENT, "metrics: HtoD time range exceeds 2^62 ns");
   clamps.negative_gap_clamps = static_cast<int64_t>(cl[0]);
   clamps.negative_interval_clamps = static_cast<int64_t>(cl[1]);
 }

@@ -63,6 +63,7 @@ struct TraceState {
   DBuf<int64_t> tok_start, tok_end;
   DBuf<uint64_t> tok_record;  // sorted-order record index (only for build_token_sequence)
   DBuf<int64_t> htod_start, htod_end, htod_size;
+  DBuf<unsigned long long> htod_range;  // [min, max] HtoD end, sign bit flipped (set by compact_main)
   uint32_t n_names = 0;
   std::vector<uint64_t> name_row;  // token id -> source row
   ScanScratch scan;
@@ -93,8 +94,10 @@ struct SuffixState {
 };
 // tokens: device int32[n]; term: unique terminator.  cap: only the first `cap` symbols matter
 // (mining with max length L_max needs cap = L_max + 1); 0xFFFFFFFF = full suffix array.
+// known_alphabet: the caller guarantees tokens in [0, term) (interned ids, term = V), which
+// skips the range/terminator scan and the init sort's trivial-pass readback (two host syncs).
 void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
-                        radix::Scratch& rs, ScanScratch& scan, uint32_t cap = 0xFFFFFFFFu);
+                        radix::Scratch& rs, ScanScratch& scan, uint32_t cap = 0xFFFFFFFFu, bool known_alphabet = false);
 
 // ------------------------------------------------------------------ mining (mine.cu)
 struct IntervalState {
@@ -121,13 +124,15 @@ struct SpanState {
   uint64_t n = 0;
   DBuf<uint32_t> start, end, extra;
 };
-void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* pattern_dev, uint64_t m, int64_t k0,
-                      SpanState& out, ScanScratch& scan);
+// `head` = pattern[0] (the caller holds the pattern on the host).
+void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* pattern_dev, int32_t head, uint64_t m,
+                      int64_t k0, SpanState& out, ScanScratch& scan);
 
 // ------------------------------------------------------------------ aggregates (metrics.cu)
 void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_end, uint64_t n_tok,
                           const int64_t* htod_start, const int64_t* htod_end, const int64_t* htod_size, uint64_t n_htod,
-                          const SpanState& spans, itt_iter_row* rows /* host, spans.n */, itt_clamps& clamps,
+                          const unsigned long long* htod_range, const SpanState& spans,
+                          itt_iter_row* rows /* host, spans.n */, itt_clamps& clamps,
                           ScanScratch& scan);
 
 }  // namespace itt

@@ -278,7 +278,7 @@ __global__ void k_lcp_gather(const uint32_t* __restrict__ sa, const uint32_t* __
 }  // namespace
 
 void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
-                        radix::Scratch& rs, ScanScratch& scan, uint32_t cap) {
+                        radix::Scratch& rs, ScanScratch& scan, uint32_t cap, bool known_alphabet) {
   const uint64_t np = n + 1;
   if (np >= 0xFFFFFFFFull) fail(ITT_E_INVALID_ARGUMENT, "pattern-mining: sequence too long for 32-bit suffix indices");
   s.n = n;
@@ -286,8 +286,8 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   s.levels.clear();
   s.rounds = 0;
   // alphabet: codes = value - lo over tokens and the terminator
-  int32_t lo = term, hi = term;
-  if (n) {
+  int32_t lo = known_alphabet ? 0 : term, hi = term;
+  if (n && !known_alphabet) {
     DBuf<int> st(c, 3);
     int init[3] = {INT_MAX, INT_MIN, 0};
     h2d(c, st.p, init, 3);
@@ -318,7 +318,9 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   launch(c, "sa_init_keys", np * (4.0 * k + 8.0), k_init_keys, dim3(grid_for(np, 256)), dim3(256), 0, s.text.p, np, cbits, k,
          ka, va);
   const int init_bits = std::min(32, cbits * k);
-  const bool a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs);
+  const bool a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
+                                                 static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr),
+                                                 /*skip_trivial=*/!known_alphabet);
   uint32_t* keys = a0 ? kb : ka;
   uint32_t* sa = a0 ? vb : va;
   uint32_t* f1 = a0 ? ka : kb;  // free buffers

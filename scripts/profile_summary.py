@@ -48,7 +48,7 @@ for r in rr[2:]:
                 key=lambda x: -(x[1] or 0))[:4]
     d["top_stalls"] = {a: b for a, b in st}
     per[nm].append(d)
-summ = {"source": f"{tag}: ncu --set full --clock-control none --import-source on, bench.py C2 (n'=10,000,017)",
+summ = {"source": f"{tag}: ncu --set full --clock-control none --import-source on, bench.py C2 (n'=10,000,017)", "workload": "C2",
         "kernels": {}}
 for nm, lst in per.items():
     avg = {k: sum(x[k] for x in lst) / len(lst) for k in keys if all(x[k] is not None for x in lst)}
