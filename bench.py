@@ -351,6 +351,21 @@ def main():
                         "GBps": (v["bytes"] / (v["total_ms"] / 1000.0) / 1e9) if v["total_ms"] > 0 else None}
                     for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])}
 
+    # ---- a12 (the north star's per-op x per-iteration profile; no reference counterpart, so it
+    # is reported as the increment over the reference-equivalent step, not inside `value`)
+    def step_a12():
+        return ctx.analyze_raw(drecs, [iters], op_profile=True)
+    step_a12()
+    ms_a12, _ = timed(step_a12, args.steps)
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    step_a12()
+    st_a12 = {k: v["total_ms"] for k, v in ctx.kernel_stats().items() if k.startswith("opprof")}
+    ctx.set_profiling(False)
+    op_profile = {"ms_per_step": ms_a12 / args.steps, "increment_ms": ms_a12 / args.steps - ms_step,
+                  "events_per_s": world * n_events / (ms_a12 / args.steps / 1000.0),
+                  "outputs": "per-op and per-iteration totals (cell grid on request)", "kernels_ms": st_a12}
+
     # ---- e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -392,7 +407,7 @@ def main():
                        "mined": {"pattern_length": L["pattern_length"], "pattern_count": L["pattern_count"],
                                  "iterations_found": int(L["rows"].shape[0])}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "gpu_launches": int(launches), "kernels": kernel_table,
+            "gpu_launches": int(launches), "kernels": kernel_table, "op_profile": op_profile,
         }
         print(json.dumps(line), flush=True)
     drecs.free()

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ITT_ABI_VERSION 1
+#define ITT_ABI_VERSION 2
 
 typedef enum itt_status {
   ITT_OK = 0,
@@ -239,13 +239,68 @@ typedef struct itt_clamps {
 int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t* record_index, uint64_t n_tokens,
                           const itt_span* spans, uint64_t n_spans, itt_iter_row** rows, itt_clamps* clamps);
 
+/* ------------------------------------------------------- a12: second-level per-op profile
+ * The north star's per-iteration segmented reduction "per op and per iteration" (SURVEY §8a
+ * row a12).  The reference has NO such function; the definition below is this library's, built
+ * on the reference's own windows (approx_match spans, match.hpp:41-85) and its op-gap rule
+ * (metrics.hpp:145-157).  For every span k = [s_k, e_k] (main-stream tokens, inclusive) and every
+ * op id v occurring in it, one cell:
+ *   count     = #{ j in [s_k, e_k] : tokens[j] = v }
+ *   kernel_ns = sum of (end_j - start_j) over those j whose record kind is ITT_KIND_KERNEL
+ *   memcpy_ns = sum of (end_j - start_j) over those j of any other kind (copies, memsets, other)
+ *   idle_ns   = sum of max(0, start_j - end_{j-1}) over those j with j > s_k: the idle gap in
+ *               front of op j inside the iteration, so that sum_v idle_ns(k, v) equals the
+ *               reference's clamped op-gap sum of iteration k (metrics.hpp:145-157)
+ * Cells are ordered by (iteration, op).  The two reductions of the cell grid: */
+typedef struct itt_op_cell {
+  uint32_t iteration;
+  int32_t op;
+  uint32_t count;
+  uint32_t pad_;
+  int64_t kernel_ns;
+  int64_t memcpy_ns;
+  int64_t idle_ns;
+} itt_op_cell;
+
+typedef struct itt_op_total { /* per op id, summed over iterations */
+  int64_t iterations; /* iterations in which the op occurs (cells of the op) */
+  int64_t count;
+  int64_t kernel_ns;
+  int64_t memcpy_ns;
+  int64_t idle_ns;
+} itt_op_total;
+
+typedef struct itt_iter_op_total { /* per iteration, summed over ops */
+  int64_t distinct_ops; /* cells of the iteration */
+  int64_t kernel_ns;
+  int64_t memcpy_ns;
+  int64_t idle_ns;      /* == the reference's clamped op-gap sum of the iteration */
+} itt_iter_op_total;
+
+enum { ITT_OP_PROFILE_AUTO = 0, ITT_OP_PROFILE_SMEM = 1, ITT_OP_PROFILE_SORT = 2 };
+
+/* Token-level entry: tokens/start/end/kind are per main-stream token (host or device memory),
+ * op ids in [0, n_ops), spans disjoint and increasing.  method: AUTO picks the shared-memory
+ * table when n_ops fits, else the sort-based segmented reduction.  op_totals [n_ops] and
+ * iter_totals [n_spans] are caller-allocated (either may be NULL).  cells: NULL to skip the cell
+ * grid, else *cells is library-allocated [*n_cells] and released by itt_free. */
+int itt_op_profile(itt_ctx* ctx, const int32_t* tokens, const int64_t* tok_start, const int64_t* tok_end,
+                   const uint8_t* tok_kind, uint64_t n, uint32_t n_ops, const itt_span* spans, uint64_t n_spans,
+                   int method, itt_op_total* op_totals, itt_iter_op_total* iter_totals, itt_op_cell** cells,
+                   uint64_t* n_cells);
+
 /* ------------------------------------------------------- L7 orchestration */
+/* itt_analyze_opts.flags: OP_PROFILE fills op_totals / iter_op_totals of every loop result;
+ * OP_CELLS also returns the (iteration, op) cell grid (size ~ tokens: large) */
+enum { ITT_ANALYZE_OP_PROFILE = 1u, ITT_ANALYZE_OP_CELLS = 2u };
+
 typedef struct itt_analyze_opts { /* AnalyzeOptions, pipeline.hpp:18-25 */
   const int64_t* loops;
   uint32_t n_loops;
   int64_t epsilon0;
   int64_t k0;           /* < 0: default_k0(pattern length) (match.hpp:19-21) */
   int64_t main_stream;  /* < 0: select_main_stream */
+  uint32_t flags;       /* ITT_ANALYZE_* (0 = the reference's outputs only) */
 } itt_analyze_opts;
 
 typedef struct itt_loop_result { /* LoopReport (report.hpp:92-103) integer fields + details rows */
@@ -259,6 +314,10 @@ typedef struct itt_loop_result { /* LoopReport (report.hpp:92-103) integer field
   uint64_t n_iterations;
   itt_iter_row* rows;      /* [n_iterations] */
   itt_clamps clamps;
+  itt_op_total* op_totals;           /* a12 (ITT_ANALYZE_OP_PROFILE): [itt_analysis.n_names], else NULL */
+  itt_iter_op_total* iter_op_totals; /* a12: [n_iterations], else NULL */
+  uint64_t n_op_cells;               /* a12 (ITT_ANALYZE_OP_CELLS), else 0 */
+  itt_op_cell* op_cells;             /* [n_op_cells], (iteration, op) order */
 } itt_loop_result;
 
 typedef struct itt_analysis {

@@ -207,6 +207,9 @@ class Oracle(_Common):
         super().__init__(os.path.join(HERE, "libitt_oracle.so"))
         self.lib.orc_sort_records.argtypes = [C.c_uint64, P(C.c_int64), P(C.c_uint64)]
         self.lib.orc_classify.argtypes = [C.c_char_p, C.c_uint64, C.c_int]
+        self.lib.orc_op_profile.argtypes = [P(C.c_int32), P(C.c_int64), P(C.c_int64), P(C.c_uint8), C.c_uint64,
+                                            C.c_uint32, P(abi.itt_span), C.c_uint64, P(P(abi.itt_op_cell)),
+                                            P(C.c_uint64)]
 
     def sort_records(self, start):
         s = np.ascontiguousarray(start, dtype=np.int64)
@@ -216,6 +219,29 @@ class Oracle(_Common):
 
     def classify(self, name: bytes, has_tp: bool) -> int:
         return self.lib.orc_classify(name, len(name), 1 if has_tp else 0)
+
+    def op_profile(self, tokens, tok_start, tok_end, tok_kind, n_ops, spans):
+        """a12 cells (abi.OP_CELL_DTYPE) by the plain-loop restatement in itt_oracle.c."""
+        t = _i32(tokens)
+        ts = np.ascontiguousarray(tok_start, dtype=np.int64)
+        te = np.ascontiguousarray(tok_end, dtype=np.int64)
+        tk = np.ascontiguousarray(tok_kind, dtype=np.uint8)
+        sp = (abi.itt_span * max(1, len(spans)))()
+        for i, s in enumerate(spans):
+            sp[i].start_token, sp[i].end_token, sp[i].extra = int(s[0]), int(s[1]), int(s[2])
+        out = P(abi.itt_op_cell)()
+        cnt = C.c_uint64()
+        rc = self.lib.orc_op_profile(t.ctypes.data_as(P(C.c_int32)), ts.ctypes.data_as(P(C.c_int64)),
+                                     te.ctypes.data_as(P(C.c_int64)), tk.ctypes.data_as(P(C.c_uint8)), t.shape[0],
+                                     n_ops, sp, len(spans), C.byref(out), C.byref(cnt))
+        if rc:
+            raise CheckerError(rc, "op_profile")
+        n = cnt.value
+        res = np.zeros(n, abi.OP_CELL_DTYPE)
+        if n:
+            C.memmove(res.ctypes.data, out, n * C.sizeof(abi.itt_op_cell))
+        self._free(out)
+        return res
 
 
 _ref = None

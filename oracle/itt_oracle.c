@@ -572,3 +572,63 @@ int orc_iteration_metrics(const itt_records* r, uint32_t main_stream, const itt_
   free(segs);
   return 0;
 }
+
+/* ---- a12 per-op profile.  No reference function exists: this restates the
+ * definition in include/itertrace_cuda.h (itt_op_cell) with plain loops — the reference's own
+ * pieces it builds on are the spans (match.hpp:41-85) and the clamped op gap
+ * (metrics.hpp:145-157: max(0, start[j+1] - end[j]) for j in [s, e)). */
+static int cmp_u32(const void* x, const void* y) {
+  const uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
+  return a < b ? -1 : a > b;
+}
+
+int orc_op_profile(const int32_t* tokens, const int64_t* tok_start, const int64_t* tok_end, const uint8_t* tok_kind,
+                   uint64_t n, uint32_t n_ops, const itt_span* spans, uint64_t I, itt_op_cell** out, uint64_t* n_out) {
+  *out = NULL;
+  *n_out = 0;
+  for (uint64_t j = 0; j < n; ++j)
+    if (tokens[j] < 0 || (uint32_t)tokens[j] >= n_ops) return ITT_E_INVALID_ARGUMENT;
+  uint32_t* cnt = calloc(n_ops + 1, sizeof(uint32_t));
+  int64_t* kern = calloc(n_ops + 1, sizeof(int64_t));
+  int64_t* mem = calloc(n_ops + 1, sizeof(int64_t));
+  int64_t* idle = calloc(n_ops + 1, sizeof(int64_t));
+  uint32_t* touched = malloc((n_ops + 1) * sizeof(uint32_t));
+  uint64_t cap = 16, m = 0;
+  itt_op_cell* cells = malloc(cap * sizeof(itt_op_cell));
+  for (uint64_t k = 0; k < I; ++k) {
+    const uint64_t s = (uint64_t)spans[k].start_token, e = (uint64_t)spans[k].end_token;
+    uint32_t nt = 0;
+    for (uint64_t j = s; j <= e; ++j) {
+      const uint32_t v = (uint32_t)tokens[j];
+      if (cnt[v]++ == 0) touched[nt++] = v;
+      const int64_t d = tok_end[j] - tok_start[j];
+      if (tok_kind[j] == ITT_KIND_KERNEL) kern[v] += d;
+      else mem[v] += d;
+      if (j > s) { /* the gap in front of op j inside the iteration */
+        const int64_t g = tok_start[j] - tok_end[j - 1];
+        if (g > 0) idle[v] += g;
+      }
+    }
+    qsort(touched, nt, sizeof(uint32_t), cmp_u32);
+    for (uint32_t q = 0; q < nt; ++q) {
+      const uint32_t v = touched[q];
+      if (m == cap) {
+        cap *= 2;
+        cells = realloc(cells, cap * sizeof(itt_op_cell));
+      }
+      itt_op_cell* c = &cells[m++];
+      c->iteration = (uint32_t)k;
+      c->op = (int32_t)v;
+      c->count = cnt[v];
+      c->pad_ = 0;
+      c->kernel_ns = kern[v];
+      c->memcpy_ns = mem[v];
+      c->idle_ns = idle[v];
+      cnt[v] = 0, kern[v] = 0, mem[v] = 0, idle[v] = 0;
+    }
+  }
+  free(cnt), free(kern), free(mem), free(idle), free(touched);
+  *out = cells;
+  *n_out = m;
+  return 0;
+}

@@ -44,6 +44,10 @@ int orc_approx_match(const int32_t* tokens, uint64_t n, const int32_t* pattern, 
 /* partition_iterations + collect_htod_records + compute_iteration_metrics: metrics.hpp:44-164 */
 int orc_iteration_metrics(const itt_records* r, uint32_t main_stream, const itt_span* spans, uint64_t n_spans,
                           ref_iter* rows, itt_clamps* clamps);
+/* a12 per-op profile — no reference function; restates include/itertrace_cuda.h itt_op_cell
+ * (parity unpinned by the reference) */
+int orc_op_profile(const int32_t* tokens, const int64_t* tok_start, const int64_t* tok_end, const uint8_t* tok_kind,
+                   uint64_t n, uint32_t n_ops, const itt_span* spans, uint64_t I, itt_op_cell** out, uint64_t* n_out);
 void orc_free(void* p);
 
 #ifdef __cplusplus

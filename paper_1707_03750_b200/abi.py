@@ -9,7 +9,7 @@ import ctypes as C
 
 import numpy as np
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # 1 + itertrace::ErrorKind (errors.hpp:8-21)
 ERROR_KINDS = [
@@ -20,6 +20,7 @@ ITT_E_CUDA = 100
 ITT_E_NCCL = 101
 ITT_E_INVALID_ARGUMENT = 102
 
+KIND_KERNEL = 0
 KIND_NAMES = ["Kernel", "MemcpyHtoD", "MemcpyDtoH", "MemcpyDtoD", "Memset", "Other"]
 CLASS_NAMES = ["Main", "CopyHtoD", "CopyDtoH", "CopyMixed", "Assist"]
 
@@ -127,7 +128,38 @@ class itt_analyze_opts(C.Structure):
         ("epsilon0", C.c_int64),
         ("k0", C.c_int64),
         ("main_stream", C.c_int64),
+        ("flags", C.c_uint32),
     ]
+
+
+ITT_ANALYZE_OP_PROFILE = 1
+ITT_ANALYZE_OP_CELLS = 2
+ITT_OP_PROFILE_AUTO, ITT_OP_PROFILE_SMEM, ITT_OP_PROFILE_SORT = 0, 1, 2
+
+
+class itt_op_cell(C.Structure):
+    """a12 (iteration, op) cell — include/itertrace_cuda.h itt_op_cell."""
+    _fields_ = [
+        ("iteration", C.c_uint32), ("op", C.c_int32), ("count", C.c_uint32), ("pad_", C.c_uint32),
+        ("kernel_ns", C.c_int64), ("memcpy_ns", C.c_int64), ("idle_ns", C.c_int64),
+    ]
+
+
+class itt_op_total(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("count", C.c_int64), ("kernel_ns", C.c_int64), ("memcpy_ns", C.c_int64),
+                ("idle_ns", C.c_int64)]
+
+
+class itt_iter_op_total(C.Structure):
+    _fields_ = [("distinct_ops", C.c_int64), ("kernel_ns", C.c_int64), ("memcpy_ns", C.c_int64), ("idle_ns", C.c_int64)]
+
+
+# numpy views of the a12 structs
+OP_CELL_DTYPE = np.dtype([("iteration", "<u4"), ("op", "<i4"), ("count", "<u4"), ("pad_", "<u4"),
+                          ("kernel_ns", "<i8"), ("memcpy_ns", "<i8"), ("idle_ns", "<i8")])
+OP_TOTAL_DTYPE = np.dtype([("iterations", "<i8"), ("count", "<i8"), ("kernel_ns", "<i8"), ("memcpy_ns", "<i8"),
+                           ("idle_ns", "<i8")])
+ITER_OP_TOTAL_DTYPE = np.dtype([("distinct_ops", "<i8"), ("kernel_ns", "<i8"), ("memcpy_ns", "<i8"), ("idle_ns", "<i8")])
 
 
 class itt_loop_result(C.Structure):
@@ -142,6 +174,10 @@ class itt_loop_result(C.Structure):
         ("n_iterations", C.c_uint64),
         ("rows", P(itt_iter_row)),
         ("clamps", itt_clamps),
+        ("op_totals", P(itt_op_total)),
+        ("iter_op_totals", P(itt_iter_op_total)),
+        ("n_op_cells", C.c_uint64),
+        ("op_cells", P(itt_op_cell)),
     ]
 
 

@@ -474,6 +474,76 @@ int itt_free_patterns(itt_ctx*, itt_pattern* p, uint32_t n_loops) {
   return ITT_OK;
 }
 
+// ------------------------------------------------------------------ a12 op profile
+namespace {
+__global__ void k_check_ops(const int32_t* __restrict__ tok, uint64_t n, uint32_t n_ops, unsigned* bad) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < n && static_cast<uint32_t>(tok[j]) >= n_ops) atomicOr(bad, 1u);
+}
+}  // namespace
+
+int itt_op_profile(itt_ctx* ctx, const int32_t* tokens, const int64_t* tok_start, const int64_t* tok_end,
+                   const uint8_t* tok_kind, uint64_t n, uint32_t n_ops, const itt_span* spans, uint64_t n_spans,
+                   int method, itt_op_total* op_totals, itt_iter_op_total* iter_totals, itt_op_cell** cells,
+                   uint64_t* n_cells) {
+  if (cells && !n_cells) return ITT_E_INVALID_ARGUMENT;
+  if (cells) *cells = nullptr;
+  if (n_cells) *n_cells = 0;
+  if (op_totals && n_ops) std::memset(op_totals, 0, static_cast<size_t>(n_ops) * sizeof(itt_op_total));
+  if (n_spans && (!tokens || !tok_start || !tok_end || !tok_kind || !spans)) return ITT_E_INVALID_ARGUMENT;
+  return guarded(ctx, [&](Ctx* c) {
+    if (n_spans == 0) return;
+    if (n >= 0xFFFFFFFFull) fail(ITT_E_INVALID_ARGUMENT, "metrics: sequence too long for 32-bit token indices");
+    int64_t prev_end = -1;
+    for (uint64_t i = 0; i < n_spans; ++i) {  // spans are approx_match output: disjoint and increasing
+      if (spans[i].start_token <= prev_end || spans[i].end_token < spans[i].start_token ||
+          static_cast<uint64_t>(spans[i].end_token) >= n)
+        fail(ITT_E_INVALID_ARGUMENT, "metrics: spans must be disjoint, increasing and inside the token sequence");
+      prev_end = spans[i].end_token;
+    }
+    auto up = [&](auto* src, auto& d) {  // host or device source (unified addressing)
+      d.alloc(c, n);
+      ITT_CUDA(cudaMemcpyAsync(d.p, src, n * sizeof(*src), cudaMemcpyDefault, c->stream));
+    };
+    DBuf<int32_t> dt;
+    DBuf<int64_t> ds, de;
+    DBuf<uint8_t> dk;
+    up(tokens, dt);
+    up(tok_start, ds);
+    up(tok_end, de);
+    up(tok_kind, dk);
+    {
+      DBuf<unsigned> bad(c, 1);
+      bad.zero();
+      // op ids must be < n_ops (the table is indexed by them)
+      launch(c, "opprof_check", n * 4.0, k_check_ops, dim3(grid_for(n, 256)), dim3(256), 0, dt.p, n, n_ops, bad.p);
+      if (read1(c, bad.p)) fail(ITT_E_INVALID_ARGUMENT, "metrics: op id outside [0, n_ops)");
+    }
+    SpanState sp;
+    sp.n = n_spans;
+    std::vector<uint32_t> s(n_spans), e(n_spans), x(n_spans);
+    for (uint64_t i = 0; i < n_spans; ++i) {
+      s[i] = static_cast<uint32_t>(spans[i].start_token);
+      e[i] = static_cast<uint32_t>(spans[i].end_token);
+      x[i] = static_cast<uint32_t>(spans[i].extra);
+    }
+    sp.start.alloc(c, n_spans);
+    sp.end.alloc(c, n_spans);
+    sp.extra.alloc(c, n_spans);
+    h2d(c, sp.start.p, s.data(), n_spans);
+    h2d(c, sp.end.p, e.data(), n_spans);
+    h2d(c, sp.extra.p, x.data(), n_spans);
+    ScanScratch sc;
+    radix::Scratch rs;
+    const OpProfile op =
+        op_profile(c, dt.p, ds.p, de.p, dk.p, n, n_ops, sp, method, cells != nullptr, op_totals, iter_totals, sc, rs);
+    if (cells) {
+      *cells = op.cells;
+      *n_cells = op.n;
+    }
+  });
+}
+
 // ------------------------------------------------------------------ matching
 int itt_approx_match(itt_ctx* ctx, const int32_t* tokens, uint64_t n, const int32_t* pattern, uint64_t m, int64_t k0,
                      itt_span** out, uint64_t* n_out) {
@@ -673,6 +743,17 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       iteration_aggregates(c, t.tok_start.p, t.tok_end.p, t.n_tok, t.htod_start.p, t.htod_end.p, t.htod_size.p, t.n_htod,
                            t.htod_range.p, sp,
                            L.rows, L.clamps, t.scan);
+      if (opts->flags & (ITT_ANALYZE_OP_PROFILE | ITT_ANALYZE_OP_CELLS)) {  // a12 (no reference counterpart)
+        StageTimer so(c, "op_profile");
+        L.op_totals = static_cast<itt_op_total*>(c->out_alloc(std::max<size_t>(1, t.n_names) * sizeof(itt_op_total)));
+        L.iter_op_totals =
+            static_cast<itt_iter_op_total*>(c->out_alloc(std::max<uint64_t>(1, sp.n) * sizeof(itt_iter_op_total)));
+        const OpProfile op = op_profile(c, t.tokens.p, t.tok_start.p, t.tok_end.p, t.tok_kind.p, t.n_tok, t.n_names, sp,
+                                        ITT_OP_PROFILE_AUTO, (opts->flags & ITT_ANALYZE_OP_CELLS) != 0, L.op_totals,
+                                        L.iter_op_totals, t.scan, t.rs);
+        L.n_op_cells = op.n;
+        L.op_cells = op.cells;
+      }
     }
     *out = a;
     hold.a = nullptr;
@@ -686,6 +767,9 @@ int itt_free_analysis(itt_ctx* ctx, itt_analysis* a) {
   for (uint32_t k = 0; k < a->n_loops; ++k) {
     std::free(a->loops[k].pattern_tokens);
     itt_free(ctx, a->loops[k].rows);
+    itt_free(ctx, a->loops[k].op_cells);
+    itt_free(ctx, a->loops[k].op_totals);
+    itt_free(ctx, a->loops[k].iter_op_totals);
   }
   std::free(a->loops);
   std::free(a);

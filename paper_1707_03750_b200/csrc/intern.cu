@@ -590,6 +590,7 @@ struct CompactF {
   uint32_t* tok_slot;
   int64_t* tok_start;
   int64_t* tok_end;
+  uint8_t* tok_kind;
   uint64_t* tok_record;  // optional
   uint32_t* tfirst;
   int64_t* htod_start;
@@ -615,6 +616,7 @@ struct CompactF {
       tok_slot[j] = sl;
       tok_start[j] = s;
       tok_end[j] = e;
+      tok_kind[j] = kind[i];
       if (tok_record) tok_record[j] = k;
       if (__ldcg(&tfirst[sl]) > j) atomicMin(&tfirst[sl], j);
     }
@@ -914,6 +916,7 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
   t.tok_slot.alloc(c, n_main + 1);
   t.tok_start.alloc(c, n_main + 1);
   t.tok_end.alloc(c, n_main + 1);
+  t.tok_kind.alloc(c, n_main + 1);
   t.tokens.alloc(c, n_main + 1);
   if (want_record_index) t.tok_record.alloc(c, n_main + 1);
   t.htod_start.alloc(c, n_htod + 1);
@@ -939,6 +942,7 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
              t.tok_slot.p,
              t.tok_start.p,
              t.tok_end.p,
+             t.tok_kind.p,
              want_record_index ? t.tok_record.p : nullptr,
              t.tfirst.p,
              t.htod_start.p,

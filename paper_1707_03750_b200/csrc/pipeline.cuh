@@ -61,6 +61,7 @@ struct TraceState {
   DBuf<uint32_t> tok_slot;
   DBuf<int32_t> tokens;
   DBuf<int64_t> tok_start, tok_end;
+  DBuf<uint8_t> tok_kind;     // ITT_KIND_* per token (a12)
   DBuf<uint64_t> tok_record;  // sorted-order record index (only for build_token_sequence)
   DBuf<int64_t> htod_start, htod_end, htod_size;
   DBuf<unsigned long long> htod_range;  // [min, max] HtoD end, sign bit flipped (set by compact_main)
@@ -134,5 +135,18 @@ void iteration_aggregates(Ctx* c, const int64_t* tok_start, const int64_t* tok_e
                           const unsigned long long* htod_range, const SpanState& spans,
                           itt_iter_row* rows /* host, spans.n */, itt_clamps& clamps,
                           ScanScratch& scan);
+
+// ------------------------------------------------------------------ a12 per-op profile (profile.cu)
+// a12 over device token columns and spans.  op_totals [n_ops] / iter_totals [spans.n]: host
+// buffers (either may be null).  With want_cells the (iteration, op) grid comes back in a pinned
+// block from c->out_alloc.  method: ITT_OP_PROFILE_*.
+struct OpProfile {
+  itt_op_cell* cells = nullptr;
+  uint64_t n = 0;
+};
+OpProfile op_profile(Ctx* c, const int32_t* tokens, const int64_t* tok_start, const int64_t* tok_end,
+                     const uint8_t* tok_kind, uint64_t n_tok, uint32_t n_ops, const SpanState& spans, int method,
+                     bool want_cells, itt_op_total* op_totals, itt_iter_op_total* iter_totals, ScanScratch& scan,
+                     radix::Scratch& rs);
 
 }  // namespace itt

@@ -68,6 +68,9 @@ def lib() -> C.CDLL:
         "itt_free_patterns": ([vp, P(abi.itt_pattern), C.c_uint32], C.c_int),
         "itt_approx_match": ([vp, P(C.c_int32), C.c_uint64, P(C.c_int32), C.c_uint64, C.c_int64, P(P(abi.itt_span)),
                               P(C.c_uint64)], C.c_int),
+        "itt_op_profile": ([vp, P(C.c_int32), P(C.c_int64), P(C.c_int64), P(C.c_uint8), C.c_uint64, C.c_uint32,
+                            P(abi.itt_span), C.c_uint64, C.c_int, vp, vp, P(P(abi.itt_op_cell)), P(C.c_uint64)],
+                           C.c_int),
         "itt_iteration_metrics": ([vp, P(abi.itt_records), P(C.c_uint64), C.c_uint64, P(abi.itt_span), C.c_uint64,
                                    P(P(abi.itt_iter_row)), P(abi.itt_clamps)], C.c_int),
         "itt_analyze": ([vp, P(abi.itt_records), P(abi.itt_analyze_opts), P(P(abi.itt_analysis))], C.c_int),
@@ -294,13 +297,20 @@ class Context:
         lib().itt_free(self.h, C.cast(rows, C.c_void_p))
         return out, (cl.negative_gap_clamps, cl.negative_interval_clamps)
 
-    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1) -> dict:
+    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1, op_profile=False) -> dict:
         """itt_analyze: device pipeline up to the per-loop integer aggregates.  The per-iteration
-        rows are zero-copy numpy views of the library's pinned output blocks; the analysis is
-        released (blocks back to the context) when the last view is dropped."""
+        rows (and the a12 op profile: op_profile=True for the per-op / per-iteration totals,
+        "cells" for the (iteration, op) grid as well) are zero-copy numpy views of the library's
+        pinned output blocks; the analysis is released (blocks back to the context) when the
+        last view is dropped."""
         c = recs.c()
         lp = (C.c_int64 * max(1, len(loops)))(*loops)
-        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream)
+        flags = 0
+        if op_profile:
+            flags |= abi.ITT_ANALYZE_OP_PROFILE
+        if op_profile == "cells":
+            flags |= abi.ITT_ANALYZE_OP_CELLS
+        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream, flags)
         out = P(abi.itt_analysis)()
         self._check(lib().itt_analyze(self.h, C.byref(c), C.byref(opts), C.byref(out)))
         owner = _AnalysisOwner(self, out)
@@ -327,7 +337,48 @@ class Context:
                 pattern_count=L.pattern_count, epsilon_used=L.epsilon_used, first_token=L.first_token,
                 k0_used=L.k0_used, rows=rows,
                 clamps=(L.clamps.negative_gap_clamps, L.clamps.negative_interval_clamps)))
+            if op_profile:
+                res["loops"][-1]["op_totals"] = _view(L.op_totals, a.n_names, abi.OP_TOTAL_DTYPE, owner)
+                res["loops"][-1]["iter_op_totals"] = _view(L.iter_op_totals, L.n_iterations, abi.ITER_OP_TOTAL_DTYPE,
+                                                           owner)
+                res["loops"][-1]["op_cells"] = _view(L.op_cells, L.n_op_cells, abi.OP_CELL_DTYPE, owner)
         return res
+
+    def op_profile(self, tokens, tok_start, tok_end, tok_kind, n_ops, spans, method=abi.ITT_OP_PROFILE_AUTO,
+                   cells=True):
+        """itt_op_profile (a12) over token-level arrays -> (cells | None, op_totals, iter_totals)."""
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        ts = np.ascontiguousarray(tok_start, dtype=np.int64)
+        te = np.ascontiguousarray(tok_end, dtype=np.int64)
+        tk = np.ascontiguousarray(tok_kind, dtype=np.uint8)
+        sp = (abi.itt_span * max(1, len(spans)))()
+        for i, s in enumerate(spans):
+            sp[i].start_token, sp[i].end_token, sp[i].extra = int(s[0]), int(s[1]), int(s[2])
+        out = P(abi.itt_op_cell)()
+        cnt = C.c_uint64()
+        ot = np.zeros(max(1, n_ops), abi.OP_TOTAL_DTYPE)
+        it = np.zeros(max(1, len(spans)), abi.ITER_OP_TOTAL_DTYPE)
+        self._check(lib().itt_op_profile(self.h, _ptr(t, C.c_int32), _ptr(ts, C.c_int64), _ptr(te, C.c_int64),
+                                         _ptr(tk, C.c_uint8), t.shape[0], n_ops, sp, len(spans), method,
+                                         ot.ctypes.data, it.ctypes.data, C.byref(out) if cells else None,
+                                         C.byref(cnt)))
+        res = None
+        if cells:
+            n = cnt.value
+            res = np.zeros(n, abi.OP_CELL_DTYPE)
+            if n:
+                C.memmove(res.ctypes.data, out, n * C.sizeof(abi.itt_op_cell))
+            lib().itt_free(self.h, out)
+        return res, ot[:n_ops], it[:len(spans)]
+
+
+def _view(ptr, n, dtype, owner):
+    """Zero-copy numpy view of a library-owned pinned block (kept alive by `owner`)."""
+    if not n or not ptr:
+        return np.zeros(0, dtype)
+    buf = (C.c_uint8 * (n * dtype.itemsize)).from_address(C.cast(ptr, C.c_void_p).value)
+    buf._owner = owner
+    return np.frombuffer(buf, dtype=dtype)
 
 
 class _AnalysisOwner:

@@ -87,6 +87,7 @@ class AnalysisResult:  # pipeline.hpp:27-30 (+ the rendered outputs)
     loops: list
     details: list
     warnings: list
+    op_profiles: list = field(default_factory=list)  # a12, one OpProfile per loop when requested
 
     def summary_json(self) -> str:
         return render_summary(self)
@@ -179,11 +180,14 @@ def rows_to_metrics(rows) -> list:
 
 def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Optional[int] = None,
                   theta_copy: float = 0.10, theta_cpu: float = 10.0, main_stream: Optional[int] = None,
-                  trace_label: str = "trace.csv", device_labels=None, names=None) -> AnalysisResult:
-    """analyze_trace (pipeline.hpp:34-134): device pipeline + host finish in reference order."""
+                  trace_label: str = "trace.csv", device_labels=None, names=None,
+                  op_profile=False) -> AnalysisResult:
+    """analyze_trace (pipeline.hpp:34-134): device pipeline + host finish in reference order.
+    op_profile=True adds the a12 second-level per-op profile of every loop ("cells": with the
+    (iteration, op) grid); no reference counterpart, and the reference's own outputs are unchanged."""
     try:
         raw = ctx.analyze_raw(recs, list(loops), epsilon0, -1 if k0 is None else k0,
-                              -1 if main_stream is None else main_stream)
+                              -1 if main_stream is None else main_stream, op_profile=op_profile)
     except IttError as e:
         raise AnalyzeError(e.kind, str(e)) from e
     label = (lambda d: device_labels[d]) if device_labels is not None else (lambda d: "dev%05u" % d)
@@ -220,8 +224,62 @@ def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Option
                                        L["epsilon_used"], L["first_token"], L["k0_used"], len(items), summ,
                                        diagnose(summ, theta_copy, theta_cpu)))
         details.append(items)
+    profiles = [OpProfile(L["op_cells"], L["op_totals"], L["iter_op_totals"], name_of) for L in raw["loops"]] \
+        if op_profile else []
     return AnalysisResult(trace_label, epsilon0, theta_copy, theta_cpu, k0, main_stream, raw["streams"],
-                          raw["main_stream"], loop_reports, details, warnings)
+                          raw["main_stream"], loop_reports, details, warnings, profiles)
+
+
+# ---------------------------------------------------------------- a12 second-level profile
+@dataclass
+class OpProfile:
+    """Per-op x per-iteration profile (definition in itertrace_cuda.h).
+    per_op: abi.OP_TOTAL_DTYPE indexed by op id; per_iteration: abi.ITER_OP_TOTAL_DTYPE;
+    cells: abi.OP_CELL_DTYPE (empty unless the cell grid was requested)."""
+    cells: object
+    per_op: object
+    per_iteration: object
+    names: Optional[list] = None
+
+    def per_op_csv(self) -> str:
+        return op_profile_csv(self)
+
+
+def reduce_cells(cells, n_ops: int, n_iterations: int):
+    """The two reductions of a cell grid (exact int64 sums) -> (per_op, per_iteration)."""
+    import numpy as np
+    per_op = np.zeros(n_ops, abi.OP_TOTAL_DTYPE)
+    per_it = np.zeros(n_iterations, abi.ITER_OP_TOTAL_DTYPE)
+    if len(cells):
+        op = cells["op"].astype(np.int64)
+        it = cells["iteration"].astype(np.int64)
+        per_op["iterations"] = np.bincount(op, minlength=n_ops)
+        per_it["distinct_ops"] = np.bincount(it, minlength=n_iterations)
+        for col in ("count", "kernel_ns", "memcpy_ns", "idle_ns"):
+            a = np.zeros(n_ops, np.int64)
+            np.add.at(a, op, cells[col].astype(np.int64))
+            per_op[col] = a
+            if col != "count":
+                b = np.zeros(n_iterations, np.int64)
+                np.add.at(b, it, cells[col].astype(np.int64))
+                per_it[col] = b
+    return per_op, per_it
+
+
+def op_profile_csv(p: OpProfile) -> str:
+    """Per-op table of the second-level profile: ops occurring in some iteration, by op id."""
+    lines = ["op,name,iterations,count,kernel_ns,memcpy_ns,idle_ns,mean_kernel_ns,mean_memcpy_ns,mean_idle_ns"]
+    for v, r in enumerate(p.per_op):
+        c = int(r["count"])
+        if c == 0:
+            continue
+        nm = p.names[v] if p.names is not None else str(v)
+        if any(ch in nm for ch in ',"\n'):
+            nm = '"' + nm.replace('"', '""') + '"'
+        lines.append("%d,%s,%d,%d,%d,%d,%d,%s,%s,%s" % (
+            v, nm, int(r["iterations"]), c, int(r["kernel_ns"]), int(r["memcpy_ns"]), int(r["idle_ns"]),
+            fmt6(int(r["kernel_ns"]) / c), fmt6(int(r["memcpy_ns"]) / c), fmt6(int(r["idle_ns"]) / c)))
+    return "\n".join(lines) + "\n"
 
 
 # ---------------------------------------------------------------- rendering (report.hpp)

@@ -8,7 +8,7 @@ iters = synth.CONFIGS[cfg]["iterations"]
 ctx = cuda.Context(0)
 d = ctx.upload(recs)
 for _ in range(3):
-    ctx.analyze_raw(d, [iters])
+    ctx.analyze_raw(d, [iters], op_profile=bool(os.environ.get('OPPROF')))
 os.environ["ITT_TRACE"] = "1"
 print("---- traced run", file=sys.stderr)
-t = time.perf_counter(); ctx.analyze_raw(d, [iters]); print("total %.2f ms" % (1000 * (time.perf_counter() - t)), file=sys.stderr)
+t = time.perf_counter(); ctx.analyze_raw(d, [iters], op_profile=bool(os.environ.get('OPPROF'))); print("total %.2f ms" % (1000 * (time.perf_counter() - t)), file=sys.stderr)

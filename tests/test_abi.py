@@ -39,7 +39,7 @@ def test_product_library_is_sm100a_only_and_has_no_oracle():
 
 STRUCTS = ["itt_records", "itt_kernel_stat", "itt_stream_summary", "itt_census", "itt_tokens", "itt_repeat",
            "itt_mining_cfg", "itt_pattern", "itt_span", "itt_iter_row", "itt_clamps", "itt_analyze_opts",
-           "itt_loop_result", "itt_analysis"]
+           "itt_loop_result", "itt_analysis", "itt_op_cell"]
 
 
 def test_ctypes_layouts_match_the_header():
