@@ -39,10 +39,13 @@ WORKLOADS = {
     "C3": ("C3: 100M-event trace, 20K iterations x 5000 ops, V=4096 (+16 init)", dict(), 20_000),
     "C4": ("C4: batch of 8192 independent 100K-event traces (500 iterations x 200 ops, V=150 + 16 init), "
            "sharded across ranks", dict(), 500),
+    "C5": ("C5: 1B-event trace, 500K iterations x 2000 ops, V=4096 (+16 init), on ONE B200: numeric columns "
+           "resident in HBM, the 80 GB of names read in place from pinned host memory by the hash pass (PCIe)",
+           dict(), 500_000),
 }
 # bounded CPU samples (same generator and shape, fewer iterations)
-CPU_SAMPLE_ITERS = {"C1": 100, "C2": 10_000, "C3": 400}
-REF_ARM_ITERS = {"C1": 100, "C2": 2_000, "C3": 100}  # ~2 s per reference step on one core
+CPU_SAMPLE_ITERS = {"C1": 100, "C2": 10_000, "C3": 400, "C5": 1_000}
+REF_ARM_ITERS = {"C1": 100, "C2": 2_000, "C3": 100, "C5": 250}  # ~2 s per reference step on one core
 
 
 def log(*a):
@@ -237,6 +240,8 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--iterations", type=int, default=None,
+                    help="override the workload's iteration count (smaller dry runs of C3/C5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
@@ -275,10 +280,14 @@ def main():
     ctx = itt.Context(dev)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", dev))
     t_gen = time.perf_counter()
-    recs, info = make_trace(args.config)
+    if args.iterations:
+        iters = args.iterations
+        workload += f" [DRY RUN: iterations overridden to {iters}]"
+    recs, info = make_trace(args.config, args.iterations)
     log(f"[rank {rank}] generated {args.config}: {info} in {time.perf_counter() - t_gen:.1f}s")
     n_events = info["n"]
-    drecs = ctx.upload(recs)
+    names_mapped = args.config == "C5"  # 80 GB of names do not fit in HBM beside the pipeline
+    drecs = ctx.upload(recs, names_mapped=names_mapped)
 
     def step_device():
         return ctx.analyze_raw(drecs, [iters])
@@ -351,6 +360,13 @@ def main():
                         "GBps": (v["bytes"] / (v["total_ms"] / 1000.0) / 1e9) if v["total_ms"] > 0 else None}
                     for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])}
 
+    # ---- device memory: resident columns + the pipeline's high-water mark
+    used0, _ = ctx.mem_stats(reset=True)
+    step_device()
+    _, high = ctx.mem_stats()
+    memory = {"resident_columns_gb": drecs.nbytes / 1e9, "pool_high_water_gb": high / 1e9,
+              "pipeline_peak_gb": (high - used0) / 1e9}
+
     # ---- a12 (the north star's per-op x per-iteration profile; no reference counterpart, so it
     # is reported as the increment over the reference-equivalent step, not inside `value`)
     def step_a12():
@@ -369,10 +385,13 @@ def main():
     # ---- e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off,
-                recs.name_bytes] + ([recs.device] if recs.device is not None else [])
+        cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off] + \
+            ([] if names_mapped else [recs.name_bytes]) + ([recs.device] if recs.device is not None else [])
         for a in cols:
             ctx.register_host(a)
+        if names_mapped:  # still registered by drecs; read in place again
+            from paper_1707_03750_b200 import abi as _abi
+            recs.mem = _abi.MEM_HOST_MAPPED_NAMES
         try:
             def step_host():
                 return ctx.analyze_raw(recs, [iters])
@@ -408,6 +427,7 @@ def main():
                                  "iterations_found": int(L["rows"].shape[0])}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(launches), "kernels": kernel_table, "op_profile": op_profile,
+            "memory": memory,
         }
         print(json.dumps(line), flush=True)
     drecs.free()

@@ -28,6 +28,7 @@ REC_HAS_SIZE = 0x1
 REC_HAS_THROUGHPUT = 0x2
 MEM_HOST = 0
 MEM_DEVICE = 1
+MEM_HOST_MAPPED_NAMES = 2  # names read in place from pinned host memory
 ORDER_UNKNOWN = 0
 ORDER_SORTED = 1
 
@@ -277,6 +278,7 @@ class Records:
         if self.name_bytes.size == 0:
             self.name_bytes = np.zeros(1, np.uint8)
         self.order = order
+        self.mem = MEM_HOST  # MEM_HOST_MAPPED_NAMES once name_bytes is registered (see Context.map_names)
         self._keepalive = keepalive
         for a in (self.duration_ns, self.stream, self.size_bytes, self.flags):
             assert a.shape[0] == n
@@ -292,7 +294,7 @@ class Records:
     def c(self) -> itt_records:
         return itt_records(self.n, _ptr(self.start_ns), _ptr(self.duration_ns), _ptr(self.size_bytes),
                            _ptr(self.flags), _ptr(self.stream), _ptr(self.device), _ptr(self.name_off),
-                           _ptr(self.name_bytes), MEM_HOST, self.order)
+                           _ptr(self.name_bytes), self.mem, self.order)
 
     def nbytes(self) -> int:
         tot = sum(a.nbytes for a in (self.start_ns, self.duration_ns, self.size_bytes, self.flags, self.stream,

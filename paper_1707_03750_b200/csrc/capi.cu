@@ -225,6 +225,21 @@ int itt_ctx_kernel_stats(itt_ctx* ctx, itt_kernel_stat* out, uint32_t cap, uint3
     if (n_out) *n_out = i;
   });
 }
+int itt_ctx_mem_stats(itt_ctx* ctx, uint64_t* used, uint64_t* used_high, int reset) {
+  return guarded(ctx, [&](Ctx* c) {
+    c->sync();
+    uint64_t u = 0, h = 0;
+    ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, &u));
+    ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemHigh, &h));
+    if (used) *used = u;
+    if (used_high) *used_high = h;
+    if (reset) {
+      uint64_t z = 0;
+      ITT_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrUsedMemHigh, &z));
+    }
+  });
+}
+
 int itt_ctx_launch_count(itt_ctx* ctx, uint64_t* out) {
   if (!ctx || !out) return ITT_E_INVALID_ARGUMENT;
   *out = ctx->c.launches;
@@ -247,6 +262,10 @@ int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
 }
 int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes) {
   return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault)); });
+}
+int itt_host_device_pointer(itt_ctx* ctx, void* host, void** dev) {
+  if (!dev) return ITT_E_INVALID_ARGUMENT;
+  return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostGetDevicePointer(dev, host, 0)); });
 }
 int itt_host_unregister(itt_ctx* ctx, void* p) {
   return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostUnregister(p)); });
@@ -666,6 +685,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
         fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
       renumber_tokens(t);
       overlaps = count_overlaps(t);
+      release_rows(t);  // row-level arrays are dead from here: HBM for the suffix array
     }
     // mining over one shared SA / LCP / interval set (pipeline.hpp:81-91)
     std::vector<itt_mining_cfg> cfgs;

@@ -713,6 +713,9 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
     d.name_bytes = r->name_bytes;
     return;
   }
+  if (r->mem != ITT_MEM_HOST && r->mem != ITT_MEM_HOST_MAPPED_NAMES)
+    fail(ITT_E_INVALID_ARGUMENT, "ingest: unknown itt_records.mem");
+  const bool mapped = r->mem == ITT_MEM_HOST_MAPPED_NAMES;
   uint64_t nb = 0;
   if (n) std::memcpy(&nb, &r->name_off[n], sizeof(nb));
   d.o_start.alloc(c, n);
@@ -721,14 +724,14 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.o_flags.alloc(c, n);
   d.o_stream.alloc(c, n);
   d.o_off.alloc(c, n + 1);
-  d.o_names.alloc(c, nb + 16);
+  if (!mapped) d.o_names.alloc(c, nb + 16);
   h2d(c, d.o_start.p, r->start_ns, n);
   h2d(c, d.o_dur.p, r->duration_ns, n);
   h2d(c, d.o_size.p, r->size_bytes, n);
   h2d(c, d.o_flags.p, r->flags, n);
   h2d(c, d.o_stream.p, r->stream, n);
   h2d(c, d.o_off.p, r->name_off, n + 1);
-  h2d(c, d.o_names.p, r->name_bytes, nb);
+  if (!mapped) h2d(c, d.o_names.p, r->name_bytes, nb);
   d.start = d.o_start.p;
   d.dur = d.o_dur.p;
   d.size = d.o_size.p;
@@ -736,11 +739,34 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.stream = d.o_stream.p;
   d.name_off = d.o_off.p;
   d.name_bytes = d.o_names.p;
+  if (mapped) {
+    if (reinterpret_cast<uintptr_t>(r->name_bytes) & 15)
+      fail(ITT_E_INVALID_ARGUMENT, "ingest: mapped name_bytes must be 16-byte aligned");
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(r->name_bytes), 0) != cudaSuccess) {
+      cudaGetLastError();
+      fail(ITT_E_INVALID_ARGUMENT, "ingest: mapped name_bytes must be pinned host memory (cudaHostRegister)");
+    }
+    d.name_bytes = static_cast<const uint8_t*>(dp);
+  }
   if (r->device) {
     d.o_device.alloc(c, n);
     h2d(c, d.o_device.p, r->device, n);
     d.device = d.o_device.p;
   }
+}
+
+void release_rows(TraceState& t) {
+  t.perm.release();
+  t.slot.release();
+  t.kind.release();
+  t.tok_slot.release();
+  t.tfirst.release();
+  DevRecords& d = t.rec;
+  d.o_start.release(), d.o_dur.release(), d.o_size.release(), d.o_flags.release(), d.o_names.release();
+  d.o_stream.release(), d.o_device.release(), d.o_off.release();
+  d.start = d.dur = d.size = nullptr;
+  d.flags = nullptr, d.stream = nullptr, d.device = nullptr, d.name_off = nullptr, d.name_bytes = nullptr;
 }
 
 void order_records(TraceState& t) {

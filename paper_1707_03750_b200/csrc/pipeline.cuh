@@ -78,6 +78,7 @@ void stream_census(TraceState& t);             // summaries over the kept record
 void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index);
 void renumber_tokens(TraceState& t);           // first-appearance ids + token map
 int64_t count_overlaps(TraceState& t);         // count_interval_overlaps on the compacted main stream
+void release_rows(TraceState& t);              // free per-record arrays (and owned column copies) after tokens
 
 // ------------------------------------------------------------------ suffix array (sa.cu)
 struct SuffixState {

@@ -61,13 +61,13 @@ std::string make_name(Rng& rng, int64_t id, int64_t lmin, int64_t lmax) {
   return s;
 }
 
-struct Rec {
+struct Rec {  // 48 bytes: a 1B-event trace keeps its records in ~48 GB of host RAM
   int64_t start, dur, size;
-  uint8_t flags;
-  uint32_t stream;
-  uint16_t device;
-  int32_t name;  // index into names table
   uint64_t seq;
+  uint32_t stream;
+  int32_t name;  // index into names table
+  uint16_t device;
+  uint8_t flags;
 };
 
 }  // namespace
@@ -139,7 +139,10 @@ extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out
   recs.reserve(static_cast<size_t>(est * 1.02));
   uint64_t seq = 0;
   auto push = [&](int64_t start, int64_t dur, int64_t size, uint8_t flags, uint32_t stream, int32_t name) {
-    recs.push_back(Rec{start, dur, size, flags, stream, 0, name, seq++});
+    Rec r;
+    r.start = start, r.dur = dur, r.size = size, r.seq = seq++;
+    r.stream = stream, r.name = name, r.device = 0, r.flags = flags;
+    recs.push_back(r);
   };
   const uint8_t SZ = 0x1, TP = 0x2;
 
@@ -204,10 +207,24 @@ extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out
       recs.push_back(r);
     }
   }
-  std::stable_sort(recs.begin(), recs.end(), [](const Rec& a, const Rec& b) {
-    if (a.start != b.start) return a.start < b.start;
-    return a.seq < b.seq;
-  });
+  // (start, seq) is unique, so any sort gives the stable order.  Without appended copies the
+  // records are emitted nearly sorted (an HtoD copy may precede the previous drain), and an
+  // in-place insertion sort is O(n) with no temporary buffer.
+  auto before = [](const Rec& a, const Rec& b) { return a.start != b.start ? a.start < b.start : a.seq < b.seq; };
+  if (cfg->extra_stream_frac > 0.0 || cfg->minority_frac > 0.0) {
+    std::sort(recs.begin(), recs.end(), before);
+  } else {
+    for (size_t i = 1; i < recs.size(); ++i) {
+      if (!before(recs[i], recs[i - 1])) continue;
+      Rec x = recs[i];
+      size_t j = i;
+      while (j > 0 && before(x, recs[j - 1])) {
+        recs[j] = recs[j - 1];
+        --j;
+      }
+      recs[j] = x;
+    }
+  }
   if (cfg->shuffle_window > 1) {
     const size_t w = static_cast<size_t>(cfg->shuffle_window);
     for (size_t b = 0; b < recs.size(); b += w) {
@@ -216,6 +233,8 @@ extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out
     }
   }
 
+  // Two phases keep the peak near max(records + numeric columns, numeric columns + names):
+  // the record vector is released before the name bytes are materialised.
   const uint64_t n = recs.size();
   uint64_t nb = 0;
   for (const auto& r : recs) nb += names[static_cast<size_t>(r.name)].size();
@@ -227,10 +246,10 @@ extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out
   out->stream = static_cast<uint32_t*>(std::malloc(n * 4));
   out->device = static_cast<uint16_t*>(std::malloc(n * 2));
   out->name_off = static_cast<uint64_t*>(std::malloc((n + 1) * 8));
-  out->name_bytes = static_cast<uint8_t*>(std::malloc(nb ? nb : 1));
-  out->name_bytes_len = nb;
-  if (!out->start_ns || !out->duration_ns || !out->size_bytes || !out->flags || !out->stream || !out->device || !out->name_off ||
-      !out->name_bytes) {
+  int32_t* name_id = static_cast<int32_t*>(std::malloc(n * 4 + 4));
+  if (!out->start_ns || !out->duration_ns || !out->size_bytes || !out->flags || !out->stream || !out->device ||
+      !out->name_off || !name_id) {
+    std::free(name_id);
     itt_synth_free(out);
     return 2;
   }
@@ -244,13 +263,26 @@ extern "C" int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out
     out->stream[i] = r.stream;
     out->device[i] = r.device;
     out->name_off[i] = off;
-    const std::string& s = names[static_cast<size_t>(r.name)];
-    std::memcpy(out->name_bytes + off, s.data(), s.size());
-    off += s.size();
+    name_id[i] = r.name;
+    off += names[static_cast<size_t>(r.name)].size();
     if (r.stream == kMain && r.device == 0) ++out->n_main;
     if (r.name == kHtoD && r.device == 0) ++out->n_htod;
   }
   out->name_off[n] = off;
+  std::vector<Rec>().swap(recs);
+  // 16 bytes of slack: the device reads names in 16-byte chunks (also in place, ITT_MEM_HOST_MAPPED_NAMES)
+  out->name_bytes = static_cast<uint8_t*>(std::calloc(nb + 16, 1));
+  out->name_bytes_len = nb;
+  if (!out->name_bytes) {
+    std::free(name_id);
+    itt_synth_free(out);
+    return 2;
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const std::string& s = names[static_cast<size_t>(name_id[i])];
+    std::memcpy(out->name_bytes + out->name_off[i], s.data(), s.size());
+  }
+  std::free(name_id);
   return 0;
 }
 

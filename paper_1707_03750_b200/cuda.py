@@ -47,6 +47,8 @@ def lib() -> C.CDLL:
         "itt_ctx_reset_stats": ([vp], C.c_int),
         "itt_ctx_kernel_stats": ([vp, P(abi.itt_kernel_stat), C.c_uint32, P(C.c_uint32)], C.c_int),
         "itt_ctx_launch_count": ([vp, P(C.c_uint64)], C.c_int),
+        "itt_host_device_pointer": ([vp, vp, P(vp)], C.c_int),
+        "itt_ctx_mem_stats": ([vp, P(C.c_uint64), P(C.c_uint64), C.c_int], C.c_int),
         "itt_device_alloc": ([vp, C.c_uint64, P(vp)], C.c_int),
         "itt_device_free": ([vp, vp], C.c_int),
         "itt_memcpy_h2d": ([vp, vp, vp, C.c_uint64], C.c_int),
@@ -102,23 +104,35 @@ def _ptr(a, t):
 
 
 class DeviceRecords:
-    """Trace columns resident in HBM (allocated through the context)."""
+    """Trace columns resident in HBM (allocated through the context).  names_mapped=True keeps
+    name_bytes in (registered, pinned) host memory, read in place by the hash pass over PCIe —
+    for traces whose names do not fit in HBM next to the pipeline (C5)."""
 
-    def __init__(self, ctx: "Context", recs: abi.Records):
+    def __init__(self, ctx: "Context", recs: abi.Records, names_mapped: bool = False):
         self.ctx = ctx
         self.n = recs.n
         self.order = recs.order
         self.bufs = {}
+        self.mapped = None
         cols = dict(start_ns=recs.start_ns, duration_ns=recs.duration_ns, size_bytes=recs.size_bytes, flags=recs.flags,
                     stream=recs.stream, name_off=recs.name_off, name_bytes=recs.name_bytes)
         if recs.device is not None:
             cols["device"] = recs.device
+        if names_mapped:
+            a = cols.pop("name_bytes")
+            ctx.register_host(a)
+            self.mapped = a
+            p = C.c_void_p()
+            ctx._check(lib().itt_host_device_pointer(ctx.h, a.ctypes.data, C.byref(p)))
+            self.names_ptr = p
         for k, a in cols.items():
             p = C.c_void_p()
             ctx._check(lib().itt_device_alloc(ctx.h, max(1, a.nbytes), C.byref(p)))
             ctx._check(lib().itt_memcpy_h2d(ctx.h, p, a.ctypes.data, a.nbytes))
             self.bufs[k] = p
-        self.nbytes = sum(a.nbytes for a in cols.values())
+        if names_mapped:
+            self.bufs["name_bytes"] = self.names_ptr
+        self.nbytes = sum(a.nbytes for a in cols.values())  # bytes resident in HBM
 
     def c(self) -> abi.itt_records:
         b = self.bufs
@@ -126,8 +140,12 @@ class DeviceRecords:
                                b.get("device"), b["name_off"], b["name_bytes"], abi.MEM_DEVICE, self.order)
 
     def free(self):
-        for p in self.bufs.values():
-            lib().itt_device_free(self.ctx.h, p)
+        for k, p in self.bufs.items():
+            if not (k == "name_bytes" and self.mapped is not None):
+                lib().itt_device_free(self.ctx.h, p)
+        if self.mapped is not None:
+            self.ctx.unregister_host(self.mapped)
+            self.mapped = None
         self.bufs = {}
 
 
@@ -174,6 +192,12 @@ class Context:
         self._check(lib().itt_ctx_launch_count(self.h, C.byref(v)))
         return v.value
 
+    def mem_stats(self, reset=False) -> tuple:
+        """(bytes in use, high-water mark) of the context's device pool."""
+        u, h = C.c_uint64(), C.c_uint64()
+        self._check(lib().itt_ctx_mem_stats(self.h, C.byref(u), C.byref(h), 1 if reset else 0))
+        return u.value, h.value
+
     def stream_ptr(self) -> int:
         v = C.c_void_p()
         self._check(lib().itt_ctx_stream(self.h, C.byref(v)))
@@ -182,8 +206,8 @@ class Context:
     def synchronize(self):
         self._check(lib().itt_ctx_synchronize(self.h))
 
-    def upload(self, recs: abi.Records) -> DeviceRecords:
-        return DeviceRecords(self, recs)
+    def upload(self, recs: abi.Records, names_mapped: bool = False) -> DeviceRecords:
+        return DeviceRecords(self, recs, names_mapped)
 
     def register_host(self, arr: np.ndarray):
         self._check(lib().itt_host_register(self.h, arr.ctypes.data, arr.nbytes))

@@ -284,3 +284,26 @@ def test_device_resident_inputs_match_host_inputs(ctx):
         d.free()
     assert a["streams"] == b["streams"] and a["name_row"] == b["name_row"]
     assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
+
+
+def test_mapped_host_names_match_copied_names(ctx):
+    """ITT_MEM_HOST_MAPPED_NAMES: the hash pass reads names in place from pinned host memory
+    (the C5 layout, where names do not fit in HBM next to the pipeline) — same results."""
+    from paper_1707_03750_b200 import abi
+    recs, _ = synth.generate_config("C1", noise_frac=0.05, shuffle_window=64, seed=9, name_max=160)
+    a = ctx.analyze_raw(recs, [100])
+    ctx.register_host(recs.name_bytes)
+    try:
+        recs.mem = abi.MEM_HOST_MAPPED_NAMES
+        b = ctx.analyze_raw(recs, [100], op_profile=True)
+    finally:
+        recs.mem = abi.MEM_HOST
+        ctx.unregister_host(recs.name_bytes)
+    assert a["streams"] == b["streams"] and a["name_row"] == b["name_row"]
+    assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
+    recs.mem = abi.MEM_HOST_MAPPED_NAMES  # not registered: refused, no silent copy
+    try:
+        with pytest.raises(cuda.IttError):
+            ctx.analyze_raw(recs, [100])
+    finally:
+        recs.mem = abi.MEM_HOST
