@@ -40,7 +40,7 @@ WORKLOADS = {
     "C4": ("C4: batch of 8192 independent 100K-event traces (500 iterations x 200 ops, V=150 + 16 init), "
            "sharded across ranks", dict(), 500),
     "C5": ("C5: 1B-event trace, 500K iterations x 2000 ops, V=4096 (+16 init), on ONE B200: numeric columns "
-           "resident in HBM, the 80 GB of names read in place from pinned host memory by the hash pass (PCIe)",
+           "resident in HBM, the 80 GB of names streamed from pinned host memory through 2 x 1 GB windows into the hash pass",
            dict(), 500_000),
 }
 # bounded CPU samples (same generator and shape, fewer iterations)
@@ -286,8 +286,8 @@ def main():
     recs, info = make_trace(args.config, args.iterations)
     log(f"[rank {rank}] generated {args.config}: {info} in {time.perf_counter() - t_gen:.1f}s")
     n_events = info["n"]
-    names_mapped = args.config == "C5"  # 80 GB of names do not fit in HBM beside the pipeline
-    drecs = ctx.upload(recs, names_mapped=names_mapped)
+    names_host = args.config == "C5"  # 80 GB of names do not fit in HBM beside the pipeline: streamed
+    drecs = ctx.upload(recs, names_host=names_host)
 
     def step_device():
         return ctx.analyze_raw(drecs, [iters])
@@ -386,12 +386,12 @@ def main():
     e2e = None
     if not args.no_e2e:
         cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off] + \
-            ([] if names_mapped else [recs.name_bytes]) + ([recs.device] if recs.device is not None else [])
+            ([] if names_host else [recs.name_bytes]) + ([recs.device] if recs.device is not None else [])
         for a in cols:
             ctx.register_host(a)
-        if names_mapped:  # still registered by drecs; read in place again
+        if names_host:  # still registered by drecs; streamed again
             from paper_1707_03750_b200 import abi as _abi
-            recs.mem = _abi.MEM_HOST_MAPPED_NAMES
+            recs.mem = _abi.MEM_HOST_STREAM_NAMES
         try:
             def step_host():
                 return ctx.analyze_raw(recs, [iters])

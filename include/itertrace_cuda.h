@@ -66,10 +66,13 @@ enum { ITT_CLASS_MAIN = 0, ITT_CLASS_COPY_HTOD, ITT_CLASS_COPY_DTOH, ITT_CLASS_C
 
 #define ITT_MEM_HOST 0
 #define ITT_MEM_DEVICE 1
-/* ITT_MEM_HOST except name_bytes, which the device reads in place from pinned host memory
- * (cudaHostRegister'd or cudaMallocHost; 16-byte-aligned base, 16 readable bytes past the end):
- * no device copy of the names, for traces whose names do not fit next to the pipeline in HBM */
-#define ITT_MEM_HOST_MAPPED_NAMES 2
+/* Names that do not fit in HBM next to the pipeline (C5: 80 GB): name_bytes stays in host memory
+ * (pinned — cudaHostRegister'd or cudaMallocHost — for overlapped DMA) and is streamed through
+ * two bounded device windows (1 GiB, ITT_STREAM_CHUNK overrides), chunk by chunk, into the hash
+ * pass; the distinct names' bytes are kept in a small device arena.  The other columns are host
+ * memory (ITT_MEM_HOST_STREAM_NAMES) or device memory (ITT_MEM_DEVICE_HOST_NAMES). */
+#define ITT_MEM_HOST_STREAM_NAMES 2
+#define ITT_MEM_DEVICE_HOST_NAMES 3
 
 #define ITT_ORDER_UNKNOWN 0 /* rows in source order; the library stable-sorts by (start, row) */
 #define ITT_ORDER_SORTED 1  /* rows already in NormalizedTrace order (ingest.hpp:396-400) */
@@ -91,7 +94,7 @@ typedef struct itt_records {
   const uint16_t* device;     /* [n] device-label rank; NULL = single device 0 */
   const uint64_t* name_off;   /* [n+1]; name of row i = name_bytes[name_off[i] .. name_off[i+1]) */
   const uint8_t* name_bytes;  /* [name_off[n]] */
-  int32_t mem;                /* ITT_MEM_HOST, ITT_MEM_DEVICE (all pointers alike) or ITT_MEM_HOST_MAPPED_NAMES */
+  int32_t mem;                /* ITT_MEM_HOST / ITT_MEM_DEVICE (all pointers alike), or a *_NAMES mode */
   int32_t order;              /* ITT_ORDER_UNKNOWN or ITT_ORDER_SORTED */
 } itt_records;
 
@@ -126,9 +129,6 @@ int itt_memcpy_h2d(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes);
 int itt_host_unregister(itt_ctx* ctx, void* p);
-/* device-side address of registered / pinned host memory (for ITT_MEM_DEVICE records whose
- * name_bytes stay in host memory and are read over PCIe) */
-int itt_host_device_pointer(itt_ctx* ctx, void* host, void** dev);
 int itt_ctx_synchronize(itt_ctx* ctx);
 /* the context's cudaStream_t (for callers that time with CUDA events on it) */
 int itt_ctx_stream(itt_ctx* ctx, void** stream);

@@ -28,7 +28,8 @@ REC_HAS_SIZE = 0x1
 REC_HAS_THROUGHPUT = 0x2
 MEM_HOST = 0
 MEM_DEVICE = 1
-MEM_HOST_MAPPED_NAMES = 2  # names read in place from pinned host memory
+MEM_HOST_STREAM_NAMES = 2  # host columns; names streamed through bounded device windows
+MEM_DEVICE_HOST_NAMES = 3  # device columns; names streamed from (pinned) host memory
 ORDER_UNKNOWN = 0
 ORDER_SORTED = 1
 
@@ -278,7 +279,7 @@ class Records:
         if self.name_bytes.size == 0:
             self.name_bytes = np.zeros(1, np.uint8)
         self.order = order
-        self.mem = MEM_HOST  # MEM_HOST_MAPPED_NAMES once name_bytes is registered (see Context.map_names)
+        self.mem = MEM_HOST  # or MEM_HOST_STREAM_NAMES (names streamed, not copied whole)
         self._keepalive = keepalive
         for a in (self.duration_ns, self.stream, self.size_bytes, self.flags):
             assert a.shape[0] == n

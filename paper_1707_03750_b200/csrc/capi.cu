@@ -2,6 +2,7 @@
 // analyze_trace orchestration (pipeline.hpp:34-134) on the device.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <set>
@@ -188,6 +189,12 @@ int itt_ctx_destroy(itt_ctx* ctx) {
   for (auto& kv : c->out_live) cudaFreeHost(kv.first);  // outputs must be released before this
   for (auto& kv : c->out_free) cudaFreeHost(kv.second);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  for (auto w : c->win)
+    if (w) cudaFree(w);
   if (c->pool) cudaMemPoolDestroy(c->pool);
   cudaStreamDestroy(c->stream);
   delete ctx;
@@ -228,9 +235,11 @@ int itt_ctx_kernel_stats(itt_ctx* ctx, itt_kernel_stat* out, uint32_t cap, uint3
 int itt_ctx_mem_stats(itt_ctx* ctx, uint64_t* used, uint64_t* used_high, int reset) {
   return guarded(ctx, [&](Ctx* c) {
     c->sync();
-    uint64_t u = 0, h = 0;
+    uint64_t u = 0, h = 0, r = 0;
     ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, &u));
     ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemHigh, &h));
+    ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    if (std::getenv("ITT_TRACE")) std::fprintf(stderr, "[itt] pool used %.2f GB high %.2f GB reserved %.2f GB\n", u / 1e9, h / 1e9, r / 1e9);
     if (used) *used = u;
     if (used_high) *used_high = h;
     if (reset) {
@@ -262,10 +271,6 @@ int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
 }
 int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes) {
   return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault)); });
-}
-int itt_host_device_pointer(itt_ctx* ctx, void* host, void** dev) {
-  if (!dev) return ITT_E_INVALID_ARGUMENT;
-  return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostGetDevicePointer(dev, host, 0)); });
 }
 int itt_host_unregister(itt_ctx* ctx, void* p) {
   return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostUnregister(p)); });

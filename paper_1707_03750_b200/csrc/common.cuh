@@ -46,6 +46,8 @@ struct Ctx {
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host->device streaming that overlaps kernels on `stream`
+  const char* last_launch = "";
   std::string last_error;
   uint64_t launches = 0;
   bool profiling = false;
@@ -114,6 +116,27 @@ struct Ctx {
     out_live.erase(it);
     return true;
   }
+  // streamed-name windows: two persistent device buffers (cudaMalloc, outside the pool) reused
+  // across calls — gigabyte-sized per-call pool blocks fragment the pool and force remapping
+  void* win[2] = {nullptr, nullptr};
+  size_t win_bytes = 0;
+  uint8_t* window(int i, size_t bytes) {
+    if (bytes > win_bytes) {
+      ITT_CUDA(cudaStreamSynchronize(stream));
+      if (copy_stream) ITT_CUDA(cudaStreamSynchronize(copy_stream));
+      for (auto& w : win) {
+        if (w) ITT_CUDA(cudaFree(w));
+        w = nullptr;
+      }
+      for (auto& w : win) ITT_CUDA(cudaMalloc(&w, bytes));
+      win_bytes = bytes;
+    }
+    return static_cast<uint8_t*>(win[i]);
+  }
+  cudaStream_t copier() {
+    if (!copy_stream) ITT_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    return copy_stream;
+  }
   void* staging(size_t bytes) {
     if (bytes > pinned_bytes) {
       if (pinned) cudaFreeHost(pinned);
@@ -138,6 +161,7 @@ struct LaunchScope {
     }
   }
   ~LaunchScope() noexcept(false) {
+    c->last_launch = name;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(ITT_E_CUDA, std::string("cuda launch ") + name + ": " + cudaGetErrorString(e));
     c->launches += 1;
@@ -182,10 +206,26 @@ struct DBuf {
     release();
     c = ctx;
     n = count;
-    if (count) ITT_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->pool, ctx->stream));
+    if (count) {
+      timespec a, b;
+      clock_gettime(CLOCK_MONOTONIC, &a);
+      ITT_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->pool, ctx->stream));
+      clock_gettime(CLOCK_MONOTONIC, &b);
+      const double ms = (b.tv_sec - a.tv_sec) * 1e3 + (b.tv_nsec - a.tv_nsec) * 1e-6;
+      if (ms > 5.0 && std::getenv("ITT_TRACE"))
+        std::fprintf(stderr, "[itt]   slow alloc %.1f ms (%.1f MB) after %s\n", ms, count * sizeof(T) / 1e6, ctx->last_launch);
+    }
   }
   void release() {
-    if (p) cudaFreeAsync(p, c->stream);
+    if (p) {
+      timespec a, b;
+      clock_gettime(CLOCK_MONOTONIC, &a);
+      cudaFreeAsync(p, c->stream);
+      clock_gettime(CLOCK_MONOTONIC, &b);
+      const double ms = (b.tv_sec - a.tv_sec) * 1e3 + (b.tv_nsec - a.tv_nsec) * 1e-6;
+      if (ms > 5.0 && std::getenv("ITT_TRACE"))
+        std::fprintf(stderr, "[itt]   slow free %.1f ms (%.1f MB) after %s\n", ms, n * sizeof(T) / 1e6, c->last_launch);
+    }
     p = nullptr;
     n = 0;
   }
@@ -251,8 +291,11 @@ template <typename T>
 inline void readback(Ctx* c, T* dst, const T* src, size_t count) {
   ++StageTimer::syncs();
   T* st = static_cast<T*>(c->staging(count * sizeof(T)));
+  const double t0 = StageTimer::on() ? StageTimer::now() : 0.0;
   d2h(c, st, src, count);
   c->sync();
+  if (StageTimer::on() && StageTimer::now() - t0 > 20.0)
+    std::fprintf(stderr, "[itt]   slow readback %.1f ms after %s\n", StageTimer::now() - t0, c->last_launch);
   std::memcpy(static_cast<void*>(dst), st, count * sizeof(T));
 }
 template <typename T>

@@ -13,6 +13,7 @@
 // collision) re-runs the dictionary with another seed.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "pipeline.cuh"
@@ -262,9 +263,13 @@ __device__ __forceinline__ bool same_bytes(const A& p, const B& q, uint32_t len)
 
 struct HashArgs {
   const uint64_t* name_off;
-  const uint8_t* bytes;
+  const uint8_t* bytes;  // bytes[o] is name byte o for o in [lo, total)
+  uint64_t lo;           // 0, or the first byte of a streamed chunk window (16-byte aligned)
   uint64_t total;
+  uint64_t row0;         // rows [row0, n) in this launch
   uint64_t n;
+  const uint8_t* arena;  // streamed names: bytes of the slot representatives of earlier chunks
+  const uint64_t* arena_off;
   const uint16_t* device;
   uint64_t* tkey;  // (32-bit hash fragment | 1) << 32 | row of the slot's first inserter; 0 = empty
   uint32_t mask;
@@ -305,11 +310,11 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
   for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x) s_dev[i] = 0;
   __syncthreads();
   uint8_t* buf = s_buf[warp];
-  const uint64_t groups = (a.n + 31) / 32;
+  const uint64_t groups = (a.n - a.row0 + 31) / 32;
   const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
   bool bad = false;
   for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp; g < groups; g += gstride) {
-    const uint64_t g0 = g * 32, g1 = min(g0 + 32, a.n);
+    const uint64_t g0 = a.row0 + g * 32, g1 = min(g0 + 32, a.n);
     const uint64_t row = g0 + lane;
     const bool valid = row < a.n;
     uint64_t base = 0;
@@ -350,9 +355,12 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
         if (same) {
           const uint64_t q0 = ro & ~15ull, q1 = (ro + len + 15) & ~15ull;
           const bool aligned = (reinterpret_cast<uintptr_t>(a.bytes) & 15) == 0;
-          if (staged && rep >= g0 && rep < g1) {
+          if (rep < a.row0) {  // streamed: the representative's chunk is gone, its bytes are in the arena
+            const GlobalBytes rb(a.arena + a.arena_off[s]);
+            same = staged ? same_bytes(SharedBytes(buf + (o - base)), rb, len) : same_bytes(GlobalBytes(a.bytes + o), rb, len);
+          } else if (staged && rep >= g0 && rep < g1) {
             same = same_bytes(SharedBytes(buf + (o - base)), SharedBytes(buf + (ro - base)), len);
-          } else if (staged && aligned && q1 - q0 <= kRepScratch && q1 <= a.total) {
+          } else if (staged && aligned && q1 - q0 <= kRepScratch && q0 >= a.lo && q1 <= a.total) {
             // the representative's bytes into this lane's scratch in one round trip (cp.async),
             // then a shared-to-shared compare instead of a chain of dependent global loads
             uint8_t* scr = s_rep[warp][lane];
@@ -395,6 +403,28 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
       if (s_dev[i]) atomicAdd(&a.dev_counts[i], static_cast<unsigned long long>(s_dev[i]));
 }
 
+// Streamed names: after each chunk, copy the names of the slots it claimed (used[snap..count))
+// into the arena, so later chunks verify against them and the classifier reads them.
+__global__ void k_save_reps(const uint32_t* __restrict__ used, const uint32_t* __restrict__ snap,
+                            const uint32_t* __restrict__ count, const uint64_t* __restrict__ tkey,
+                            const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes, uint8_t* arena,
+                            uint64_t arena_cap, uint64_t* __restrict__ arena_off, unsigned long long* top,
+                            uint32_t* overflow) {
+  const uint32_t u0 = *snap, u1 = *count;
+  for (uint32_t u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += gridDim.x * blockDim.x) {
+    const uint32_t s = used[u];
+    const uint32_t r = static_cast<uint32_t>(tkey[s]);
+    const uint64_t o = name_off[r], len = name_off[r + 1] - o;
+    const unsigned long long at = atomicAdd(top, static_cast<unsigned long long>(len));
+    if (at + len > arena_cap) {
+      atomicOr(overflow, 1u);
+      continue;
+    }
+    for (uint64_t i = 0; i < len; ++i) arena[at + i] = bytes[o + i];
+    arena_off[s] = at;
+  }
+}
+
 __device__ __forceinline__ bool contains_ci(const uint8_t* h, uint32_t hl, const char* needle, uint32_t nl) {
   if (hl < nl) return false;
   for (uint32_t i = 0; i + nl <= hl; ++i) {
@@ -413,12 +443,13 @@ __device__ __forceinline__ bool contains_ci(const uint8_t* h, uint32_t hl, const
 // classify each distinct name once (trace.hpp:103-113)
 __global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint64_t* __restrict__ tkey,
                                  const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes,
+                                 const uint8_t* __restrict__ arena, const uint64_t* __restrict__ arena_off,
                                  uint8_t* __restrict__ tflags) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n_used) return;
   const uint32_t s = used[u];
   const uint32_t r = static_cast<uint32_t>(tkey[s]);  // first inserter's row
-  const uint8_t* p = bytes + name_off[r];
+  const uint8_t* p = arena ? arena + arena_off[s] : bytes + name_off[r];
   const uint32_t len = static_cast<uint32_t>(name_off[r + 1] - name_off[r]);
   uint8_t f = 0;
   if (contains_ci(p, len, "memcpy", 6)) f |= NB_MEMCPY;
@@ -431,6 +462,12 @@ __global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_u
 
 // per record: kind from the slot's classify bits and throughput presence; per slot: the smallest
 // row carrying the name (deterministic name_row, whichever warp inserted first)
+__global__ void k_name_bounds(const uint64_t* __restrict__ name_off, uint64_t n, uint64_t rows_per_chunk,
+                              uint64_t chunks, uint64_t* __restrict__ out) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c <= chunks) out[c] = name_off[min(c * rows_per_chunk, n)];
+}
+
 __global__ void k_kinds_minrow(const uint32_t* __restrict__ slot, const uint8_t* __restrict__ rflags, uint64_t n,
                                const uint8_t* __restrict__ tflags, uint8_t* __restrict__ kind, uint32_t* __restrict__ trep) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -702,7 +739,11 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.n = r->n;
   d.order = r->order;
   const uint64_t n = r->n;
-  if (r->mem == ITT_MEM_DEVICE) {
+  if (r->mem < ITT_MEM_HOST || r->mem > ITT_MEM_DEVICE_HOST_NAMES)
+    fail(ITT_E_INVALID_ARGUMENT, "ingest: unknown itt_records.mem");
+  const bool streamed = r->mem == ITT_MEM_HOST_STREAM_NAMES || r->mem == ITT_MEM_DEVICE_HOST_NAMES;
+  if (streamed) d.host_names = r->name_bytes;
+  if (r->mem == ITT_MEM_DEVICE || r->mem == ITT_MEM_DEVICE_HOST_NAMES) {
     d.start = r->start_ns;
     d.dur = r->duration_ns;
     d.size = r->size_bytes;
@@ -710,12 +751,9 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
     d.stream = r->stream;
     d.device = r->device;
     d.name_off = r->name_off;
-    d.name_bytes = r->name_bytes;
+    d.name_bytes = streamed ? nullptr : r->name_bytes;
     return;
   }
-  if (r->mem != ITT_MEM_HOST && r->mem != ITT_MEM_HOST_MAPPED_NAMES)
-    fail(ITT_E_INVALID_ARGUMENT, "ingest: unknown itt_records.mem");
-  const bool mapped = r->mem == ITT_MEM_HOST_MAPPED_NAMES;
   uint64_t nb = 0;
   if (n) std::memcpy(&nb, &r->name_off[n], sizeof(nb));
   d.o_start.alloc(c, n);
@@ -724,31 +762,23 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.o_flags.alloc(c, n);
   d.o_stream.alloc(c, n);
   d.o_off.alloc(c, n + 1);
-  if (!mapped) d.o_names.alloc(c, nb + 16);
   h2d(c, d.o_start.p, r->start_ns, n);
   h2d(c, d.o_dur.p, r->duration_ns, n);
   h2d(c, d.o_size.p, r->size_bytes, n);
   h2d(c, d.o_flags.p, r->flags, n);
   h2d(c, d.o_stream.p, r->stream, n);
   h2d(c, d.o_off.p, r->name_off, n + 1);
-  if (!mapped) h2d(c, d.o_names.p, r->name_bytes, nb);
+  if (!streamed) {
+    d.o_names.alloc(c, nb + 16);
+    h2d(c, d.o_names.p, r->name_bytes, nb);
+  }
   d.start = d.o_start.p;
   d.dur = d.o_dur.p;
   d.size = d.o_size.p;
   d.flags = d.o_flags.p;
   d.stream = d.o_stream.p;
   d.name_off = d.o_off.p;
-  d.name_bytes = d.o_names.p;
-  if (mapped) {
-    if (reinterpret_cast<uintptr_t>(r->name_bytes) & 15)
-      fail(ITT_E_INVALID_ARGUMENT, "ingest: mapped name_bytes must be 16-byte aligned");
-    void* dp = nullptr;
-    if (cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(r->name_bytes), 0) != cudaSuccess) {
-      cudaGetLastError();
-      fail(ITT_E_INVALID_ARGUMENT, "ingest: mapped name_bytes must be pinned host memory (cudaHostRegister)");
-    }
-    d.name_bytes = static_cast<const uint8_t*>(dp);
-  }
+  d.name_bytes = streamed ? nullptr : d.o_names.p;
   if (r->device) {
     d.o_device.alloc(c, n);
     h2d(c, d.o_device.p, r->device, n);
@@ -812,7 +842,7 @@ void build_dictionary(TraceState& t) {
   if (n) total = read1(c, t.rec.name_off + n);
   t.slot.alloc(c, n);
   t.kind.alloc(c, n);
-  DBuf<uint32_t> counters(c, 4);  // used count, overflow, collision
+  DBuf<uint32_t> counters(c, 4);  // used count, overflow, collision, streamed-name arena overflow
   DBuf<unsigned long long> dev_counts;
   DBuf<uint32_t> dev_max(c, 1);
   if (t.rec.device) {
@@ -825,6 +855,48 @@ void build_dictionary(TraceState& t) {
   constexpr unsigned kWarpsPerBlock = kHashBlock / 32;
   const unsigned grid =
       std::max(1u, std::min<unsigned>((groups + kWarpsPerBlock - 1) / kWarpsPerBlock, c->sm_count * 12));
+  // streamed names: row chunks of ~kStreamChunk bytes through two device windows (copy stream),
+  // overlapping the copy of chunk k+1 with the hash pass over chunk k
+  const bool streamed = t.rec.host_names != nullptr;
+  std::vector<uint64_t> bounds;  // name_off at chunk boundaries
+  uint64_t rows_per_chunk = n, chunks = 1, window = 0;
+  uint8_t* win[2] = {nullptr, nullptr};
+  DBuf<uint8_t> arena;
+  DBuf<uint64_t> arena_off;
+  DBuf<unsigned long long> arena_top;
+  DBuf<uint32_t> snap;
+  uint64_t arena_cap = 0;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+  struct Events {
+    cudaEvent_t* e[2];
+    ~Events() {
+      for (auto* p : e)
+        for (int i = 0; i < 2; ++i)
+          if (p[i]) cudaEventDestroy(p[i]);
+    }
+  } ev_guard{{copied, done}};
+  if (streamed && n) {
+    uint64_t chunk_bytes = 1ull << 30;
+    if (const char* e = std::getenv("ITT_STREAM_CHUNK")) chunk_bytes = std::max<uint64_t>(64, std::strtoull(e, nullptr, 10));
+    chunks = std::max<uint64_t>(1, (total + chunk_bytes - 1) / chunk_bytes);
+    rows_per_chunk = ((n + chunks - 1) / chunks + 31) & ~31ull;
+    chunks = (n + rows_per_chunk - 1) / rows_per_chunk;
+    DBuf<uint64_t> db(c, chunks + 1);
+    launch(c, "intern_name_bounds", 0.0, k_name_bounds, dim3(grid_for(chunks + 1, 128)), dim3(128), 0, t.rec.name_off, n,
+           rows_per_chunk, chunks, db.p);
+    bounds.resize(chunks + 1);
+    readback(c, bounds.data(), db.p, chunks + 1);
+    for (uint64_t k = 0; k < chunks; ++k) window = std::max<uint64_t>(window, bounds[k + 1] + 16 - (bounds[k] & ~15ull));
+    win[0] = c->window(0, window);
+    win[1] = c->window(1, window);
+    arena_cap = std::min<uint64_t>(total + 16, 64ull << 20);
+    snap.alloc(c, 1);
+    arena_top.alloc(c, 1);
+    for (int i = 0; i < 2; ++i) {
+      ITT_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+      ITT_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+  }
   for (int attempt = 0;; ++attempt) {
     const uint32_t cap = 1u << bits;
     t.tkey.alloc(c, cap);
@@ -836,15 +908,56 @@ void build_dictionary(TraceState& t) {
     counters.zero();
     dev_max.zero();
     if (t.rec.device) dev_counts.zero();
-    HashArgs ha{t.rec.name_off, t.rec.name_bytes, total, n,          t.rec.device, t.tkey.p,  cap - 1,
-                seed,           t.slot.p,         t.used.p, counters.p, dev_counts.p, dev_max.p};
-    launch(c, "intern_hash", 2.0 * static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0,
-           ha);
-    uint32_t cnt[3];
-    readback(c, cnt, counters.p, 3);
+    if (!streamed) {
+      HashArgs ha{t.rec.name_off, t.rec.name_bytes, 0,       total,      0,           n,           nullptr,  nullptr,
+                  t.rec.device,   t.tkey.p,         cap - 1, seed,       t.slot.p,    t.used.p,    counters.p,
+                  dev_counts.p,   dev_max.p};
+      launch(c, "intern_hash", 2.0 * static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0,
+             ha);
+    } else if (n) {
+      if (arena.n < arena_cap) arena.alloc(c, arena_cap);
+      arena_off.alloc(c, cap);
+      arena_top.zero();
+      cudaStream_t cp = c->copier();
+      ITT_CUDA(cudaEventRecord(done[0], c->stream));  // windows free; the copy stream starts after prior work
+      ITT_CUDA(cudaEventRecord(done[1], c->stream));
+      for (uint64_t k = 0; k < chunks; ++k) {
+        const int b = static_cast<int>(k & 1);
+        const uint64_t r0 = k * rows_per_chunk, r1 = std::min(n, r0 + rows_per_chunk);
+        // window [lo, hi): 16-byte aligned start, 16 bytes of slack past the chunk (zeros past the
+        // last name, so the host buffer needs no slack)
+        const uint64_t lo = bounds[k] & ~15ull, hi = bounds[k + 1] + 16, hc = std::min<uint64_t>(hi, total);
+        ITT_CUDA(cudaStreamWaitEvent(cp, done[b], 0));
+        ITT_CUDA(cudaMemcpyAsync(win[b], t.rec.host_names + lo, hc - lo, cudaMemcpyHostToDevice, cp));
+        if (hi > hc) ITT_CUDA(cudaMemsetAsync(win[b] + (hc - lo), 0, hi - hc, cp));
+        ITT_CUDA(cudaEventRecord(copied[b], cp));
+        ITT_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
+        ITT_CUDA(cudaMemcpyAsync(snap.p, counters.p, 4, cudaMemcpyDeviceToDevice, c->stream));
+        const uint8_t* bytes = win[b] - lo;  // bytes[o] valid for o in [lo, hi)
+        const uint64_t cgroups = (r1 - r0 + 31) / 32;
+        const unsigned cgrid = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>((cgroups + kWarpsPerBlock - 1) / kWarpsPerBlock, c->sm_count * 12)));
+        HashArgs ha{t.rec.name_off, bytes,   lo,       hi,          r0,          r1,          arena.p,  arena_off.p,
+                    t.rec.device,   t.tkey.p, cap - 1, seed,        t.slot.p,    t.used.p,    counters.p,
+                    dev_counts.p,   dev_max.p};
+        launch(c, "intern_hash", 2.0 * static_cast<double>(bounds[k + 1] - bounds[k]) + (r1 - r0) * 16.0, k_hash_insert,
+               dim3(cgrid), dim3(kHashBlock), 0, ha);
+        launch(c, "intern_save_reps", 0.0, k_save_reps, dim3(c->sm_count), dim3(128), 0, t.used.p, snap.p, counters.p,
+               t.tkey.p, t.rec.name_off, bytes, arena.p, arena_cap, arena_off.p, arena_top.p, counters.p + 3);
+        ITT_CUDA(cudaEventRecord(done[b], c->stream));
+      }
+    }
+    uint32_t cnt[4];
+    readback(c, cnt, counters.p, 4);
     if (cnt[1] || cnt[0] > cap / 2) {  // table too full: grow and redo
       if (bits >= 30) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: name dictionary overflow");
       bits += 2;
+      continue;
+    }
+    if (cnt[3]) {  // streamed names: the representatives' bytes outgrew the arena
+      if (arena_cap >= total + 16) fail(ITT_E_CUDA, "internal: streamed-name arena overflow");
+      arena_cap = std::min<uint64_t>(total + 16, arena_cap * 8);
+      counters.zero();
       continue;
     }
     if (cnt[2]) {  // a true 64-bit collision between different names: new seed
@@ -858,7 +971,8 @@ void build_dictionary(TraceState& t) {
   }
   if (t.n_used)
     launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(t.n_used, 128)), dim3(128), 0, t.used.p,
-           t.n_used, t.tkey.p, t.rec.name_off, t.rec.name_bytes, t.tflags.p);
+           t.n_used, t.tkey.p, t.rec.name_off, t.rec.name_bytes, streamed ? arena.p : nullptr,
+           streamed ? arena_off.p : nullptr, t.tflags.p);
   if (n) {
     const unsigned g2 = std::min<unsigned>(grid_for(n, 256), c->sm_count * 16);
     launch(c, "intern_kinds", n * 6.0, k_kinds_minrow, dim3(g2), dim3(256), 0, t.slot.p, t.rec.flags, n, t.tflags.p,

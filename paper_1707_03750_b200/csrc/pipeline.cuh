@@ -21,7 +21,8 @@ struct DevRecords {
   const uint32_t* stream = nullptr;
   const uint16_t* device = nullptr;  // may be null
   const uint64_t* name_off = nullptr;
-  const uint8_t* name_bytes = nullptr;
+  const uint8_t* name_bytes = nullptr;  // null when the names are streamed from host memory
+  const uint8_t* host_names = nullptr;  // streamed names (ITT_MEM_*_NAMES modes)
   int order = ITT_ORDER_UNKNOWN;
   // owned copies when the caller passed host memory
   DBuf<int64_t> o_start, o_dur, o_size;

@@ -47,7 +47,6 @@ def lib() -> C.CDLL:
         "itt_ctx_reset_stats": ([vp], C.c_int),
         "itt_ctx_kernel_stats": ([vp, P(abi.itt_kernel_stat), C.c_uint32, P(C.c_uint32)], C.c_int),
         "itt_ctx_launch_count": ([vp, P(C.c_uint64)], C.c_int),
-        "itt_host_device_pointer": ([vp, vp, P(vp)], C.c_int),
         "itt_ctx_mem_stats": ([vp, P(C.c_uint64), P(C.c_uint64), C.c_int], C.c_int),
         "itt_device_alloc": ([vp, C.c_uint64, P(vp)], C.c_int),
         "itt_device_free": ([vp, vp], C.c_int),
@@ -104,11 +103,11 @@ def _ptr(a, t):
 
 
 class DeviceRecords:
-    """Trace columns resident in HBM (allocated through the context).  names_mapped=True keeps
-    name_bytes in (registered, pinned) host memory, read in place by the hash pass over PCIe —
+    """Trace columns resident in HBM (allocated through the context).  names_host=True keeps
+    name_bytes in (registered, pinned) host memory, streamed chunk by chunk into the hash pass —
     for traces whose names do not fit in HBM next to the pipeline (C5)."""
 
-    def __init__(self, ctx: "Context", recs: abi.Records, names_mapped: bool = False):
+    def __init__(self, ctx: "Context", recs: abi.Records, names_host: bool = False):
         self.ctx = ctx
         self.n = recs.n
         self.order = recs.order
@@ -118,26 +117,25 @@ class DeviceRecords:
                     stream=recs.stream, name_off=recs.name_off, name_bytes=recs.name_bytes)
         if recs.device is not None:
             cols["device"] = recs.device
-        if names_mapped:
+        if names_host:
             a = cols.pop("name_bytes")
-            ctx.register_host(a)
+            ctx.register_host(a)  # pinned: the chunk copies overlap the hash pass
             self.mapped = a
-            p = C.c_void_p()
-            ctx._check(lib().itt_host_device_pointer(ctx.h, a.ctypes.data, C.byref(p)))
-            self.names_ptr = p
+            self.names_ptr = C.c_void_p(a.ctypes.data)
         for k, a in cols.items():
             p = C.c_void_p()
             ctx._check(lib().itt_device_alloc(ctx.h, max(1, a.nbytes), C.byref(p)))
             ctx._check(lib().itt_memcpy_h2d(ctx.h, p, a.ctypes.data, a.nbytes))
             self.bufs[k] = p
-        if names_mapped:
+        if names_host:
             self.bufs["name_bytes"] = self.names_ptr
         self.nbytes = sum(a.nbytes for a in cols.values())  # bytes resident in HBM
 
     def c(self) -> abi.itt_records:
         b = self.bufs
         return abi.itt_records(self.n, b["start_ns"], b["duration_ns"], b["size_bytes"], b["flags"], b["stream"],
-                               b.get("device"), b["name_off"], b["name_bytes"], abi.MEM_DEVICE, self.order)
+                               b.get("device"), b["name_off"], b["name_bytes"],
+                               abi.MEM_DEVICE_HOST_NAMES if self.mapped is not None else abi.MEM_DEVICE, self.order)
 
     def free(self):
         for k, p in self.bufs.items():
@@ -206,8 +204,8 @@ class Context:
     def synchronize(self):
         self._check(lib().itt_ctx_synchronize(self.h))
 
-    def upload(self, recs: abi.Records, names_mapped: bool = False) -> DeviceRecords:
-        return DeviceRecords(self, recs, names_mapped)
+    def upload(self, recs: abi.Records, names_host: bool = False) -> DeviceRecords:
+        return DeviceRecords(self, recs, names_host)
 
     def register_host(self, arr: np.ndarray):
         self._check(lib().itt_host_register(self.h, arr.ctypes.data, arr.nbytes))

@@ -286,24 +286,29 @@ def test_device_resident_inputs_match_host_inputs(ctx):
     assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
 
 
-def test_mapped_host_names_match_copied_names(ctx):
-    """ITT_MEM_HOST_MAPPED_NAMES: the hash pass reads names in place from pinned host memory
-    (the C5 layout, where names do not fit in HBM next to the pipeline) — same results."""
+@pytest.mark.parametrize("chunk", [None, "4096", "200000"])
+def test_streamed_host_names_match_copied_names(ctx, chunk, monkeypatch):
+    """ITT_MEM_HOST_STREAM_NAMES / ITT_MEM_DEVICE_HOST_NAMES: names streamed through bounded
+    device windows (the C5 layout) — identical results, with many chunks (ITT_STREAM_CHUNK) so
+    representatives from earlier chunks are verified from the arena."""
     from paper_1707_03750_b200 import abi
-    recs, _ = synth.generate_config("C1", noise_frac=0.05, shuffle_window=64, seed=9, name_max=160)
-    a = ctx.analyze_raw(recs, [100])
-    ctx.register_host(recs.name_bytes)
+    if chunk:
+        monkeypatch.setenv("ITT_STREAM_CHUNK", chunk)
+    recs, _ = synth.generate_config("C1", noise_frac=0.05, shuffle_window=64, seed=9, name_max=160,
+                                    minority_frac=0.02)
+    a = ctx.analyze_raw(recs, [100], op_profile=True)
+    recs.mem = abi.MEM_HOST_STREAM_NAMES
     try:
-        recs.mem = abi.MEM_HOST_MAPPED_NAMES
         b = ctx.analyze_raw(recs, [100], op_profile=True)
     finally:
         recs.mem = abi.MEM_HOST
-        ctx.unregister_host(recs.name_bytes)
-    assert a["streams"] == b["streams"] and a["name_row"] == b["name_row"]
-    assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
-    recs.mem = abi.MEM_HOST_MAPPED_NAMES  # not registered: refused, no silent copy
+    d = ctx.upload(recs, names_host=True)
     try:
-        with pytest.raises(cuda.IttError):
-            ctx.analyze_raw(recs, [100])
+        e = ctx.analyze_raw(d, [100], op_profile=True)
     finally:
-        recs.mem = abi.MEM_HOST
+        d.free()
+    for x in (b, e):
+        assert a["streams"] == x["streams"] and a["name_row"] == x["name_row"]
+        assert a["loops"][0]["pattern_tokens"] == x["loops"][0]["pattern_tokens"]
+        assert np.array_equal(a["loops"][0]["rows"], x["loops"][0]["rows"])
+        assert np.array_equal(a["loops"][0]["op_totals"], x["loops"][0]["op_totals"])
