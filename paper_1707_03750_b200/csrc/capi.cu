@@ -195,6 +195,8 @@ int itt_ctx_destroy(itt_ctx* ctx) {
   }
   for (auto w : c->win)
     if (w) cudaFree(w);
+  for (auto b : c->bounce)
+    if (b) cudaFreeHost(b);
   if (c->pool) cudaMemPoolDestroy(c->pool);
   cudaStreamDestroy(c->stream);
   delete ctx;

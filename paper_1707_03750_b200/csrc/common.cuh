@@ -31,9 +31,11 @@ struct Error : std::runtime_error {
 #define ITT_CUDA(call)                                                                                   \
   do {                                                                                                   \
     cudaError_t e_ = (call);                                                                             \
-    if (e_ != cudaSuccess)                                                                               \
+    if (e_ != cudaSuccess) {                                                                             \
+      cudaGetLastError(); /* a non-sticky error must not resurface at the next launch check */           \
       ::itt::fail(ITT_E_CUDA, std::string("cuda: ") + cudaGetErrorString(e_) + " at " + __FILE__ + ":" + \
                                   std::to_string(__LINE__));                                             \
+    }                                                                                                    \
   } while (0)
 
 // ---------------------------------------------------------------- context
@@ -132,6 +134,21 @@ struct Ctx {
       win_bytes = bytes;
     }
     return static_cast<uint8_t*>(win[i]);
+  }
+  // pinned bounce buffers for streaming names out of pageable host memory
+  void* bounce[2] = {nullptr, nullptr};
+  size_t bounce_bytes = 0;
+  uint8_t* bounce_buf(int i, size_t bytes) {
+    if (bytes > bounce_bytes) {
+      if (copy_stream) ITT_CUDA(cudaStreamSynchronize(copy_stream));
+      for (auto& b : bounce) {
+        if (b) ITT_CUDA(cudaFreeHost(b));
+        b = nullptr;
+      }
+      for (auto& b : bounce) ITT_CUDA(cudaMallocHost(&b, bytes));
+      bounce_bytes = bytes;
+    }
+    return static_cast<uint8_t*>(bounce[i]);
   }
   cudaStream_t copier() {
     if (!copy_stream) ITT_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));

@@ -15,6 +15,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 #include "pipeline.cuh"
 
@@ -835,6 +836,24 @@ void order_records(TraceState& t) {
   t.perm = alt ? std::move(v1) : std::move(v0);
 }
 
+// host memcpy split across threads (pageable source -> pinned bounce buffer)
+void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t bytes) {
+  constexpr uint64_t kMinPerThread = 32ull << 20;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = static_cast<unsigned>(std::min<uint64_t>(hw, std::max<uint64_t>(1, bytes / kMinPerThread)));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const uint64_t per = (bytes + nt - 1) / nt;
+  for (unsigned i = 0; i < nt; ++i) {
+    const uint64_t a = i * per, b = std::min(bytes, a + per);
+    if (a < b) th.emplace_back([=] { std::memcpy(dst + a, src + a, b - a); });
+  }
+  for (auto& x : th) x.join();
+}
+
 void build_dictionary(TraceState& t) {
   Ctx* c = t.c;
   const uint64_t n = t.rec.n;
@@ -861,6 +880,7 @@ void build_dictionary(TraceState& t) {
   std::vector<uint64_t> bounds;  // name_off at chunk boundaries
   uint64_t rows_per_chunk = n, chunks = 1, window = 0;
   uint8_t* win[2] = {nullptr, nullptr};
+  uint8_t* bnc[2] = {nullptr, nullptr};
   DBuf<uint8_t> arena;
   DBuf<uint64_t> arena_off;
   DBuf<unsigned long long> arena_top;
@@ -889,6 +909,12 @@ void build_dictionary(TraceState& t) {
     for (uint64_t k = 0; k < chunks; ++k) window = std::max<uint64_t>(window, bounds[k + 1] + 16 - (bounds[k] & ~15ull));
     win[0] = c->window(0, window);
     win[1] = c->window(1, window);
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, t.rec.host_names) != cudaSuccess) cudaGetLastError();
+    if (pa.type != cudaMemoryTypeHost) {  // pageable: bounce through pinned buffers (parallel host memcpy)
+      bnc[0] = c->bounce_buf(0, window);
+      bnc[1] = c->bounce_buf(1, window);
+    }
     arena_cap = std::min<uint64_t>(total + 16, 64ull << 20);
     snap.alloc(c, 1);
     arena_top.alloc(c, 1);
@@ -928,7 +954,13 @@ void build_dictionary(TraceState& t) {
         // last name, so the host buffer needs no slack)
         const uint64_t lo = bounds[k] & ~15ull, hi = bounds[k + 1] + 16, hc = std::min<uint64_t>(hi, total);
         ITT_CUDA(cudaStreamWaitEvent(cp, done[b], 0));
-        ITT_CUDA(cudaMemcpyAsync(win[b], t.rec.host_names + lo, hc - lo, cudaMemcpyHostToDevice, cp));
+        const uint8_t* src = t.rec.host_names + lo;
+        if (bnc[b]) {  // the DMA that last read this bounce buffer (chunk k-2) must be finished
+          if (k >= 2) ITT_CUDA(cudaEventSynchronize(copied[b]));
+          parallel_memcpy(bnc[b], src, hc - lo);
+          src = bnc[b];
+        }
+        ITT_CUDA(cudaMemcpyAsync(win[b], src, hc - lo, cudaMemcpyHostToDevice, cp));
         if (hi > hc) ITT_CUDA(cudaMemsetAsync(win[b] + (hc - lo), 0, hi - hc, cp));
         ITT_CUDA(cudaEventRecord(copied[b], cp));
         ITT_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));

@@ -117,9 +117,14 @@ class DeviceRecords:
                     stream=recs.stream, name_off=recs.name_off, name_bytes=recs.name_bytes)
         if recs.device is not None:
             cols["device"] = recs.device
+        self.names_pinned = False
         if names_host:
             a = cols.pop("name_bytes")
-            ctx.register_host(a)  # pinned: the chunk copies overlap the hash pass
+            try:
+                ctx.register_host(a)  # pinned: full-speed chunk copies that overlap the hash pass
+                self.names_pinned = True
+            except IttError:
+                pass  # the OS refused to lock that much memory: streamed from pageable memory
             self.mapped = a
             self.names_ptr = C.c_void_p(a.ctypes.data)
         for k, a in cols.items():
@@ -142,7 +147,8 @@ class DeviceRecords:
             if not (k == "name_bytes" and self.mapped is not None):
                 lib().itt_device_free(self.ctx.h, p)
         if self.mapped is not None:
-            self.ctx.unregister_host(self.mapped)
+            if self.names_pinned:
+                self.ctx.unregister_host(self.mapped)
             self.mapped = None
         self.bufs = {}
 
