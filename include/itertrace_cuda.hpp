@@ -234,6 +234,42 @@ inline IterationAnalysis compute_iteration_metrics(const NormalizedTrace& trace,
   return out;
 }
 
+// a12, the north star's per-op x per-iteration profile (no reference counterpart; definition
+// in itertrace_cuda.h, itt_op_cell): over the reference's own token sequence and windows.
+struct OpProfile {
+  std::vector<itt_op_total> per_op;             // [seq.names.size()], by token id
+  std::vector<itt_iter_op_total> per_iteration;  // [windows.size()]
+  std::vector<itt_op_cell> cells;               // (iteration, op) order; empty unless requested
+};
+inline OpProfile op_profile(const NormalizedTrace& trace, const TokenSequence& seq,
+                            const std::vector<IterationWindow>& windows, bool with_cells = false) {
+  Context& ctx = Context::thread_default();
+  const size_t n = seq.tokens.size();
+  std::vector<int64_t> ts(n), te(n);
+  std::vector<uint8_t> kind(n);
+  for (size_t j = 0; j < n; ++j) {
+    const TraceRecord& r = trace.records[seq.record_index[j]];
+    ts[j] = r.start_ns;
+    te[j] = r.end_ns();
+    kind[j] = static_cast<uint8_t>(kind_of(r));  // OpKind order == ITT_KIND_* order
+  }
+  std::vector<itt_span> spans;
+  for (const auto& w : windows) spans.push_back(itt_span{w.span.start_token, w.span.end_token, w.span.extra});
+  OpProfile out;
+  out.per_op.resize(seq.names.size());
+  out.per_iteration.resize(spans.size());
+  itt_op_cell* cells = nullptr;
+  uint64_t n_cells = 0;
+  ctx.check(itt_op_profile(ctx.get(), seq.tokens.data(), ts.data(), te.data(), kind.data(), n,
+                           static_cast<uint32_t>(seq.names.size()), spans.data(), spans.size(), ITT_OP_PROFILE_AUTO,
+                           out.per_op.data(), out.per_iteration.data(), with_cells ? &cells : nullptr, &n_cells));
+  if (cells) {
+    out.cells.assign(cells, cells + n_cells);
+    itt_free(ctx.get(), cells);
+  }
+  return out;
+}
+
 // analyze_trace (pipeline.hpp:34-134): the device runs filter -> census -> tokens -> SA/LCP ->
 // mining -> matching -> integer aggregates in one call; the host finishes with the reference's
 // own compute_summary / diagnose and assembles warnings in the reference's order.

@@ -102,6 +102,22 @@ void compare_trace(const std::string& tag, const NormalizedTrace& trace, const A
            a.extra_ops == b.extra_ops && a.span == b.span;
   }
   expect(same, tag + " compute_iteration_metrics");
+  // a12 (no reference function): its idle column must reproduce the reference's op-gap means
+  // and its counts the span lengths; cells and totals must agree with each other
+  const auto op = itertrace::cuda::op_profile(filtered, seq, windows, true);
+  bool a12 = op.per_iteration.size() == ma.iterations.size();
+  for (size_t i = 0; a12 && i < ma.iterations.size(); ++i) {
+    const auto& m = ma.iterations[i];
+    const int64_t gc = m.span.end_token - m.span.start_token;
+    const double mean = gc > 0 ? static_cast<double>(op.per_iteration[i].idle_ns) / static_cast<double>(gc) : 0.0;
+    a12 = mean == m.op_gap_mean_ns;
+  }
+  std::vector<int64_t> cnt(op.per_iteration.size(), 0), idle(op.per_op.size(), 0);
+  for (const auto& c : op.cells) cnt[c.iteration] += c.count, idle[c.op] += c.idle_ns;
+  for (size_t i = 0; a12 && i < cnt.size(); ++i)
+    a12 = cnt[i] == ma.iterations[i].span.end_token - ma.iterations[i].span.start_token + 1;
+  for (size_t v = 0; a12 && v < idle.size(); ++v) a12 = idle[v] == op.per_op[v].idle_ns;
+  expect(a12, tag + " op_profile (a12) vs reference gap means");
 }
 
 NormalizedTrace trace_of(const SynthConfig& cfg) {
