@@ -240,6 +240,28 @@ struct SharedBytes {
     return static_cast<uint8_t>(v);
   }
 };
+// Sequential 4-byte reads of an unaligned run in shared memory: one aligned LDS per step (the
+// previous aligned word is reused), instead of two per unaligned 4-byte read.  Reads at most
+// one aligned word past the run (the staging buffers are padded).
+struct SharedStream {
+  uint32_t addr;  // next aligned word to load
+  uint32_t sh;    // byte misalignment in bits
+  uint32_t cur;
+  __device__ __forceinline__ static uint32_t lds(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  __device__ __forceinline__ explicit SharedStream(const SharedBytes& p)
+      : addr((p.base & ~3u) + 4), sh((p.base & 3u) * 8), cur(lds(p.base & ~3u)) {}
+  __device__ __forceinline__ uint32_t next4() {
+    const uint32_t nw = lds(addr);
+    addr += 4;
+    const uint32_t v = __funnelshift_r(cur, nw, sh);
+    cur = nw;
+    return v;
+  }
+};
 struct GlobalBytes {
   const uint8_t* p;
   __device__ __forceinline__ explicit GlobalBytes(const uint8_t* q) : p(q) {}
@@ -257,6 +279,18 @@ __device__ __forceinline__ bool same_bytes(const A& p, const B& q, uint32_t len)
   uint32_t i = 0;
   for (; i + 8 <= len; i += 4)
     if (p.load4(i) != q.load4(i)) return false;
+  for (; i < len; ++i)
+    if (p.byte(i) != q.byte(i)) return false;
+  return true;
+}
+// both runs in shared memory: two streams, one LDS per side per 4 bytes
+__device__ __forceinline__ bool same_bytes(const SharedBytes& p, const SharedBytes& q, uint32_t len) {
+  uint32_t i = 0;
+  if (len >= 8) {
+    SharedStream a(p), b(q);
+    for (; i + 8 <= len; i += 4)
+      if (a.next4() != b.next4()) return false;
+  }
   for (; i < len; ++i)
     if (p.byte(i) != q.byte(i)) return false;
   return true;
@@ -287,9 +321,13 @@ struct HashArgs {
 __device__ __forceinline__ uint64_t hash_staged(const SharedBytes& p, uint32_t len, uint64_t seed) {
   uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
   uint32_t i = 0;
-  for (; i + 8 <= len; i += 8) {
-    const uint64_t w = static_cast<uint64_t>(p.load4(i)) | (static_cast<uint64_t>(p.load4(i + 4)) << 32);
-    h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
+  if (len >= 8) {
+    SharedStream st(p);
+    for (; i + 8 <= len; i += 8) {
+      const uint32_t lo = st.next4();
+      const uint64_t w = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(st.next4()) << 32);
+      h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
+    }
   }
   uint64_t w = 0;
   for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(p.byte(i + j)) << (8 * j);
