@@ -70,8 +70,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval_ms: int = 20):
         self.index = index
+        self.interval_ms = interval_ms
         self.rows = []
         self.proc = None
         self.t0 = self.t1 = None
@@ -79,7 +80,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -194,7 +195,7 @@ def bench_batch(args, world, rank, local, workload):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
-    clk = ClockSampler(dev).__enter__()
+    clk = ClockSampler(dev, args.clock_ms).__enter__()
     time.sleep(0.3)
     bar()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -244,6 +245,7 @@ def main():
                     help="override the workload's iteration count (smaller dry runs of C3/C5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
+    ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi sampling interval during the timed region")
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
     ap.add_argument("--workers", type=int, default=8, help="C4: concurrent streams (host threads) per GPU")
@@ -317,7 +319,7 @@ def main():
             ms = float(t.item())
         return ms, res
 
-    clk = ClockSampler(dev).__enter__()
+    clk = ClockSampler(dev, args.clock_ms).__enter__()
     for _ in range(max(3, args.warmup)):
         res = step_device()
     # correctness guard: the mined period must be the planted body

@@ -36,7 +36,7 @@ namespace {
 constexpr int kChunk = 16;
 constexpr int kLiftAfter = 24;
 constexpr int kRankBlock = 256;
-constexpr int kRankItems = 16;
+constexpr int kRankItems = 8;  // smaller tiles, 8 CTAs per SM: more look-back chains and scatters in flight (A/B: 182 vs 197 us at 16)
 constexpr int kMaxPasses = 4;  // ids < 2^32
 
 __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int* out /*min,max,termhits*/) {
@@ -98,7 +98,7 @@ struct EmitLoader {
 // sorted keys) and r2 = old id of SA_j + h (gathered here; none when SA_j + h >= n' or when
 // rank_old is null in the init round).  id_j = inclusive count of flags - 1 (decoupled look-back
 // sum scan); rank_new[SA_j] = id_j; hist_next[p][digit_p(id_j)] += 1.
-__global__ void __launch_bounds__(kRankBlock, 4) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
+__global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
                                                             const uint32_t* __restrict__ rank_old, uint32_t h, uint64_t np,
                                                             uint32_t* __restrict__ rank_new, uint32_t* __restrict__ hist_next,
                                                             int passes, uint64_t* status, uint32_t* counter) {
