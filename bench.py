@@ -181,15 +181,23 @@ def bench_batch(args, world, rank, local, workload):
     dev_pool = {t: (up_ctx.upload(recs), info) for t, (recs, info) in pool.items()}
     traces = [dev_pool[t % args.distinct][0] for t in range(args.traces)]  # global index -> resident trace
     events = sum(dev_pool[t % args.distinct][1]["n"] for t in range(lo, hi))
-    process = batch.cuda_processor(dev)
     loops_of = lambda i: [500]  # noqa: E731
+    if args.batch_impl == "native":  # C++ worker threads (itt_batch_*), no interpreter between traces
+        executor = itt.Batch(dev, args.workers)
 
-    def one_pass():
-        return batch.run_shard(traces, loops_of, lo, hi, process, workers=args.workers)
+        def one_pass():
+            return batch.run_shard_native(executor, traces, [500], lo, hi)
+        launch_count = executor.launch_count
+    else:  # Python threads, one library context each
+        process = batch.cuda_processor(dev)
+
+        def one_pass():
+            return batch.run_shard(traces, loops_of, lo, hi, process, workers=args.workers)
+        launch_count = lambda: sum(c.launch_count() for c in process.contexts)  # noqa: E731
 
     for _ in range(max(1, args.warmup)):
         res = one_pass()
-    l0 = sum(c.launch_count() for c in process.contexts)
+    l0 = launch_count()
 
     def bar():
         if world > 1:
@@ -217,14 +225,14 @@ def bench_batch(args, world, rank, local, workload):
         torch.distributed.all_reduce(t[1:2], op=torch.distributed.ReduceOp.MAX)
         ev_total[1] = t[1]
     total_events, ms = float(ev_total[0].item()), float(ev_total[1].item())
-    launches = (sum(c.launch_count() for c in process.contexts) - l0) // max(1, args.steps)
+    launches = (launch_count() - l0) // max(1, args.steps)
     ok = all(r["loops"][0]["pattern_length"] == 200 and r["loops"][0]["iterations"] == 500 for r in res)
     if rank == 0:
         line = {"metric": METRIC, "value": total_events / (ms / args.steps / 1000.0), "unit": "events/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
                 "config": {"workload": workload, "traces": args.traces, "distinct_traces": args.distinct,
-                           "events_per_step": int(total_events), "workers_per_gpu": args.workers,
+                           "events_per_step": int(total_events), "workers_per_gpu": args.workers, "executor": args.batch_impl,
                            "parallelism": f"shard{world}", "mined_ok": bool(ok)},
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
@@ -249,6 +257,8 @@ def main():
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
     ap.add_argument("--workers", type=int, default=8, help="C4: concurrent streams (host threads) per GPU")
+    ap.add_argument("--batch-impl", default="native", choices=["native", "threads"],
+                    help="C4 executor: native C++ worker threads (itt_batch_*) or Python threads")
     args = ap.parse_args()
     world, rank, local = dist_env()
     workload, _, iters = WORKLOADS[args.config]

@@ -342,12 +342,33 @@ typedef struct itt_analysis {
   int64_t overlapping_kernels; /* count_interval_overlaps on the main stream */
   uint32_t n_loops;
   itt_loop_result* loops;
+  itt_ctx* owner;             /* the context whose pinned blocks hold the rows (itt_free_analysis) */
 } itt_analysis;
 
 /* analyze_trace (pipeline.hpp:34-134) up to the per-loop integer aggregates; the
  * host finishes compute_summary / diagnose / warnings in reference order. */
 int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* opts, itt_analysis** out);
-int itt_free_analysis(itt_ctx* ctx, itt_analysis* a);
+int itt_free_analysis(itt_ctx* ctx, itt_analysis* a); /* ctx may be NULL: a->owner is used */
+
+/* ------------------------------------------------------- batches of independent traces (C4)
+ * A native executor: `workers` host threads, each with its own context (CUDA
+ * stream + memory pool) on `device`, pull traces from a shared counter and run itt_analyze, so
+ * the small, latency-bound traces overlap on the GPU with no interpreter in the loop.  Multi-GPU
+ * sharding of a batch is the caller's (one executor per GPU, contiguous shards; no collective). */
+typedef struct itt_batch itt_batch;
+int itt_batch_create(int device, uint32_t workers, itt_batch** out);
+int itt_batch_destroy(itt_batch* b);
+/* out[i] and status[i] for trace i (status = itt_analyze's return code; on failure out[i] = NULL
+ * and itt_batch_error(b, i) holds the message until the next call).  opts: one shared options
+ * struct, or n structs when opts_per_trace != 0.  Returns ITT_OK when every trace ran (per-trace
+ * failures are reported in status), else a context-creation error. */
+int itt_batch_analyze(itt_batch* b, const itt_records* traces, uint64_t n, const itt_analyze_opts* opts,
+                      int opts_per_trace, itt_analysis** out, int* status);
+const char* itt_batch_error(itt_batch* b, uint64_t i);
+/* kernels launched by the executor's worker contexts since creation */
+int itt_batch_launch_count(itt_batch* b, uint64_t* out);
+/* frees every non-NULL analysis (not concurrently with a running itt_batch_analyze) */
+int itt_batch_free(itt_batch* b, itt_analysis** out, uint64_t n);
 
 #ifdef __cplusplus
 }

@@ -196,6 +196,7 @@ class itt_analysis(C.Structure):
         ("overlapping_kernels", C.c_int64),
         ("n_loops", C.c_uint32),
         ("loops", P(itt_loop_result)),
+        ("owner", C.c_void_p),
     ]
 
 

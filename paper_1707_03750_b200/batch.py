@@ -40,6 +40,33 @@ def summarize(raw: dict) -> dict:
     return out
 
 
+def summarize_c(a) -> dict:
+    """summarize() over a live itt_analysis struct (the native batch path)."""
+    import ctypes as C
+
+    import numpy as np
+    out = {"main_stream": a.main_stream, "n_tokens": a.n_tokens, "loops": []}
+    for k in range(a.n_loops):
+        L = a.loops[k]
+        n = int(L.n_iterations)
+        if n:
+            buf = (C.c_int64 * (n * 11)).from_address(C.cast(L.rows, C.c_void_p).value)
+            rows = np.frombuffer(buf, dtype=np.int64).reshape(n, 11)
+            iv, hb = int(rows[:, 5].sum()), int(rows[:, 7].sum())
+        else:
+            iv = hb = 0
+        out["loops"].append({"pattern_length": L.pattern_length, "pattern_count": L.pattern_count,
+                             "first_token": L.first_token, "epsilon_used": L.epsilon_used, "iterations": n,
+                             "interval_sum": iv, "htod_bytes": hb})
+    return out
+
+
+def run_shard_native(executor, traces: Sequence, loops: Sequence[int], lo: int, hi: int) -> list:
+    """traces[lo:hi] through the native executor (cuda.Batch: C++ worker threads, one context
+    each) — the C4 hot path; same summaries as run_shard."""
+    return executor.analyze([traces[i] for i in range(lo, hi)], list(loops), summarize=summarize_c)
+
+
 def cuda_processor(device: int = 0) -> Callable:
     """Per-thread library contexts on `device`; returns process(trace, loops) -> summary dict."""
     from .cuda import Context

@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <thread>
+#include <atomic>
 #include <new>
 #include <set>
 
@@ -186,6 +188,7 @@ int itt_ctx_destroy(itt_ctx* ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->sync_event) cudaEventDestroy(c->sync_event);
   for (auto& kv : c->out_live) cudaFreeHost(kv.first);  // outputs must be released before this
   for (auto& kv : c->out_free) cudaFreeHost(kv.second);
   if (c->pinned) cudaFreeHost(c->pinned);
@@ -734,6 +737,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
     } hold;
     hold.ctx = ctx;
     itt_analysis* a = hold.a = host_alloc<itt_analysis>(1);
+    a->owner = ctx;
     fill_census(t, &a->census);
     a->main_stream = main_stream;
     a->n_main_streams = n_main_streams;
@@ -789,6 +793,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
 
 int itt_free_analysis(itt_ctx* ctx, itt_analysis* a) {
   if (!a) return ITT_OK;
+  if (a->owner) ctx = a->owner;  // the pinned row blocks go back to the context that made them
   std::free(a->census.streams);
   std::free(a->name_row);
   for (uint32_t k = 0; k < a->n_loops; ++k) {
@@ -800,6 +805,84 @@ int itt_free_analysis(itt_ctx* ctx, itt_analysis* a) {
   }
   std::free(a->loops);
   std::free(a);
+  return ITT_OK;
+}
+
+// ------------------------------------------------------------------ batch executor (C4)
+struct itt_batch {
+  int device = 0;
+  std::vector<itt_ctx*> ctx;
+  std::vector<std::string> errors;
+};
+
+int itt_batch_create(int device, uint32_t workers, itt_batch** out) {
+  if (!out || workers == 0) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  itt_batch* b = new (std::nothrow) itt_batch;
+  if (!b) return ITT_E_CUDA;
+  b->device = device;
+  for (uint32_t w = 0; w < workers; ++w) {
+    itt_ctx* c = nullptr;
+    const int rc = itt_ctx_create(device, &c);
+    if (rc != ITT_OK) {
+      for (auto* x : b->ctx) itt_ctx_destroy(x);
+      delete b;
+      return rc;
+    }
+    if (const char* e = std::getenv("ITT_BATCH_BLOCKING")) c->c.blocking_sync = std::atoi(e) != 0;
+    b->ctx.push_back(c);
+  }
+  *out = b;
+  return ITT_OK;
+}
+
+int itt_batch_destroy(itt_batch* b) {
+  if (!b) return ITT_OK;
+  for (auto* c : b->ctx) itt_ctx_destroy(c);
+  delete b;
+  return ITT_OK;
+}
+
+int itt_batch_analyze(itt_batch* b, const itt_records* traces, uint64_t n, const itt_analyze_opts* opts,
+                      int opts_per_trace, itt_analysis** out, int* status) {
+  if (!b || (n && (!traces || !opts || !out || !status))) return ITT_E_INVALID_ARGUMENT;
+  b->errors.assign(n, std::string());
+  std::atomic<uint64_t> next{0};
+  auto work = [&](itt_ctx* c) {
+    cudaSetDevice(b->device);
+    for (uint64_t i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
+      out[i] = nullptr;
+      status[i] = itt_analyze(c, &traces[i], opts_per_trace ? &opts[i] : opts, &out[i]);
+      if (status[i] != ITT_OK) b->errors[i] = itt_last_error(c);
+    }
+  };
+  std::vector<std::thread> th;
+  for (size_t w = 1; w < b->ctx.size(); ++w) th.emplace_back(work, b->ctx[w]);
+  work(b->ctx[0]);
+  for (auto& t : th) t.join();
+  return ITT_OK;
+}
+
+int itt_batch_launch_count(itt_batch* b, uint64_t* out) {
+  if (!b || !out) return ITT_E_INVALID_ARGUMENT;
+  uint64_t t = 0;
+  for (auto* c : b->ctx) t += c->c.launches;
+  *out = t;
+  return ITT_OK;
+}
+
+const char* itt_batch_error(itt_batch* b, uint64_t i) {
+  if (!b || i >= b->errors.size()) return "";
+  return b->errors[i].c_str();
+}
+
+int itt_batch_free(itt_batch* b, itt_analysis** out, uint64_t n) {
+  (void)b;
+  if (!out) return ITT_OK;
+  for (uint64_t i = 0; i < n; ++i) {
+    itt_free_analysis(nullptr, out[i]);
+    out[i] = nullptr;
+  }
   return ITT_OK;
 }
 

@@ -89,8 +89,18 @@ struct Ctx {
     }
     pending.clear();
   }
+  // blocking_sync: host waits sleep on an event instead of spinning — for many concurrent
+  // contexts (the batch executor), where spinning waiters starve each other's host threads
+  bool blocking_sync = false;
+  cudaEvent_t sync_event = nullptr;
   void sync() {
-    ITT_CUDA(cudaStreamSynchronize(stream));
+    if (blocking_sync) {
+      if (!sync_event) ITT_CUDA(cudaEventCreateWithFlags(&sync_event, cudaEventBlockingSync | cudaEventDisableTiming));
+      ITT_CUDA(cudaEventRecord(sync_event, stream));
+      ITT_CUDA(cudaEventSynchronize(sync_event));
+    } else {
+      ITT_CUDA(cudaStreamSynchronize(stream));
+    }
     if (!pending.empty()) resolve_profile();
   }
   // Pinned host blocks for large variable-size outputs (per-iteration rows): the device writes them

@@ -47,6 +47,12 @@ def lib() -> C.CDLL:
         "itt_ctx_reset_stats": ([vp], C.c_int),
         "itt_ctx_kernel_stats": ([vp, P(abi.itt_kernel_stat), C.c_uint32, P(C.c_uint32)], C.c_int),
         "itt_ctx_launch_count": ([vp, P(C.c_uint64)], C.c_int),
+        "itt_batch_create": ([C.c_int, C.c_uint32, P(vp)], C.c_int),
+        "itt_batch_destroy": ([vp], C.c_int),
+        "itt_batch_analyze": ([vp, vp, C.c_uint64, vp, C.c_int, P(P(abi.itt_analysis)), P(C.c_int)], C.c_int),
+        "itt_batch_error": ([vp, C.c_uint64], C.c_char_p),
+        "itt_batch_launch_count": ([vp, P(C.c_uint64)], C.c_int),
+        "itt_batch_free": ([vp, P(P(abi.itt_analysis)), C.c_uint64], C.c_int),
         "itt_ctx_mem_stats": ([vp, P(C.c_uint64), P(C.c_uint64), C.c_int], C.c_int),
         "itt_device_alloc": ([vp, C.c_uint64, P(vp)], C.c_int),
         "itt_device_free": ([vp, vp], C.c_int),
@@ -398,6 +404,61 @@ class Context:
                 C.memmove(res.ctypes.data, out, n * C.sizeof(abi.itt_op_cell))
             lib().itt_free(self.h, out)
         return res, ot[:n_ops], it[:len(spans)]
+
+
+class Batch:
+    """Native batch executor (itt_batch_*): `workers` C++ threads, one context each, on `device`."""
+
+    def __init__(self, device: int = 0, workers: int = 8):
+        h = C.c_void_p()
+        rc = lib().itt_batch_create(device, workers, C.byref(h))
+        if rc != 0:
+            raise IttError(rc, f"itt_batch_create({device}, {workers}) failed")
+        self.h = h
+        self.workers = workers
+
+    def close(self):
+        if self.h:
+            lib().itt_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        lib().itt_batch_launch_count(self.h, C.byref(v))
+        return v.value
+
+    def analyze(self, traces, loops, epsilon0=1, k0=-1, main_stream=-1, summarize=None):
+        """Analyze every trace (abi.Records or DeviceRecords); returns per-trace results:
+        summarize(itt_analysis) if given (read while the analyses are alive), else
+        (status, pattern_length, pattern_count, iterations) of loop 0; errors as IttError."""
+        n = len(traces)
+        recs = (abi.itt_records * max(1, n))(*[t.c() for t in traces])
+        lp = (C.c_int64 * max(1, len(loops)))(*loops)
+        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream, 0)
+        out = (P(abi.itt_analysis) * max(1, n))()
+        st = (C.c_int * max(1, n))()
+        rc = lib().itt_batch_analyze(self.h, recs, n, C.byref(opts), 0, out, st)
+        if rc != 0:
+            raise IttError(rc, "itt_batch_analyze failed")
+        try:
+            res = []
+            for i in range(n):
+                if st[i] != 0:
+                    res.append(IttError(st[i], lib().itt_batch_error(self.h, i).decode(errors="replace")))
+                elif summarize is not None:
+                    res.append(summarize(out[i][0]))
+                else:
+                    L = out[i][0].loops[0]
+                    res.append((0, L.pattern_length, L.pattern_count, L.n_iterations))
+            return res
+        finally:
+            lib().itt_batch_free(self.h, out, n)
 
 
 def _view(ptr, n, dtype, owner):

@@ -312,3 +312,24 @@ def test_streamed_host_names_match_copied_names(ctx, chunk, monkeypatch):
         assert a["loops"][0]["pattern_tokens"] == x["loops"][0]["pattern_tokens"]
         assert np.array_equal(a["loops"][0]["rows"], x["loops"][0]["rows"])
         assert np.array_equal(a["loops"][0]["op_totals"], x["loops"][0]["op_totals"])
+
+
+def test_native_batch_executor_matches_single_trace_calls(ctx):
+    """itt_batch_* (C4's executor): C++ worker threads with their own contexts give the same
+    per-trace results as one-at-a-time itt_analyze, including per-trace errors."""
+    from paper_1707_03750_b200 import batch
+    traces = [synth.generate(iterations=20 + t % 5, body_len=15 + t % 4, vocab=12, seed=500 + t)[0] for t in range(24)]
+    traces.append(records_from_ops([(13, "k", 0, 5)]))  # one token: mining fails for this trace
+    ex = cuda.Batch(0, 4)
+    try:
+        got = ex.analyze(traces, [20], summarize=batch.summarize_c)
+        assert ex.launch_count() > 0
+    finally:
+        ex.close()
+    for t, g in zip(traces, got):
+        try:
+            want = batch.summarize(ctx.analyze_raw(t, [20]))
+        except cuda.IttError as e:
+            assert isinstance(g, cuda.IttError) and g.status == e.status and str(g) == str(e)
+            continue
+        assert g == want
