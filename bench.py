@@ -244,7 +244,7 @@ def bench_batch(args, world, rank, local, workload):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
@@ -253,7 +253,7 @@ def main():
                     help="override the workload's iteration count (smaller dry runs of C3/C5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
-    ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi sampling interval during the timed region")
+    ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling interval during the timed region")
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
     ap.add_argument("--workers", type=int, default=8, help="C4: concurrent streams (host threads) per GPU")

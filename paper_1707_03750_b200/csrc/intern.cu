@@ -708,6 +708,138 @@ struct CompactF {
   }
 };
 
+// Compaction when the row order is block-local (rows already sorted, or the 256-row block sort
+// was the whole order): a tile of 2048 sorted positions reads exactly the source rows of the same
+// range, so the tile stages stream / device / kind / slot / start / dur in shared memory with
+// coalesced loads and resolves the permutation there, instead of one scattered global gather
+// per column per record.  Same outputs as CompactF (one packed look-back scan).
+constexpr int kCompactBlock = 256, kCompactItems = 8, kCompactTile = kCompactBlock * kCompactItems;
+static_assert(kCompactTile % 256 == 0, "tiles must be whole order blocks");
+struct CompactLocalSmem {
+  int64_t start[kCompactTile];
+  int64_t dur[kCompactTile];
+  uint32_t stream[kCompactTile];
+  uint32_t slot[kCompactTile];
+  uint16_t device[kCompactTile];
+  uint8_t kind[kCompactTile];
+};
+__global__ void __launch_bounds__(kCompactBlock) k_compact_local(CompactF f, uint64_t* status, uint32_t* tile_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CompactLocalSmem& S = *reinterpret_cast<CompactLocalSmem*>(smem_raw);
+  __shared__ uint64_t s_warp[kCompactBlock / 32];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t r0 = static_cast<uint64_t>(tile) * kCompactTile;
+  const uint32_t len = static_cast<uint32_t>(umin64(kCompactTile, f.n - r0));
+  {  // coalesced: the source rows of this tile, every load in flight before the first store
+    int64_t st[kCompactItems], du[kCompactItems];
+    uint32_t sm[kCompactItems], sl[kCompactItems];
+    uint8_t kd[kCompactItems];
+#pragma unroll
+    for (int q = 0; q < kCompactItems; ++q) {
+      const uint32_t i = threadIdx.x + q * kCompactBlock;
+      if (i < len) {
+        const uint64_t r = r0 + i;
+        st[q] = __ldcs(&f.start[r]);
+        du[q] = __ldcs(&f.dur[r]);
+        sm[q] = __ldcs(&f.stream[r]);
+        sl[q] = __ldcs(&f.slot[r]);
+        kd[q] = f.kind[r];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kCompactItems; ++q) {
+      const uint32_t i = threadIdx.x + q * kCompactBlock;
+      if (i < len) {
+        S.start[i] = st[q];
+        S.dur[i] = du[q];
+        S.stream[i] = sm[q];
+        S.slot[i] = sl[q];
+        S.kind[i] = kd[q];
+        if (f.filter) S.device[i] = f.device[r0 + i];
+      }
+    }
+  }
+  __syncthreads();
+  // warp-striped positions (k = r0 + warp*256 + q*32 + lane): ballots give every prefix, and
+  // consecutive lanes write consecutive outputs (coalesced token columns)
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t wbase = r0 + static_cast<uint64_t>(warp) * (32 * kCompactItems);
+  const unsigned lt = lanemask_lt();
+  unsigned mm[kCompactItems], hm[kCompactItems];
+  uint32_t loc[kCompactItems];
+  uint32_t wm = 0, wh = 0;
+#pragma unroll
+  for (int q = 0; q < kCompactItems; ++q) {
+    const uint64_t k = wbase + q * 32 + lane;
+    bool is_main = false, is_htod = false;
+    loc[q] = 0;
+    if (k < f.n) {
+      const uint32_t il = f.perm ? static_cast<uint32_t>(__ldcs(&f.perm[k]) - r0) : static_cast<uint32_t>(k - r0);
+      loc[q] = il;
+      if (!(f.filter && S.device[il] != f.majority)) {
+        is_main = S.stream[il] == f.main_stream;
+        is_htod = S.kind[il] == ITT_KIND_HTOD;
+      }
+    }
+    mm[q] = __ballot_sync(0xffffffffu, is_main);
+    hm[q] = __ballot_sync(0xffffffffu, is_htod);
+    wm += __popc(mm[q]);
+    wh += __popc(hm[q]);
+  }
+  const uint64_t wtot = static_cast<uint64_t>(wm) | (static_cast<uint64_t>(wh) << 31);
+  // block scan over the warps' packed totals (one value per warp: lane 0 contributes)
+  uint64_t total;
+  const uint64_t wexcl =
+      block_exclusive_scan<uint64_t, SumOp<uint64_t>, kCompactBlock>(lane == 0 ? wtot : 0ull, SumOp<uint64_t>(), &total, s_warp);
+  if (threadIdx.x < 32) {
+    const uint64_t p = tile_lookback<uint64_t, SumOp<uint64_t>>(status, tile, total, SumOp<uint64_t>());
+    if (threadIdx.x == 0) s_prefix = p;
+  }
+  __syncthreads();
+  const uint64_t start_acc = s_prefix + __shfl_sync(0xffffffffu, wexcl, 0);
+  uint32_t jm = static_cast<uint32_t>(start_acc & 0x7FFFFFFFull);
+  uint64_t jh = start_acc >> 31;
+  // first-appearance candidates: all eight tfirst reads in flight before any compare
+  uint32_t tf[kCompactItems];
+#pragma unroll
+  for (int q = 0; q < kCompactItems; ++q)
+    tf[q] = (mm[q] >> lane & 1u) ? __ldcg(&f.tfirst[S.slot[loc[q]]]) : 0u;
+#pragma unroll
+  for (int q = 0; q < kCompactItems; ++q) {
+    const uint32_t il = loc[q];
+    if ((mm[q] | hm[q]) >> lane & 1u) {
+      const int64_t st = S.start[il];
+      const int64_t en = st + S.dur[il];
+      if (mm[q] >> lane & 1u) {
+        const uint32_t j = jm + __popc(mm[q] & lt);
+        const uint32_t sl = S.slot[il];
+        f.tok_slot[j] = sl;
+        f.tok_start[j] = st;
+        f.tok_end[j] = en;
+        f.tok_kind[j] = S.kind[il];
+        if (f.tok_record) f.tok_record[j] = wbase + q * 32 + lane;
+        if (tf[q] > j) atomicMin(&f.tfirst[sl], j);
+      }
+      if (hm[q] >> lane & 1u) {
+        const uint64_t h = jh + __popc(hm[q] & lt);
+        const uint64_t i = r0 + il;
+        f.htod_start[h] = st;
+        f.htod_end[h] = en;
+        f.htod_size[h] = (f.rflags[i] & ITT_REC_HAS_SIZE) ? f.size[i] : 0;
+        const unsigned long long fe = static_cast<unsigned long long>(en) ^ (1ull << 63);
+        atomicMin(&f.htod_range[0], fe);
+        atomicMax(&f.htod_range[1], fe);
+      }
+    }
+    jm += __popc(mm[q]);
+    jh += __popc(hm[q]);
+  }
+}
+
 // ------------------------------------------------------------------ renumber
 // rank of each used slot among slots with a main-stream first position (first-appearance id)
 __global__ void k_rank_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ tfirst,
@@ -861,6 +993,7 @@ void order_records(TraceState& t) {
   t.sorted = false;
   if (h[3] == 0) {  // locally shuffled rows (the usual profiler export): the block sort is the order
     t.perm = std::move(perm);
+    t.perm_local = true;
     return;
   }
   perm.release();
@@ -1159,8 +1292,18 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
              t.htod_end.p,
              t.htod_size.p,
              t.htod_range.p};
-  device_scan<uint64_t, SumOp<uint64_t>>(c, "compact", n * (t.sorted ? 14.0 : 18.0) + n_main * 28.0 + n_htod * 24.0, f, n,
-                                         t.scan);
+  if (t.sorted || t.perm_local) {  // block-local order: stage each tile's rows in shared memory
+    const uint64_t tiles = (n + kCompactTile - 1) / kCompactTile;
+    t.scan.prepare(c, tiles);
+    const size_t smem = sizeof(CompactLocalSmem);
+    ITT_CUDA(cudaFuncSetAttribute(k_compact_local, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (n)
+      launch(c, "compact", n * (t.sorted ? 27.0 : 31.0) + n_main * 25.0 + n_htod * 24.0, k_compact_local,
+             dim3(static_cast<unsigned>(tiles)), dim3(kCompactBlock), smem, f, t.scan.buf.p + 1,
+             reinterpret_cast<uint32_t*>(t.scan.buf.p));
+  } else {
+    device_scan<uint64_t, SumOp<uint64_t>>(c, "compact", n * 18.0 + n_main * 28.0 + n_htod * 24.0, f, n, t.scan);
+  }
   if (t.streams.empty()) fail(ITT_E_INVALID_ARGUMENT, "internal: compact_main needs the stream census");
   t.n_tok = n_main;
   t.n_htod = n_htod;

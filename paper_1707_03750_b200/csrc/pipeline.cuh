@@ -39,6 +39,7 @@ struct TraceState {
   // ordering (K1)
   bool sorted = true;
   DBuf<uint32_t> perm;  // sorted position -> source row (only when !sorted)
+  bool perm_local = false;  // perm only moves rows inside their 256-row block (the block-sort fast path)
   // name dictionary (K2)
   uint32_t table_bits = 0;
   DBuf<uint64_t> tkey;     // 64-bit name hash per slot (0 = empty)
