@@ -78,6 +78,8 @@ class ClockSampler:
         self.t0 = self.t1 = None
 
     def __enter__(self):
+        if self.interval_ms <= 0:  # diagnosis only: no sampler (the JSON then has no clock samples)
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],

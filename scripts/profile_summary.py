@@ -16,7 +16,7 @@ for r in rows[hi + 1:]:
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(v[1] for v in agg.values())
-out = [f"# {tag}: ncu launch list of `python bench.py --steps 1 --warmup 3` (C2), gpu__time_duration.sum,",
+out = [f"# {tag}: ncu launch list of `python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e` (C2; first 400 launches), gpu__time_duration.sum,",
        "# --clock-control none; cold-cache and serialised per launch: compare SHARES, not absolutes",
        "kernel,launches,total_us,share"]
 for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -33,7 +33,7 @@ keys = {"duration_us": "gpu__time_duration.sum", "dram_read_MB": "dram__bytes_re
         "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active", "registers": "launch__registers_per_thread",
         "l2_hit_pct": "lts__t_sector_hit_rate.pct", "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active"}
-names = {"k_onesweep": "radix_onesweep", "k_rank_update": "sa_rank_update", "k_hash_insert": "intern_hash", "k_plcp": "lcp_plcp",
+names = {"k_onesweep": "radix_onesweep", "k_rank_update": "sa_rank_update", "k_hash_insert": "intern_hash", "k_plcp": "lcp_plcp", "k_compact_local": "compact",
          "k_ansv": "ansv_intervals", "k_scan": "compact"}
 per = collections.defaultdict(list)
 for r in rr[2:]:
