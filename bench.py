@@ -258,7 +258,7 @@ def main():
     ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling interval during the timed region")
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
-    ap.add_argument("--workers", type=int, default=8, help="C4: concurrent streams (host threads) per GPU")
+    ap.add_argument("--workers", type=int, default=16, help="C4: concurrent streams (host threads) per GPU")
     ap.add_argument("--batch-impl", default="native", choices=["native", "threads"],
                     help="C4 executor: native C++ worker threads (itt_batch_*) or Python threads")
     args = ap.parse_args()

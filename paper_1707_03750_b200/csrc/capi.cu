@@ -35,6 +35,7 @@ int guarded(itt_ctx* ctx, F&& f) {
   Ctx* c = &ctx->c;
   try {
     ITT_CUDA(cudaSetDevice(c->device));
+    c->arena_top = 0;  // the previous call synchronized: its small buffers are dead
     f(c);
     c->sync();
     c->last_error.clear();
@@ -198,6 +199,7 @@ int itt_ctx_destroy(itt_ctx* ctx) {
   }
   for (auto w : c->win)
     if (w) cudaFree(w);
+  if (c->arena) cudaFree(c->arena);
   for (auto b : c->bounce)
     if (b) cudaFreeHost(b);
   if (c->pool) cudaMemPoolDestroy(c->pool);

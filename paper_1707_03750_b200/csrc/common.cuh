@@ -160,6 +160,22 @@ struct Ctx {
     }
     return static_cast<uint8_t*>(bounce[i]);
   }
+  // Small-allocation arena: one device block, bump-allocated during a call and reset when the
+  // next call starts (guarded() synchronizes at the end of every call, and every DBuf of a call is
+  // dead by then).  A 100K-event trace makes ~60 small allocations per analyze; taking them here
+  // saves the allocator API calls that bound many-small-trace batches (C4).
+  static constexpr size_t kArenaBytes = 64ull << 20, kArenaMaxAlloc = 2ull << 20;
+  uint8_t* arena = nullptr;
+  size_t arena_top = 0;
+  void* arena_take(size_t bytes) {
+    bytes = (bytes + 255) & ~static_cast<size_t>(255);
+    if (bytes > kArenaMaxAlloc) return nullptr;
+    if (!arena) ITT_CUDA(cudaMalloc(&arena, kArenaBytes));
+    if (arena_top + bytes > kArenaBytes) return nullptr;
+    void* p = arena + arena_top;
+    arena_top += bytes;
+    return p;
+  }
   cudaStream_t copier() {
     if (!copy_stream) ITT_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     return copy_stream;
@@ -220,19 +236,24 @@ struct DBuf {
   DBuf(Ctx* ctx, size_t count) { alloc(ctx, count); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : c(o.c), p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf(DBuf&& o) noexcept : c(o.c), p(o.p), n(o.n), from_arena(o.from_arena) { o.p = nullptr, o.n = 0, o.from_arena = false; }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      c = o.c, p = o.p, n = o.n;
-      o.p = nullptr, o.n = 0;
+      c = o.c, p = o.p, n = o.n, from_arena = o.from_arena;
+      o.p = nullptr, o.n = 0, o.from_arena = false;
     }
     return *this;
   }
+  bool from_arena = false;
   void alloc(Ctx* ctx, size_t count) {
     release();
     c = ctx;
     n = count;
+    if (count && (p = static_cast<T*>(ctx->arena_take(count * sizeof(T))))) {
+      from_arena = true;
+      return;
+    }
     if (count) {
       timespec a, b;
       clock_gettime(CLOCK_MONOTONIC, &a);
@@ -244,6 +265,12 @@ struct DBuf {
     }
   }
   void release() {
+    if (p && from_arena) {
+      p = nullptr;
+      n = 0;
+      from_arena = false;
+      return;
+    }
     if (p) {
       timespec a, b;
       clock_gettime(CLOCK_MONOTONIC, &a);
