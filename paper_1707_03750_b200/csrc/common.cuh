@@ -10,6 +10,7 @@
 #include <cstring>
 #include <ctime>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -189,6 +190,20 @@ struct Ctx {
     return pinned;
   }
 };
+
+// Opt a kernel in to `bytes` of dynamic shared memory once per (kernel, device, size): the
+// attribute is per device, and setting it on every call is an avoidable driver call.
+template <typename K>
+inline void smem_optin(Ctx* c, K* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{reinterpret_cast<const void*>(kernel), c->device}];
+  if (have >= bytes) return;
+  ITT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  have = bytes;
+}
 
 // Profiled launch: records CUDA events on the context stream around the launch when
 // profiling is on; `bytes` is the launch's algorithmic HBM traffic.

@@ -1296,7 +1296,7 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
     const uint64_t tiles = (n + kCompactTile - 1) / kCompactTile;
     t.scan.prepare(c, tiles);
     const size_t smem = sizeof(CompactLocalSmem);
-    ITT_CUDA(cudaFuncSetAttribute(k_compact_local, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    smem_optin(c, k_compact_local, smem);
     if (n)
       launch(c, "compact", n * (t.sorted ? 27.0 : 31.0) + n_main * 25.0 + n_htod * 24.0, k_compact_local,
              dim3(static_cast<unsigned>(tiles)), dim3(kCompactBlock), smem, f, t.scan.buf.p + 1,

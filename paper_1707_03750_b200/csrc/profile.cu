@@ -300,8 +300,7 @@ OpProfile op_profile(Ctx* c, const int32_t* tokens, const int64_t* tok_start, co
            dim3(kOpBlock), bits_smem, tokens, tok_start, tok_end, tok_kind, spans.start.p, spans.end.p, n_ops,
            want_cells ? distinct.p : nullptr, iter_totals ? dit.p : nullptr);
     if (op_totals) {
-      if (table_smem > 48 * 1024)
-        ITT_CUDA(cudaFuncSetAttribute(k_op_totals, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(table_smem)));
+      smem_optin(c, k_op_totals, table_smem);
       const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(I, static_cast<uint64_t>(c->sm_count) * 2));
       launch(c, "opprof_totals", static_cast<double>(n_tok) * 21.0, k_op_totals, dim3(grid), dim3(kOpBlock), table_smem,
              tokens, tok_start, tok_end, tok_kind, spans.start.p, spans.end.p, I, n_ops, dot.p);
@@ -312,9 +311,7 @@ OpProfile op_profile(Ctx* c, const int32_t* tokens, const int64_t* tok_start, co
       out.n = scan.total(c);
       if (out.n) {
         dc.alloc(c, out.n);
-        if (table_smem > 48 * 1024)
-          ITT_CUDA(cudaFuncSetAttribute(k_op_cells_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(table_smem)));
+        smem_optin(c, k_op_cells_smem, table_smem);
         CellArgs a{tokens, tok_start, tok_end, tok_kind, spans.start.p, spans.end.p, offs.p, n_ops, dc.p};
         launch(c, "opprof_cells", static_cast<double>(n_tok) * 21.0 + out.n * sizeof(itt_op_cell), k_op_cells_smem,
                dim3(static_cast<unsigned>(I)), dim3(kOpBlock), table_smem, a);

@@ -263,9 +263,8 @@ void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int 
                  uint32_t* st, bool first_use) {
   constexpr int TILE = BLOCK * ITEMS;
   const size_t smem = sizeof(SmemLayout<K, BLOCK, ITEMS>);
-  if (first_use)
-    ITT_CUDA(cudaFuncSetAttribute(k_onesweep<K, BLOCK, ITEMS, Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+  (void)first_use;
+  smem_optin(c, k_onesweep<K, BLOCK, ITEMS, Loader>, smem);
   const uint64_t tiles = (n + TILE - 1) / TILE;
   launch(c, "radix_onesweep", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), k_onesweep<K, BLOCK, ITEMS, Loader>,
          dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, offs, st + 1, st);
