@@ -367,6 +367,18 @@ inline void readback(Ctx* c, T* dst, const T* src, size_t count) {
     std::fprintf(stderr, "[itt]   slow readback %.1f ms after %s\n", StageTimer::now() - t0, c->last_launch);
   std::memcpy(static_cast<void*>(dst), st, count * sizeof(T));
 }
+// two device ranges in one host round trip
+template <typename T, typename U>
+inline void readback2(Ctx* c, T* a, const T* da, size_t na, U* b, const U* db, size_t nb) {
+  ++StageTimer::syncs();
+  const size_t ba = (na * sizeof(T) + 15) & ~static_cast<size_t>(15);
+  uint8_t* st = static_cast<uint8_t*>(c->staging(ba + nb * sizeof(U)));
+  d2h(c, reinterpret_cast<T*>(st), da, na);
+  d2h(c, reinterpret_cast<U*>(st + ba), db, nb);
+  c->sync();
+  std::memcpy(static_cast<void*>(a), st, na * sizeof(T));
+  std::memcpy(static_cast<void*>(b), st + ba, nb * sizeof(U));
+}
 template <typename T>
 inline T read1(Ctx* c, const T* src) {
   T v;

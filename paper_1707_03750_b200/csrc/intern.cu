@@ -638,6 +638,14 @@ __global__ void __launch_bounds__(256) k_stream_census(CensusArgs a) {
   }
 }
 
+// dense copy of the used census entries: out[0].key = count, out[1 + u] = entry of list slot u
+__global__ void k_pack_streams(const StreamEntry* __restrict__ table, const uint32_t* __restrict__ list,
+                               StreamEntry* __restrict__ out) {
+  const uint32_t ns = list[0];
+  if (threadIdx.x == 0) out[0].key = ns;
+  for (uint32_t u = threadIdx.x; u < ns; u += blockDim.x) out[1 + u] = table[list[1 + u]];
+}
+
 __global__ void k_init_stream_table(StreamEntry* t) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < kStreamTableCap) {
@@ -927,6 +935,7 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   }
   uint64_t nb = 0;
   if (n) std::memcpy(&nb, &r->name_off[n], sizeof(nb));
+  d.name_total = static_cast<int64_t>(nb);
   d.o_start.alloc(c, n);
   d.o_dur.alloc(c, n);
   d.o_size.alloc(c, n);
@@ -1029,7 +1038,7 @@ void build_dictionary(TraceState& t) {
   Ctx* c = t.c;
   const uint64_t n = t.rec.n;
   uint64_t total = 0;
-  if (n) total = read1(c, t.rec.name_off + n);
+  if (n) total = t.rec.name_total >= 0 ? static_cast<uint64_t>(t.rec.name_total) : read1(c, t.rec.name_off + n);
   t.slot.alloc(c, n);
   t.kind.alloc(c, n);
   DBuf<uint32_t> counters(c, 4);  // used count, overflow, collision, streamed-name arena overflow
@@ -1187,9 +1196,13 @@ void build_dictionary(TraceState& t) {
   t.filtering = false;
   t.kept = n;
   if (t.rec.device && n) {
-    const uint32_t mx = read1(c, dev_max.p);
-    t.dev_counts.assign(mx + 1, 0);
-    readback(c, reinterpret_cast<unsigned long long*>(t.dev_counts.data()), dev_counts.p, mx + 1);
+    // device max and the first 64 label counts in one round trip (traces carry a handful of devices)
+    constexpr uint32_t kFewDev = 64;
+    uint32_t mx = 0;
+    t.dev_counts.assign(kFewDev, 0);
+    readback2(c, &mx, dev_max.p, 1, reinterpret_cast<unsigned long long*>(t.dev_counts.data()), dev_counts.p, kFewDev);
+    t.dev_counts.resize(mx + 1, 0);
+    if (mx >= kFewDev) readback(c, reinterpret_cast<unsigned long long*>(t.dev_counts.data()), dev_counts.p, mx + 1);
     uint64_t best = 0;
     t.n_devices = 0;
     for (uint32_t d = 0; d <= mx; ++d) {
@@ -1216,14 +1229,20 @@ void stream_census(TraceState& t) {
     const unsigned grid = std::min<unsigned>(grid_for(n, 256), c->sm_count * 8);
     launch(c, "census", n * 23.0, k_stream_census, dim3(grid), dim3(256), 0, ca);
   }
-  const uint32_t ns = read1(c, list.p);
-  std::vector<uint32_t> slots(ns);
-  readback(c, slots.data(), list.p + 1, ns);
-  std::vector<StreamEntry> all(kStreamTableCap);
-  readback(c, all.data(), table.p, kStreamTableCap);
+  // one round trip for the usual handful of streams: count + the first kFew packed entries
+  constexpr uint32_t kFew = 63;
+  DBuf<StreamEntry> packed(c, kStreamTableCap + 1);
+  launch(c, "census_pack", 0.0, k_pack_streams, dim3(1), dim3(256), 0, table.p, list.p, packed.p);
+  std::vector<StreamEntry> all(kFew + 1);
+  readback(c, all.data(), packed.p, kFew + 1);
+  const uint32_t ns = static_cast<uint32_t>(all[0].key);
+  if (ns > kFew) {
+    all.resize(ns + 1);
+    readback(c, all.data(), packed.p, ns + 1);
+  }
   t.streams.clear();
-  for (uint32_t s : slots) {
-    const StreamEntry& e = all[s];
+  for (uint32_t u = 0; u < ns; ++u) {
+    const StreamEntry& e = all[1 + u];
     itt_stream_summary o{};
     o.stream = static_cast<uint32_t>(e.key - 1);
     for (int k = 0; k < 6; ++k) o.counts[k] = static_cast<int64_t>(e.counts[k]);

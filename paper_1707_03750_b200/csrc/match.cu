@@ -90,9 +90,14 @@ struct OkF {  // compaction of successful anchors
 };
 
 // succ(x) = first ok anchor >= last(x) + 1; flags a conflict when succ(x) != x + 1
-__global__ void k_succ(const uint32_t* __restrict__ o_pos, const uint32_t* __restrict__ o_last, uint32_t n_ok,
-                       uint32_t* __restrict__ succ, uint32_t* __restrict__ conflict) {
+// n_ok comes from the ok-compaction scan's last status word (inclusive total), so this kernel is
+// launched over all anchors and the host reads n_ok and the conflict flag in one round trip
+__global__ void k_succ(const uint32_t* __restrict__ o_pos, const uint32_t* __restrict__ o_last,
+                       const uint64_t* __restrict__ scan_last, uint32_t* __restrict__ succ,
+                       uint32_t* __restrict__ conflict /* [0] flag, [1] n_ok */) {
+  const uint32_t n_ok = static_cast<uint32_t>(*scan_last & kValMask);
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x == 0) conflict[1] = n_ok;
   if (x >= n_ok) return;
   const uint64_t target = static_cast<uint64_t>(o_last[x]) + 1;
   uint32_t lo = x + 1, hi = n_ok;  // ok anchors after x; positions strictly increase
@@ -158,14 +163,16 @@ void approx_match_dev(Ctx* c, const int32_t* tokens, uint64_t n, const int32_t* 
   DBuf<uint32_t> o_pos(c, na), o_last(c, na), o_extra(c, na);
   device_scan<uint32_t, SumOp<uint32_t>>(c, "match_ok", na * 13.0,
                                          OkF{ok.p, anchors.p, last.p, extra.p, o_pos.p, o_last.p, o_extra.p}, na, scan);
-  const uint32_t n_ok = static_cast<uint32_t>(scan.total(c));
-  if (n_ok == 0) return;
-  DBuf<uint32_t> succ(c, n_ok + 1);
-  DBuf<uint32_t> conflict(c, 1);
+  DBuf<uint32_t> succ(c, na + 1);
+  DBuf<uint32_t> conflict(c, 2);
   conflict.zero();
-  launch(c, "match_succ", n_ok * 16.0, k_succ, dim3(grid_for(n_ok, 256)), dim3(256), 0, o_pos.p, o_last.p, n_ok, succ.p,
-         conflict.p);
-  if (read1(c, conflict.p) == 0) {  // chain = every ok anchor
+  launch(c, "match_succ", na * 16.0, k_succ, dim3(grid_for(na, 256)), dim3(256), 0, o_pos.p, o_last.p,
+         scan.buf.p + scan.tiles, succ.p, conflict.p);
+  uint32_t hc[2];
+  readback(c, hc, conflict.p, 2);
+  const uint32_t n_ok = hc[1];
+  if (n_ok == 0) return;
+  if (hc[0] == 0) {  // chain = every ok anchor
     out.n = n_ok;
     out.start = std::move(o_pos);
     out.end = std::move(o_last);

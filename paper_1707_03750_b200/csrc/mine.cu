@@ -311,6 +311,25 @@ __global__ void __launch_bounds__(256) k_tied_wide(const uint32_t* __restrict__ 
   if (lane_id() == 0 && m != 0xFFFFFFFFu) atomicMin(result, m);
 }
 
+// Result of one loop in one buffer (a single host round trip): the winning key, the pattern's
+// first occurrence and its tokens (text codes + lo).  out = [best.hi, best.lo, start, tokens...]
+__global__ void k_pattern_out(const Best* __restrict__ best, const unsigned int* __restrict__ start,
+                              const int32_t* __restrict__ text, int32_t lo, uint32_t max_out,
+                              uint32_t* __restrict__ out) {
+  const Best b = *best;
+  const uint32_t st = *start;
+  const uint32_t len = static_cast<uint32_t>(b.hi & 0xFFFFFFFFull);
+  if (threadIdx.x == 0) {
+    reinterpret_cast<unsigned long long*>(out)[0] = b.hi;
+    reinterpret_cast<unsigned long long*>(out)[1] = b.lo;
+    out[4] = st;
+    out[5] = 0;
+  }
+  if (b.hi == 0 && b.lo == 0) return;
+  for (uint32_t q = threadIdx.x; q < len && q < max_out; q += blockDim.x)
+    out[6 + q] = static_cast<uint32_t>(text[st + q] + lo);
+}
+
 }  // namespace
 
 void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv) {
@@ -376,11 +395,8 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
   DBuf<Best> bb(c, grid + 1);
   launch(c, "mine_reduce", s.np * 12.0, k_mine_reduce, dim3(grid), dim3(256), 0, a, bb.p);
   launch(c, "mine_final", grid * 16.0, k_best_final, dim3(1), dim3(32), 0, bb.p, grid, bb.p + grid);
-  const Best best = read1(c, bb.p + grid);
-  if (best.hi == 0 && best.lo == 0) {
-    no_pattern();
-    return r;
-  }
+  // the tie-break kernels run whether or not a candidate exists (no candidate key equals the
+  // empty key), so the whole result comes back in one round trip
   DBuf<unsigned int> start(c, 2);
   start.fill_bytes(0xFF);
   ITT_CUDA(cudaMemsetAsync(start.p + 1, 0, 4, c->stream));
@@ -390,18 +406,34 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
          wide.p, start.p + 1);
   launch(c, "mine_tied_wide", 0.0, k_tied_wide, dim3(static_cast<unsigned>(c->sm_count) * 4), dim3(256), 0, wide.p, start.p + 1,
          s.sa.p, start.p);
-  const uint32_t st = read1(c, start.p);
+  constexpr uint32_t kFirstRead = 4096;  // pattern tokens read back with the key; longer ones need a second trip
+  const uint32_t max_out = static_cast<uint32_t>(std::min<int64_t>(max_len, 0xFFFFFFF));
+  DBuf<uint32_t> res(c, 6 + static_cast<size_t>(max_out));
+  launch(c, "mine_pattern_out", max_out * 8.0, k_pattern_out, dim3(1), dim3(256), 0, bb.p + grid, start.p, s.text.p, s.lo,
+         max_out, res.p);
+  std::vector<uint32_t> h(6 + std::min(max_out, kFirstRead));
+  readback(c, h.data(), res.p, h.size());
+  Best best;
+  std::memcpy(&best.hi, &h[0], 8);
+  std::memcpy(&best.lo, &h[2], 8);
+  if (best.hi == 0 && best.lo == 0) {
+    no_pattern();
+    return r;
+  }
+  const uint32_t st = h[4];
   const int64_t len = static_cast<int64_t>(best.hi & 0xFFFFFFFFull);
   const int pass = 63 - static_cast<int>(best.hi >> 32);
-  r.tokens.resize(static_cast<size_t>(len));
   r.count = static_cast<int64_t>(best.lo);
   r.first_token = st;
   r.epsilon_used = eps[static_cast<size_t>(pass)];
-  // pattern = text[start, start+len) as codes; the caller maps codes back to token values
-  std::vector<int32_t> codes(static_cast<size_t>(len));
-  readback(c, codes.data(), s.text.p + st, static_cast<size_t>(len));
-  for (auto& v : codes) v += s.lo;
-  r.tokens = codes;
+  r.tokens.resize(static_cast<size_t>(len));
+  if (len > static_cast<int64_t>(kFirstRead)) {
+    std::vector<uint32_t> all(static_cast<size_t>(len));
+    readback(c, all.data(), res.p + 6, static_cast<size_t>(len));
+    std::memcpy(r.tokens.data(), all.data(), static_cast<size_t>(len) * 4);
+  } else {
+    std::memcpy(r.tokens.data(), &h[6], static_cast<size_t>(len) * 4);
+  }
   return r;
 }
 

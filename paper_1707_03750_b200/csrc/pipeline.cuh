@@ -23,6 +23,7 @@ struct DevRecords {
   const uint64_t* name_off = nullptr;
   const uint8_t* name_bytes = nullptr;  // null when the names are streamed from host memory
   const uint8_t* host_names = nullptr;  // streamed names (ITT_MEM_*_NAMES modes)
+  int64_t name_total = -1;               // name_off[n] when known on the host (host columns)
   int order = ITT_ORDER_UNKNOWN;
   // owned copies when the caller passed host memory
   DBuf<int64_t> o_start, o_dur, o_size;
