@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
   for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x) s_dev[i] = 0;
   __syncthreads();
   uint8_t* buf = s_buf[warp];
+  if (a.total == ~0ull) a.total = __ldg(&a.name_off[a.n]);  // resident names: end of the byte buffer
   const uint64_t groups = (a.n - a.row0 + 31) / 32;
   const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
   bool bad = false;
@@ -1037,8 +1038,13 @@ void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t bytes) {
 void build_dictionary(TraceState& t) {
   Ctx* c = t.c;
   const uint64_t n = t.rec.n;
-  uint64_t total = 0;
-  if (n) total = t.rec.name_total >= 0 ? static_cast<uint64_t>(t.rec.name_total) : read1(c, t.rec.name_off + n);
+  // the byte total is only needed on the host to plan streamed chunks (and for the profiler's
+  // byte count); resident names let the hash kernel read name_off[n] itself
+  const bool streamed = t.rec.host_names != nullptr;
+  uint64_t total = ~0ull;
+  if (n && t.rec.name_total >= 0) total = static_cast<uint64_t>(t.rec.name_total);
+  else if (n && (streamed || c->profiling)) total = read1(c, t.rec.name_off + n);
+  const double name_bytes = total == ~0ull ? 0.0 : static_cast<double>(total);
   t.slot.alloc(c, n);
   t.kind.alloc(c, n);
   DBuf<uint32_t> counters(c, 4);  // used count, overflow, collision, streamed-name arena overflow
@@ -1056,7 +1062,6 @@ void build_dictionary(TraceState& t) {
       std::max(1u, std::min<unsigned>((groups + kWarpsPerBlock - 1) / kWarpsPerBlock, c->sm_count * 12));
   // streamed names: row chunks of ~kStreamChunk bytes through two device windows (copy stream),
   // overlapping the copy of chunk k+1 with the hash pass over chunk k
-  const bool streamed = t.rec.host_names != nullptr;
   std::vector<uint64_t> bounds;  // name_off at chunk boundaries
   uint64_t rows_per_chunk = n, chunks = 1, window = 0;
   uint8_t* win[2] = {nullptr, nullptr};
@@ -1118,8 +1123,7 @@ void build_dictionary(TraceState& t) {
       HashArgs ha{t.rec.name_off, t.rec.name_bytes, 0,       total,      0,           n,           nullptr,  nullptr,
                   t.rec.device,   t.tkey.p,         cap - 1, seed,       t.slot.p,    t.used.p,    counters.p,
                   dev_counts.p,   dev_max.p};
-      launch(c, "intern_hash", 2.0 * static_cast<double>(total) + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0,
-             ha);
+      launch(c, "intern_hash", 2.0 * name_bytes + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0, ha);
     } else if (n) {
       if (arena.n < arena_cap) arena.alloc(c, arena_cap);
       arena_off.alloc(c, cap);
