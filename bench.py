@@ -117,13 +117,17 @@ class ClockSampler:
 
     def summary(self):
         rows = [r for ts, r in self.rows if self.t0 is None or (self.t0 - 0.02 <= ts <= (self.t1 or ts) + 0.02)]
+        in_window = bool(rows)
+        if not rows and self.rows and self.t0 is not None:  # window shorter than the interval: nearest samples
+            near = sorted(self.rows, key=lambda tr: min(abs(tr[0] - self.t0), abs(tr[0] - (self.t1 or self.t0))))
+            rows = [r for _, r in near[:2]]
         ok = [r for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
         sm = [float(r[0]) for r in ok]
         mx = [float(r[1]) for r in ok if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in ok for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(ok)}
+                "reasons": reasons, "samples": len(ok), "in_window": in_window, "interval_ms": self.interval_ms}
 
 
 def dist_env():
@@ -246,7 +250,7 @@ def bench_batch(args, world, rank, local, workload):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
@@ -255,7 +259,9 @@ def main():
                     help="override the workload's iteration count (smaller dry runs of C3/C5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
-    ap.add_argument("--clock-ms", type=int, default=50, help="nvidia-smi sampling interval during the timed region")
+    ap.add_argument("--clock-ms", type=int, default=200,
+                    help="nvidia-smi sampling interval during the timed region (the profiling recipe's 200 ms: "
+                         "NVML queries can stall the driver for milliseconds)")
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
     ap.add_argument("--workers", type=int, default=16, help="C4: concurrent streams (host threads) per GPU")
