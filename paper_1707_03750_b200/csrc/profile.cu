@@ -23,66 +23,86 @@ namespace itt {
 namespace {
 
 constexpr int kOpBlock = 256;
-// 36 B of shared memory per op id (3 x u64 sums + u32 count, last span, iterations): 6144 ops
-// = 216 KiB, under the 227 KiB cap
-constexpr uint32_t kSmemOps = 6144;
-constexpr size_t kOpSmemBytes = 36;
+// 28 B of shared memory per op id (3 x u64 sums + u32 count): 7936 ops = 217 KiB, under the
+// 227 KiB cap
+constexpr uint32_t kSmemOps = 7936;
+constexpr size_t kOpSmemBytes = 28;
 
 __device__ __forceinline__ int64_t clamped_gap(const int64_t* ts, const int64_t* te, uint64_t j) {
   const int64_t g = ts[j] - te[j - 1];
   return g > 0 ? g : 0;
 }
 
-// Per span (one CTA): the distinct-op bit set gives distinct_ops, thread-local sums the
-// iteration totals.
+// Per span: the distinct-op bit set gives distinct_ops (and +1 iteration for every op present),
+// thread-local sums the iteration totals.  Each CTA walks a contiguous range of spans; the
+// per-op iteration counts stay in shared memory and are flushed once per CTA.
 __global__ void __launch_bounds__(kOpBlock) k_op_iter(const int32_t* __restrict__ tokens, const int64_t* __restrict__ ts,
                                                       const int64_t* __restrict__ te, const uint8_t* __restrict__ kind,
                                                       const uint32_t* __restrict__ sp_start,
-                                                      const uint32_t* __restrict__ sp_end, uint32_t n_ops,
-                                                      uint32_t* __restrict__ distinct, itt_iter_op_total* __restrict__ it_tot) {
-  extern __shared__ uint32_t s_bits[];
+                                                      const uint32_t* __restrict__ sp_end, uint64_t I, uint32_t n_ops,
+                                                      uint32_t* __restrict__ distinct, itt_iter_op_total* __restrict__ it_tot,
+                                                      itt_op_total* __restrict__ op_tot) {
+  extern __shared__ uint32_t s_dyn[];
+  const uint32_t words = (n_ops + 31) / 32;
+  uint32_t* s_bits = s_dyn;
+  uint32_t* s_iters = s_dyn + words;  // [n_ops] when op_tot
   __shared__ unsigned long long s_red[3][kOpBlock / 32];
   __shared__ uint32_t s_warp[kOpBlock / 32];
-  const uint32_t words = (n_ops + 31) / 32;
-  for (uint32_t w = threadIdx.x; w < words; w += kOpBlock) s_bits[w] = 0;
-  __syncthreads();
-  const uint32_t s = sp_start[blockIdx.x], e = sp_end[blockIdx.x];
-  unsigned long long kern = 0, mem = 0, idle = 0;
-  for (uint32_t j = s + threadIdx.x; j <= e; j += kOpBlock) {
-    const uint32_t v = static_cast<uint32_t>(__ldg(&tokens[j]));
-    atomicOr(&s_bits[v >> 5], 1u << (v & 31));
-    const unsigned long long d = static_cast<unsigned long long>(te[j] - ts[j]);
-    if (kind[j] == ITT_KIND_KERNEL) kern += d;
-    else mem += d;
-    if (j > s) idle += static_cast<unsigned long long>(clamped_gap(ts, te, j));
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    kern += __shfl_xor_sync(0xffffffffu, kern, o);
-    mem += __shfl_xor_sync(0xffffffffu, mem, o);
-    idle += __shfl_xor_sync(0xffffffffu, idle, o);
-  }
-  if (lane_id() == 0) s_red[0][threadIdx.x >> 5] = kern, s_red[1][threadIdx.x >> 5] = mem, s_red[2][threadIdx.x >> 5] = idle;
-  __syncthreads();
-  uint32_t cnt = 0;
-  for (uint32_t w = threadIdx.x; w < words; w += kOpBlock) cnt += __popc(s_bits[w]);
-  uint32_t total;
-  block_exclusive_scan<uint32_t, SumOp<uint32_t>, kOpBlock>(cnt, SumOp<uint32_t>(), &total, s_warp);
-  if (threadIdx.x == 0) {
-    if (distinct) distinct[blockIdx.x] = total;
-    if (it_tot) {
-      unsigned long long a = 0, b = 0, c = 0;
-      for (int w = 0; w < kOpBlock / 32; ++w) a += s_red[0][w], b += s_red[1][w], c += s_red[2][w];
-      it_tot[blockIdx.x] = itt_iter_op_total{static_cast<int64_t>(total), static_cast<int64_t>(a), static_cast<int64_t>(b),
-                                             static_cast<int64_t>(c)};
+  if (op_tot)
+    for (uint32_t v = threadIdx.x; v < n_ops; v += kOpBlock) s_iters[v] = 0;
+  const uint64_t k0 = I * blockIdx.x / gridDim.x, k1 = I * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t k = k0; k < k1; ++k) {
+    for (uint32_t w = threadIdx.x; w < words; w += kOpBlock) s_bits[w] = 0;
+    __syncthreads();
+    const uint32_t s = sp_start[k], e = sp_end[k];
+    unsigned long long kern = 0, mem = 0, idle = 0;
+    for (uint32_t j = s + threadIdx.x; j <= e; j += kOpBlock) {
+      const uint32_t v = static_cast<uint32_t>(__ldg(&tokens[j]));
+      atomicOr(&s_bits[v >> 5], 1u << (v & 31));
+      const unsigned long long d = static_cast<unsigned long long>(te[j] - ts[j]);
+      if (kind[j] == ITT_KIND_KERNEL) kern += d;
+      else mem += d;
+      if (j > s) idle += static_cast<unsigned long long>(clamped_gap(ts, te, j));
     }
+    for (int o = 16; o > 0; o >>= 1) {
+      kern += __shfl_xor_sync(0xffffffffu, kern, o);
+      mem += __shfl_xor_sync(0xffffffffu, mem, o);
+      idle += __shfl_xor_sync(0xffffffffu, idle, o);
+    }
+    if (lane_id() == 0) s_red[0][threadIdx.x >> 5] = kern, s_red[1][threadIdx.x >> 5] = mem, s_red[2][threadIdx.x >> 5] = idle;
+    __syncthreads();
+    uint32_t cnt = 0;
+    for (uint32_t w = threadIdx.x; w < words; w += kOpBlock) {
+      uint32_t bits = s_bits[w];
+      cnt += __popc(bits);
+      if (op_tot)  // one thread per word: plain increments
+        while (bits) {
+          s_iters[w * 32 + __ffs(bits) - 1] += 1;
+          bits &= bits - 1;
+        }
+    }
+    uint32_t total;
+    block_exclusive_scan<uint32_t, SumOp<uint32_t>, kOpBlock>(cnt, SumOp<uint32_t>(), &total, s_warp);
+    if (threadIdx.x == 0) {
+      if (distinct) distinct[k] = total;
+      if (it_tot) {
+        unsigned long long x = 0, y = 0, z = 0;
+        for (int w = 0; w < kOpBlock / 32; ++w) x += s_red[0][w], y += s_red[1][w], z += s_red[2][w];
+        it_tot[k] = itt_iter_op_total{static_cast<int64_t>(total), static_cast<int64_t>(x), static_cast<int64_t>(y),
+                                      static_cast<int64_t>(z)};
+      }
+    }
+    __syncthreads();  // s_bits / s_red reuse
   }
+  if (op_tot)
+    for (uint32_t v = threadIdx.x; v < n_ops; v += kOpBlock)
+      if (s_iters[v]) atomicAdd(reinterpret_cast<unsigned long long*>(&op_tot[v].iterations), static_cast<unsigned long long>(s_iters[v]));
 }
 
 // Per-op totals at token level: each CTA takes a contiguous range of spans, accumulates a
-// shared table (count / kernel / memcpy / idle / iterations per op) and flushes its non-zero
-// entries with global atomics — CTAs x n_ops atomics instead of one per token or cell.  An op's
-// first token in a span bumps its iteration count (s_last holds the last span that saw it; a
-// barrier between spans keeps the threads on the same span).
+// shared table (count / kernel / memcpy / idle per op) and flushes its non-zero entries with
+// global atomics — CTAs x n_ops atomics instead of one per token or cell.  (Iterations per op come
+// from k_op_iter's per-span bit sets.)
 __global__ void __launch_bounds__(kOpBlock) k_op_totals(const int32_t* __restrict__ tokens, const int64_t* __restrict__ ts,
                                                         const int64_t* __restrict__ te, const uint8_t* __restrict__ kind,
                                                         const uint32_t* __restrict__ sp_start,
@@ -94,30 +114,25 @@ __global__ void __launch_bounds__(kOpBlock) k_op_totals(const int32_t* __restric
   unsigned long long* s_mem = s_acc + V;
   unsigned long long* s_idle = s_acc + 2 * static_cast<size_t>(V);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_acc + 3 * static_cast<size_t>(V));
-  uint32_t* s_last = s_cnt + V;
-  uint32_t* s_iters = s_last + V;
-  for (uint32_t v = threadIdx.x; v < V; v += kOpBlock)
-    s_kern[v] = 0, s_mem[v] = 0, s_idle[v] = 0, s_cnt[v] = 0, s_last[v] = kNone, s_iters[v] = 0;
+  for (uint32_t v = threadIdx.x; v < V; v += kOpBlock) s_kern[v] = 0, s_mem[v] = 0, s_idle[v] = 0, s_cnt[v] = 0;
   __syncthreads();
   const uint64_t k0 = I * blockIdx.x / gridDim.x, k1 = I * (blockIdx.x + 1) / gridDim.x;
-  for (uint64_t k = k0; k < k1; ++k) {
+  for (uint64_t k = k0; k < k1; ++k) {  // no per-span state: no barrier between spans
     const uint32_t s = sp_start[k], e = sp_end[k];
     for (uint32_t j = s + threadIdx.x; j <= e; j += kOpBlock) {
       const uint32_t v = static_cast<uint32_t>(__ldg(&tokens[j]));
       atomicAdd(&s_cnt[v], 1u);
-      if (atomicExch(&s_last[v], static_cast<uint32_t>(k)) != static_cast<uint32_t>(k)) atomicAdd(&s_iters[v], 1u);
       atomicAdd(kind[j] == ITT_KIND_KERNEL ? &s_kern[v] : &s_mem[v], static_cast<unsigned long long>(te[j] - ts[j]));
       if (j > s) {
         const int64_t g = clamped_gap(ts, te, j);
         if (g) atomicAdd(&s_idle[v], static_cast<unsigned long long>(g));
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (uint32_t v = threadIdx.x; v < V; v += kOpBlock) {
     if (!s_cnt[v]) continue;
     unsigned long long* o = reinterpret_cast<unsigned long long*>(&tot[v]);
-    atomicAdd(&o[0], static_cast<unsigned long long>(s_iters[v]));
     atomicAdd(&o[1], static_cast<unsigned long long>(s_cnt[v]));
     if (s_kern[v]) atomicAdd(&o[2], s_kern[v]);
     if (s_mem[v]) atomicAdd(&o[3], s_mem[v]);
@@ -295,10 +310,14 @@ OpProfile op_profile(Ctx* c, const int32_t* tokens, const int64_t* tok_start, co
     const size_t table_smem = static_cast<size_t>(n_ops) * kOpSmemBytes;
     DBuf<uint32_t> distinct;
     if (want_cells) distinct.alloc(c, I);
-    if (want_cells || iter_totals)
-      launch(c, "opprof_iter", static_cast<double>(n_tok) * 21.0 + I * 40.0, k_op_iter, dim3(static_cast<unsigned>(I)),
-           dim3(kOpBlock), bits_smem, tokens, tok_start, tok_end, tok_kind, spans.start.p, spans.end.p, n_ops,
-           want_cells ? distinct.p : nullptr, iter_totals ? dit.p : nullptr);
+    const unsigned span_grid = static_cast<unsigned>(std::min<uint64_t>(I, static_cast<uint64_t>(c->sm_count) * 8));
+    if (want_cells || iter_totals || op_totals) {
+      const size_t iter_smem = bits_smem + (op_totals ? static_cast<size_t>(n_ops) * 4 : 0);
+      smem_optin(c, k_op_iter, iter_smem);
+      launch(c, "opprof_iter", static_cast<double>(n_tok) * 21.0 + I * 40.0, k_op_iter, dim3(span_grid), dim3(kOpBlock),
+             iter_smem, tokens, tok_start, tok_end, tok_kind, spans.start.p, spans.end.p, I, n_ops,
+             want_cells ? distinct.p : nullptr, iter_totals ? dit.p : nullptr, op_totals ? dot.p : nullptr);
+    }
     if (op_totals) {
       smem_optin(c, k_op_totals, table_smem);
       const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(I, static_cast<uint64_t>(c->sm_count) * 2));

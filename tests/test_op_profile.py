@@ -110,7 +110,7 @@ def test_device_op_profile_random(ctx, O, method):
     rng = random.Random(5 + method)
     for trial in range(40):
         n = rng.randrange(1, 3000)
-        n_ops = rng.choice([1, 2, 7, 150, 4112, 6144])
+        n_ops = rng.choice([1, 2, 7, 150, 4112, 7936])
         tokens, ts, te, kind, spans = random_tokens(rng, n, n_ops, rng.randrange(0, 40))
         want = O.op_profile(tokens, ts, te, kind, n_ops, spans)
         got, ot, it = ctx.op_profile(tokens, ts, te, kind, n_ops, spans, method)
