@@ -465,43 +465,45 @@ __global__ void k_save_reps(const uint32_t* __restrict__ used, const uint32_t* _
   }
 }
 
-__device__ __forceinline__ bool contains_ci(const uint8_t* h, uint32_t hl, const char* needle, uint32_t nl) {
-  if (hl < nl) return false;
-  for (uint32_t i = 0; i + nl <= hl; ++i) {
-    uint32_t j = 0;
-    while (j < nl) {
-      uint8_t ch = h[i + j];
-      if (ch >= 'A' && ch <= 'Z') ch += 32;
-      if (ch != static_cast<uint8_t>(needle[j])) break;
-      ++j;
+// classify each distinct name once (trace.hpp:103-113): one warp per name, the lanes testing
+// different start positions of each needle
+__device__ __forceinline__ bool warp_contains_ci(const uint8_t* h, uint32_t hl, const char* needle, uint32_t nl) {
+  bool hit = false;
+  for (uint32_t base = 0; base + nl <= hl; base += 32) {  // uniform trip count across the warp
+    const uint32_t i = base + lane_id();
+    if (i + nl <= hl) {
+      uint32_t j = 0;
+      while (j < nl) {
+        uint8_t ch = h[i + j];
+        if (ch >= 'A' && ch <= 'Z') ch += 32;
+        if (ch != static_cast<uint8_t>(needle[j])) break;
+        ++j;
+      }
+      hit |= j == nl;
     }
-    if (j == nl) return true;
   }
-  return false;
+  return __any_sync(0xffffffffu, hit);
 }
 
-// classify each distinct name once (trace.hpp:103-113)
 __global__ void k_classify_slots(const uint32_t* __restrict__ used, uint32_t n_used, const uint64_t* __restrict__ tkey,
                                  const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes,
                                  const uint8_t* __restrict__ arena, const uint64_t* __restrict__ arena_off,
                                  uint8_t* __restrict__ tflags) {
-  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= n_used) return;
+  const uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= n_used) return;  // whole warps exit together
   const uint32_t s = used[u];
   const uint32_t r = static_cast<uint32_t>(tkey[s]);  // first inserter's row
   const uint8_t* p = arena ? arena + arena_off[s] : bytes + name_off[r];
   const uint32_t len = static_cast<uint32_t>(name_off[r + 1] - name_off[r]);
   uint8_t f = 0;
-  if (contains_ci(p, len, "memcpy", 6)) f |= NB_MEMCPY;
-  if (contains_ci(p, len, "htod", 4)) f |= NB_HTOD;
-  if (contains_ci(p, len, "dtoh", 4)) f |= NB_DTOH;
-  if (contains_ci(p, len, "dtod", 4)) f |= NB_DTOD;
-  if (contains_ci(p, len, "memset", 6)) f |= NB_MEMSET;
-  tflags[s] = f;
+  if (warp_contains_ci(p, len, "memcpy", 6)) f |= NB_MEMCPY;
+  if (warp_contains_ci(p, len, "htod", 4)) f |= NB_HTOD;
+  if (warp_contains_ci(p, len, "dtoh", 4)) f |= NB_DTOH;
+  if (warp_contains_ci(p, len, "dtod", 4)) f |= NB_DTOD;
+  if (warp_contains_ci(p, len, "memset", 6)) f |= NB_MEMSET;
+  if (lane_id() == 0) tflags[s] = f;
 }
 
-// per record: kind from the slot's classify bits and throughput presence; per slot: the smallest
-// row carrying the name (deterministic name_row, whichever warp inserted first)
 __global__ void k_name_bounds(const uint64_t* __restrict__ name_off, uint64_t n, uint64_t rows_per_chunk,
                               uint64_t chunks, uint64_t* __restrict__ out) {
   const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1186,7 +1188,8 @@ void build_dictionary(TraceState& t) {
     break;
   }
   if (t.n_used)
-    launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(t.n_used, 128)), dim3(128), 0, t.used.p,
+    launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(static_cast<uint64_t>(t.n_used) * 32, 128)),
+           dim3(128), 0, t.used.p,
            t.n_used, t.tkey.p, t.rec.name_off, t.rec.name_bytes, streamed ? arena.p : nullptr,
            streamed ? arena_off.p : nullptr, t.tflags.p);
   if (n) {

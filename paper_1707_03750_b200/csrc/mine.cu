@@ -92,6 +92,21 @@ __global__ void k_sparse_level(uint32_t* st, uint32_t nt, int l) {
   st[static_cast<uint64_t>(l) * nt + t] = v;
 }
 
+// all sparse-table levels in one CTA (small tile counts): one launch instead of one per level
+__global__ void __launch_bounds__(1024) k_sparse_all(uint32_t* st, uint32_t nt, int levels) {
+  for (int l = 1; l < levels; ++l) {
+    const uint32_t half = 1u << (l - 1);
+    const uint32_t* prev = st + static_cast<uint64_t>(l - 1) * nt;
+    uint32_t* cur = st + static_cast<uint64_t>(l) * nt;
+    for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
+      uint32_t v = prev[t];
+      if (t + half < nt) v = min(v, prev[t + half]);
+      cur[t] = v;
+    }
+    __syncthreads();  // level l complete (global writes visible to the block)
+  }
+}
+
 struct AnsvArgs {
   const uint32_t* lcp;
   const uint32_t* premin;
@@ -340,14 +355,18 @@ void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv) {
   while ((1u << tlevels) <= nt) ++tlevels;
   DBuf<uint32_t> tst(c, static_cast<size_t>(tlevels) * nt);
   launch(c, "ansv_tile_minima", np * 12.0, k_tile_minima, dim3(nt), dim3(kTileA), 0, s.lcp.p, np, premin.p, sufmin.p, tst.p);
-  for (int l = 1; l < tlevels; ++l)
-    launch(c, "ansv_sparse", nt * 12.0, k_sparse_level, dim3(grid_for(nt, 256)), dim3(256), 0, tst.p, nt, l);
+  if (nt <= 65536) {
+    if (tlevels > 1)
+      launch(c, "ansv_sparse", nt * 12.0 * (tlevels - 1), k_sparse_all, dim3(1), dim3(1024), 0, tst.p, nt, tlevels);
+  } else {
+    for (int l = 1; l < tlevels; ++l)
+      launch(c, "ansv_sparse", nt * 12.0, k_sparse_level, dim3(grid_for(nt, 256)), dim3(256), 0, tst.p, nt, l);
+  }
   iv.cnt.alloc(c, np);
   iv.par.alloc(c, np);
   iv.lb.alloc(c, np);
   AnsvArgs a{s.lcp.p, premin.p, sufmin.p, tst.p, nt, tlevels, np, iv.cnt.p, iv.par.p, iv.lb.p};
   launch(c, "ansv_intervals", np * 16.0, k_ansv, dim3(nt), dim3(kAnsvBlock), 0, a);
-  c->sync();
 }
 
 MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, const itt_mining_cfg& cfg,

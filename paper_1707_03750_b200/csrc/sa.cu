@@ -387,7 +387,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p, s.cap);
   s.lcp.alloc(c, np);
   launch(c, "lcp_gather", np * 12.0, k_lcp_gather, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, plcp.p, np, s.lcp.p);
-  c->sync();  // dlv must outlive the kernels
+  // dlv is released stream-ordered (or lives in the call's arena): no host wait needed
 }
 
 }  // namespace itt
