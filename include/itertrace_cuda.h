@@ -299,6 +299,29 @@ int itt_op_profile(itt_ctx* ctx, const int32_t* tokens, const int64_t* tok_start
                    int method, itt_op_total* op_totals, itt_iter_op_total* iter_totals, itt_op_cell** cells,
                    uint64_t* n_cells);
 
+/* ------------------------------------------------------- CSV ingest
+ * parse_trace_text (ingest.hpp:154-402) on the GPU: the header / units rows are read on the host,
+ * every data line is parsed by one device thread with the reference's exact rules (quoted fields,
+ * inline units, exact decimal scaling, strtod acceptance of Throughput), skipped rows and their
+ * reasons, the 10% TooManyBadRows rule and the unit warnings.  The records stay in HBM in source
+ * line order (itt_analyze sorts them by (start, row) like ingest.hpp:396-400); device labels are
+ * interned to ranks in byte-lexicographic order. */
+typedef struct itt_parsed_trace {
+  itt_records records;               /* ITT_MEM_DEVICE columns owned by this object, ITT_ORDER_UNKNOWN */
+  const uint64_t* line;              /* [records.n] 1-based source line (TraceRecord::row) */
+  uint32_t n_device_labels;
+  const char* const* device_labels;  /* records.device indexes this, byte-lexicographic */
+  uint64_t rows_total, rows_parsed, rows_skipped;   /* IngestReport (ingest.hpp:21-28) */
+  uint64_t n_skips;
+  const uint64_t* skip_line;         /* [n_skips] */
+  const char* const* skip_reason;    /* [n_skips], the reference's reason text */
+  int32_t column[7];                 /* field index of Start, Duration, Size, Throughput, Device, Stream, Name; -1 absent */
+  uint32_t n_warnings;
+  const char* const* warnings;       /* NormalizedTrace::warnings (unit row) */
+} itt_parsed_trace;
+int itt_parse_csv(itt_ctx* ctx, const char* text, uint64_t len, const char* origin_label, itt_parsed_trace** out);
+int itt_free_parsed(itt_ctx* ctx, itt_parsed_trace* p);
+
 /* ------------------------------------------------------- L7 orchestration */
 /* itt_analyze_opts.flags: OP_PROFILE fills op_totals / iter_op_totals of every loop result;
  * OP_CELLS also returns the (iteration, op) cell grid (size ~ tokens: large) */

@@ -162,8 +162,44 @@ class Ref(_Common):
 
     def __init__(self):
         super().__init__(os.path.join(HERE, "_ref", "libitertrace_ref.so"))
+        L = self.lib
+        L.ref_parse_csv.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, P(abi.ref_parsed)]
+        L.ref_free_parsed.argtypes = [P(abi.ref_parsed)]
+        L.ref_synth_csv.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_int64, C.c_int32,
+                                    C.c_int32, P(C.c_uint64)]
+        L.ref_synth_csv.restype = C.c_void_p
+        L.ref_analyze_csv.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, P(abi.itt_analyze_opts), P(abi.ref_analysis)]
         self.lib.ref_analyze.argtypes = [P(abi.itt_records), P(abi.itt_analyze_opts), C.c_int, P(abi.ref_analysis)]
         self.lib.ref_free_analysis.argtypes = [P(abi.ref_analysis)]
+
+    def parse_csv(self, text: bytes, label: str = "trace.csv") -> dict:
+        """parse_trace_text (ingest.hpp:154-402), the reference itself."""
+        return _ref_parse(self.lib, text, label)
+
+    def synth_csv(self, seed=42, pattern_len=6, iterations=40, vocab_size=16, insert_prob=0.0, max_inserts=0,
+                  inside_pattern=False, pathology=0) -> bytes:
+        """The reference generator's CSV (synth.hpp:187)."""
+        n = C.c_uint64()
+        p = self.lib.ref_synth_csv(seed, pattern_len, iterations, vocab_size, insert_prob, max_inserts,
+                                   1 if inside_pattern else 0, pathology, C.byref(n))
+        try:
+            return C.string_at(p, n.value)
+        finally:
+            self._free(p)
+
+    def analyze_csv(self, text: bytes, loops, label="trace.csv", epsilon0=1, k0=-1, main_stream=-1) -> dict:
+        """parse_trace_text + analyze_trace: summary JSON / details CSV as the reference CLI writes them."""
+        lp = (C.c_int64 * max(1, len(loops)))(*loops)
+        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream, 0)
+        out = abi.ref_analysis()
+        rc = self.lib.ref_analyze_csv(text, len(text), label.encode(), C.byref(opts), C.byref(out))
+        try:
+            if rc:
+                return {"status": rc, "error": out.error.decode("utf-8", "surrogateescape")}
+            return {"status": 0, "summary_json": out.summary_json.decode(), "details_csv": out.details_csv.decode(),
+                    "warnings": out.warnings.decode().split("\n") if out.warnings else []}
+        finally:
+            self.lib.ref_free_analysis(C.byref(out))
 
     def analyze(self, recs: abi.Records, loops, epsilon0=1, k0=-1, main_stream=-1, staged=False):
         lp = (C.c_int64 * max(1, len(loops)))(*loops)
@@ -198,6 +234,38 @@ class Ref(_Common):
             return res
         finally:
             self.lib.ref_free_analysis(C.byref(out))
+
+
+def _ref_parse(lib, text: bytes, label: str) -> dict:
+    out = abi.ref_parsed()
+    rc = lib.ref_parse_csv(text, len(text), label.encode(), C.byref(out))
+    try:
+        if rc:
+            return {"status": rc, "error": out.error.decode("utf-8", "surrogateescape")}
+        n = out.n
+
+        def arr(ptr, dt, cnt):
+            return np.ctypeslib.as_array(ptr, shape=(cnt,)).astype(dt, copy=True) if cnt else np.zeros(0, dt)
+        name_off = arr(out.name_off, np.uint64, n + 1)
+        dev_off = arr(out.device_off, np.uint64, n + 1)
+        names = bytes(arr(out.name_bytes, np.uint8, int(name_off[-1]))) if n else b""
+        devs = bytes(arr(out.device_bytes, np.uint8, int(dev_off[-1]))) if n else b""
+        cols = ("Start", "Duration", "Size", "Throughput", "Device", "Stream", "Name")
+        return {
+            "status": 0, "n": n,
+            "start_ns": arr(out.start_ns, np.int64, n), "duration_ns": arr(out.duration_ns, np.int64, n),
+            "size_bytes": arr(out.size_bytes, np.int64, n), "flags": arr(out.flags, np.uint8, n),
+            "stream": arr(out.stream, np.uint32, n), "row": arr(out.row, np.uint64, n),
+            "names": [names[name_off[i]:name_off[i + 1]] for i in range(n)],
+            "devices": [devs[dev_off[i]:dev_off[i + 1]].decode("utf-8", "surrogateescape") for i in range(n)],
+            "rows_total": out.rows_total, "rows_parsed": out.rows_parsed, "rows_skipped": out.rows_skipped,
+            "skips": list(zip([int(x) for x in arr(out.skip_line, np.uint64, out.n_skips)],
+                              out.skip_reasons.decode("utf-8", "surrogateescape").split("\n") if out.n_skips else [])),
+            "column": {cols[i]: int(out.column[i]) for i in range(7) if out.column[i] >= 0},
+            "warnings": out.warnings.decode("utf-8", "surrogateescape").split("\n") if out.warnings else [],
+        }
+    finally:
+        lib.ref_free_parsed(C.byref(out))
 
 
 class Oracle(_Common):

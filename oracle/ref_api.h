@@ -83,6 +83,36 @@ int ref_summarize_streams(const itt_records* recs, int filter_device, itt_stream
                           uint32_t* n_out, uint64_t* dropped);
 void ref_free(void* p);
 
+/* ---- CSV ingest (ingest.hpp:154-402) */
+typedef struct ref_parsed {
+  int32_t status;        /* 0 or 1 + ErrorKind */
+  char* error;
+  uint64_t n;            /* records, in the reference's output order (stable-sorted by (start, row)) */
+  int64_t* start_ns;
+  int64_t* duration_ns;
+  int64_t* size_bytes;   /* 0 when absent */
+  uint8_t* flags;        /* ITT_REC_HAS_SIZE | ITT_REC_HAS_THROUGHPUT */
+  uint32_t* stream;
+  uint64_t* row;
+  uint64_t* name_off;    /* [n+1] */
+  uint8_t* name_bytes;
+  uint64_t* device_off;  /* [n+1] device label bytes per record */
+  uint8_t* device_bytes;
+  uint64_t rows_total, rows_parsed, rows_skipped;
+  uint64_t n_skips;
+  uint64_t* skip_line;
+  char* skip_reasons;    /* '\n'-joined */
+  int32_t column[7];     /* Start, Duration, Size, Throughput, Device, Stream, Name; -1 absent */
+  char* warnings;        /* '\n'-joined NormalizedTrace::warnings */
+} ref_parsed;
+int ref_parse_csv(const char* text, uint64_t len, const char* label, ref_parsed* out);
+void ref_free_parsed(ref_parsed* p);
+/* the reference generator's CSV (synth.hpp:187): malloc'd text */
+char* ref_synth_csv(uint64_t seed, int64_t pattern_len, int64_t iterations, int64_t vocab_size, double insert_prob,
+                    int64_t max_inserts, int32_t inside_pattern, int32_t pathology, uint64_t* len);
+/* parse_trace_text + analyze_trace end to end (summary JSON / details CSV as the CLI writes them) */
+int ref_analyze_csv(const char* text, uint64_t len, const char* label, const itt_analyze_opts* opts, ref_analysis* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -411,3 +411,128 @@ extern "C" int ref_summarize_streams(const itt_records* recs, int filter_device,
 }
 
 extern "C" void ref_free(void* p) { std::free(p); }
+
+// ---- CSV ingest through the reference (test infrastructure)
+extern "C" int ref_parse_csv(const char* text, uint64_t len, const char* label, ref_parsed* out) {
+  std::memset(out, 0, sizeof(*out));
+  try {
+    auto [trace, rep] = parse_trace_text(std::string_view(text, len), label);
+    const size_t n = trace.records.size();
+    out->n = n;
+    out->start_ns = static_cast<int64_t*>(std::calloc(n + 1, 8));
+    out->duration_ns = static_cast<int64_t*>(std::calloc(n + 1, 8));
+    out->size_bytes = static_cast<int64_t*>(std::calloc(n + 1, 8));
+    out->flags = static_cast<uint8_t*>(std::calloc(n + 1, 1));
+    out->stream = static_cast<uint32_t*>(std::calloc(n + 1, 4));
+    out->row = static_cast<uint64_t*>(std::calloc(n + 1, 8));
+    out->name_off = static_cast<uint64_t*>(std::calloc(n + 1, 8));
+    out->device_off = static_cast<uint64_t*>(std::calloc(n + 1, 8));
+    std::string names, devs;
+    for (size_t i = 0; i < n; ++i) {
+      const TraceRecord& r = trace.records[i];
+      out->start_ns[i] = r.start_ns;
+      out->duration_ns[i] = r.duration_ns;
+      if (r.size_bytes) out->size_bytes[i] = *r.size_bytes, out->flags[i] |= ITT_REC_HAS_SIZE;
+      if (r.throughput_bps) out->flags[i] |= ITT_REC_HAS_THROUGHPUT;
+      out->stream[i] = r.stream;
+      out->row[i] = r.row;
+      out->name_off[i] = names.size();
+      names += r.name;
+      out->device_off[i] = devs.size();
+      devs += r.device;
+    }
+    out->name_off[n] = names.size();
+    out->device_off[n] = devs.size();
+    out->name_bytes = static_cast<uint8_t*>(std::malloc(names.size() + 1));
+    std::memcpy(out->name_bytes, names.data(), names.size());
+    out->device_bytes = static_cast<uint8_t*>(std::malloc(devs.size() + 1));
+    std::memcpy(out->device_bytes, devs.data(), devs.size());
+    out->rows_total = rep.rows_total;
+    out->rows_parsed = rep.rows_parsed;
+    out->rows_skipped = rep.rows_skipped;
+    out->n_skips = rep.skip_reasons.size();
+    out->skip_line = static_cast<uint64_t*>(std::calloc(rep.skip_reasons.size() + 1, 8));
+    std::string why;
+    for (size_t i = 0; i < rep.skip_reasons.size(); ++i) {
+      out->skip_line[i] = rep.skip_reasons[i].first;
+      if (i) why += '\n';
+      why += rep.skip_reasons[i].second;
+    }
+    out->skip_reasons = dup_str(why);
+    const char* cols[7] = {"Start", "Duration", "Size", "Throughput", "Device", "Stream", "Name"};
+    for (int q = 0; q < 7; ++q) {
+      auto it = rep.column_map.find(cols[q]);
+      out->column[q] = it == rep.column_map.end() ? -1 : static_cast<int32_t>(it->second);
+    }
+    std::string w;
+    for (size_t i = 0; i < trace.warnings.size(); ++i) {
+      if (i) w += '\n';
+      w += trace.warnings[i];
+    }
+    out->warnings = dup_str(w);
+  } catch (const Error& e) {
+    out->status = status_of(e);
+    out->error = dup_str(e.what());
+  } catch (const std::exception& e) {
+    out->status = 1000;
+    out->error = dup_str(e.what());
+  }
+  return out->status;
+}
+
+extern "C" void ref_free_parsed(ref_parsed* p) {
+  if (!p) return;
+  for (void* x : {static_cast<void*>(p->start_ns), static_cast<void*>(p->duration_ns), static_cast<void*>(p->size_bytes),
+                  static_cast<void*>(p->flags), static_cast<void*>(p->stream), static_cast<void*>(p->row),
+                  static_cast<void*>(p->name_off), static_cast<void*>(p->name_bytes), static_cast<void*>(p->device_off),
+                  static_cast<void*>(p->device_bytes), static_cast<void*>(p->skip_line), static_cast<void*>(p->skip_reasons),
+                  static_cast<void*>(p->error), static_cast<void*>(p->warnings)})
+    std::free(x);
+  std::memset(p, 0, sizeof(*p));
+}
+
+extern "C" char* ref_synth_csv(uint64_t seed, int64_t pattern_len, int64_t iterations, int64_t vocab_size, double insert_prob,
+                               int64_t max_inserts, int32_t inside_pattern, int32_t pathology, uint64_t* len) {
+  SynthConfig cfg;
+  cfg.seed = seed;
+  cfg.pattern_len = pattern_len;
+  cfg.iterations = iterations;
+  cfg.vocab_size = vocab_size;
+  cfg.insert_prob = insert_prob;
+  cfg.max_inserts = max_inserts;
+  cfg.insert_placement = inside_pattern ? InsertPlacement::inside_pattern : InsertPlacement::after_pattern;
+  cfg.pathology = static_cast<Pathology>(pathology);
+  const std::string csv = generate(cfg).trace_csv;
+  *len = csv.size();
+  return dup_str(csv);
+}
+
+extern "C" int ref_analyze_csv(const char* text, uint64_t len, const char* label, const itt_analyze_opts* opts,
+                               ref_analysis* out) {
+  std::memset(out, 0, sizeof(*out));
+  try {
+    AnalyzeOptions opt;
+    for (uint32_t i = 0; i < opts->n_loops; ++i) opt.loops.push_back(opts->loops[i]);
+    opt.epsilon0 = opts->epsilon0;
+    if (opts->k0 >= 0) opt.k0 = opts->k0;
+    if (opts->main_stream >= 0) opt.main_stream = static_cast<uint32_t>(opts->main_stream);
+    auto [trace, rep] = parse_trace_text(std::string_view(text, len), label);
+    (void)rep;
+    const AnalysisResult res = analyze_trace(std::move(trace), label, opt);
+    std::string w;
+    for (size_t i = 0; i < res.report.warnings.size(); ++i) {
+      if (i) w += '\n';
+      w += res.report.warnings[i];
+    }
+    out->warnings = dup_str(w);
+    out->summary_json = dup_str(summary_to_json(res.report).dump(2) + "\n");
+    out->details_csv = dup_str(res.details.empty() ? std::string() : details_to_csv(res.details[0]));
+  } catch (const Error& e) {
+    out->status = status_of(e);
+    out->error = dup_str(e.what());
+  } catch (const std::exception& e) {
+    out->status = 1000;
+    out->error = dup_str(e.what());
+  }
+  return out->status;
+}

@@ -183,6 +183,22 @@ class itt_loop_result(C.Structure):
     ]
 
 
+class itt_parsed_trace(C.Structure):
+    _fields_ = [
+        ("records", itt_records),
+        ("line", P(C.c_uint64)),
+        ("n_device_labels", C.c_uint32),
+        ("device_labels", P(C.c_char_p)),
+        ("rows_total", C.c_uint64), ("rows_parsed", C.c_uint64), ("rows_skipped", C.c_uint64),
+        ("n_skips", C.c_uint64),
+        ("skip_line", P(C.c_uint64)),
+        ("skip_reason", P(C.c_char_p)),
+        ("column", C.c_int32 * 7),
+        ("n_warnings", C.c_uint32),
+        ("warnings", P(C.c_char_p)),
+    ]
+
+
 class itt_analysis(C.Structure):
     _fields_ = [
         ("census", itt_census),
@@ -221,6 +237,19 @@ class ref_loop(C.Structure):
         ("avg_size_bytes", C.c_double),
         ("max_interval_ns", C.c_int64),
         ("insufficient_intervals", C.c_int32), ("diagnosis", C.c_int32),
+    ]
+
+
+class ref_parsed(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("error", C.c_char_p), ("n", C.c_uint64),
+        ("start_ns", P(C.c_int64)), ("duration_ns", P(C.c_int64)), ("size_bytes", P(C.c_int64)),
+        ("flags", P(C.c_uint8)), ("stream", P(C.c_uint32)), ("row", P(C.c_uint64)),
+        ("name_off", P(C.c_uint64)), ("name_bytes", P(C.c_uint8)),
+        ("device_off", P(C.c_uint64)), ("device_bytes", P(C.c_uint8)),
+        ("rows_total", C.c_uint64), ("rows_parsed", C.c_uint64), ("rows_skipped", C.c_uint64),
+        ("n_skips", C.c_uint64), ("skip_line", P(C.c_uint64)), ("skip_reasons", C.c_char_p),
+        ("column", C.c_int32 * 7), ("warnings", C.c_char_p),
     ]
 
 

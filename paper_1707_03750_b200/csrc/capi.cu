@@ -9,6 +9,7 @@
 #include <new>
 #include <set>
 
+#include "ingest.cuh"
 #include "pipeline.cuh"
 
 using namespace itt;
@@ -807,6 +808,58 @@ int itt_free_analysis(itt_ctx* ctx, itt_analysis* a) {
   }
   std::free(a->loops);
   std::free(a);
+  return ITT_OK;
+}
+
+// ------------------------------------------------------------------ CSV ingest
+struct ParsedHolder {
+  itt_parsed_trace pub;  // first member: the C handle points here
+  ParsedCsv csv;
+  std::vector<const char*> labels, reasons, warnings;
+};
+
+int itt_parse_csv(itt_ctx* ctx, const char* text, uint64_t len, const char* origin_label, itt_parsed_trace** out) {
+  if (!out || (len && !text)) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  ParsedHolder* h = new (std::nothrow) ParsedHolder;
+  if (!h) return ITT_E_CUDA;
+  const int rc = guarded(ctx, [&](Ctx* c) {
+    parse_csv(c, text, len, origin_label ? origin_label : "trace.csv", h->csv);
+    ParsedCsv& p = h->csv;
+    itt_parsed_trace& o = h->pub;
+    o.records = itt_records{p.n,      p.start, p.dur,    p.size,          p.flags, p.stream, p.device,
+                            p.name_off, p.name_bytes, ITT_MEM_DEVICE, ITT_ORDER_UNKNOWN};
+    o.line = p.line.data();
+    for (const auto& x : p.device_labels) h->labels.push_back(x.c_str());
+    for (const auto& x : p.skip_reason) h->reasons.push_back(x.c_str());
+    for (const auto& x : p.warnings) h->warnings.push_back(x.c_str());
+    o.n_device_labels = static_cast<uint32_t>(h->labels.size());
+    o.device_labels = h->labels.data();
+    o.rows_total = p.rows_total;
+    o.rows_parsed = p.rows_parsed;
+    o.rows_skipped = p.rows_skipped;
+    o.n_skips = p.skip_line.size();
+    o.skip_line = p.skip_line.data();
+    o.skip_reason = h->reasons.data();
+    for (int q = 0; q < kIngestCols; ++q) o.column[q] = p.col[q];
+    o.n_warnings = static_cast<uint32_t>(h->warnings.size());
+    o.warnings = h->warnings.data();
+  });
+  if (rc != ITT_OK) {
+    h->csv.release();
+    delete h;
+    return rc;
+  }
+  *out = &h->pub;
+  return ITT_OK;
+}
+
+int itt_free_parsed(itt_ctx* ctx, itt_parsed_trace* p) {
+  if (!p) return ITT_OK;
+  ParsedHolder* h = reinterpret_cast<ParsedHolder*>(p);
+  if (ctx) cudaSetDevice(ctx->c.device);
+  h->csv.release();
+  delete h;
   return ITT_OK;
 }
 

@@ -53,6 +53,8 @@ def lib() -> C.CDLL:
         "itt_batch_error": ([vp, C.c_uint64], C.c_char_p),
         "itt_batch_launch_count": ([vp, P(C.c_uint64)], C.c_int),
         "itt_batch_free": ([vp, P(P(abi.itt_analysis)), C.c_uint64], C.c_int),
+        "itt_parse_csv": ([vp, C.c_char_p, C.c_uint64, C.c_char_p, P(P(abi.itt_parsed_trace))], C.c_int),
+        "itt_free_parsed": ([vp, P(abi.itt_parsed_trace)], C.c_int),
         "itt_ctx_mem_stats": ([vp, P(C.c_uint64), P(C.c_uint64), C.c_int], C.c_int),
         "itt_device_alloc": ([vp, C.c_uint64, P(vp)], C.c_int),
         "itt_device_free": ([vp, vp], C.c_int),
@@ -215,6 +217,12 @@ class Context:
 
     def synchronize(self):
         self._check(lib().itt_ctx_synchronize(self.h))
+
+    def parse_csv(self, text: bytes, label: str = "trace.csv") -> "ParsedTrace":
+        """itt_parse_csv: parse_trace_text on the GPU."""
+        out = P(abi.itt_parsed_trace)()
+        self._check(lib().itt_parse_csv(self.h, text, len(text), label.encode(), C.byref(out)))
+        return ParsedTrace(self, out)
 
     def upload(self, recs: abi.Records, names_host: bool = False) -> DeviceRecords:
         return DeviceRecords(self, recs, names_host)
@@ -404,6 +412,57 @@ class Context:
                 C.memmove(res.ctypes.data, out, n * C.sizeof(abi.itt_op_cell))
             lib().itt_free(self.h, out)
         return res, ot[:n_ops], it[:len(spans)]
+
+
+class ParsedTrace:
+    """itt_parse_csv result: records resident in HBM (source line order) + the IngestReport.
+    Pass it to Context.analyze_raw like any record set."""
+
+    def __init__(self, ctx: "Context", ptr):
+        self.ctx = ctx
+        self.ptr = ptr
+        p = ptr[0]
+        self.n = int(p.records.n)
+        self.rows_total, self.rows_parsed, self.rows_skipped = int(p.rows_total), int(p.rows_parsed), int(p.rows_skipped)
+        self.column = {k: int(p.column[i]) for i, k in enumerate(
+            ("Start", "Duration", "Size", "Throughput", "Device", "Stream", "Name")) if p.column[i] >= 0}
+        self.device_labels = [p.device_labels[i].decode("utf-8", "surrogateescape") for i in range(p.n_device_labels)]
+        self.skips = [(int(p.skip_line[i]), p.skip_reason[i].decode("utf-8", "surrogateescape")) for i in range(p.n_skips)]
+        self.warnings = [p.warnings[i].decode("utf-8", "surrogateescape") for i in range(p.n_warnings)]
+        self.line = np.ctypeslib.as_array(p.line, shape=(self.n,)).copy() if self.n else np.zeros(0, np.uint64)
+
+    def c(self) -> abi.itt_records:
+        return self.ptr[0].records
+
+    def columns(self) -> dict:
+        """Host copies of the device columns (tests)."""
+        r = self.ptr[0].records
+        out = {}
+        for name, dt, cnt in (("start_ns", np.int64, self.n), ("duration_ns", np.int64, self.n),
+                              ("size_bytes", np.int64, self.n), ("flags", np.uint8, self.n),
+                              ("stream", np.uint32, self.n), ("device", np.uint16, self.n),
+                              ("name_off", np.uint64, self.n + 1)):
+            a = np.zeros(max(1, cnt), dt)
+            self.ctx._check(lib().itt_memcpy_d2h(self.ctx.h, a.ctypes.data, C.cast(getattr(r, name), C.c_void_p),
+                                                a.nbytes if cnt else 0))
+            out[name] = a[:cnt]
+        nb = int(out["name_off"][-1]) if self.n else 0
+        b = np.zeros(max(1, nb), np.uint8)
+        self.ctx._check(lib().itt_memcpy_d2h(self.ctx.h, b.ctypes.data, C.cast(r.name_bytes, C.c_void_p), nb))
+        out["name_bytes"] = b[:nb]
+        self.ctx.synchronize()
+        return out
+
+    def free(self):
+        if self.ptr is not None and self.ctx.h:
+            lib().itt_free_parsed(self.ctx.h, self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class Batch:

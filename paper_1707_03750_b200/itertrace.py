@@ -181,7 +181,7 @@ def rows_to_metrics(rows) -> list:
 def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Optional[int] = None,
                   theta_copy: float = 0.10, theta_cpu: float = 10.0, main_stream: Optional[int] = None,
                   trace_label: str = "trace.csv", device_labels=None, names=None,
-                  op_profile=False) -> AnalysisResult:
+                  op_profile=False, trace_warnings=()) -> AnalysisResult:
     """analyze_trace (pipeline.hpp:34-134): device pipeline + host finish in reference order.
     op_profile=True adds the a12 second-level per-op profile of every loop ("cells": with the
     (iteration, op) grid); no reference counterpart, and the reference's own outputs are unchanged."""
@@ -191,7 +191,7 @@ def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Option
     except IttError as e:
         raise AnalyzeError(e.kind, str(e)) from e
     label = (lambda d: device_labels[d]) if device_labels is not None else (lambda d: "dev%05u" % d)
-    warnings = []
+    warnings = list(trace_warnings)  # the trace's own (ingest) warnings come first (pipeline.hpp:51)
     if raw["n_devices"] > 1:  # streams.hpp:198-203
         warnings.append("MultiDeviceTrace: kept majority device '%s', dropped %d records from other devices"
                         % (label(raw["majority_device"]), raw["dropped"]))
@@ -206,7 +206,9 @@ def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Option
         warnings.append("OverlappingKernels: %d consecutive main-stream records report overlapping intervals "
                         "(timer granularity)" % raw["overlapping_kernels"])
     name_of = None
-    if names is not None:
+    if isinstance(names, _LazyNames):
+        name_of = names.bind(raw["name_row"])
+    elif names is not None:
         name_of = names
     elif hasattr(recs, "name"):
         name_of = [recs.name(r).decode("utf-8", "surrogateescape") for r in raw["name_row"]]
@@ -228,6 +230,41 @@ def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Option
         if op_profile else []
     return AnalysisResult(trace_label, epsilon0, theta_copy, theta_cpu, k0, main_stream, raw["streams"],
                           raw["main_stream"], loop_reports, details, warnings, profiles)
+
+
+def analyze_csv(ctx: Context, text: bytes, loops: list, trace_label: str = "trace.csv", **kw) -> AnalysisResult:
+    """parse_trace_text + analyze_trace (what the reference CLI's `analyze` runs, itertrace_main.cpp:143),
+    both on the GPU: the CSV is parsed by itt_parse_csv and stays in HBM for itt_analyze."""
+    try:
+        parsed = ctx.parse_csv(text, trace_label)
+    except IttError as e:
+        raise AnalyzeError(e.kind, str(e)) from e
+    names = None
+    if kw.get("names") is None:
+        cols = parsed.columns()
+        off, nb = cols["name_off"], cols["name_bytes"].tobytes()
+        names_all = lambda r: nb[int(off[r]):int(off[r + 1])].decode("utf-8", "surrogateescape")  # noqa: E731
+        names = _LazyNames(names_all)
+    try:
+        return analyze_trace(ctx, parsed, loops, trace_label=trace_label, device_labels=parsed.device_labels,
+                             trace_warnings=parsed.warnings, names=names, **kw)
+    finally:
+        parsed.free()
+
+
+class _LazyNames:
+    """token id -> name, resolved through name_row on first use (analyze_trace indexes by token id)."""
+
+    def __init__(self, by_row):
+        self.by_row = by_row
+        self.rows = None
+
+    def bind(self, name_row):
+        self.rows = name_row
+        return self
+
+    def __getitem__(self, t):
+        return self.by_row(self.rows[t])
 
 
 # ---------------------------------------------------------------- a12 second-level profile
