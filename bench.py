@@ -258,6 +258,7 @@ def main():
     ap.add_argument("--iterations", type=int, default=None,
                     help="override the workload's iteration count (smaller dry runs of C3/C5)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ingest", action="store_true", help="skip the GPU CSV ingest measurement")
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--clock-ms", type=int, default=200,
                     help="nvidia-smi sampling interval during the timed region (the profiling recipe's 200 ms: "
@@ -434,6 +435,41 @@ def main():
                "ms_per_step": ms_e / args.steps, "pinned_columns": f"{len(registered)}/{len(cols)}"}
         log(f"[rank {rank}] e2e: {e2e['ms_per_step']:.2f} ms/step, {e2e['value'] / 1e9:.3f}G events/s")
 
+    # ---- GPU CSV ingest: the same trace as profiler CSV text, parsed by
+    # itt_parse_csv (host text -> HBM records), against the reference's parse_trace_text on a sample
+    ingest = None
+    if rank == 0 and not args.no_ingest and args.config in ("C1", "C2"):
+        try:
+            from paper_1707_03750_b200 import synth as _synth
+            text = _synth.to_csv(recs)
+            times = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                pt = ctx.parse_csv(text, "bench.csv")
+                times.append(time.perf_counter() - t0)
+                assert pt.n == n_events and pt.rows_skipped == 0
+                pt.free()
+            ctx.set_profiling(True)
+            ctx.reset_stats()
+            ctx.parse_csv(text, "bench.csv").free()
+            kst = {k: v["total_ms"] for k, v in ctx.kernel_stats().items() if k.startswith("ingest")}
+            ctx.set_profiling(False)
+            best = min(times)
+            ingest = {"rows": n_events, "csv_bytes": len(text), "wall_ms": best * 1000,
+                      "rows_per_s": n_events / best, "csv_GBps": len(text) / best / 1e9,
+                      "kernels_ms": kst, "note": "wall time of itt_parse_csv on pageable host text (H2D inside)"}
+            if not args.no_cpu_baseline:
+                from oracle.bindings import ref as _ref
+                sample = text[:text.index(b"\n", min(len(text) - 1, 200_000_000)) + 1]
+                t0 = time.perf_counter()
+                rp = _ref().parse_csv(sample, "bench.csv")
+                dt = time.perf_counter() - t0
+                ingest["reference_rows_per_s"] = rp["rows_total"] / dt
+                ingest["reference_sample_rows"] = rp["rows_total"]
+            log(f"[rank {rank}] ingest: {ingest['rows_per_s'] / 1e6:.1f}M rows/s ({ingest['csv_GBps']:.2f} GB/s of CSV)")
+        except Exception as e:  # a failure here must not lose the main measurement
+            ingest = {"error": repr(e)}
+
     # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -456,7 +492,7 @@ def main():
                                  "iterations_found": int(L["rows"].shape[0])}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(launches), "kernels": kernel_table, "op_profile": op_profile,
-            "memory": memory,
+            "memory": memory, "ingest": ingest,
         }
         print(json.dumps(line), flush=True)
     drecs.free()

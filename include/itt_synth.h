@@ -55,6 +55,9 @@ void itt_synth_default(itt_synth_cfg* cfg);
 /* returns 0 on success; free with itt_synth_free */
 int itt_synth_generate(const itt_synth_cfg* cfg, itt_synth_trace* out);
 void itt_synth_free(itt_synth_trace* t);
+/* the trace as profiler CSV text in the reference's format (header + "ns,ns,B,B/s,,," units row,
+ * rows in source order, names quoted); *text is malloc'd, release with free() */
+int itt_synth_to_csv(const itt_synth_trace* t, char** text, uint64_t* len);
 
 #ifdef __cplusplus
 }

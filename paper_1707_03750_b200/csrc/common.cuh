@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -13,6 +14,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "itertrace_cuda.h"
@@ -367,6 +369,54 @@ inline void readback(Ctx* c, T* dst, const T* src, size_t count) {
     std::fprintf(stderr, "[itt]   slow readback %.1f ms after %s\n", StageTimer::now() - t0, c->last_launch);
   std::memcpy(static_cast<void*>(dst), st, count * sizeof(T));
 }
+// host memcpy split across threads (pageable source -> pinned bounce buffer)
+inline void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t bytes) {
+  constexpr uint64_t kMinPerThread = 32ull << 20;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = static_cast<unsigned>(std::min<uint64_t>(hw, std::max<uint64_t>(1, bytes / kMinPerThread)));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const uint64_t per = (bytes + nt - 1) / nt;
+  for (unsigned i = 0; i < nt; ++i) {
+    const uint64_t a = i * per, b = std::min(bytes, a + per);
+    if (a < b) th.emplace_back([=] { std::memcpy(dst + a, src + a, b - a); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// Host -> device from memory that may be pageable: large unpinned copies go through the
+// context's two pinned bounce buffers (multi-threaded host memcpy overlapping the DMA of the
+// previous chunk) instead of the driver's single-threaded staging (~11 GB/s measured).
+inline void h2d_bulk(Ctx* c, void* dst, const void* src, uint64_t bytes) {
+  if (!bytes) return;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, src) != cudaSuccess) cudaGetLastError();
+  if (pa.type == cudaMemoryTypeHost || bytes < (64ull << 20)) {
+    ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return;
+  }
+  constexpr uint64_t kChunk = 256ull << 20;
+  cudaEvent_t done[2];
+  for (auto& e : done) ITT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  uint8_t* d = static_cast<uint8_t*>(dst);
+  int k = 0;
+  for (uint64_t off = 0; off < bytes; off += kChunk, ++k) {
+    const int b = k & 1;
+    const uint64_t n = std::min(kChunk, bytes - off);
+    uint8_t* bb = c->bounce_buf(b, kChunk);
+    if (k >= 2) ITT_CUDA(cudaEventSynchronize(done[b]));  // the DMA that last read this buffer
+    parallel_memcpy(bb, s + off, n);
+    ITT_CUDA(cudaMemcpyAsync(d + off, bb, n, cudaMemcpyHostToDevice, c->stream));
+    ITT_CUDA(cudaEventRecord(done[b], c->stream));
+  }
+  ITT_CUDA(cudaStreamSynchronize(c->stream));  // the bounce buffers are reused by later calls
+  for (auto& e : done) cudaEventDestroy(e);
+}
+
 // two device ranges in one host round trip
 template <typename T, typename U>
 inline void readback2(Ctx* c, T* a, const T* da, size_t na, U* b, const U* db, size_t nb) {

@@ -666,7 +666,10 @@ __global__ void k_dev_insert(const uint8_t* __restrict__ text, const LineOut* __
       atomicOr(&counters[1], 1u);
       return;
     }
-    unsigned long long k = atomicCAS(&table[s], 0ull, frag | r);
+    // a plain read first: nearly every record finds its (few) labels already inserted, and a CAS
+    // per record on one hot slot would serialize
+    unsigned long long k = __ldcg(&table[s]);
+    if (k == 0) k = atomicCAS(&table[s], 0ull, frag | r);
     if (k == 0) {
       used[atomicAdd(&counters[0], 1u)] = s;
       break;
@@ -848,7 +851,7 @@ void parse_csv(Ctx* c, const char* text, uint64_t len, const std::string& label,
   }
   // ---- device: lines, per-line parse, compaction
   DBuf<uint8_t> dtext(c, len + 16);
-  h2d(c, dtext.p, reinterpret_cast<const uint8_t*>(text), len);
+  h2d_bulk(c, dtext.p, text, len);
   ScanScratch scan;
   const uint64_t chunks = (len + 15) / 16;
   const uint64_t nl_cap = len + 1;

@@ -945,15 +945,15 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.o_flags.alloc(c, n);
   d.o_stream.alloc(c, n);
   d.o_off.alloc(c, n + 1);
-  h2d(c, d.o_start.p, r->start_ns, n);
-  h2d(c, d.o_dur.p, r->duration_ns, n);
-  h2d(c, d.o_size.p, r->size_bytes, n);
-  h2d(c, d.o_flags.p, r->flags, n);
-  h2d(c, d.o_stream.p, r->stream, n);
-  h2d(c, d.o_off.p, r->name_off, n + 1);
+  h2d_bulk(c, d.o_start.p, r->start_ns, n * 8);
+  h2d_bulk(c, d.o_dur.p, r->duration_ns, n * 8);
+  h2d_bulk(c, d.o_size.p, r->size_bytes, n * 8);
+  h2d_bulk(c, d.o_flags.p, r->flags, n);
+  h2d_bulk(c, d.o_stream.p, r->stream, n * 4);
+  h2d_bulk(c, d.o_off.p, r->name_off, (n + 1) * 8);
   if (!streamed) {
     d.o_names.alloc(c, nb + 16);
-    h2d(c, d.o_names.p, r->name_bytes, nb);
+    h2d_bulk(c, d.o_names.p, r->name_bytes, nb);
   }
   d.start = d.o_start.p;
   d.dur = d.o_dur.p;
@@ -964,7 +964,7 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.name_bytes = streamed ? nullptr : d.o_names.p;
   if (r->device) {
     d.o_device.alloc(c, n);
-    h2d(c, d.o_device.p, r->device, n);
+    h2d_bulk(c, d.o_device.p, r->device, n * 2);
     d.device = d.o_device.p;
   }
 }
@@ -1017,24 +1017,6 @@ void order_records(TraceState& t) {
   // LSD radix sort is stable, so equal starts keep source-row order (ingest.hpp:396-400)
   const bool alt = radix_sort_pairs<uint64_t>(c, k0.p, v0.p, k1.p, v1.p, n, 0, bits, t.rs);
   t.perm = alt ? std::move(v1) : std::move(v0);
-}
-
-// host memcpy split across threads (pageable source -> pinned bounce buffer)
-void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t bytes) {
-  constexpr uint64_t kMinPerThread = 32ull << 20;
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const unsigned nt = static_cast<unsigned>(std::min<uint64_t>(hw, std::max<uint64_t>(1, bytes / kMinPerThread)));
-  if (nt <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
-  }
-  std::vector<std::thread> th;
-  const uint64_t per = (bytes + nt - 1) / nt;
-  for (unsigned i = 0; i < nt; ++i) {
-    const uint64_t a = i * per, b = std::min(bytes, a + per);
-    if (a < b) th.emplace_back([=] { std::memcpy(dst + a, src + a, b - a); });
-  }
-  for (auto& x : th) x.join();
 }
 
 void build_dictionary(TraceState& t) {

@@ -298,3 +298,33 @@ extern "C" void itt_synth_free(itt_synth_trace* t) {
   std::free(t->name_bytes);
   std::memset(t, 0, sizeof(*t));
 }
+
+extern "C" int itt_synth_to_csv(const itt_synth_trace* t, char** text, uint64_t* len) {
+  if (!t || !text || !len) return 1;
+  std::string out;
+  out.reserve(static_cast<size_t>(t->n) * 48 + t->name_bytes_len + 128);
+  out += "Start,Duration,Size,Throughput,Device,Stream,Name\nns,ns,B,B/s,,,\n";
+  char buf[128];
+  for (uint64_t i = 0; i < t->n; ++i) {
+    int k = std::snprintf(buf, sizeof(buf), "%lld,%lld,", static_cast<long long>(t->start_ns[i]),
+                          static_cast<long long>(t->duration_ns[i]));
+    out.append(buf, static_cast<size_t>(k));
+    if (t->flags[i] & 0x1) out += std::to_string(t->size_bytes[i]);
+    out += ',';
+    if (t->flags[i] & 0x2) out += "1e9";
+    k = std::snprintf(buf, sizeof(buf), ",gpu%u,%u,\"", static_cast<unsigned>(t->device[i]), t->stream[i]);
+    out.append(buf, static_cast<size_t>(k));
+    for (uint64_t b = t->name_off[i]; b < t->name_off[i + 1]; ++b) {
+      const char c = static_cast<char>(t->name_bytes[b]);
+      if (c == '"') out += '"';
+      out += c;
+    }
+    out += "\"\n";
+  }
+  *text = static_cast<char*>(std::malloc(out.size() + 1));
+  if (!*text) return 2;
+  std::memcpy(*text, out.data(), out.size());
+  (*text)[out.size()] = 0;
+  *len = out.size();
+  return 0;
+}

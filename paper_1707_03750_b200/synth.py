@@ -47,6 +47,7 @@ def lib():
         _lib.itt_synth_default.argtypes = [C.POINTER(itt_synth_cfg)]
         _lib.itt_synth_generate.argtypes = [C.POINTER(itt_synth_cfg), C.POINTER(itt_synth_trace)]
         _lib.itt_synth_free.argtypes = [C.POINTER(itt_synth_trace)]
+        _lib.itt_synth_to_csv.argtypes = [C.POINTER(itt_synth_trace), C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
     return _lib
 
 
@@ -97,6 +98,18 @@ def generate(**kw) -> tuple[Records, dict]:
         device=arr(t.device, np.uint16, n), order=ORDER_UNKNOWN, keepalive=owner)
     info = dict(n=n, n_main=int(t.n_main), n_htod=int(t.n_htod), name_bytes=int(t.name_bytes_len))
     return recs, info
+
+
+def to_csv(recs: Records) -> bytes:
+    """Profiler CSV text of a generated trace (the reference's format; itt_synth_to_csv)."""
+    owner = recs._keepalive
+    p, n = C.c_void_p(), C.c_uint64()
+    if lib().itt_synth_to_csv(C.byref(owner.t), C.byref(p), C.byref(n)) != 0:
+        raise RuntimeError("itt_synth_to_csv failed")
+    try:
+        return C.string_at(p, n.value)
+    finally:
+        C.CDLL(None).free(p)
 
 
 def generate_config(name: str, **override) -> tuple[Records, dict]:
