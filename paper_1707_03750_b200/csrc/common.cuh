@@ -390,12 +390,13 @@ inline void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t bytes) {
 // Host -> device from memory that may be pageable: large unpinned copies go through the
 // context's two pinned bounce buffers (multi-threaded host memcpy overlapping the DMA of the
 // previous chunk) instead of the driver's single-threaded staging (~11 GB/s measured).
-inline void h2d_bulk(Ctx* c, void* dst, const void* src, uint64_t bytes) {
+inline void h2d_bulk(Ctx* c, void* dst, const void* src, uint64_t bytes, cudaStream_t stream = nullptr) {
   if (!bytes) return;
+  if (!stream) stream = c->stream;
   cudaPointerAttributes pa{};
   if (cudaPointerGetAttributes(&pa, src) != cudaSuccess) cudaGetLastError();
   if (pa.type == cudaMemoryTypeHost || bytes < (64ull << 20)) {
-    ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
     return;
   }
   constexpr uint64_t kChunk = 256ull << 20;
@@ -410,10 +411,10 @@ inline void h2d_bulk(Ctx* c, void* dst, const void* src, uint64_t bytes) {
     uint8_t* bb = c->bounce_buf(b, kChunk);
     if (k >= 2) ITT_CUDA(cudaEventSynchronize(done[b]));  // the DMA that last read this buffer
     parallel_memcpy(bb, s + off, n);
-    ITT_CUDA(cudaMemcpyAsync(d + off, bb, n, cudaMemcpyHostToDevice, c->stream));
-    ITT_CUDA(cudaEventRecord(done[b], c->stream));
+    ITT_CUDA(cudaMemcpyAsync(d + off, bb, n, cudaMemcpyHostToDevice, stream));
+    ITT_CUDA(cudaEventRecord(done[b], stream));
   }
-  ITT_CUDA(cudaStreamSynchronize(c->stream));  // the bounce buffers are reused by later calls
+  ITT_CUDA(cudaStreamSynchronize(stream));  // the bounce buffers are reused by later calls
   for (auto& e : done) cudaEventDestroy(e);
 }
 

@@ -939,34 +939,47 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   uint64_t nb = 0;
   if (n) std::memcpy(&nb, &r->name_off[n], sizeof(nb));
   d.name_total = static_cast<int64_t>(nb);
+  // Large host traces: only `start` goes first on the compute stream (the order stage needs nothing
+  // else); the other columns follow on the copy stream while the order stage runs, and the names
+  // are streamed in 64 MiB chunks behind them, each hashed as soon as it lands — the PCIe transfer
+  // overlaps the first stages instead of preceding them.
+  const bool overlap = r->mem == ITT_MEM_HOST && nb >= (256ull << 20);
+  if (overlap) {
+    d.host_names = r->name_bytes;
+    d.stream_chunk = 64ull << 20;
+  }
   d.o_start.alloc(c, n);
   d.o_dur.alloc(c, n);
   d.o_size.alloc(c, n);
   d.o_flags.alloc(c, n);
   d.o_stream.alloc(c, n);
   d.o_off.alloc(c, n + 1);
+  if (r->device) d.o_device.alloc(c, n);
+  if (!streamed && !overlap) d.o_names.alloc(c, nb + 16);
   h2d_bulk(c, d.o_start.p, r->start_ns, n * 8);
-  h2d_bulk(c, d.o_dur.p, r->duration_ns, n * 8);
-  h2d_bulk(c, d.o_size.p, r->size_bytes, n * 8);
-  h2d_bulk(c, d.o_flags.p, r->flags, n);
-  h2d_bulk(c, d.o_stream.p, r->stream, n * 4);
-  h2d_bulk(c, d.o_off.p, r->name_off, (n + 1) * 8);
-  if (!streamed) {
-    d.o_names.alloc(c, nb + 16);
-    h2d_bulk(c, d.o_names.p, r->name_bytes, nb);
+  cudaStream_t cs = c->stream;
+  if (overlap) {
+    cs = c->copier();
+    ITT_CUDA(cudaEventCreateWithFlags(&d.cols_ready, cudaEventDisableTiming));
+    ITT_CUDA(cudaEventRecord(d.cols_ready, c->stream));  // the allocations above are stream-ordered
+    ITT_CUDA(cudaStreamWaitEvent(cs, d.cols_ready, 0));
   }
+  h2d_bulk(c, d.o_off.p, r->name_off, (n + 1) * 8, cs);
+  h2d_bulk(c, d.o_dur.p, r->duration_ns, n * 8, cs);
+  h2d_bulk(c, d.o_size.p, r->size_bytes, n * 8, cs);
+  h2d_bulk(c, d.o_flags.p, r->flags, n, cs);
+  h2d_bulk(c, d.o_stream.p, r->stream, n * 4, cs);
+  if (r->device) h2d_bulk(c, d.o_device.p, r->device, n * 2, cs);
+  if (!streamed && !overlap) h2d_bulk(c, d.o_names.p, r->name_bytes, nb, cs);
+  if (overlap) ITT_CUDA(cudaEventRecord(d.cols_ready, cs));  // the compute stream waits before the dictionary
   d.start = d.o_start.p;
   d.dur = d.o_dur.p;
   d.size = d.o_size.p;
   d.flags = d.o_flags.p;
   d.stream = d.o_stream.p;
   d.name_off = d.o_off.p;
-  d.name_bytes = streamed ? nullptr : d.o_names.p;
-  if (r->device) {
-    d.o_device.alloc(c, n);
-    h2d_bulk(c, d.o_device.p, r->device, n * 2);
-    d.device = d.o_device.p;
-  }
+  d.name_bytes = (streamed || overlap) ? nullptr : d.o_names.p;
+  d.device = r->device ? d.o_device.p : nullptr;
 }
 
 void release_rows(TraceState& t) {
@@ -1064,8 +1077,9 @@ void build_dictionary(TraceState& t) {
           if (p[i]) cudaEventDestroy(p[i]);
     }
   } ev_guard{{copied, done}};
+  if (t.rec.cols_ready) ITT_CUDA(cudaStreamWaitEvent(c->stream, t.rec.cols_ready, 0));  // host columns landed
   if (streamed && n) {
-    uint64_t chunk_bytes = 1ull << 30;
+    uint64_t chunk_bytes = t.rec.stream_chunk ? t.rec.stream_chunk : (1ull << 30);
     if (const char* e = std::getenv("ITT_STREAM_CHUNK")) chunk_bytes = std::max<uint64_t>(64, std::strtoull(e, nullptr, 10));
     chunks = std::max<uint64_t>(1, (total + chunk_bytes - 1) / chunk_bytes);
     rows_per_chunk = ((n + chunks - 1) / chunks + 31) & ~31ull;

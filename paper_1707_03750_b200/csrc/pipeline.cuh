@@ -24,6 +24,11 @@ struct DevRecords {
   const uint8_t* name_bytes = nullptr;  // null when the names are streamed from host memory
   const uint8_t* host_names = nullptr;  // streamed names (ITT_MEM_*_NAMES modes)
   int64_t name_total = -1;               // name_off[n] when known on the host (host columns)
+  uint64_t stream_chunk = 0;             // streamed-name chunk bytes (0: default 1 GiB)
+  cudaEvent_t cols_ready = nullptr;      // host columns copied on the copy stream (auto-streamed names)
+  ~DevRecords() {
+    if (cols_ready) cudaEventDestroy(cols_ready);
+  }
   int order = ITT_ORDER_UNKNOWN;
   // owned copies when the caller passed host memory
   DBuf<int64_t> o_start, o_dur, o_size;

@@ -141,3 +141,19 @@ def test_repeated_runs_are_deterministic(ctx):
     b = ctx.analyze_raw(recs, [5_000])
     assert a["name_row"] == b["name_row"] and a["streams"] == b["streams"]
     assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
+
+
+def test_c2_host_columns_overlapped_upload_matches_resident(ctx):
+    """Large host inputs take the overlapped upload (columns on the copy stream, names streamed in
+    64 MiB chunks into the hash pass): same analysis as device-resident columns."""
+    recs, info = synth.generate_config("C2")
+    d = ctx.upload(recs)
+    try:
+        want = ctx.analyze_raw(d, [50_000], op_profile=True)
+    finally:
+        d.free()
+    got = ctx.analyze_raw(recs, [50_000], op_profile=True)
+    assert got["streams"] == want["streams"] and got["name_row"] == want["name_row"]
+    a, b = got["loops"][0], want["loops"][0]
+    assert a["pattern_tokens"] == b["pattern_tokens"] and np.array_equal(a["rows"], b["rows"])
+    assert np.array_equal(a["op_totals"], b["op_totals"])
