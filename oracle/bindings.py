@@ -182,6 +182,8 @@ class Ref(_Common):
         n = C.c_uint64()
         p = self.lib.ref_synth_csv(seed, pattern_len, iterations, vocab_size, insert_prob, max_inserts,
                                    1 if inside_pattern else 0, pathology, C.byref(n))
+        if not p:
+            raise ValueError("reference generator rejected the config")
         try:
             return C.string_at(p, n.value)
         finally:

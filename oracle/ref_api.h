@@ -113,6 +113,9 @@ char* ref_synth_csv(uint64_t seed, int64_t pattern_len, int64_t iterations, int6
 /* parse_trace_text + analyze_trace end to end (summary JSON / details CSV as the CLI writes them) */
 int ref_analyze_csv(const char* text, uint64_t len, const char* label, const itt_analyze_opts* opts, ref_analysis* out);
 
+/* nlohmann::json(v).dump() — pins paper_1707_03750_b200/jsonfloat.py */
+int ref_json_double(double v, char* out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

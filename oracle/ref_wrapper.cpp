@@ -502,9 +502,14 @@ extern "C" char* ref_synth_csv(uint64_t seed, int64_t pattern_len, int64_t itera
   cfg.max_inserts = max_inserts;
   cfg.insert_placement = inside_pattern ? InsertPlacement::inside_pattern : InsertPlacement::after_pattern;
   cfg.pathology = static_cast<Pathology>(pathology);
-  const std::string csv = generate(cfg).trace_csv;
-  *len = csv.size();
-  return dup_str(csv);
+  try {
+    const std::string csv = generate(cfg).trace_csv;
+    *len = csv.size();
+    return dup_str(csv);
+  } catch (const std::exception&) {  // invalid generator config
+    *len = 0;
+    return nullptr;
+  }
 }
 
 extern "C" int ref_analyze_csv(const char* text, uint64_t len, const char* label, const itt_analyze_opts* opts,
@@ -535,4 +540,12 @@ extern "C" int ref_analyze_csv(const char* text, uint64_t len, const char* label
     out->error = dup_str(e.what());
   }
   return out->status;
+}
+
+// nlohmann::json(v).dump() of one double (pins the Python Grisu2 restatement, jsonfloat.py)
+extern "C" int ref_json_double(double v, char* out, int cap) {
+  const std::string s = nlohmann::json(v).dump();
+  if (static_cast<int>(s.size()) + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
 }

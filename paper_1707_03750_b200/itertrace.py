@@ -17,6 +17,7 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 from . import abi
+from .jsonfloat import dump_float
 from .cuda import Context, IttError
 
 TOOL = "itertrace"
@@ -347,17 +348,8 @@ def _json_str(s: str) -> str:
 
 
 def _json_float(v: float) -> str:
-    """nlohmann::json number_float dump: shortest round-trip digits, '.0' for integral values,
-    exponent form outside (1e-5, 1e15]."""
-    if math.isnan(v) or math.isinf(v):
-        return "null"
-    r = repr(float(v))
-    a = abs(v)
-    if a != 0.0 and 1e15 <= a < 1e16:  # nlohmann switches to exponent one decade earlier than Python
-        digits = repr(a)[:-2].replace(".", "").rstrip("0")  # repr(a) == "dddddddddddddddd.0" here
-        mant = digits[0] + ("." + digits[1:] if len(digits) > 1 else "")
-        return ("-" if v < 0 else "") + mant + "e+15"
-    return r
+    """nlohmann::json number_float dump (Grisu2 digits + %g-like layout): jsonfloat.dump_float."""
+    return dump_float(v)
 
 
 def _dump(v, indent: int, level: int) -> str:

@@ -88,3 +88,35 @@ def test_json_float_format():
     assert [f(x) for x in (0.1, 10.0, 1000.0, 0.05, 4096.0, 1e-05, 1e16, 0.0001, 2.5e-07)] == \
         ["0.1", "10.0", "1000.0", "0.05", "4096.0", "1e-05", "1e+16", "0.0001", "2.5e-07"]
     assert f(1e15) == "1e+15" and f(1234567890123456.0) == "1.234567890123456e+15"
+
+
+def test_json_float_matches_the_reference_json_library():
+    """jsonfloat.dump_float restates the reference JSON library's Grisu2 double printing; Python's
+    shortest repr differs for ~0.1% of doubles (e.g. 4957.0239520958085), so it is pinned against
+    nlohmann::json(v).dump() from the reference build itself."""
+    import ctypes as C
+    import math
+    import random
+    import struct
+
+    from oracle.bindings import ref
+    from paper_1707_03750_b200.jsonfloat import dump_float
+    L = ref().lib
+    L.ref_json_double.argtypes = [C.c_double, C.c_char_p, C.c_int]
+    buf = C.create_string_buffer(64)
+    vals = [4957.0239520958085, 0.049589542629412633, 0.0030392262455614452, 1e15, 1e16, 123456789012345.0,
+            1e-5, 1e-4, 5e-324, 1.7976931348623157e308, 2.2250738585072014e-308, -0.0, 0.0, 1.0, 0.1, 1e21]
+    rng = random.Random(7)
+    while len(vals) < 30000:
+        k = rng.random()
+        if k < 0.3:
+            v = struct.unpack("<d", struct.pack("<Q", rng.getrandbits(64)))[0]
+        elif k < 0.7:
+            v = rng.random() * 10 ** rng.randint(-8, 20)
+        else:
+            v = rng.randint(0, 10 ** 7) / rng.randint(1, 10 ** 5)
+        if not (math.isnan(v) or math.isinf(v)):
+            vals.append(v)
+    for v in vals:
+        L.ref_json_double(v, buf, 64)
+        assert dump_float(v) == buf.value.decode(), repr(v)
