@@ -216,6 +216,49 @@ int itt_mine_patterns(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t t
                       uint32_t n_loops, int multi, itt_pattern** out);
 int itt_free_patterns(itt_ctx* ctx, itt_pattern* p, uint32_t n_loops);
 
+/* mine_pattern / mine_patterns_multi over a suffix array built elsewhere (the distributed
+ * prefix doubling below, gathered to one device).  All pointers are DEVICE memory: tokens[n] in
+ * [0, term), sa[n+1], lcp[n+1] with lcp values min(lcp, cap) for a cap >= max L_max + 1
+ * (mine.hpp:64-67) — what itt_dsa_* produce.  Same results and errors as itt_mine_patterns. */
+int itt_mine_patterns_sa(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, const uint32_t* sa,
+                         const uint32_t* lcp, const itt_mining_cfg* loops, uint32_t n_loops, int multi, itt_pattern** out);
+
+/* ------------------------------------------------------- distributed suffix array (C5)
+ * Per-rank device steps of prefix doubling with a sample-sort all-to-all over G ranks; the
+ * exchanges are the host driver's (paper_1707_03750_b200/dist_sa.py).  Every pointer is DEVICE
+ * memory unless marked host.  Suffix positions are block-partitioned: a rank owns [lo, lo+cnt).
+ * Records are (u64 a, u32 b) pairs.  Replaces, for traces beyond one device, the same suffix
+ * order and node depths as itt_suffix_array (SuffixTree, suffix_tree.hpp:21-190); n+1 < 2^31. */
+/* keys of own positions: rank == NULL: a = first k symbols of text[i..] (sym_bits each, text =
+ * tokens + [term], np entries, replicated); else a = rank[j] << b | (j < n2 ? rank2[j] + 1 : 0)
+ * with rank2 = ranks of positions lo+h.. ; v = i. */
+int itt_dsa_keys(itt_ctx* ctx, const int32_t* text, uint64_t np, uint64_t lo, uint64_t cnt, int sym_bits, int k,
+                 const uint32_t* rank, const uint32_t* rank2, uint64_t n2, int b, uint64_t* a, uint32_t* v);
+/* stable partition by destination rank: mode 0 = number of splitters (spl_a, spl_b)[nspl] <= (a, b);
+ * mode 1 = owner of position (uint32)a under bounds[P+1].  counts: host[P]. */
+int itt_dsa_partition(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, int mode, const uint64_t* spl_a,
+                      const uint32_t* spl_b, uint32_t nspl, const uint64_t* bounds, uint32_t P, uint64_t* out_a,
+                      uint32_t* out_b, uint64_t* counts);
+/* stable sort of (a, b) by the low `bits` bits of a, in place */
+int itt_dsa_sort(itt_ctx* ctx, uint64_t* a, uint32_t* b, uint64_t cnt, int bits);
+/* dense group ids over this rank's slice of the sorted records: flag_j = a_j != a_{j-1} (a_{-1} =
+ * prev when has_prev); out_j = (offset + #flags<=j - 1) << 32 | b_j; n_groups: host, #flags. */
+int itt_dsa_ids(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, int has_prev, uint64_t prev,
+                uint32_t offset, uint64_t* out, uint64_t* n_groups);
+/* dst[(uint32)p_j - lo] = p_j >> 32 */
+int itt_dsa_scatter(itt_ctx* ctx, const uint64_t* p, uint64_t cnt, uint64_t lo, uint32_t* dst);
+/* LCP requests from the sorted slice (packed (id << 32) | SA, global positions kbase..):
+ * a = k << 32 | SA_k, b = SA_{k-1} | 1 << 31 when in the same final group (0x7FFFFFFF at k = 0) */
+int itt_dsa_lcp_requests(itt_ctx* ctx, const uint64_t* packed, uint64_t cnt, uint64_t kbase, int has_prev, uint64_t prev,
+                         uint64_t* a, uint32_t* b);
+/* capped Kasai over own positions from the requests routed to their owner: out_j = plcp << 32 | k
+ * (in text order of [lo, lo+cnt)) */
+int itt_dsa_kasai(itt_ctx* ctx, const int32_t* text, uint64_t np, uint64_t lo, uint64_t cnt, const uint64_t* req_a,
+                  const uint32_t* req_b, uint32_t cap, uint64_t* out);
+/* s evenly spaced records (splitter candidates) */
+int itt_dsa_sample(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, uint32_t s, uint64_t* out_a,
+                   uint32_t* out_b);
+
 /* ------------------------------------------------------- L4 matching (a7) */
 typedef struct itt_span { /* MatchSpan, match.hpp:28-34 */
   int64_t start_token;

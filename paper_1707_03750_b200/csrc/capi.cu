@@ -19,7 +19,7 @@ int itt::radix::config_index() {
   static int cfg = [] {
     const char* e = std::getenv("ITT_RADIX_CFG");
     const int v = e ? std::atoi(e) : 0;
-    return (v >= 0 && v < 5) ? v : 0;
+    return (v >= 0 && v < 13) ? v : 0;
   }();
   return cfg;
 }
@@ -504,6 +504,100 @@ int itt_free_patterns(itt_ctx*, itt_pattern* p, uint32_t n_loops) {
   for (uint32_t i = 0; i < n_loops; ++i) std::free(p[i].tokens);
   std::free(p);
   return ITT_OK;
+}
+
+int itt_mine_patterns_sa(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, const uint32_t* sa,
+                         const uint32_t* lcp, const itt_mining_cfg* loops, uint32_t n_loops, int multi, itt_pattern** out) {
+  if (!out) return ITT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  return guarded(ctx, [&](Ctx* c) {
+    if (!sa || !lcp || (n && !tokens) || !loops || !n_loops) fail(ITT_E_INVALID_ARGUMENT, "mine_pattern: bad arguments");
+    std::vector<itt_mining_cfg> cfgs(loops, loops + n_loops);
+    if (!multi) cfgs.resize(1);
+    SuffixState s;
+    s.n = n;
+    s.np = n + 1;
+    s.lo = 0;
+    s.text.alloc(c, n + 1);
+    if (n) ITT_CUDA(cudaMemcpyAsync(s.text.p, tokens, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    h2d(c, s.text.p + n, &term, 1);
+    s.sa.alloc(c, n + 1);
+    s.lcp.alloc(c, n + 1);
+    ITT_CUDA(cudaMemcpyAsync(s.sa.p, sa, (n + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
+    ITT_CUDA(cudaMemcpyAsync(s.lcp.p, lcp, (n + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
+    IntervalState iv;
+    lcp_intervals(c, s, iv);
+    const auto res = mine_loops(c, s, iv, cfgs, multi != 0);
+    for (const auto& r : res)
+      if (r.status) fail(r.status, r.error);
+    if (multi)
+      for (size_t a = 0; a < res.size(); ++a)
+        for (size_t b = a + 1; b < res.size(); ++b)
+          if (res[a].tokens == res[b].tokens)
+            fail(ITT_E_AMBIGUOUS_LOOPS, "pattern-mining: loops " + std::to_string(a + 1) + " and " + std::to_string(b + 1) +
+                                            " mined the same pattern; the loop specs are ambiguous");
+    itt_pattern* o = host_alloc<itt_pattern>(res.size());
+    for (size_t i = 0; i < res.size(); ++i) {
+      o[i].length = static_cast<int64_t>(res[i].tokens.size());
+      o[i].tokens = host_alloc<int32_t>(res[i].tokens.size());
+      std::memcpy(o[i].tokens, res[i].tokens.data(), res[i].tokens.size() * 4);
+      o[i].count = res[i].count;
+      o[i].first_token = res[i].first_token;
+      o[i].epsilon_used = res[i].epsilon_used;
+    }
+    *out = o;
+  });
+}
+
+// ------------------------------------------------------------------ distributed SA steps (dist.cu)
+int itt_dsa_keys(itt_ctx* ctx, const int32_t* text, uint64_t np, uint64_t lo, uint64_t cnt, int sym_bits, int k,
+                 const uint32_t* rank, const uint32_t* rank2, uint64_t n2, int b, uint64_t* a, uint32_t* v) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (np >= 0x7FFFFFFFull || lo + cnt > np) fail(ITT_E_INVALID_ARGUMENT, "dsa: positions out of range");
+    if (rank ? (b < 1 || b > 32) : (sym_bits < 1 || k < 1 || sym_bits * k > 64)) fail(ITT_E_INVALID_ARGUMENT, "dsa: bad key width");
+    dsa::keys(c, text, np, lo, cnt, sym_bits, k, rank, rank2, n2, b, a, v);
+  });
+}
+int itt_dsa_partition(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, int mode, const uint64_t* spl_a,
+                      const uint32_t* spl_b, uint32_t nspl, const uint64_t* bounds, uint32_t P, uint64_t* out_a,
+                      uint32_t* out_b, uint64_t* counts) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (!counts || P < 1 || P > 256 || (mode == 0 && (nspl + 1 != P || (nspl && (!spl_a || !spl_b)) || (cnt && !b))) ||
+        (mode == 1 && !bounds) || (mode != 0 && mode != 1))
+      fail(ITT_E_INVALID_ARGUMENT, "dsa: bad partition arguments");
+    dsa::partition(c, a, b, cnt, mode, spl_a, spl_b, nspl, bounds, P, out_a, out_b, counts);
+  });
+}
+int itt_dsa_sort(itt_ctx* ctx, uint64_t* a, uint32_t* b, uint64_t cnt, int bits) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (bits < 0 || bits > 64) fail(ITT_E_INVALID_ARGUMENT, "dsa: bad sort width");
+    dsa::sort(c, a, b, cnt, bits);
+  });
+}
+int itt_dsa_ids(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, int has_prev, uint64_t prev,
+                uint32_t offset, uint64_t* out, uint64_t* n_groups) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (!n_groups) fail(ITT_E_INVALID_ARGUMENT, "dsa: null n_groups");
+    *n_groups = dsa::ids(c, a, b, cnt, has_prev != 0, prev, offset, out);
+  });
+}
+int itt_dsa_scatter(itt_ctx* ctx, const uint64_t* p, uint64_t cnt, uint64_t lo, uint32_t* dst) {
+  return guarded(ctx, [&](Ctx* c) { dsa::scatter_hi(c, p, cnt, lo, dst); });
+}
+int itt_dsa_lcp_requests(itt_ctx* ctx, const uint64_t* packed, uint64_t cnt, uint64_t kbase, int has_prev, uint64_t prev,
+                         uint64_t* a, uint32_t* b) {
+  return guarded(ctx, [&](Ctx* c) { dsa::lcp_requests(c, packed, cnt, kbase, has_prev != 0, prev, a, b); });
+}
+int itt_dsa_kasai(itt_ctx* ctx, const int32_t* text, uint64_t np, uint64_t lo, uint64_t cnt, const uint64_t* req_a,
+                  const uint32_t* req_b, uint32_t cap, uint64_t* out) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (cap < 1) fail(ITT_E_INVALID_ARGUMENT, "dsa: cap must be >= 1");
+    dsa::kasai(c, text, np, lo, cnt, req_a, req_b, cap, out);
+  });
+}
+int itt_dsa_sample(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, uint32_t s, uint64_t* out_a,
+                   uint32_t* out_b) {
+  return guarded(ctx, [&](Ctx* c) { dsa::sample(c, a, b, cnt, s, out_a, out_b); });
 }
 
 // ------------------------------------------------------------------ a12 op profile

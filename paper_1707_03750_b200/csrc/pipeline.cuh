@@ -158,4 +158,22 @@ OpProfile op_profile(Ctx* c, const int32_t* tokens, const int64_t* tok_start, co
                      bool want_cells, itt_op_total* op_totals, itt_iter_op_total* iter_totals, ScanScratch& scan,
                      radix::Scratch& rs);
 
+// ------------------------------------------------------------------ distributed SA steps (dist.cu)
+namespace dsa {
+void keys(Ctx* c, const int32_t* text, uint64_t np, uint64_t lo, uint64_t cnt, int bits, int k, const uint32_t* rank,
+          const uint32_t* rank2, uint64_t n2, int b, uint64_t* a, uint32_t* v);
+void partition(Ctx* c, const uint64_t* a, const uint32_t* b, uint64_t cnt, int mode, const uint64_t* spl_a,
+               const uint32_t* spl_b, uint32_t nspl, const uint64_t* bounds, uint32_t P, uint64_t* oa, uint32_t* ob,
+               uint64_t* counts_host);
+void sort(Ctx* c, uint64_t* a, uint32_t* b, uint64_t cnt, int bits);
+uint64_t ids(Ctx* c, const uint64_t* a, const uint32_t* b, uint64_t cnt, bool has_prev, uint64_t prev, uint32_t offset,
+             uint64_t* out);
+void scatter_hi(Ctx* c, const uint64_t* p, uint64_t cnt, uint64_t lo, uint32_t* dst);
+void lcp_requests(Ctx* c, const uint64_t* packed, uint64_t cnt, uint64_t kbase, bool has_prev, uint64_t prev, uint64_t* a,
+                  uint32_t* b);
+void kasai(Ctx* c, const int32_t* text, uint64_t np, uint64_t lo, uint64_t cnt, const uint64_t* req_a, const uint32_t* req_b,
+           uint32_t cap, uint64_t* out);
+void sample(Ctx* c, const uint64_t* a, const uint32_t* b, uint64_t cnt, uint32_t s, uint64_t* oa, uint32_t* ob);
+}  // namespace dsa
+
 }  // namespace itt

@@ -39,6 +39,11 @@ struct ArrayLoader {
     k = __ldcs(&keys[i]);  // streaming: evict-first, keeps L2 for the random-access arrays
     v = __ldcs(&vals[i]);
   }
+  // bulk (TMA) staging: the tile's keys and values are copied to shared memory as they are
+  static constexpr bool kBulkKeys = true;
+  __host__ __device__ const K* bulk_keys() const { return keys; }
+  __host__ __device__ const uint32_t* bulk_vals() const { return vals; }
+  __device__ __forceinline__ void fix(uint64_t, K&, uint32_t&) const {}
 };
 
 // Lanes of the warp holding the same 8-bit digit (valid lanes only among themselves): nine
@@ -123,8 +128,8 @@ struct SmemLayout {
   uint32_t tile;
 };
 
-template <typename K, int BLOCK, int ITEMS, typename Loader>
-__global__ void __launch_bounds__(BLOCK) k_onesweep(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                     uint64_t n, int shift, const uint32_t* __restrict__ digit_offs,
                                                     uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
   static_assert(BLOCK >= kBins, "one thread per digit");
@@ -245,6 +250,243 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep(Loader ld, K* __restrict__ k
   }
 }
 
+
+// ---------------------------------------------------------------- persistent, TMA-staged pass
+// Same pass as k_onesweep, restructured so HBM latency leaves the per-tile critical path:
+//  * persistent CTAs (grid = resident capacity) claim tiles in order from the counter;
+//  * while tile t is ranked / scattered / looked back / written, the NEXT tile's keys and values
+//    are already streaming into the other half of a double-buffered shared-memory stage by
+//    cp.async.bulk (the TMA bulk-copy engine; one thread issues it, completion on an mbarrier),
+//    so no register file is spent holding loads in flight;
+//  * ranks are computed from the staged tile (LDS, conflict-free) and the scatter re-reads it, so
+//    only the 8 ranks live in registers across the block barriers.
+// Progress: every claimed tile publishes its aggregate right after ranking, before it waits on
+// anything; a CTA's prefetched tile is always larger than the tile it is processing, so the
+// smallest unpublished tile is always a CTA's current tile and never waits (no deadlock).
+// Partial last tile (bulk sizes must be 16-B multiples): plain cooperative loads.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <typename K, int BLOCK, int ITEMS>
+struct TmaLayout {
+  static constexpr int kTile = BLOCK * ITEMS;
+  static constexpr int kWarps = BLOCK / 32;
+  K in_keys[2][kTile];
+  uint32_t in_vals[2][kTile];
+  K out_keys[kTile];
+  uint32_t out_vals[kTile];
+  uint16_t warp_hist[kWarps][kBins];
+  uint32_t local_off[kBins];
+  uint32_t global_base[kBins];
+  uint32_t group_sum[8];
+  uint64_t bar[2];
+  uint32_t tile[2];
+};
+
+template <typename K, int BLOCK, int ITEMS, typename Loader>
+__global__ void __launch_bounds__(BLOCK) k_onesweep_tma(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                                                        uint64_t n, int shift, const uint32_t* __restrict__ digit_offs,
+                                                        uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+  static_assert(BLOCK >= kBins, "one thread per digit");
+  static_assert(ITEMS <= 16, "16-bit ranks");
+  using S_t = TmaLayout<K, BLOCK, ITEMS>;
+  constexpr int kTile = S_t::kTile;
+  constexpr int kWarps = S_t::kWarps;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  S_t& S = *reinterpret_cast<S_t*>(smem_raw);
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  const uint64_t full_tiles = n / kTile;
+
+  auto issue = [&](uint32_t t, int b) {  // thread 0: stage full tile t into buffer b
+    fence_proxy_async_smem();
+    const uint64_t base = static_cast<uint64_t>(t) * kTile;
+    const uint32_t vb = kTile * 4;
+    if constexpr (Loader::kBulkKeys) {
+      mbar_expect_tx(&S.bar[b], vb + kTile * sizeof(K));
+      bulk_g2s(S.in_keys[b], ld.bulk_keys() + base, kTile * sizeof(K), &S.bar[b]);
+    } else {
+      mbar_expect_tx(&S.bar[b], vb);
+    }
+    bulk_g2s(S.in_vals[b], ld.bulk_vals() + base, vb, &S.bar[b]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t t0 = atomicAdd(counter, 1u);
+    S.tile[0] = t0;
+    if (t0 < full_tiles) issue(t0, 0);
+  }
+  __syncthreads();
+  uint32_t parity = 0;  // bit b: phase of bar[b]
+  int cur = 0;
+  for (;;) {
+    const uint32_t tile = S.tile[cur];
+    if (tile >= tiles) break;
+    if (threadIdx.x == 0) {  // claim and prefetch the next tile into the other buffer
+      const uint32_t tn = atomicAdd(counter, 1u);
+      S.tile[cur ^ 1] = tn;
+      if (tn < full_tiles) issue(tn, cur ^ 1);
+    }
+    {
+      uint4* wh4 = reinterpret_cast<uint4*>(&S.warp_hist[0][0]);
+      for (int i = threadIdx.x; i < kWarps * kBins * 2 / 16; i += BLOCK) wh4[i] = make_uint4(0, 0, 0, 0);
+    }
+    const uint64_t tile_base = static_cast<uint64_t>(tile) * kTile;
+    const uint32_t valid = static_cast<uint32_t>(umin64(n - tile_base, kTile));
+    K* ik = S.in_keys[cur];
+    uint32_t* iv = S.in_vals[cur];
+    if (tile < full_tiles) {
+      mbar_wait(&S.bar[cur], (parity >> cur) & 1u);
+      parity ^= 1u << cur;
+    } else {
+      for (uint32_t p = threadIdx.x; p < valid; p += BLOCK) ld(tile_base + p, ik[p], iv[p]);
+    }
+    __syncthreads();
+    // ---- stable per-warp ranking over the staged tile (warp-striped)
+    const uint32_t wbase = warp * (32 * ITEMS);
+    uint16_t* wh = S.warp_hist[warp];
+    uint32_t rank[ITEMS];
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      const uint32_t idx = wbase + r * 32 + lane;
+      const bool ok = idx < valid;
+      K k = K(0);
+      if (ok) {
+        k = ik[idx];
+        if constexpr (!Loader::kBulkKeys) {
+          if (tile < full_tiles) {
+            uint32_t v = iv[idx];
+            ld.fix(tile_base + idx, k, v);
+            ik[idx] = k;
+            iv[idx] = v;
+          }
+        }
+      }
+      const uint32_t d = ok ? digit_of(k, shift) : 0u;
+      const unsigned peers = digit_peers(d, ok);
+      uint32_t base = 0;
+      if (ok) base = wh[d];
+      __syncwarp();
+      if (ok && lane == static_cast<unsigned>(__ffs(peers) - 1)) wh[d] = static_cast<uint16_t>(base + __popc(peers));
+      __syncwarp();
+      rank[r] = base + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    uint32_t my_count = 0;
+    if (threadIdx.x < kBins) {
+      const int d = threadIdx.x;
+      uint32_t sum = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = S.warp_hist[w][d];
+        S.warp_hist[w][d] = static_cast<uint16_t>(sum);
+        sum += c;
+      }
+      my_count = sum;
+      st_relaxed_u32(status + static_cast<uint64_t>(tile) * kBins + d, (tile == 0 ? kStP : kStA) | sum);
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (static_cast<int>(lane) >= o) inc += u;
+      }
+      S.local_off[d] = inc - sum;
+      if (lane == 31) S.group_sum[d >> 5] = inc;
+    }
+    __syncthreads();
+    if (threadIdx.x < kBins) {
+      uint32_t add = 0;
+      const int g = threadIdx.x >> 5;
+      for (int h = 0; h < g; ++h) add += S.group_sum[h];
+      S.local_off[threadIdx.x] += add;
+    }
+    __syncthreads();
+    // ---- scatter the staged tile into digit order
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+      const uint32_t idx = wbase + r * 32 + lane;
+      if (idx < valid) {
+        const K k = ik[idx];
+        const uint32_t d = digit_of(k, shift);
+        const uint32_t pos = S.local_off[d] + S.warp_hist[warp][d] + rank[r];
+        S.out_keys[pos] = k;
+        S.out_vals[pos] = iv[idx];
+      }
+    }
+    if (threadIdx.x < kBins) {
+      const int d = threadIdx.x;
+      uint32_t excl = 0;
+      if (tile > 0) {
+        int64_t t = static_cast<int64_t>(tile) - 1;
+        for (bool done = false; !done; t -= kLook) {
+          uint32_t sv[kLook];
+#pragma unroll
+          for (int u = 0; u < kLook; ++u) sv[u] = t - u >= 0 ? ld_relaxed_u32(status + static_cast<uint64_t>(t - u) * kBins + d) : 0u;
+#pragma unroll
+          for (int u = 0; u < kLook; ++u) {
+            if (done) break;
+            uint32_t v = sv[u];
+            while ((v >> 30) == 0) v = ld_relaxed_u32(status + static_cast<uint64_t>(t - u) * kBins + d);
+            excl += v & kStMask;
+            done = (v >> 30) == 2;
+          }
+        }
+        st_relaxed_u32(status + static_cast<uint64_t>(tile) * kBins + d, kStP | (excl + my_count));
+      }
+      S.global_base[d] = digit_offs[d] + excl;
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < valid; p += BLOCK) {
+      const K k = S.out_keys[p];
+      const uint32_t d = digit_of(k, shift);
+      const uint32_t o = S.global_base[d] + (p - S.local_off[d]);
+      __stcs(&keys_out[o], k);
+      __stcs(&vals_out[o], S.out_vals[p]);
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+}
+
+template <typename K, int BLOCK, int ITEMS, typename Loader>
+void launch_pass_tma(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* offs, uint32_t* st) {
+  constexpr int TILE = BLOCK * ITEMS;
+  const size_t smem = sizeof(TmaLayout<K, BLOCK, ITEMS>);
+  auto kern = k_onesweep_tma<K, BLOCK, ITEMS, Loader>;
+  smem_optin(c, kern, smem);
+  static int per_sm[64] = {0};  // resident CTAs per SM, per device
+  int& occ = per_sm[c->device & 63];
+  if (occ == 0) {
+    ITT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, smem));
+    if (occ < 1) occ = 1;
+  }
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+  const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(c->sm_count) * occ);
+  launch(c, "radix_onesweep", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), kern, dim3(static_cast<unsigned>(grid)), dim3(BLOCK),
+         smem, ld, ko, vo, n, shift, offs, st + 1, st);
+}
+
 // Scratch reused across sorts on one context.
 struct Scratch {
   DBuf<uint32_t> hist;    // passes*256 counts
@@ -254,33 +496,45 @@ struct Scratch {
 };
 
 // tile shapes (BLOCK, ITEMS); selected at runtime (ITT_RADIX_CFG) for tuning sweeps
-constexpr int kCfgBlock[] = {512, 256, 384, 256, 512};
-constexpr int kCfgItems[] = {8, 16, 12, 8, 16};
+constexpr int kCfgBlock[] = {512, 256, 384, 256, 512, 512, 512, 256, 256, 256, 512, 256, 256};
+constexpr int kCfgItems[] = {8, 16, 12, 8, 16, 8, 8, 8, 16, 12, 8, 8, 16};
 int config_index();
 
-template <typename K, int BLOCK, int ITEMS, typename Loader>
+template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB = 1024 / BLOCK>
 void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* offs,
                  uint32_t* st, bool first_use) {
   constexpr int TILE = BLOCK * ITEMS;
   const size_t smem = sizeof(SmemLayout<K, BLOCK, ITEMS>);
   (void)first_use;
-  smem_optin(c, k_onesweep<K, BLOCK, ITEMS, Loader>, smem);
+  smem_optin(c, k_onesweep<K, BLOCK, ITEMS, Loader, MINB>, smem);
   const uint64_t tiles = (n + TILE - 1) / TILE;
-  launch(c, "radix_onesweep", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), k_onesweep<K, BLOCK, ITEMS, Loader>,
+  launch(c, "radix_onesweep", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), k_onesweep<K, BLOCK, ITEMS, Loader, MINB>,
          dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, offs, st + 1, st);
 }
 
 template <typename K, typename Loader>
 void dispatch_pass(Ctx* c, int cfg, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* offs,
                    uint32_t* st) {
-  static bool seen[8] = {false};
+  static bool seen[16] = {false};
   const bool first = !seen[cfg];
   seen[cfg] = true;
+  if (cfg >= 10) {  // bulk copies need 16-byte aligned sources
+    const uintptr_t a = reinterpret_cast<uintptr_t>(ld.bulk_vals()) | reinterpret_cast<uintptr_t>(ld.bulk_keys());
+    if (a & 15u) fail(ITT_E_INVALID_ARGUMENT, "internal: radix staging needs 16-byte aligned arrays");
+  }
   switch (cfg) {
     case 1: launch_pass<K, 256, 16>(c, ld, ko, vo, n, shift, offs, st, first); break;
     case 2: launch_pass<K, 384, 12>(c, ld, ko, vo, n, shift, offs, st, first); break;
     case 3: launch_pass<K, 256, 8>(c, ld, ko, vo, n, shift, offs, st, first); break;
     case 4: launch_pass<K, 512, 16>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 5: launch_pass<K, 512, 8, Loader, 3>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 6: launch_pass<K, 512, 8, Loader, 4>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 7: launch_pass<K, 256, 8, Loader, 6>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 8: launch_pass<K, 256, 16, Loader, 4>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 9: launch_pass<K, 256, 12, Loader, 5>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 10: launch_pass_tma<K, 512, 8>(c, ld, ko, vo, n, shift, offs, st); break;
+    case 11: launch_pass_tma<K, 256, 8>(c, ld, ko, vo, n, shift, offs, st); break;
+    case 12: launch_pass_tma<K, 256, 16>(c, ld, ko, vo, n, shift, offs, st); break;
     default: launch_pass<K, 512, 8>(c, ld, ko, vo, n, shift, offs, st, first); break;
   }
 }

@@ -92,6 +92,16 @@ struct EmitLoader {
     k = __ldg(&rank[i]);
     v = i;
   }
+  // bulk (TMA) staging: only the SA slice is copied; fix() turns SA_j into (rank[E_j], E_j)
+  static constexpr bool kBulkKeys = false;
+  __host__ __device__ const uint32_t* bulk_keys() const { return nullptr; }
+  __host__ __device__ const uint32_t* bulk_vals() const { return sa; }
+  __device__ __forceinline__ void fix(uint64_t, uint32_t& k, uint32_t& v) const {
+    const uint32_t x = v;
+    const uint32_t i = x >= h ? x - h : static_cast<uint32_t>(x + np - h);
+    k = __ldg(&rank[i]);
+    v = i;
+  }
 };
 
 // New dense ids.  flag_j = (key_j, r2_j) != (key_{j-1}, r2_{j-1}) with key = old id of SA_j (the

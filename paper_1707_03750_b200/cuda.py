@@ -75,6 +75,18 @@ def lib() -> C.CDLL:
         "itt_mine_patterns": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, P(abi.itt_mining_cfg), C.c_uint32, C.c_int,
                                P(P(abi.itt_pattern))], C.c_int),
         "itt_free_patterns": ([vp, P(abi.itt_pattern), C.c_uint32], C.c_int),
+        "itt_mine_patterns_sa": ([vp, vp, C.c_uint64, C.c_int32, vp, vp, P(abi.itt_mining_cfg), C.c_uint32, C.c_int,
+                                  P(P(abi.itt_pattern))], C.c_int),
+        "itt_dsa_keys": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int, vp, vp, C.c_uint64, C.c_int, vp, vp],
+                         C.c_int),
+        "itt_dsa_partition": ([vp, vp, vp, C.c_uint64, C.c_int, vp, vp, C.c_uint32, vp, C.c_uint32, vp, vp, P(C.c_uint64)],
+                              C.c_int),
+        "itt_dsa_sort": ([vp, vp, vp, C.c_uint64, C.c_int], C.c_int),
+        "itt_dsa_ids": ([vp, vp, vp, C.c_uint64, C.c_int, C.c_uint64, C.c_uint32, vp, P(C.c_uint64)], C.c_int),
+        "itt_dsa_scatter": ([vp, vp, C.c_uint64, C.c_uint64, vp], C.c_int),
+        "itt_dsa_lcp_requests": ([vp, vp, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, vp, vp], C.c_int),
+        "itt_dsa_kasai": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp, C.c_uint32, vp], C.c_int),
+        "itt_dsa_sample": ([vp, vp, vp, C.c_uint64, C.c_uint32, vp, vp], C.c_int),
         "itt_approx_match": ([vp, P(C.c_int32), C.c_uint64, P(C.c_int32), C.c_uint64, C.c_int64, P(P(abi.itt_span)),
                               P(C.c_uint64)], C.c_int),
         "itt_op_profile": ([vp, P(C.c_int32), P(C.c_int64), P(C.c_int64), P(C.c_uint8), C.c_uint64, C.c_uint32,
@@ -169,6 +181,7 @@ class Context:
         if rc != 0:
             raise IttError(rc, f"itt_ctx_create({device}) failed: no usable sm_100 device")
         self.h = h
+        self.device = device
 
     def close(self):
         if self.h:
@@ -275,6 +288,23 @@ class Context:
         out = P(abi.itt_pattern)()
         self._check(lib().itt_mine_patterns(self.h, _ptr(t, C.c_int32), t.shape[0], term, cfgs, len(loops),
                                             1 if multi else 0, C.byref(out)))
+        k = len(loops) if multi else 1
+        res = [dict(tokens=[out[i].tokens[j] for j in range(out[i].length)], count=out[i].count,
+                    first_token=out[i].first_token, epsilon_used=out[i].epsilon_used) for i in range(k)]
+        lib().itt_free_patterns(self.h, out, k)
+        return res
+
+    def mine_patterns_sa(self, tokens_ptr, n, term, sa_ptr, lcp_ptr, loops, multi=False):
+        """mine_pattern(s) over a suffix array built elsewhere (device pointers: tokens[n],
+        sa[n+1], lcp[n+1] capped at >= max L_max + 1), e.g. the distributed one (dist_sa.py)."""
+        cfgs = (abi.itt_mining_cfg * max(1, len(loops)))()
+        for i, lp in enumerate(loops):
+            cfgs[i].iterations = lp[0]
+            cfgs[i].epsilon0 = lp[1] if len(lp) > 1 else 1
+            cfgs[i].epsilon_cap = lp[2] if len(lp) > 2 else 0
+        out = P(abi.itt_pattern)()
+        self._check(lib().itt_mine_patterns_sa(self.h, C.c_void_p(tokens_ptr), n, term, C.c_void_p(sa_ptr),
+                                               C.c_void_p(lcp_ptr), cfgs, len(loops), 1 if multi else 0, C.byref(out)))
         k = len(loops) if multi else 1
         res = [dict(tokens=[out[i].tokens[j] for j in range(out[i].length)], count=out[i].count,
                     first_token=out[i].first_token, epsilon_used=out[i].epsilon_used) for i in range(k)]

@@ -1,0 +1,87 @@
+"""GPU: the distributed suffix array's device steps (itt_dsa_*, dist.cu) driven by dist_sa.py
+over virtual ranks on one B200 (threads, one library context each; the exchange is a host-side
+copy, so no kernel of one rank waits on another's).  Parity: SA and LCP bit-exact against the
+single-GPU itt_suffix_array and the oracle (full), capped LCP = min(full LCP, cap) with the same
+groups (capped), and mining over the gathered distributed SA/LCP (itt_mine_patterns_sa) equal to
+itt_mine_patterns, including a planted-period trace of 2M tokens."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1707_03750_b200 import cuda, dist_sa
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(P, tokens, term, cap=0xFFFFFFFF):
+    text = torch.tensor(np.concatenate([np.asarray(tokens, np.int32), [term]]), dtype=torch.int32, device="cuda")
+    ctxs = [cuda.Context(0) for _ in range(P)]
+    try:
+        res = dist_sa.run_virtual(P, lambda ex, r: dist_sa.suffix_array_dist(ex, dist_sa.CudaOps(ctxs[r]), text,
+                                                                             len(tokens), term, cap))
+    finally:
+        for c in ctxs:
+            c.close()
+    sa = torch.cat([r.sa for r in res]).cpu().numpy().view(np.uint32)
+    lcp = torch.cat([r.lcp for r in res]).cpu().numpy().view(np.uint32)
+    return sa, lcp, res
+
+
+def _cases():
+    rng = np.random.default_rng(11)
+    out = [("one", [0], 1)]
+    for t in range(6):
+        n = int(rng.integers(50, 5000))
+        V = int(rng.integers(2, 300))
+        out.append((f"random{t}", rng.integers(0, V, n), V))
+    body = rng.integers(0, 40, 57)
+    out.append(("periodic", np.tile(body, 80)[:4500], 40))
+    out.append(("runs", np.array([0] * 3000 + [1] + [0] * 100), 2))
+    out.append(("random_200k", rng.integers(0, 1000, 200_000), 1000))
+    return out
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_dist_full_sa_matches_single_gpu(ctx, P):
+    for name, tok, term in _cases():
+        want_sa, want_lcp = ctx.suffix_array(tok, term)
+        sa, lcp, _ = _run(P, tok, term)
+        assert np.array_equal(sa, want_sa), (name, P)
+        assert np.array_equal(lcp, want_lcp), (name, P)
+
+
+def _groups_equal(sa, want_sa, lcp, cap):
+    bounds = np.flatnonzero(np.concatenate([[True], lcp[1:] < cap, [True]]))
+    return all(np.array_equal(np.sort(sa[a:b]), np.sort(want_sa[a:b])) for a, b in zip(bounds[:-1], bounds[1:]))
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_dist_capped_sa(ctx, P):
+    for name, tok, term in _cases():
+        want_sa, want_lcp = ctx.suffix_array(tok, term)
+        for cap in (2, 17, 201):
+            sa, lcp, res = _run(P, tok, term, cap)
+            full = res[0].cap == 0xFFFFFFFF
+            assert np.array_equal(lcp, want_lcp if full else np.minimum(want_lcp, cap)), (name, cap)
+            assert _groups_equal(sa, want_sa, lcp, 0xFFFFFFFF if full else cap), (name, cap)
+
+
+def test_dist_mining_planted_period(ctx):
+    rng = np.random.default_rng(3)
+    V, body, iters = 150, 200, 10_000
+    tok = np.concatenate([np.arange(150, 166) % V, np.tile(rng.integers(0, V, body), iters)]).astype(np.int32)
+    tok[:16] = rng.integers(0, V, 16)
+    n = tok.size
+    loops = [(iters, 1)]
+    cap = (n - 1) // iters + 1
+    want = ctx.mine_patterns(tok, V, loops)
+    for P in (2, 4):
+        _, _, res = _run(P, tok, V, cap)
+        sa = torch.cat([r.sa for r in res])
+        lcp = torch.cat([r.lcp for r in res])
+        dtok = torch.from_numpy(tok).cuda()
+        got = ctx.mine_patterns_sa(dtok.data_ptr(), n, V, sa.data_ptr(), lcp.data_ptr(), loops)
+        assert got == want, P
+        assert len(got[0]["tokens"]) == body and got[0]["count"] == iters
