@@ -247,6 +247,68 @@ def bench_batch(args, world, rank, local, workload):
     return 0
 
 
+def bench_dist_sa(args, world, rank, local, workload, iters):
+    """One trace, suffix array over all ranks (SURVEY §8e C5 path): rank 0 runs itt_analyze on the
+    trace with the distributed suffix array plugged in (itt_analyze_opts.sa_provider); every rank
+    builds its share of the SA/LCP (dist_sa.py over NCCL), rank 0 mines / matches / aggregates."""
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    from paper_1707_03750_b200 import cuda as itt, dist_sa
+    dev = local
+    ops_ctx = itt.Context(dev)
+    prov = dist_sa.DistributedSAProvider(dist_sa.TorchExchange(device=torch.device("cuda", dev)), dist_sa.CudaOps(ops_ctx))
+    if rank != 0:
+        prov.serve()
+        dist.barrier()
+        dist.destroy_process_group()
+        return 0
+    ctx = itt.Context(dev)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", dev))
+    if args.iterations:
+        iters = args.iterations
+        workload += f" [DRY RUN: iterations overridden to {iters}]"
+    recs, info = make_trace(args.config, args.iterations)
+    drecs = ctx.upload(recs, names_host=args.config == "C5")
+    n_events = info["n"]
+
+    def step():
+        return ctx.analyze_raw(drecs, [iters], sa_provider=prov)
+
+    for _ in range(max(3, args.warmup)):
+        res = step()
+    want = ctx.analyze_raw(drecs, [iters])  # single-GPU path: the distributed SA must not change a thing
+    same = all(a["pattern_tokens"] == b["pattern_tokens"] and np.array_equal(a["rows"], b["rows"])
+               for a, b in zip(res["loops"], want["loops"]))
+    torch.cuda.synchronize(dev)
+    ctx.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    e1.record(stream)
+    e1.synchronize()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    prov.stop()
+    last = prov.last
+    line = {"metric": METRIC, "value": n_events / (ms_step / 1000.0), "unit": "events/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": workload + " -- suffix array distributed over the ranks (sample-sort prefix doubling)",
+                       "events": n_events, "tokens": res["n_tokens"], "parallelism": f"dist-sa{world}",
+                       "doubling_rounds": last.rounds, "groups": last.groups, "cap": last.cap,
+                       "equal_to_single_gpu_path": bool(same)},
+            "gpu_launches": None}
+    print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -266,6 +328,8 @@ def main():
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
     ap.add_argument("--workers", type=int, default=16, help="C4: concurrent streams (host threads) per GPU")
+    ap.add_argument("--dist-sa", action="store_true",
+                    help="one trace with its suffix array distributed over all ranks (NCCL; C5's multi-GPU path)")
     ap.add_argument("--batch-impl", default="native", choices=["native", "threads"],
                     help="C4 executor: native C++ worker threads (itt_batch_*) or Python threads")
     args = ap.parse_args()
@@ -288,6 +352,8 @@ def main():
 
     if args.config == "C4":
         return bench_batch(args, world, rank, local, workload)
+    if args.dist_sa:
+        return bench_dist_sa(args, world, rank, local, workload, iters)
 
     import torch
     if world > 1:

@@ -127,6 +127,8 @@ int itt_device_alloc(itt_ctx* ctx, uint64_t bytes, void** out);
 int itt_device_free(itt_ctx* ctx, void* p);
 int itt_memcpy_h2d(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+/* any direction (unified addressing), synchronous like the others */
+int itt_memcpy(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes);
 int itt_host_unregister(itt_ctx* ctx, void* p);
 int itt_ctx_synchronize(itt_ctx* ctx);
@@ -377,6 +379,14 @@ typedef struct itt_analyze_opts { /* AnalyzeOptions, pipeline.hpp:18-25 */
   int64_t k0;           /* < 0: default_k0(pattern length) (match.hpp:19-21) */
   int64_t main_stream;  /* < 0: select_main_stream */
   uint32_t flags;       /* ITT_ANALYZE_* (0 = the reference's outputs only) */
+  /* Suffix array provider (NULL: the single-device capped doubling, sa.cu).  Called once per
+   * analyze on the calling thread, after the token sequence exists and the library's stream is
+   * idle, with DEVICE pointers: tokens[n] (ids in [0, term)), and sa / lcp [n+1] to fill with the
+   * suffix array of tokens+[term] and its LCP capped at `cap` (= max L_max + 1, mine.hpp:64-67).
+   * The distributed suffix array (dist_sa.py, itt_dsa_*) plugs in here; 0 = success. */
+  int (*sa_provider)(void* user, const int32_t* tokens, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa,
+                     uint32_t* lcp);
+  void* sa_user;
 } itt_analyze_opts;
 
 typedef struct itt_loop_result { /* LoopReport (report.hpp:92-103) integer fields + details rows */

@@ -123,6 +123,10 @@ class itt_clamps(C.Structure):
     _fields_ = [("negative_gap_clamps", C.c_int64), ("negative_interval_clamps", C.c_int64)]
 
 
+# int (*)(void* user, const int32_t* tokens, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa, uint32_t* lcp)
+SA_PROVIDER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p)
+
+
 class itt_analyze_opts(C.Structure):
     _fields_ = [
         ("loops", P(C.c_int64)),
@@ -131,6 +135,8 @@ class itt_analyze_opts(C.Structure):
         ("k0", C.c_int64),
         ("main_stream", C.c_int64),
         ("flags", C.c_uint32),
+        ("sa_provider", SA_PROVIDER),
+        ("sa_user", C.c_void_p),
     ]
 
 

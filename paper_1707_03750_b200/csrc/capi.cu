@@ -277,6 +277,11 @@ int itt_memcpy_h2d(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
 int itt_memcpy_d2h(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
   return guarded(ctx, [&](Ctx* c) { ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream)); });
 }
+int itt_memcpy(itt_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (bytes) ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+  });
+}
 int itt_host_register(itt_ctx* ctx, void* p, uint64_t bytes) {
   return guarded(ctx, [&](Ctx*) { ITT_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault)); });
 }
@@ -808,8 +813,24 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
     SuffixState s;
     {
       StageTimer st(c, "sa+lcp");
-      build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan,
-                         mining_cap(t.n_tok, cfgs), /*known_alphabet=*/true);
+      if (opts->sa_provider) {  // e.g. the distributed suffix array (dist_sa.py)
+        const uint64_t n = t.n_tok;
+        const int32_t term = static_cast<int32_t>(t.n_names);
+        s.n = n;
+        s.np = n + 1;
+        s.lo = 0;
+        s.text.alloc(c, n + 1);
+        ITT_CUDA(cudaMemcpyAsync(s.text.p, t.tokens.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+        h2d(c, s.text.p + n, &term, 1);
+        s.sa.alloc(c, n + 1);
+        s.lcp.alloc(c, n + 1);
+        c->sync();
+        if (opts->sa_provider(opts->sa_user, s.text.p, n, term, mining_cap(n, cfgs), s.sa.p, s.lcp.p) != 0)
+          fail(ITT_E_CUDA, "pattern-mining: the suffix-array provider failed");
+      } else {
+        build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan,
+                           mining_cap(t.n_tok, cfgs), /*known_alphabet=*/true);
+      }
     }
     IntervalState iv;
     std::vector<MinedPattern> pats;

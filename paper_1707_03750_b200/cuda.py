@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
         "itt_device_free": ([vp, vp], C.c_int),
         "itt_memcpy_h2d": ([vp, vp, vp, C.c_uint64], C.c_int),
         "itt_memcpy_d2h": ([vp, vp, vp, C.c_uint64], C.c_int),
+        "itt_memcpy": ([vp, vp, vp, C.c_uint64], C.c_int),
         "itt_host_register": ([vp, vp, C.c_uint64], C.c_int),
         "itt_host_unregister": ([vp, vp], C.c_int),
         "itt_ctx_synchronize": ([vp], C.c_int),
@@ -369,7 +370,7 @@ class Context:
         lib().itt_free(self.h, C.cast(rows, C.c_void_p))
         return out, (cl.negative_gap_clamps, cl.negative_interval_clamps)
 
-    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1, op_profile=False) -> dict:
+    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1, op_profile=False, sa_provider=None) -> dict:
         """itt_analyze: device pipeline up to the per-loop integer aggregates.  The per-iteration
         rows (and the a12 op profile: op_profile=True for the per-op / per-iteration totals,
         "cells" for the (iteration, op) grid as well) are zero-copy numpy views of the library's
@@ -383,8 +384,22 @@ class Context:
         if op_profile == "cells":
             flags |= abi.ITT_ANALYZE_OP_CELLS
         opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream, flags)
+        if sa_provider is not None:  # fn(tokens_ptr, n, term, cap, sa_ptr, lcp_ptr); raises on failure
+            failure = []
+
+            def _cb(user, tok, n, term, cap, sa, lcp):
+                try:
+                    sa_provider(tok, n, term, cap, sa, lcp)
+                    return 0
+                except BaseException as e:  # noqa: BLE001 (reported after the call returns)
+                    failure.append(e)
+                    return 1
+            opts.sa_provider = abi.SA_PROVIDER(_cb)
         out = P(abi.itt_analysis)()
-        self._check(lib().itt_analyze(self.h, C.byref(c), C.byref(opts), C.byref(out)))
+        rc = lib().itt_analyze(self.h, C.byref(c), C.byref(opts), C.byref(out))
+        if sa_provider is not None and failure:
+            raise failure[0]
+        self._check(rc)
         owner = _AnalysisOwner(self, out)
         a = out[0]
         res = dict(

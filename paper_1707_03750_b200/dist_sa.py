@@ -61,6 +61,10 @@ class Exchange:
     def all_gather_tensor(self, t: torch.Tensor) -> list[torch.Tensor]:
         raise NotImplementedError
 
+    def broadcast(self, t: torch.Tensor, root: int = 0) -> torch.Tensor:
+        """t on root (same shape/dtype expected elsewhere: pass a buffer); returns root's data."""
+        raise NotImplementedError
+
 
 class TorchExchange(Exchange):
     """torch.distributed collectives (NCCL for CUDA tensors, gloo for CPU tensors)."""
@@ -84,7 +88,15 @@ class TorchExchange(Exchange):
         out = torch.empty(sum(rc), dtype=send.dtype, device=send.device)
         self.dist.all_to_all_single(out, send.contiguous(), output_split_sizes=rc, input_split_sizes=list(counts),
                                     group=self.group)
+        self._settle(out)
         return out
+
+    @staticmethod
+    def _settle(t):
+        # NCCL orders the collective only against torch's current stream; the device steps run on
+        # the library context's own stream, so the host waits for the result here
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
 
     def all_gather_ints(self, vals):
         t = torch.tensor(vals, dtype=torch.int64, device=self.device)
@@ -100,6 +112,11 @@ class TorchExchange(Exchange):
         out = [torch.empty_like(pad) for _ in range(self.size)]
         self.dist.all_gather(out, pad, group=self.group)
         return [o[: x[0]] for o, x in zip(out, n)]
+
+    def broadcast(self, t, root=0):
+        self.dist.broadcast(t, src=root, group=self.group)
+        self._settle(t)
+        return t
 
 
 class _Board:
@@ -150,6 +167,17 @@ class ThreadExchange(Exchange):
     def all_gather_tensor(self, t):
         got = self._post(t)
         return [g.clone() for g in got]
+
+    def broadcast(self, t, root=0):
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+        got = self._post(t if self.rank == root else None)
+        if self.rank != root:
+            t.copy_(got[root])
+            if t.is_cuda:
+                torch.cuda.synchronize(t.device)
+        self.board.barrier.wait()
+        return t
 
 
 # --------------------------------------------------------------------------- device steps
@@ -225,6 +253,11 @@ class CudaOps:
 
     def to_device(self, arr: np.ndarray, dtype):
         return torch.from_numpy(np.ascontiguousarray(arr)).to(dtype=dtype, device=self.device)
+
+    def copy(self, dst_ptr, src_ptr, nbytes):
+        if torch.cuda.is_available():
+            torch.cuda.synchronize(self.device)  # torch-side producers of src / consumers of dst
+        self.ctx._check(self.L.itt_memcpy(self.ctx.h, C.c_void_p(dst_ptr), C.c_void_p(src_ptr), nbytes))
 
 
 # --------------------------------------------------------------------------- driver
@@ -393,3 +426,51 @@ def run_virtual(P: int, fn):
     if err:
         raise err[0]
     return res
+
+
+# --------------------------------------------------------------------------- analyze over G ranks
+class DistributedSAProvider:
+    """itt_analyze's suffix-array hook (itt_analyze_opts.sa_provider) on the root rank: the root
+    analyzes the trace (ingest, dictionary, tokens, then mining / matching / aggregates); the
+    suffix array and LCP in between are built by all G ranks.  Per analyze the root broadcasts
+    (n, term, cap) and the tokens (the text is replicated: 4 B per token), every rank runs
+    suffix_array_dist, and the slices are gathered back into the library's sa / lcp buffers.
+    The other ranks sit in serve() until the root calls stop()."""
+
+    def __init__(self, ex: Exchange, ops, root: int = 0):
+        self.ex, self.ops, self.root = ex, ops, root
+        self.last: DistSA | None = None
+
+    def _header(self, vals):
+        t = torch.tensor(vals, dtype=torch.int64, device=self.ops.device)
+        return self.ex.broadcast(t, self.root).cpu().tolist()
+
+    def _round(self, n, term, cap, text):
+        r = suffix_array_dist(self.ex, self.ops, text, n, term, cap)
+        self.last = r
+        sa = gather_to_root(self.ex, r.sa, self.root)
+        lcp = gather_to_root(self.ex, r.lcp, self.root)
+        return sa, lcp
+
+    def __call__(self, tok_ptr, n, term, cap, sa_ptr, lcp_ptr):
+        self._header([n, term, cap])
+        text = self.ops.empty(n + 1, torch.int32)
+        self.ops.copy(text.data_ptr(), tok_ptr, (n + 1) * 4)
+        self.ex.broadcast(text, self.root)
+        sa, lcp = self._round(n, term, cap, text)
+        self.ops.copy(sa_ptr, sa.data_ptr(), (n + 1) * 4)
+        self.ops.copy(lcp_ptr, lcp.data_ptr(), (n + 1) * 4)
+
+    def serve(self):
+        """Non-root ranks: take part in every distributed suffix array until stop()."""
+        while True:
+            n, term, cap = self._header([0, 0, 0])
+            if n < 0:
+                return
+            text = self.ops.empty(n + 1, torch.int32)
+            self.ex.broadcast(text, self.root)
+            self._round(n, term, cap, text)
+
+    def stop(self):
+        self._header([-1, 0, 0])
+

@@ -182,13 +182,15 @@ def rows_to_metrics(rows) -> list:
 def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Optional[int] = None,
                   theta_copy: float = 0.10, theta_cpu: float = 10.0, main_stream: Optional[int] = None,
                   trace_label: str = "trace.csv", device_labels=None, names=None,
-                  op_profile=False, trace_warnings=()) -> AnalysisResult:
+                  op_profile=False, trace_warnings=(), sa_provider=None) -> AnalysisResult:
     """analyze_trace (pipeline.hpp:34-134): device pipeline + host finish in reference order.
     op_profile=True adds the a12 second-level per-op profile of every loop ("cells": with the
-    (iteration, op) grid); no reference counterpart, and the reference's own outputs are unchanged."""
+    (iteration, op) grid); no reference counterpart, and the reference's own outputs are unchanged.
+    sa_provider: build the suffix array elsewhere (dist_sa.DistributedSAProvider: over G GPUs)."""
     try:
         raw = ctx.analyze_raw(recs, list(loops), epsilon0, -1 if k0 is None else k0,
-                              -1 if main_stream is None else main_stream, op_profile=op_profile)
+                              -1 if main_stream is None else main_stream, op_profile=op_profile,
+                              sa_provider=sa_provider)
     except IttError as e:
         raise AnalyzeError(e.kind, str(e)) from e
     label = (lambda d: device_labels[d]) if device_labels is not None else (lambda d: "dev%05u" % d)

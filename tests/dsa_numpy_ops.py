@@ -147,3 +147,7 @@ class NumpyOps:
             z ^= z >> np.uint64(31)
         j = (z % np.uint64(max(n, 1))).astype(np.int64)
         return _t64(_u64(a)[j]), _t32(_u32(b)[j])
+
+    def copy(self, dst_ptr, src_ptr, nbytes):
+        import ctypes
+        ctypes.memmove(dst_ptr, src_ptr, nbytes)

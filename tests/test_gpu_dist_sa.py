@@ -85,3 +85,32 @@ def test_dist_mining_planted_period(ctx):
         got = ctx.mine_patterns_sa(dtok.data_ptr(), n, V, sa.data_ptr(), lcp.data_ptr(), loops)
         assert got == want, P
         assert len(got[0]["tokens"]) == body and got[0]["count"] == iters
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_analyze_with_distributed_sa_provider(ctx, P):
+    """itt_analyze with the suffix array built by P virtual ranks (itt_analyze_opts.sa_provider):
+    summary JSON and details CSV byte-identical to the single-GPU analyze."""
+    from paper_1707_03750_b200 import itertrace, synth
+    for seed, cfg in ((5, "C1"), (9, "C1")):
+        recs, _ = synth.generate_config(cfg, noise_frac=0.05, shuffle_window=64, seed=seed)
+        want = itertrace.analyze_trace(ctx, recs, [100])
+        ctxs = [cuda.Context(0) for _ in range(P)]
+        main = cuda.Context(0)
+        try:
+            def body(ex, r):
+                prov = dist_sa.DistributedSAProvider(ex, dist_sa.CudaOps(ctxs[r]))
+                if r != 0:
+                    prov.serve()
+                    return None
+                try:
+                    return itertrace.analyze_trace(main, recs, [100], sa_provider=prov), prov.last
+                finally:
+                    prov.stop()
+            got, last = dist_sa.run_virtual(P, body)[0]
+        finally:
+            for c in ctxs + [main]:
+                c.close()
+        assert last is not None and last.groups > 0
+        assert got.summary_json() == want.summary_json()
+        assert got.details_csv(0) == want.details_csv(0)
