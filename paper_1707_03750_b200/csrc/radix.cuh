@@ -46,16 +46,28 @@ struct ArrayLoader {
   __device__ __forceinline__ void fix(uint64_t, K&, uint32_t&) const {}
 };
 
-// Lanes of the warp holding the same 8-bit digit (valid lanes only among themselves): nine
-// ballots instead of MATCH.ANY, whose long MIO latency dominated the ranking loop on sm_100a.
+// Lanes of the warp holding the same 8-bit digit (valid lanes only among themselves): ballots
+// instead of MATCH.ANY, whose long MIO latency dominated the ranking loop on sm_100a.  Only the
+// digit bits that vary across the warp need a ballot (two warp reductions find them): the keys of
+// periodic traces (dense group ids in SA order) are mostly equal within a warp, so most rounds
+// take no ballot at all; all 8 bits varying takes the unrolled path.
 __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool valid) {
   const unsigned vm = __ballot_sync(0xffffffffu, valid);
   unsigned peers = valid ? vm : ~vm;
+  const unsigned vary = (__reduce_or_sync(0xffffffffu, d) ^ __reduce_and_sync(0xffffffffu, d)) & 0xFFu;
+  if (vary == 0xFFu) {
 #pragma unroll
-  for (int b = 0; b < kRadixBits; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const unsigned m = __ballot_sync(0xffffffffu, bit);
-    peers &= bit ? m : ~m;
+    for (int b = 0; b < kRadixBits; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
+  } else {
+    for (unsigned v = vary; v; v &= v - 1) {
+      const bool bit = (d >> (__ffs(v) - 1)) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
   }
   return peers;
 }
