@@ -307,6 +307,27 @@ int itt_iteration_metrics(itt_ctx* ctx, const itt_records* recs, const uint64_t*
  *               front of op j inside the iteration, so that sum_v idle_ns(k, v) equals the
  *               reference's clamped op-gap sum of iteration k (metrics.hpp:145-157)
  * Cells are ordered by (iteration, op).  The two reductions of the cell grid: */
+/* ------------------------------------------------------- host finish at scale (§8f row 4)
+ * The reference's host-side finish over the integer rows, natively: I reaches 500K at C5, where
+ * an interpreted finish costs seconds.  Both are pure host functions (ctx only carries errors). */
+typedef struct itt_summary { /* SummaryMetrics, metrics.hpp:33-42 */
+  double avg_interval_ns;
+  int64_t max_interval_ns;
+  double avg_overlap;
+  double avg_operation_ns;
+  double avg_size_bytes;
+  int64_t iterations_found;
+  int64_t iterations_declared;
+  int32_t insufficient_intervals;
+  int32_t pad_;
+} itt_summary;
+/* compute_summary (metrics.hpp:166-202): same operations in the same order (bit-identical
+ * doubles); 1 + NoIterations with the reference's message when n == 0. */
+int itt_compute_summary(itt_ctx* ctx, const itt_iter_row* rows, uint64_t n, int64_t iterations_declared, itt_summary* out);
+/* details_to_csv (report.hpp:191-220) of rows[n], byte for byte, formatted by host threads in
+ * row blocks; *out is NUL-terminated, released with itt_free. */
+int itt_render_details_csv(itt_ctx* ctx, const itt_iter_row* rows, uint64_t n, char** out, uint64_t* len);
+
 typedef struct itt_op_cell {
   uint32_t iteration;
   int32_t op;

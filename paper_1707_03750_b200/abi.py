@@ -127,6 +127,20 @@ class itt_clamps(C.Structure):
 SA_PROVIDER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p)
 
 
+class itt_summary(C.Structure):  # SummaryMetrics, metrics.hpp:33-42
+    _fields_ = [
+        ("avg_interval_ns", C.c_double),
+        ("max_interval_ns", C.c_int64),
+        ("avg_overlap", C.c_double),
+        ("avg_operation_ns", C.c_double),
+        ("avg_size_bytes", C.c_double),
+        ("iterations_found", C.c_int64),
+        ("iterations_declared", C.c_int64),
+        ("insufficient_intervals", C.c_int32),
+        ("pad_", C.c_int32),
+    ]
+
+
 class itt_analyze_opts(C.Structure):
     _fields_ = [
         ("loops", P(C.c_int64)),

@@ -211,6 +211,12 @@ int itt_ctx_destroy(itt_ctx* ctx) {
 
 const char* itt_last_error(itt_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : "null context"; }
 
+// error text for the host-only entry points (report.cu)
+extern "C" __attribute__((visibility("hidden"))) int itt_ctx_set_error_(itt_ctx* ctx, const char* msg) {
+  if (ctx) ctx->c.last_error = msg ? msg : "";
+  return 0;
+}
+
 int itt_free(itt_ctx* ctx, void* p) {
   if (!p) return ITT_OK;
   if (ctx && ctx->c.out_release(p)) return ITT_OK;  // pinned output block: back to the context

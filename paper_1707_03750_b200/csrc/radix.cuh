@@ -111,21 +111,6 @@ __global__ void __launch_bounds__(256) k_hist(const K* __restrict__ keys, uint64
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-// exclusive scan of each pass histogram (one block of 256 threads per pass)
-static __global__ void k_hist_offsets(const uint32_t* __restrict__ hist, uint32_t* __restrict__ offs) {
-  __shared__ uint32_t s[kBins];
-  const int p = blockIdx.x, d = threadIdx.x;
-  s[d] = hist[p * kBins + d];
-  __syncthreads();
-  for (int o = 1; o < kBins; o <<= 1) {
-    uint32_t v = d >= o ? s[d - o] : 0;
-    __syncthreads();
-    s[d] += v;
-    __syncthreads();
-  }
-  offs[p * kBins + d] = s[d] - hist[p * kBins + d];
-}
-
 template <typename K, int BLOCK, int ITEMS>
 struct SmemLayout {
   static constexpr int kTile = BLOCK * ITEMS;
@@ -136,13 +121,15 @@ struct SmemLayout {
   uint32_t tile_count[kBins];
   uint32_t local_off[kBins];
   uint32_t global_base[kBins];
+  uint32_t digit_off[kBins];
   uint32_t group_sum[8];
+  uint32_t hgroup_sum[8];
   uint32_t tile;
 };
 
 template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                                                    uint64_t n, int shift, const uint32_t* __restrict__ digit_offs,
+                                                    uint64_t n, int shift, const uint32_t* __restrict__ digit_hist,
                                                     uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
   static_assert(BLOCK >= kBins, "one thread per digit");
   using S_t = SmemLayout<K, BLOCK, ITEMS>;
@@ -151,6 +138,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S_t& S = *reinterpret_cast<S_t*>(smem_raw);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t hv = threadIdx.x < kBins ? __ldg(&digit_hist[threadIdx.x]) : 0u;  // this pass's digit counts
 
   if (threadIdx.x == 0) S.tile = atomicAdd(counter, 1u);
   for (int i = threadIdx.x; i < kWarps * kBins; i += BLOCK) (&S.warp_hist[0][0])[i] = 0;
@@ -205,13 +193,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
     }
     S.local_off[d] = inc - sum;
     if (lane == 31) S.group_sum[d >> 5] = inc;
+    // this pass's global digit offsets: exclusive scan of the histogram (no separate launch)
+    uint32_t hinc = hv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, hinc, o);
+      if (static_cast<int>(lane) >= o) hinc += u;
+    }
+    S.digit_off[d] = hinc - hv;
+    if (lane == 31) S.hgroup_sum[d >> 5] = hinc;
   }
   __syncthreads();
   if (threadIdx.x < kBins) {
-    uint32_t add = 0;
+    uint32_t add = 0, hadd = 0;
     const int g = threadIdx.x >> 5;
-    for (int h = 0; h < g; ++h) add += S.group_sum[h];
+    for (int h = 0; h < g; ++h) add += S.group_sum[h], hadd += S.hgroup_sum[h];
     S.local_off[threadIdx.x] += add;
+    S.digit_off[threadIdx.x] += hadd;
   }
   __syncthreads();
   // ---- scatter into shared memory in digit order
@@ -248,7 +246,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
       }
       st_relaxed_u32(status + static_cast<uint64_t>(tile) * kBins + d, kStP | (excl + my_count));
     }
-    S.global_base[d] = digit_offs[d] + excl;
+    S.global_base[d] = S.digit_off[d] + excl;
   }
   __syncthreads();
   // ---- write out
@@ -309,14 +307,16 @@ struct TmaLayout {
   uint16_t warp_hist[kWarps][kBins];
   uint32_t local_off[kBins];
   uint32_t global_base[kBins];
+  uint32_t digit_off[kBins];
   uint32_t group_sum[8];
+  uint32_t hgroup_sum[8];
   uint64_t bar[2];
   uint32_t tile[2];
 };
 
 template <typename K, int BLOCK, int ITEMS, typename Loader>
 __global__ void __launch_bounds__(BLOCK) k_onesweep_tma(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                                                        uint64_t n, int shift, const uint32_t* __restrict__ digit_offs,
+                                                        uint64_t n, int shift, const uint32_t* __restrict__ digit_hist,
                                                         uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
   static_assert(BLOCK >= kBins, "one thread per digit");
   static_assert(ITEMS <= 16, "16-bit ranks");
@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep_tma(Loader ld, K* __restrict
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S_t& S = *reinterpret_cast<S_t*>(smem_raw);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t hv = threadIdx.x < kBins ? __ldg(&digit_hist[threadIdx.x]) : 0u;  // this pass's digit counts
   const uint64_t tiles = (n + kTile - 1) / kTile;
   const uint64_t full_tiles = n / kTile;
 
@@ -425,13 +426,23 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep_tma(Loader ld, K* __restrict
       }
       S.local_off[d] = inc - sum;
       if (lane == 31) S.group_sum[d >> 5] = inc;
+      // this pass's global digit offsets: exclusive scan of the histogram (no separate launch)
+      uint32_t hinc = hv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, hinc, o);
+        if (static_cast<int>(lane) >= o) hinc += u;
+      }
+      S.digit_off[d] = hinc - hv;
+      if (lane == 31) S.hgroup_sum[d >> 5] = hinc;
     }
     __syncthreads();
     if (threadIdx.x < kBins) {
-      uint32_t add = 0;
+      uint32_t add = 0, hadd = 0;
       const int g = threadIdx.x >> 5;
-      for (int h = 0; h < g; ++h) add += S.group_sum[h];
+      for (int h = 0; h < g; ++h) add += S.group_sum[h], hadd += S.hgroup_sum[h];
       S.local_off[threadIdx.x] += add;
+      S.digit_off[threadIdx.x] += hadd;
     }
     __syncthreads();
     // ---- scatter the staged tile into digit order
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep_tma(Loader ld, K* __restrict
         }
         st_relaxed_u32(status + static_cast<uint64_t>(tile) * kBins + d, kStP | (excl + my_count));
       }
-      S.global_base[d] = digit_offs[d] + excl;
+      S.global_base[d] = S.digit_off[d] + excl;
     }
     __syncthreads();
     for (uint32_t p = threadIdx.x; p < valid; p += BLOCK) {
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(BLOCK) k_onesweep_tma(Loader ld, K* __restrict
 }
 
 template <typename K, int BLOCK, int ITEMS, typename Loader>
-void launch_pass_tma(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* offs, uint32_t* st) {
+void launch_pass_tma(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* dhist, uint32_t* st) {
   constexpr int TILE = BLOCK * ITEMS;
   const size_t smem = sizeof(TmaLayout<K, BLOCK, ITEMS>);
   auto kern = k_onesweep_tma<K, BLOCK, ITEMS, Loader>;
@@ -496,13 +507,12 @@ void launch_pass_tma(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, 
   const uint64_t tiles = (n + TILE - 1) / TILE;
   const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(c->sm_count) * occ);
   launch(c, "radix_onesweep", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), kern, dim3(static_cast<unsigned>(grid)), dim3(BLOCK),
-         smem, ld, ko, vo, n, shift, offs, st + 1, st);
+         smem, ld, ko, vo, n, shift, dhist, st + 1, st);
 }
 
 // Scratch reused across sorts on one context.
 struct Scratch {
   DBuf<uint32_t> hist;    // passes*256 counts
-  DBuf<uint32_t> offs;    // passes*256 exclusive offsets
   DBuf<uint32_t> status;  // passes * (tiles * 256 look-back words + counter)
   std::vector<uint32_t> host_hist;
 };
@@ -513,7 +523,7 @@ constexpr int kCfgItems[] = {8, 16, 12, 8, 16, 8, 8, 8, 16, 12, 8, 8, 16};
 int config_index();
 
 template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB = 1024 / BLOCK>
-void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* offs,
+void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* dhist,
                  uint32_t* st, bool first_use) {
   constexpr int TILE = BLOCK * ITEMS;
   const size_t smem = sizeof(SmemLayout<K, BLOCK, ITEMS>);
@@ -521,11 +531,11 @@ void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int 
   smem_optin(c, k_onesweep<K, BLOCK, ITEMS, Loader, MINB>, smem);
   const uint64_t tiles = (n + TILE - 1) / TILE;
   launch(c, "radix_onesweep", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), k_onesweep<K, BLOCK, ITEMS, Loader, MINB>,
-         dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, offs, st + 1, st);
+         dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, dhist, st + 1, st);
 }
 
 template <typename K, typename Loader>
-void dispatch_pass(Ctx* c, int cfg, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* offs,
+void dispatch_pass(Ctx* c, int cfg, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* dhist,
                    uint32_t* st) {
   static bool seen[16] = {false};
   const bool first = !seen[cfg];
@@ -535,19 +545,19 @@ void dispatch_pass(Ctx* c, int cfg, const Loader& ld, K* ko, uint32_t* vo, uint6
     if (a & 15u) fail(ITT_E_INVALID_ARGUMENT, "internal: radix staging needs 16-byte aligned arrays");
   }
   switch (cfg) {
-    case 1: launch_pass<K, 256, 16>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 2: launch_pass<K, 384, 12>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 3: launch_pass<K, 256, 8>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 4: launch_pass<K, 512, 16>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 5: launch_pass<K, 512, 8, Loader, 3>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 6: launch_pass<K, 512, 8, Loader, 4>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 7: launch_pass<K, 256, 8, Loader, 6>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 8: launch_pass<K, 256, 16, Loader, 4>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 9: launch_pass<K, 256, 12, Loader, 5>(c, ld, ko, vo, n, shift, offs, st, first); break;
-    case 10: launch_pass_tma<K, 512, 8>(c, ld, ko, vo, n, shift, offs, st); break;
-    case 11: launch_pass_tma<K, 256, 8>(c, ld, ko, vo, n, shift, offs, st); break;
-    case 12: launch_pass_tma<K, 256, 16>(c, ld, ko, vo, n, shift, offs, st); break;
-    default: launch_pass<K, 512, 8>(c, ld, ko, vo, n, shift, offs, st, first); break;
+    case 1: launch_pass<K, 256, 16>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 2: launch_pass<K, 384, 12>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 3: launch_pass<K, 256, 8>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 4: launch_pass<K, 512, 16>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 5: launch_pass<K, 512, 8, Loader, 3>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 6: launch_pass<K, 512, 8, Loader, 4>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 7: launch_pass<K, 256, 8, Loader, 6>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 8: launch_pass<K, 256, 16, Loader, 4>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 9: launch_pass<K, 256, 12, Loader, 5>(c, ld, ko, vo, n, shift, dhist, st, first); break;
+    case 10: launch_pass_tma<K, 512, 8>(c, ld, ko, vo, n, shift, dhist, st); break;
+    case 11: launch_pass_tma<K, 256, 8>(c, ld, ko, vo, n, shift, dhist, st); break;
+    case 12: launch_pass_tma<K, 256, 16>(c, ld, ko, vo, n, shift, dhist, st); break;
+    default: launch_pass<K, 512, 8>(c, ld, ko, vo, n, shift, dhist, st, first); break;
   }
 }
 
@@ -572,7 +582,6 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
   if (n == 0) return false;
   if (s.hist.n < static_cast<size_t>(passes) * kBins) {
     s.hist.alloc(c, static_cast<size_t>(passes) * kBins);
-    s.offs.alloc(c, static_cast<size_t>(passes) * kBins);
   }
   const uint32_t* hist = hist_in;
   if (!hist) {
@@ -583,7 +592,6 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
            static_cast<size_t>(passes) * kBins * 4, keys, n, begin_bit, passes, s.hist.p);
     hist = s.hist.p;
   }
-  launch(c, "radix_offsets", 0.0, k_hist_offsets, dim3(passes), dim3(kBins), 0, hist, s.offs.p);
   std::vector<int> live;
   if (skip_trivial) {
     s.host_hist.resize(static_cast<size_t>(passes) * kBins);
@@ -609,10 +617,10 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
     K* ko = alt ? keys : keys_alt;
     uint32_t* vo = alt ? vals : vals_alt;
     if (q == 0 && first_loader) {
-      dispatch_pass<K>(c, cfg, *first_loader, ko, vo, n, begin_bit + p * kRadixBits, s.offs.p + p * kBins, st);
+      dispatch_pass<K>(c, cfg, *first_loader, ko, vo, n, begin_bit + p * kRadixBits, hist + p * kBins, st);
     } else {
       const ArrayLoader<K> ld{alt ? keys_alt : keys, alt ? vals_alt : vals};
-      dispatch_pass<K>(c, cfg, ld, ko, vo, n, begin_bit + p * kRadixBits, s.offs.p + p * kBins, st);
+      dispatch_pass<K>(c, cfg, ld, ko, vo, n, begin_bit + p * kRadixBits, hist + p * kBins, st);
     }
     alt = !alt;
   }

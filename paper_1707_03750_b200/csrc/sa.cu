@@ -60,20 +60,19 @@ __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32
   }
 }
 
-// codes: tokens - lo, terminator appended at n
-__global__ void k_text_codes(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int32_t lo, int32_t* __restrict__ text) {
+// codes (tokens - lo, terminator appended at n) and the first k symbols of every suffix packed
+// into 32 bits, in one pass over the tokens
+__global__ void k_text_keys(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int32_t lo, int bits, int k,
+                            int32_t* __restrict__ text, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) text[i] = tok[i] - lo;
-  else if (i == n) text[n] = term - lo;
-}
-
-__global__ void k_init_keys(const int32_t* __restrict__ text, uint64_t np, int bits, int k, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
-  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t np = n + 1;
   if (i >= np) return;
   uint32_t key = 0;
   for (int q = 0; q < k; ++q) {
-    const uint32_t c = i + q < np ? static_cast<uint32_t>(text[i + q]) : 0u;  // padding past the unique terminator is never decisive
+    // padding past the unique terminator is never decisive
+    const uint64_t j = i + q;
+    const uint32_t c = j < n ? static_cast<uint32_t>(__ldg(&tok[j]) - lo) : (j == n ? static_cast<uint32_t>(term - lo) : 0u);
+    if (q == 0) text[i] = static_cast<int32_t>(c);
     key = (key << bits) | c;
   }
   keys[i] = key;
@@ -315,7 +314,6 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   s.h0 = static_cast<uint32_t>(k);
   s.lo = lo;
   s.text.alloc(c, np);
-  launch(c, "sa_text", np * 8.0, k_text_codes, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, s.text.p);
 
   // five rotating buffers: the current SA plus the sort's (keys, vals) double buffer
   DBuf<uint32_t> bufs[5];
@@ -325,8 +323,8 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   uint32_t* kb = bufs[2].p;
   uint32_t* vb = bufs[3].p;
   uint32_t* spare = bufs[4].p;
-  launch(c, "sa_init_keys", np * (4.0 * k + 8.0), k_init_keys, dim3(grid_for(np, 256)), dim3(256), 0, s.text.p, np, cbits, k,
-         ka, va);
+  launch(c, "sa_init_keys", np * 16.0, k_text_keys, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, cbits, k,
+         s.text.p, ka, va);
   const int init_bits = std::min(32, cbits * k);
   const bool a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
                                                  static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr),

@@ -61,6 +61,8 @@ def lib() -> C.CDLL:
         "itt_memcpy_h2d": ([vp, vp, vp, C.c_uint64], C.c_int),
         "itt_memcpy_d2h": ([vp, vp, vp, C.c_uint64], C.c_int),
         "itt_memcpy": ([vp, vp, vp, C.c_uint64], C.c_int),
+        "itt_compute_summary": ([vp, vp, C.c_uint64, C.c_int64, P(abi.itt_summary)], C.c_int),
+        "itt_render_details_csv": ([vp, vp, C.c_uint64, P(C.c_void_p), P(C.c_uint64)], C.c_int),
         "itt_host_register": ([vp, vp, C.c_uint64], C.c_int),
         "itt_host_unregister": ([vp, vp], C.c_int),
         "itt_ctx_synchronize": ([vp], C.c_int),
@@ -294,6 +296,27 @@ class Context:
                     first_token=out[i].first_token, epsilon_used=out[i].epsilon_used) for i in range(k)]
         lib().itt_free_patterns(self.h, out, k)
         return res
+
+    # ---------------------------------------------------------------- host finish (report.cu)
+    def compute_summary(self, rows: np.ndarray, iterations_declared: int):
+        """compute_summary (metrics.hpp:166-202) over analyze_raw rows ([n, 11] int64)."""
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        out = abi.itt_summary()
+        self._check(lib().itt_compute_summary(self.h, C.c_void_p(r.ctypes.data) if r.size else None, r.shape[0],
+                                              iterations_declared, C.byref(out)))
+        return out
+
+    def render_details_csv(self, rows: np.ndarray) -> str:
+        """details_to_csv (report.hpp:191-220) of analyze_raw rows, rendered natively."""
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        p = C.c_void_p()
+        n = C.c_uint64()
+        self._check(lib().itt_render_details_csv(self.h, C.c_void_p(r.ctypes.data) if r.size else None, r.shape[0],
+                                                 C.byref(p), C.byref(n)))
+        try:
+            return C.string_at(p, n.value).decode()
+        finally:
+            lib().itt_free(self.h, p)
 
     def mine_patterns_sa(self, tokens_ptr, n, term, sa_ptr, lcp_ptr, loops, multi=False):
         """mine_pattern(s) over a suffix array built elsewhere (device pointers: tokens[n],

@@ -94,7 +94,37 @@ class AnalysisResult:  # pipeline.hpp:27-30 (+ the rendered outputs)
         return render_summary(self)
 
     def details_csv(self, k: int = 0) -> str:
+        if isinstance(self.details, LazyDetails):
+            return self.details.csv(k)
         return details_to_csv(self.details[k])
+
+
+class LazyDetails:
+    """Per-loop IterationMetrics over the device's integer rows, built only when indexed; the CSV
+    is rendered natively from the rows (itt_render_details_csv) — at C5's 500K iterations an
+    interpreted finish would cost seconds."""
+
+    def __init__(self, ctx: Context, rows: list):
+        self._ctx = ctx
+        self._rows = rows
+        self._items = [None] * len(rows)
+
+    def __len__(self):
+        return len(self._rows)
+
+    def __getitem__(self, k):
+        if self._items[k] is None:
+            self._items[k] = rows_to_metrics(self._rows[k])
+        return self._items[k]
+
+    def __iter__(self):
+        return (self[k] for k in range(len(self)))
+
+    def rows(self, k):
+        return self._rows[k]
+
+    def csv(self, k):
+        return self._ctx.render_details_csv(self._rows[k])
 
 
 class AnalyzeError(Exception):
@@ -215,20 +245,26 @@ def analyze_trace(ctx: Context, recs, loops: list, epsilon0: int = 1, k0: Option
         name_of = names
     elif hasattr(recs, "name"):
         name_of = [recs.name(r).decode("utf-8", "surrogateescape") for r in raw["name_row"]]
-    loop_reports, details = [], []
+    loop_reports, rows = [], []
     for k, L in enumerate(raw["loops"]):
-        items = rows_to_metrics(L["rows"])
         ng, ni = L["clamps"]
         if ng > 0:
             warnings.append("NegativeGaps: %d negative dispatch gaps clamped to zero" % ng)
         if ni > 0:
             warnings.append("NegativeIntervals: %d negative iteration intervals clamped to zero" % ni)
-        summ = compute_summary(items, loops[k])
+        try:  # compute_summary natively, same accumulation order (report.cu)
+            n = ctx.compute_summary(L["rows"], loops[k])
+        except IttError as e:
+            raise AnalyzeError(e.kind, str(e)) from e
+        summ = SummaryMetrics(n.avg_interval_ns, n.max_interval_ns, n.avg_overlap, n.avg_operation_ns,
+                              n.avg_size_bytes, n.iterations_found, n.iterations_declared,
+                              bool(n.insufficient_intervals))
         pnames = [name_of[t] for t in L["pattern_tokens"]] if name_of is not None else [str(t) for t in L["pattern_tokens"]]
         loop_reports.append(LoopReport(loops[k], pnames, L["pattern_tokens"], L["pattern_length"], L["pattern_count"],
-                                       L["epsilon_used"], L["first_token"], L["k0_used"], len(items), summ,
+                                       L["epsilon_used"], L["first_token"], L["k0_used"], len(L["rows"]), summ,
                                        diagnose(summ, theta_copy, theta_cpu)))
-        details.append(items)
+        rows.append(L["rows"])
+    details = LazyDetails(ctx, rows)
     profiles = [OpProfile(L["op_cells"], L["op_totals"], L["iter_op_totals"], name_of) for L in raw["loops"]] \
         if op_profile else []
     return AnalysisResult(trace_label, epsilon0, theta_copy, theta_cpu, k0, main_stream, raw["streams"],
@@ -424,3 +460,30 @@ def details_to_csv(items: list) -> str:
 
 def _llround(x: float) -> int:  # std::llround: half away from zero
     return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
+
+
+def stream_table(streams) -> str:
+    """print_stream_table (itertrace_main.cpp:61-77): the per-stream census as the CLI prints it
+    (std::setw columns, right-aligned).  streams: (stream, class, counts[6], first, last)."""
+    out = ["  %7s%11s%9s%7s%7s%7s%8s%7s%15s%15s" % ("stream", "class", "kernel", "htod", "dtoh", "dtod", "memset",
+                                                    "other", "first_ns", "last_ns")]
+    for stream, cls, c, first, last in streams:
+        name = abi.CLASS_NAMES[cls] if 0 <= cls < len(abi.CLASS_NAMES) else "Assist"
+        out.append("  %7d%11s%9d%7d%7d%7d%8d%7d%15d%15d" % (stream, name, c[0], c[1], c[2], c[3], c[4], c[5], first, last))
+    return "\n".join(out) + "\n"
+
+
+def inspect_csv(ctx: Context, text: bytes, trace_path: str = "trace.csv") -> str:
+    """The CLI's `inspect` (run_inspect, itertrace_main.cpp:151-160) on the GPU: parse_trace_text
+    (itt_parse_csv) + summarize_streams / classify_streams over the whole trace (no device
+    filter, as there) on the device; returns the exact stdout text."""
+    try:
+        parsed = ctx.parse_csv(text, trace_path)
+    except IttError as e:
+        raise AnalyzeError(e.kind, str(e)) from e
+    try:
+        streams, _ = ctx.summarize_streams(parsed, filter_device=False)
+        return ("trace: %s\nrows: %d parsed, %d skipped of %d\n" % (trace_path, parsed.rows_parsed, parsed.rows_skipped,
+                                                                    parsed.rows_total)) + stream_table(streams)
+    finally:
+        parsed.free()

@@ -32,7 +32,11 @@ keys = {"duration_us": "gpu__time_duration.sum", "dram_read_MB": "dram__bytes_re
         "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active", "registers": "launch__registers_per_thread",
-        "l2_hit_pct": "lts__t_sector_hit_rate.pct", "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active"}
+        "l2_hit_pct": "lts__t_sector_hit_rate.pct", "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        # sector efficiency of global loads / stores (bytes used per 32-B sector moved, %): the
+        # random-access gathers' figure of merit
+        "ld_bytes_per_sector_pct": "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
+        "st_bytes_per_sector_pct": "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct"}
 names = {"k_onesweep": "radix_onesweep", "k_rank_update": "sa_rank_update", "k_hash_insert": "intern_hash", "k_plcp": "lcp_plcp", "k_compact_local": "compact",
          "k_ansv": "ansv_intervals", "k_scan": "compact"}
 per = collections.defaultdict(list)
@@ -52,10 +56,13 @@ summ = {"source": f"{tag}: ncu --set full --clock-control none --import-source o
         "kernels": {}}
 for nm, lst in per.items():
     avg = {k: sum(x[k] for x in lst) / len(lst) for k in keys if all(x[k] is not None for x in lst)}
+    avg.setdefault("dram_read_MB", 0.0)
+    avg.setdefault("dram_write_MB", 0.0)
     avg["dram_bytes_per_launch"] = (avg["dram_read_MB"] + avg["dram_write_MB"]) * 1e6
     avg["launches_profiled"] = len(lst)
     avg["top_stalls"] = lst[0]["top_stalls"]
     summ["kernels"][nm] = avg
 json.dump(summ, open("profiles/ncu_summary.json", "w"), indent=1)
 for k, v in summ["kernels"].items():
-    print(f"{k:24s} {v['duration_us']:7.1f}us dram {v['dram_bytes_per_launch']/1e6:6.1f}MB {v['dram_throughput_pct']:4.0f}% warps {v['warps_active_pct']:3.0f}% regs {v['registers']:.0f}")
+    print(f"{k:24s} {v.get('duration_us', 0):7.1f}us dram {v['dram_bytes_per_launch']/1e6:6.1f}MB warps {v.get('warps_active_pct', 0):3.0f}% "
+          f"ld-sector {v.get('ld_bytes_per_sector_pct', float('nan')):5.1f}% st-sector {v.get('st_bytes_per_sector_pct', float('nan')):5.1f}% L2hit {v.get('l2_hit_pct', 0):3.0f}%")
