@@ -37,6 +37,7 @@ int guarded(itt_ctx* ctx, F&& f) {
   try {
     ITT_CUDA(cudaSetDevice(c->device));
     c->arena_top = 0;  // the previous call synchronized: its small buffers are dead
+    c->upload_top = 0;  // ... and its pinned uploads have completed
     f(c);
     c->sync();
     c->last_error.clear();
@@ -86,11 +87,15 @@ void prepare(Ctx* c, TraceState& t, const itt_records* r, bool device_filter) {
   }
   {
     StageTimer st(c, "order");
-    order_records(t);
+    order_launch(t);  // the dictionary does not depend on the order: its verdict is read after it
   }
   {
     StageTimer st(c, "dictionary");
     build_dictionary(t);
+  }
+  {
+    StageTimer st(c, "order-finish");
+    order_finish(t);
   }
   if (!device_filter) {
     t.filtering = false;
@@ -194,6 +199,9 @@ int itt_ctx_destroy(itt_ctx* ctx) {
   for (auto& kv : c->out_live) cudaFreeHost(kv.first);  // outputs must be released before this
   for (auto& kv : c->out_free) cudaFreeHost(kv.second);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->deferred) cudaFreeHost(c->deferred);
+  if (c->deferred_ev) cudaEventDestroy(c->deferred_ev);
+  if (c->upload) cudaFreeHost(c->upload);
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamDestroy(c->copy_stream);

@@ -79,7 +79,12 @@ struct Ctx {
     return e;
   }
   // resolve event pairs after a stream synchronize
+  // ITT_TIMELINE=1 (with profiling on): idle time of the stream between consecutive profiled
+  // launches, booked as "gap:<previous>-><next>" (host round trips and launch latency)
+  cudaEvent_t tl_last = nullptr;
+  std::string tl_last_name;
   void resolve_profile() {
+    static const bool timeline = std::getenv("ITT_TIMELINE") != nullptr;
     for (auto& p : pending) {
       float ms = 0;
       ITT_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
@@ -87,8 +92,21 @@ struct Ctx {
       s.launches += 1;
       s.total_ms += ms;
       s.bytes += p.bytes;
+      if (timeline) {
+        if (tl_last) {
+          float g = 0;
+          ITT_CUDA(cudaEventElapsedTime(&g, tl_last, p.a));
+          KStat& gs = stats["gap:" + tl_last_name + "->" + p.name];
+          gs.launches += 1;
+          gs.total_ms += g;
+          event_pool.push_back(tl_last);
+        }
+        tl_last = p.b;
+        tl_last_name = p.name;
+      } else {
+        event_pool.push_back(p.b);
+      }
       event_pool.push_back(p.a);
-      event_pool.push_back(p.b);
     }
     pending.clear();
   }
@@ -182,6 +200,29 @@ struct Ctx {
   cudaStream_t copier() {
     if (!copy_stream) ITT_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     return copy_stream;
+  }
+  // a second small pinned block for reads whose result is only needed after a later sync
+  // (deferred_ev marks the copy): they must not share the staging buffer readback() reuses
+  void* deferred = nullptr;
+  cudaEvent_t deferred_ev = nullptr;
+  // pinned ring for small host->device uploads (h2d), bump-allocated per call
+  uint8_t* upload = nullptr;
+  size_t upload_top = 0;
+  static constexpr size_t kUploadBytes = 1u << 20;
+  void* upload_slot(size_t bytes) {
+    if (bytes > (64u << 10)) return nullptr;
+    if (!upload) ITT_CUDA(cudaMallocHost(reinterpret_cast<void**>(&upload), kUploadBytes));
+    const size_t at = (upload_top + 15) & ~static_cast<size_t>(15);
+    if (at + bytes > kUploadBytes) return nullptr;
+    upload_top = at + bytes;
+    return upload + at;
+  }
+  void* deferred_block() {
+    if (!deferred) {
+      ITT_CUDA(cudaMallocHost(&deferred, 4096));
+      ITT_CUDA(cudaEventCreateWithFlags(&deferred_ev, cudaEventDisableTiming));
+    }
+    return deferred;
   }
   void* staging(size_t bytes) {
     if (bytes > pinned_bytes) {
@@ -313,7 +354,16 @@ struct DBuf {
 
 template <typename T>
 inline void h2d(Ctx* c, T* dst, const T* src, size_t count) {
-  if (count) ITT_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  if (!count) return;
+  // small uploads go through the per-call pinned ring: a copy from pageable memory may wait for
+  // the stream (a hidden round trip); the ring is reset when the next call starts (the previous
+  // one synchronized), so a slot is never rewritten while its copy is pending
+  const size_t bytes = count * sizeof(T);
+  if (void* slot = c->upload_slot(bytes)) {
+    std::memcpy(slot, src, bytes);
+    src = static_cast<const T*>(slot);
+  }
+  ITT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
 }
 template <typename T>
 inline void d2h(Ctx* c, T* dst, const T* src, size_t count) {

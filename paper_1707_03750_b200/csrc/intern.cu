@@ -995,33 +995,52 @@ void release_rows(TraceState& t) {
   d.flags = nullptr, d.stream = nullptr, d.device = nullptr, d.name_off = nullptr, d.name_bytes = nullptr;
 }
 
-void order_records(TraceState& t) {
+// K1 in two halves around the dictionary (which does not depend on the order): the block sort and
+// its check are launched first, their 32-byte verdict is copied to pinned memory, and the host
+// reads it only after the dictionary's own readback — no round trip of its own.
+void order_launch(TraceState& t) {
   Ctx* c = t.c;
   const uint64_t n = t.rec.n;
   t.sorted = true;
+  t.order_pending = false;
   if (n <= 1 || t.rec.order == ITT_ORDER_SORTED) return;
   // fast path: sort 256-row blocks locally; if block ranges do not overlap the result is global
   const uint64_t nb = (n + kOrderBlock - 1) / kOrderBlock;
-  DBuf<unsigned long long> st(c, 4);  // min, max, descents, overlapping block boundaries
+  t.order_stats.alloc(c, 4);  // min, max, descents, overlapping block boundaries
   unsigned long long init[4] = {static_cast<unsigned long long>(LLONG_MAX), static_cast<unsigned long long>(LLONG_MIN), 0, 0};
-  h2d(c, st.p, init, 4);
-  DBuf<uint32_t> perm(c, n);
+  h2d(c, t.order_stats.p, init, 4);
+  t.perm.alloc(c, n);
   DBuf<int64_t> bmin(c, nb), bmax(c, nb);
   DBuf<uint8_t> bdesc(c, nb);
   launch(c, "order_blocks", n * 12.0, k_order_block_sort, dim3(static_cast<unsigned>(nb)), dim3(kOrderBlock), 0, t.rec.start, n,
-         perm.p, bmin.p, bmax.p, bdesc.p);
+         t.perm.p, bmin.p, bmax.p, bdesc.p);
   launch(c, "order_check", nb * 17.0, k_order_check, dim3(grid_for(nb, 256)), dim3(256), 0, bmin.p, bmax.p, bdesc.p, nb,
-         st.p);
+         t.order_stats.p);
+  ITT_CUDA(cudaMemcpyAsync(c->deferred_block(), t.order_stats.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+  ITT_CUDA(cudaEventRecord(c->deferred_ev, c->stream));
+  t.order_pending = true;
+}
+
+void order_finish(TraceState& t) {
+  if (!t.order_pending) return;
+  Ctx* c = t.c;
+  t.order_pending = false;
+  ITT_CUDA(cudaEventSynchronize(c->deferred_ev));  // normally long complete: the dictionary synchronized
   unsigned long long h[4];
-  readback(c, h, st.p, 4);
-  if (h[2] == 0) return;  // already in (start,row) order
+  std::memcpy(h, c->deferred, sizeof h);
+  t.order_stats.release();
+  const uint64_t n = t.rec.n;
+  if (h[2] == 0) {  // already in (start,row) order
+    t.perm.release();
+    return;
+  }
   t.sorted = false;
   if (h[3] == 0) {  // locally shuffled rows (the usual profiler export): the block sort is the order
-    t.perm = std::move(perm);
     t.perm_local = true;
     return;
   }
-  perm.release();
+  t.perm.release();
   const int64_t mn = static_cast<int64_t>(h[0]), mx = static_cast<int64_t>(h[1]);
   const int bits = bits_for(static_cast<uint64_t>(mx - mn));
   DBuf<uint64_t> k0(c, n), k1(c, n);
@@ -1030,6 +1049,11 @@ void order_records(TraceState& t) {
   // LSD radix sort is stable, so equal starts keep source-row order (ingest.hpp:396-400)
   const bool alt = radix_sort_pairs<uint64_t>(c, k0.p, v0.p, k1.p, v1.p, n, 0, bits, t.rs);
   t.perm = alt ? std::move(v1) : std::move(v0);
+}
+
+void order_records(TraceState& t) {
+  order_launch(t);
+  order_finish(t);
 }
 
 void build_dictionary(TraceState& t) {

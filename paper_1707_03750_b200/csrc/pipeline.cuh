@@ -45,6 +45,8 @@ struct TraceState {
   // ordering (K1)
   bool sorted = true;
   DBuf<uint32_t> perm;  // sorted position -> source row (only when !sorted)
+  DBuf<unsigned long long> order_stats;
+  bool order_pending = false;  // order_launch ran; order_finish has not read the verdict yet
   bool perm_local = false;  // perm only moves rows inside their 256-row block (the block-sort fast path)
   // name dictionary (K2)
   uint32_t table_bits = 0;
@@ -81,6 +83,8 @@ struct TraceState {
 
 void upload_records(Ctx* c, const itt_records* r, DevRecords& d);
 void order_records(TraceState& t);
+void order_launch(TraceState& t);  // order_records in two halves: launches + deferred verdict copy
+void order_finish(TraceState& t);  // reads the verdict (after a later sync), radix fallback if needed
 void build_dictionary(TraceState& t);          // hash + verify + classify + device census
 void stream_census(TraceState& t);             // summaries over the kept records (classified)
 void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index);

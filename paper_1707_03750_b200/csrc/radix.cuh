@@ -570,10 +570,21 @@ inline uint64_t tile_of(int cfg) { return static_cast<uint64_t>(kCfgBlock[cfg]) 
 //  * hist_in: precomputed per-pass histograms (passes*256) — skips the histogram kernel;
 //  * first_loader: produces the first pass's input instead of reading (keys, vals);
 //  * skip_trivial: read the histograms back and drop passes whose digit is constant.
+// Zero the look-back words of a later sort of n keys with up to `passes` passes now (e.g. while the
+// host waits on a readback anyway), so that sort can pass status_zeroed = true.
+inline void radix_prezero_status(Ctx* c, radix::Scratch& s, uint64_t n, int passes) {
+  const int cfg = radix::config_index();
+  const uint64_t tiles = (n + radix::tile_of(cfg) - 1) / radix::tile_of(cfg);
+  const size_t need = (tiles * radix::kBins + 1) * static_cast<size_t>(passes);
+  if (s.status.n < need) s.status.alloc(c, need);
+  ITT_CUDA(cudaMemsetAsync(s.status.p, 0, need * 4, c->stream));
+}
+
 template <typename K, typename FirstLoader = radix::ArrayLoader<K>>
 bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, uint64_t n, int begin_bit,
                       int end_bit, radix::Scratch& s, const uint32_t* hist_in = nullptr,
-                      const FirstLoader* first_loader = nullptr, bool skip_trivial = true) {
+                      const FirstLoader* first_loader = nullptr, bool skip_trivial = true,
+                      bool status_zeroed = false) {
   using namespace radix;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
   const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
@@ -608,8 +619,12 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
   if (first_loader && (live.empty() || live[0] != 0)) live.insert(live.begin(), 0);  // the loader must run
   if (live.empty()) return false;
   const size_t per_pass = tiles * kBins + 1;
-  if (s.status.n < per_pass * live.size()) s.status.alloc(c, per_pass * live.size());
-  ITT_CUDA(cudaMemsetAsync(s.status.p, 0, per_pass * live.size() * 4, c->stream));
+  if (status_zeroed) {  // the caller zeroed the look-back words ahead of time (prezero_status)
+    if (s.status.n < per_pass * live.size()) fail(ITT_E_INVALID_ARGUMENT, "internal: radix status not prepared");
+  } else {
+    if (s.status.n < per_pass * live.size()) s.status.alloc(c, per_pass * live.size());
+    ITT_CUDA(cudaMemsetAsync(s.status.p, 0, per_pass * live.size() * 4, c->stream));
+  }
   bool alt = false;
   for (size_t q = 0; q < live.size(); ++q) {
     const int p = live[q];

@@ -335,19 +335,44 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   uint32_t* f2 = a0 ? va : vb;
 
   const int max_passes = (bits_for(np - 1) + 7) / 8;
-  DBuf<uint32_t> hist(c, static_cast<size_t>(kMaxPasses) * 256);
   const uint64_t rtiles = (np + kRankBlock * kRankItems - 1) / (kRankBlock * kRankItems);
+  // two sets of per-round scratch (histograms of the next round's digits, look-back words): the
+  // set for round r+1 and the next sort's radix look-back words are zeroed right after round r's
+  // rank update is launched, so the only thing between its group-count readback and the next
+  // sort is the host itself
+  DBuf<uint32_t> hists[2];
+  for (auto& hb : hists) hb.alloc(c, static_cast<size_t>(kMaxPasses) * 256);
+  ScanScratch scan2;
+  ScanScratch* scans[2] = {&scan, &scan2};
+  int cur = 0;
+  hists[0].zero();
+  scans[0]->prepare(c, rtiles);
+  uint32_t* hist_p = nullptr;  // the histograms the latest rank update produced
   auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, const uint32_t* rank_old, uint32_t h,
-                         uint32_t* rank_new) -> uint64_t {
-    hist.zero();
-    scan.prepare(c, rtiles);
+                         uint32_t* rank_new, bool more) -> uint64_t {
+    ScanScratch& sc = *scans[cur];
+    hist_p = hists[cur].p;
     launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
-           dim3(kRankBlock), 0, kk, ss, rank_old, h, np, rank_new, hist.p, max_passes, scan.buf.p + 1,
-           reinterpret_cast<uint32_t*>(scan.buf.p));
-    return scan.total(c);  // group count G (synchronizes)
+           dim3(kRankBlock), 0, kk, ss, rank_old, h, np, rank_new, hist_p, max_passes, sc.buf.p + 1,
+           reinterpret_cast<uint32_t*>(sc.buf.p));
+    // group count G: the last tile's inclusive word, copied out and waited on by event, so the
+    // next round's scratch zeroing (queued after the copy) runs while the host wakes up
+    ++StageTimer::syncs();
+    uint64_t* word = static_cast<uint64_t*>(c->deferred_block()) + 8;  // [0, 64) holds the order verdict
+    ITT_CUDA(cudaMemcpyAsync(word, sc.buf.p + rtiles, 8, cudaMemcpyDeviceToHost, c->stream));
+    ITT_CUDA(cudaEventRecord(c->deferred_ev, c->stream));
+    if (more) {
+      hists[cur ^ 1].zero();
+      scans[cur ^ 1]->prepare(c, rtiles);
+      radix_prezero_status(c, rs, np, max_passes);
+    }
+    ITT_CUDA(cudaEventSynchronize(c->deferred_ev));
+    const uint64_t total = *word & kValMask;
+    cur ^= 1;
+    return total;
   };
   s.levels.emplace_back(c, np);
-  uint64_t g = rank_update(keys, sa, nullptr, 0, s.levels.back().p);
+  uint64_t g = rank_update(keys, sa, nullptr, 0, s.levels.back().p, s.h0 < cap);
   uint32_t h = s.h0;  // prefix length the newest level separates
   // stop when every suffix is alone, or when the groups already separate `cap` symbols (mining
   // never looks deeper than its L_max; see k_plcp for why the capped LCP stays exact below cap)
@@ -359,13 +384,14 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     // pass 1: loader(sa) -> (f1, f2); pass 2: (f1, f2) -> (kx, vx); pass 3: -> (f1, f2) ...
     uint32_t* kx = keys;  // the previous round's sorted keys are dead now
     uint32_t* vx = spare;
-    const bool alt = radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist.p, &ld, false);
+    const bool alt = radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist_p, &ld, false,
+                                                            /*status_zeroed=*/true);
     uint32_t* nkeys = alt ? f1 : kx;
     uint32_t* nsa = alt ? f2 : vx;
     uint32_t* other_k = alt ? kx : f1;
     uint32_t* other_v = alt ? vx : f2;
     s.levels.emplace_back(c, np);
-    g = rank_update(nkeys, nsa, rank, h, s.levels.back().p);
+    g = rank_update(nkeys, nsa, rank, h, s.levels.back().p, static_cast<uint64_t>(h) * 2 < cap);
     ++s.rounds;
     // rotate: new SA / keys; the old SA and the unused pair become free
     spare = sa;
