@@ -446,6 +446,23 @@ def main():
     roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "share_of_step": st["total_ms"] / tot, "launches_per_step": st["launches"] / args.profile_steps}
+    # the random-access kernels are judged on sector efficiency too: the committed
+    # ncu metrics pass of the same workload (scripts/sector_profile.sh)
+    sect = os.path.join(ROOT, "profiles", "r01g_sector_efficiency.csv")
+    kmap = {"sa_rank_update": "k_rank_update", "radix_onesweep": "k_onesweep", "lcp_plcp": "k_plcp", "lcp_phi": "k_phi",
+            "lcp_gather": "k_lcp_gather", "ansv_intervals": "k_ansv"}
+    if args.config == "C2" and os.path.exists(sect) and name in kmap:
+        for ln in open(sect):
+            f = ln.strip().split(",")
+            if f and f[0] == kmap[name]:
+                roofline["sector_efficiency"] = {"ld_bytes_per_sector_pct": float(f[5]), "st_bytes_per_sector_pct": float(f[6]),
+                                                 "l2_hit_pct": float(f[4]), "source": "profiles/r01g_sector_efficiency.csv"}
+    # the north star's radix-pass figure: 16 B per key-value pair per onesweep pass
+    if "radix_onesweep" in stats:
+        rs_ = stats["radix_onesweep"]
+        ra = rs_["bytes"] / (rs_["total_ms"] / 1000.0) / 1e9
+        roofline["radix_pass"] = {"achieved": ra, "frac": ra / peak, "passes_per_step": rs_["launches"] / args.profile_steps,
+                                  "us_per_pass": 1000.0 * rs_["total_ms"] / rs_["launches"]}
     kernel_table = {k: {"ms_per_step": v["total_ms"] / args.profile_steps,
                         "GBps": (v["bytes"] / (v["total_ms"] / 1000.0) / 1e9) if v["total_ms"] > 0 else None}
                     for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])}
