@@ -19,7 +19,7 @@ int itt::radix::config_index() {
   static int cfg = [] {
     const char* e = std::getenv("ITT_RADIX_CFG");
     const int v = e ? std::atoi(e) : 0;
-    return (v >= 0 && v < 13) ? v : 0;
+    return (v >= 0 && v < 10) ? v : 0;
   }();
   return cfg;
 }

@@ -37,7 +37,8 @@ constexpr int kChunk = 16;
 constexpr int kLiftAfter = 24;
 constexpr int kRankBlock = 256;
 constexpr int kRankItems = 8;  // smaller tiles, 8 CTAs per SM: more look-back chains and scatters in flight (A/B: 182 vs 197 us at 16)
-constexpr int kMaxPasses = 4;  // ids < 2^32
+constexpr int kMaxPasses = 4;   // ids < 2^32 in 8-bit digits
+constexpr uint32_t kWideGroups = 1u << (2 * radix::kWideBits);  // wide digits for up to 2 passes (G <= 2^20)
 
 __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int* out /*min,max,termhits*/) {
   int mn = INT_MAX, mx = INT_MIN, hits = 0;
@@ -91,16 +92,6 @@ struct EmitLoader {
     k = __ldg(&rank[i]);
     v = i;
   }
-  // bulk (TMA) staging: only the SA slice is copied; fix() turns SA_j into (rank[E_j], E_j)
-  static constexpr bool kBulkKeys = false;
-  __host__ __device__ const uint32_t* bulk_keys() const { return nullptr; }
-  __host__ __device__ const uint32_t* bulk_vals() const { return sa; }
-  __device__ __forceinline__ void fix(uint64_t, uint32_t& k, uint32_t& v) const {
-    const uint32_t x = v;
-    const uint32_t i = x >= h ? x - h : static_cast<uint32_t>(x + np - h);
-    k = __ldg(&rank[i]);
-    v = i;
-  }
 };
 
 // New dense ids.  flag_j = (key_j, r2_j) != (key_{j-1}, r2_{j-1}) with key = old id of SA_j (the
@@ -110,7 +101,8 @@ struct EmitLoader {
 __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
                                                             const uint32_t* __restrict__ rank_old, uint32_t h, uint64_t np,
                                                             uint32_t* __restrict__ rank_new, uint32_t* __restrict__ hist_next,
-                                                            int passes, uint64_t* status, uint32_t* counter) {
+                                                            int passes, uint32_t* __restrict__ gstart,
+                                                            uint64_t* status, uint32_t* counter) {
   __shared__ uint32_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_hist[kMaxPasses][256];
@@ -180,6 +172,8 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
     if (j < np) {
       const uint32_t id = pre + __popc(fmask & ((2u << q) - 1u)) - 1;
       rank_new[s_idx[q]] = id;
+      // group starts (SA position of each group's first suffix) for the wide-digit histograms
+      if (gstart && ((fmask >> q) & 1u) && id < kWideGroups) gstart[id] = static_cast<uint32_t>(j);
 #pragma unroll
       for (int p = 0; p < kMaxPasses; ++p) {
         if (p >= passes) break;
@@ -201,6 +195,25 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
     const uint32_t v = (&s_hist[0][0])[i];
     if (v) atomicAdd(&hist_next[i], v);
   }
+}
+
+// 10-bit digit histograms of the next round's keys from the group sizes: every suffix carries its
+// group's id, so digit d of pass p counts the suffixes of the groups whose id has digit d
+// (G <= kWideGroups groups, one thread each)
+__global__ void k_wide_hist(const uint32_t* __restrict__ gstart, uint64_t g, uint64_t np, int passes,
+                            uint32_t* __restrict__ hist) {
+  constexpr int kW = 1 << radix::kWideBits;
+  __shared__ uint32_t sh[2 * kW];
+  for (int i = threadIdx.x; i < passes * kW; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (uint64_t id = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; id < g;
+       id += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t size = static_cast<uint32_t>((id + 1 < g ? gstart[id + 1] : np) - gstart[id]);
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kW + ((id >> (radix::kWideBits * p)) & (kW - 1))], size);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kW; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
 // ---------------------------------------------------------------- LCP
@@ -335,13 +348,16 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   uint32_t* f2 = a0 ? va : vb;
 
   const int max_passes = (bits_for(np - 1) + 7) / 8;
+  constexpr size_t kWideBins = 1u << radix::kWideBits;
+  DBuf<uint32_t> gstart(c, std::min<uint64_t>(np, kWideGroups));
   const uint64_t rtiles = (np + kRankBlock * kRankItems - 1) / (kRankBlock * kRankItems);
   // two sets of per-round scratch (histograms of the next round's digits, look-back words): the
   // set for round r+1 and the next sort's radix look-back words are zeroed right after round r's
   // rank update is launched, so the only thing between its group-count readback and the next
   // sort is the host itself
-  DBuf<uint32_t> hists[2];
-  for (auto& hb : hists) hb.alloc(c, static_cast<size_t>(kMaxPasses) * 256);
+  DBuf<uint32_t> hists[2];  // [kMaxPasses * 256 (8-bit layout) | 2 * 1024 (10-bit layout, k_wide_hist)]
+  const size_t hist_words = static_cast<size_t>(kMaxPasses) * 256 + 2 * kWideBins;
+  for (auto& hb : hists) hb.alloc(c, hist_words);
   ScanScratch scan2;
   ScanScratch* scans[2] = {&scan, &scan2};
   int cur = 0;
@@ -353,7 +369,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     ScanScratch& sc = *scans[cur];
     hist_p = hists[cur].p;
     launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
-           dim3(kRankBlock), 0, kk, ss, rank_old, h, np, rank_new, hist_p, max_passes, sc.buf.p + 1,
+           dim3(kRankBlock), 0, kk, ss, rank_old, h, np, rank_new, hist_p, max_passes, gstart.p, sc.buf.p + 1,
            reinterpret_cast<uint32_t*>(sc.buf.p));
     // group count G: the last tile's inclusive word, copied out and waited on by event, so the
     // next round's scratch zeroing (queued after the copy) runs while the host wakes up
@@ -364,7 +380,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     if (more) {
       hists[cur ^ 1].zero();
       scans[cur ^ 1]->prepare(c, rtiles);
-      radix_prezero_status(c, rs, np, max_passes);
+      radix_prezero_status(c, rs, np, max_passes, 0);  // a wide sort zeroes its own (rare, larger)
     }
     ITT_CUDA(cudaEventSynchronize(c->deferred_ev));
     const uint64_t total = *word & kValMask;
@@ -384,8 +400,22 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     // pass 1: loader(sa) -> (f1, f2); pass 2: (f1, f2) -> (kx, vx); pass 3: -> (f1, f2) ...
     uint32_t* kx = keys;  // the previous round's sorted keys are dead now
     uint32_t* vx = spare;
-    const bool alt = radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist_p, &ld, false,
-                                                            /*status_zeroed=*/true);
+    // 10-bit digits when they save a pass (e.g. the 9-bit ids of a periodic trace: one pass, not two)
+    static const bool no_wide = [] {
+      const char* e = std::getenv("ITT_NO_WIDE_DIGITS");
+      return e && *e && *e != '0';
+    }();
+    const bool wide = !no_wide && g <= kWideGroups && (b + radix::kWideBits - 1) / radix::kWideBits < (b + 7) / 8;
+    uint32_t* whist = hist_p + kMaxPasses * 256;
+    if (wide) {
+      const int pw = (b + radix::kWideBits - 1) / radix::kWideBits;
+      launch(c, "sa_wide_hist", g * 8.0, k_wide_hist, dim3(grid_for(g, 256, c->sm_count * 4)), dim3(256), 0, gstart.p, g, np, pw,
+             whist);
+    }
+    const bool alt = wide ? radix_sort_pairs<uint32_t, EmitLoader, radix::kWideBits>(c, kx, vx, f1, f2, np, 0, b, rs, whist,
+                                                                                       &ld, false, false)
+                          : radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist_p, &ld, false,
+                                                                   /*status_zeroed=*/true);
     uint32_t* nkeys = alt ? f1 : kx;
     uint32_t* nsa = alt ? f2 : vx;
     uint32_t* other_k = alt ? kx : f1;
