@@ -24,7 +24,7 @@ namespace itt {
 namespace {
 
 constexpr int kHashBlock = 128;
-constexpr int kRepScratch = 128;  // per-lane staging of the slot representative's name
+constexpr int kRepScratch = 144;  // per-lane staging of the slot representative's name (any name <= 120 B at any alignment)
 constexpr int kWarpBuf = 4096;  // staged name bytes per warp
 constexpr uint32_t kDevSmem = 64;
 constexpr uint32_t kStreamTableCap = 4096;
@@ -288,6 +288,11 @@ __device__ __forceinline__ bool same_bytes(const SharedBytes& p, const SharedByt
   uint32_t i = 0;
   if (len >= 8) {
     SharedStream a(p), b(q);
+    for (; i + 12 <= len; i += 8) {  // 8 bytes and one branch per step
+      const uint32_t x0 = a.next4(), y0 = b.next4();
+      const uint32_t x1 = a.next4(), y1 = b.next4();
+      if ((x0 ^ y0) | (x1 ^ y1)) return false;
+    }
     for (; i + 8 <= len; i += 4)
       if (a.next4() != b.next4()) return false;
   }
