@@ -198,6 +198,7 @@ int itt_ctx_destroy(itt_ctx* ctx) {
   if (c->sync_event) cudaEventDestroy(c->sync_event);
   for (auto& kv : c->out_live) cudaFreeHost(kv.first);  // outputs must be released before this
   for (auto& kv : c->out_free) cudaFreeHost(kv.second);
+  for (auto& kv : c->big_cap) cudaFree(kv.first);  // cached large blocks (live ones are the caller's bug)
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->deferred) cudaFreeHost(c->deferred);
   if (c->deferred_ev) cudaEventDestroy(c->deferred_ev);
@@ -261,12 +262,16 @@ int itt_ctx_mem_stats(itt_ctx* ctx, uint64_t* used, uint64_t* used_high, int res
     ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, &u));
     ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemHigh, &h));
     ITT_CUDA(cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    // large blocks live outside the pool (Ctx::big_take): added to both figures
+    u += c->big_live;
+    h += c->big_high;
     if (std::getenv("ITT_TRACE")) std::fprintf(stderr, "[itt] pool used %.2f GB high %.2f GB reserved %.2f GB\n", u / 1e9, h / 1e9, r / 1e9);
     if (used) *used = u;
     if (used_high) *used_high = h;
     if (reset) {
       uint64_t z = 0;
       ITT_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrUsedMemHigh, &z));
+      c->big_high = c->big_live;
     }
   });
 }

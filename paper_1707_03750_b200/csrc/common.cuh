@@ -188,6 +188,50 @@ struct Ctx {
   static constexpr size_t kArenaBytes = 64ull << 20, kArenaMaxAlloc = 2ull << 20;
   uint8_t* arena = nullptr;
   size_t arena_top = 0;
+  // Large buffers (>= kBigBytes) bypass the stream-ordered pool: a per-context best-fit cache of
+  // cudaMalloc'd blocks.  Calls repeat the same sizes, so steady state allocates nothing; the
+  // pool, by contrast, fragments under mixed sizes and then maps fresh memory mid-call (measured:
+  // 6-25 ms stalls for 100-400 MB requests on C3).  Single stream per context: a block handed
+  // back is only reused by later work on the same stream, so stream order protects it.
+  static constexpr size_t kBigBytes = 16u << 20;
+  std::multimap<size_t, void*> big_free;  // capacity -> block
+  std::map<void*, size_t> big_cap;        // every cached block (live or free) -> capacity
+  size_t big_live = 0, big_high = 0;
+  void big_trim() {  // give every free cached block back to the driver (allocation pressure)
+    if (big_free.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto& kv : big_free) {
+      cudaFree(kv.second);
+      big_cap.erase(kv.second);
+    }
+    big_free.clear();
+  }
+  void* big_take(size_t bytes) {
+    auto it = big_free.lower_bound(bytes);
+    void* p = nullptr;
+    if (it != big_free.end() && it->first <= bytes + bytes / 4) {
+      p = it->second;
+      big_free.erase(it);
+    } else {
+      if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        big_trim();
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+          cudaGetLastError();
+          fail(ITT_E_CUDA, "cuda: out of device memory (" + std::to_string(bytes >> 20) + " MiB block)");
+        }
+      }
+      big_cap[p] = bytes;
+    }
+    big_live += big_cap[p];
+    big_high = std::max(big_high, big_live);
+    return p;
+  }
+  void big_give(void* p) {
+    const size_t cap = big_cap.at(p);
+    big_live -= cap;
+    big_free.emplace(cap, p);
+  }
   void* arena_take(size_t bytes) {
     bytes = (bytes + 255) & ~static_cast<size_t>(255);
     if (bytes > kArenaMaxAlloc) return nullptr;
@@ -294,16 +338,19 @@ struct DBuf {
   DBuf(Ctx* ctx, size_t count) { alloc(ctx, count); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : c(o.c), p(o.p), n(o.n), from_arena(o.from_arena) { o.p = nullptr, o.n = 0, o.from_arena = false; }
+  DBuf(DBuf&& o) noexcept : c(o.c), p(o.p), n(o.n), from_arena(o.from_arena), from_big(o.from_big) {
+    o.p = nullptr, o.n = 0, o.from_arena = false, o.from_big = false;
+  }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      c = o.c, p = o.p, n = o.n, from_arena = o.from_arena;
-      o.p = nullptr, o.n = 0, o.from_arena = false;
+      c = o.c, p = o.p, n = o.n, from_arena = o.from_arena, from_big = o.from_big;
+      o.p = nullptr, o.n = 0, o.from_arena = false, o.from_big = false;
     }
     return *this;
   }
   bool from_arena = false;
+  bool from_big = false;
   void alloc(Ctx* ctx, size_t count) {
     release();
     c = ctx;
@@ -312,10 +359,19 @@ struct DBuf {
       from_arena = true;
       return;
     }
+    if (count * sizeof(T) >= Ctx::kBigBytes) {
+      p = static_cast<T*>(ctx->big_take(count * sizeof(T)));
+      from_big = true;
+      return;
+    }
     if (count) {
       timespec a, b;
       clock_gettime(CLOCK_MONOTONIC, &a);
-      ITT_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->pool, ctx->stream));
+      if (cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->pool, ctx->stream) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->big_trim();  // cached large blocks back to the driver, then retry
+        ITT_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx->pool, ctx->stream));
+      }
       clock_gettime(CLOCK_MONOTONIC, &b);
       const double ms = (b.tv_sec - a.tv_sec) * 1e3 + (b.tv_nsec - a.tv_nsec) * 1e-6;
       if (ms > 5.0 && std::getenv("ITT_TRACE"))
@@ -327,6 +383,13 @@ struct DBuf {
       p = nullptr;
       n = 0;
       from_arena = false;
+      return;
+    }
+    if (p && from_big) {
+      c->big_give(p);
+      p = nullptr;
+      n = 0;
+      from_big = false;
       return;
     }
     if (p) {

@@ -729,7 +729,7 @@ struct CompactF {
 // range, so the tile stages stream / device / kind / slot / start / dur in shared memory with
 // coalesced loads and resolves the permutation there, instead of one scattered global gather
 // per column per record.  Same outputs as CompactF (one packed look-back scan).
-constexpr int kCompactBlock = 256, kCompactItems = 8, kCompactTile = kCompactBlock * kCompactItems;
+constexpr int kCompactBlock = 256, kCompactItems = 4, kCompactTile = kCompactBlock * kCompactItems;
 static_assert(kCompactTile % 256 == 0, "tiles must be whole order blocks");
 struct CompactLocalSmem {
   int64_t start[kCompactTile];
