@@ -73,13 +73,14 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool valid) {
   return peers;
 }
 
-// hist[p*256 + d] += count of keys with 8-bit digit d at pass p.  Each thread walks a contiguous
+// hist[p*2^RB + d] += count of keys with RB-bit digit d at pass p.  Each thread walks a contiguous
 // run of keys and issues one shared atomic per run of equal digits (skewed / structured keys are cheap).
-template <typename K>
+template <typename K, int RB = kRadixBits>
 __global__ void __launch_bounds__(256) k_hist(const K* __restrict__ keys, uint64_t n, int begin_bit, int passes,
                                               uint32_t* __restrict__ hist) {
-  extern __shared__ uint32_t sh[];  // passes * 256
-  for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) sh[i] = 0;
+  extern __shared__ uint32_t sh[];  // passes * 2^RB
+  constexpr int kD = 1 << RB;
+  for (int i = threadIdx.x; i < passes * kD; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   constexpr int kPer = 16;
   const uint64_t chunks = (n + kPer - 1) / kPer;
@@ -91,24 +92,24 @@ __global__ void __launch_bounds__(256) k_hist(const K* __restrict__ keys, uint64
 #pragma unroll
     for (int q = 0; q < kPer; ++q) kk[q] = q < cnt ? keys[i0 + q] : K(0);
     for (int p = 0; p < passes; ++p) {
-      const int sh_bits = begin_bit + p * kRadixBits;
-      uint32_t cur = digit_of<kRadixBits>(kk[0], sh_bits), len = 0;
+      const int sh_bits = begin_bit + p * RB;
+      uint32_t cur = digit_of<RB>(kk[0], sh_bits), len = 0;
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         if (q >= cnt) break;
-        const uint32_t d = digit_of<kRadixBits>(kk[q], sh_bits);
+        const uint32_t d = digit_of<RB>(kk[q], sh_bits);
         if (d != cur) {
-          atomicAdd(&sh[p * kBins + cur], len);
+          atomicAdd(&sh[p * kD + cur], len);
           cur = d;
           len = 0;
         }
         ++len;
       }
-      if (len) atomicAdd(&sh[p * kBins + cur], len);
+      if (len) atomicAdd(&sh[p * kD + cur], len);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x)
+  for (int i = threadIdx.x; i < passes * kD; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
@@ -356,8 +357,7 @@ inline void radix_prezero_status(Ctx* c, radix::Scratch& s, uint64_t n, int pass
 
 // Sort n (key, value) pairs on bits [begin_bit, end_bit) with RB-bit digits.  Double-buffered: the
 // result is in (keys, vals) when the return value is false, in (keys_alt, vals_alt) when true.
-//  * hist_in: precomputed per-pass histograms (passes * 2^RB) — skips the histogram kernel
-//    (required for RB != 8);
+//  * hist_in: precomputed per-pass histograms (passes * 2^RB) — skips the histogram kernel;
 //  * first_loader: produces the first pass's input instead of reading (keys, vals);
 //  * skip_trivial: read the histograms back and drop passes whose digit is constant.
 template <typename K, typename FirstLoader = radix::ArrayLoader<K>, int RB = radix::kRadixBits>
@@ -374,13 +374,14 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
   if (n == 0) return false;
   const uint32_t* hist = hist_in;
   if (!hist) {
-    if (RB != kRadixBits) fail(ITT_E_INVALID_ARGUMENT, "internal: wide radix digits need precomputed histograms");
     if (first_loader) fail(ITT_E_INVALID_ARGUMENT, "internal: a first-pass loader needs precomputed histograms");
-    if (s.hist.n < static_cast<size_t>(passes) * kBins) s.hist.alloc(c, static_cast<size_t>(passes) * kBins);
-    ITT_CUDA(cudaMemsetAsync(s.hist.p, 0, static_cast<size_t>(passes) * kBins * 4, c->stream));
+    if (s.hist.n < static_cast<size_t>(passes) * kD) s.hist.alloc(c, static_cast<size_t>(passes) * kD);
+    ITT_CUDA(cudaMemsetAsync(s.hist.p, 0, static_cast<size_t>(passes) * kD * 4, c->stream));
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(c->sm_count) * 8));
-    launch(c, "radix_hist", static_cast<double>(n) * sizeof(K), k_hist<K>, dim3(grid), dim3(256),
-           static_cast<size_t>(passes) * kBins * 4, keys, n, begin_bit, passes, s.hist.p);
+    auto kh = k_hist<K, RB>;
+    smem_optin(c, kh, static_cast<size_t>(passes) * kD * 4);
+    launch(c, "radix_hist", static_cast<double>(n) * sizeof(K), kh, dim3(grid), dim3(256), static_cast<size_t>(passes) * kD * 4,
+           keys, n, begin_bit, passes, s.hist.p);
     hist = s.hist.p;
   }
   std::vector<int> live;
