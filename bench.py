@@ -448,7 +448,7 @@ def main():
                 "share_of_step": st["total_ms"] / tot, "launches_per_step": st["launches"] / args.profile_steps}
     # the random-access kernels are judged on sector efficiency too: the committed
     # ncu metrics pass of the same workload (scripts/sector_profile.sh)
-    sect = os.path.join(ROOT, "profiles", "r01g_sector_efficiency.csv")
+    sect = os.path.join(ROOT, "profiles", "r01h_sector_efficiency.csv")
     kmap = {"sa_rank_update": "k_rank_update", "radix_onesweep": "k_onesweep", "lcp_plcp": "k_plcp", "lcp_phi": "k_phi",
             "lcp_gather": "k_lcp_gather", "ansv_intervals": "k_ansv"}
     if args.config == "C2" and os.path.exists(sect) and name in kmap:
@@ -456,7 +456,7 @@ def main():
             f = ln.strip().split(",")
             if f and f[0] == kmap[name]:
                 roofline["sector_efficiency"] = {"ld_bytes_per_sector_pct": float(f[5]), "st_bytes_per_sector_pct": float(f[6]),
-                                                 "l2_hit_pct": float(f[4]), "source": "profiles/r01g_sector_efficiency.csv"}
+                                                 "l2_hit_pct": float(f[4]), "source": "profiles/r01h_sector_efficiency.csv"}
     # the north star's radix-pass figure: 16 B per key-value pair per onesweep pass
     if "radix_onesweep" in stats:
         rs_ = stats["radix_onesweep"]

@@ -10,7 +10,7 @@ SHORT="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-inge
 if timeout 300 $SHORT > $O/short.log 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv $SHORT > $O/ncu_launch.log 2>&1
   timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_onesweep|k_rank_update|k_hash_insert|k_plcp|k_phi|k_lcp_gather|k_compact_local|k_ansv" -c 16 \
+    -k regex:"k_onesweep|k_rank_update|k_hash_insert|k_plcp|k_phi|k_lcp_gather|k_compact_local|k_ansv" -c 24 \
     -o $O/full $SHORT > $O/ncu_full.log 2>&1
   echo "ncu rc=$?"
 fi
