@@ -515,13 +515,32 @@ __global__ void k_name_bounds(const uint64_t* __restrict__ name_off, uint64_t n,
   if (c <= chunks) out[c] = name_off[min(c * rows_per_chunk, n)];
 }
 
+// kind per record and the smallest source row per slot.  Four consecutive rows per thread (one
+// 16-byte slot load, one 4-byte kind store); the representative check reads trep through L1
+// (ld.ca) — a stale value only costs a redundant atomicMin, which is the authority.
 __global__ void k_kinds_minrow(const uint32_t* __restrict__ slot, const uint8_t* __restrict__ rflags, uint64_t n,
-                               const uint8_t* __restrict__ tflags, uint8_t* __restrict__ kind, uint32_t* __restrict__ trep) {
+                               const uint8_t* __restrict__ tflags, uint8_t* __restrict__ kind, uint32_t* trep) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+  // the caller's flags column may sit at any byte address: quads only when it is 4-byte aligned
+  const uint64_t quads = (reinterpret_cast<uintptr_t>(rflags) & 3u) ? 0 : n / 4;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < quads; q += stride) {
+    const uint64_t i = q * 4;
+    const uint4 sl = __ldcs(reinterpret_cast<const uint4*>(slot) + q);
+    const uint32_t fl = __ldcs(reinterpret_cast<const uint32_t*>(rflags) + q);
+    const uint32_t s4[4] = {sl.x, sl.y, sl.z, sl.w};
+    uint32_t kd = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t s = s4[u];
+      kd |= static_cast<uint32_t>(kind_from(__ldg(&tflags[s]), ((fl >> (8 * u)) & ITT_REC_HAS_THROUGHPUT) != 0)) << (8 * u);
+      if (__ldca(&trep[s]) > i + u) atomicMin(&trep[s], static_cast<uint32_t>(i + u));
+    }
+    reinterpret_cast<uint32_t*>(kind)[q] = kd;
+  }
+  for (uint64_t i = quads * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t s = slot[i];
     kind[i] = static_cast<uint8_t>(kind_from(__ldg(&tflags[s]), (rflags[i] & ITT_REC_HAS_THROUGHPUT) != 0));
-    if (__ldcg(&trep[s]) > i) atomicMin(&trep[s], static_cast<uint32_t>(i));
+    if (__ldca(&trep[s]) > i) atomicMin(&trep[s], static_cast<uint32_t>(i));
   }
 }
 

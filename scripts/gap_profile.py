@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1707_03750_b200 import cuda, synth
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
-iters = {"C1": 100, "C2": 50_000, "C3": 20_000}[cfg]
+iters = {"C1": 100, "C2": 50_000, "C3": 20_000, "C4": 500}[cfg]
 ctx = cuda.Context(0)
 recs, info = synth.generate_config(cfg)
 d = ctx.upload(recs)
