@@ -145,11 +145,35 @@ __global__ void __launch_bounds__(kOrderBlock) k_order_block_sort(const int64_t*
   // descent in the source order: against the previous row of the block / of the previous block
   const long long prev = t > 0 ? s[t - 1] : (base > 0 ? start[base - 1] : LLONG_MIN);
   const int any_desc = __syncthreads_or(t < len && prev > a);
+  long long bmn = wmn[0], bmx = wmx[0];
+  for (int w = 1; w < kOrderBlock / 32; ++w) bmn = min(bmn, wmn[w]), bmx = max(bmx, wmx[w]);
   if (t == 0) {
-    for (int w = 0; w < kOrderBlock / 32; ++w) mn = min(mn, wmn[w]), mx = max(mx, wmx[w]);
-    bmin[blockIdx.x] = mn;
-    bmax[blockIdx.x] = mx;
+    bmin[blockIdx.x] = bmn;
+    bmax[blockIdx.x] = bmx;
     bdesc[blockIdx.x] = any_desc ? 1 : 0;
+  }
+  if (static_cast<unsigned long long>(bmx) - static_cast<unsigned long long>(bmn) < (1ull << 24)) {
+    // narrow block (the usual case: 256 consecutive records span far less than 16.7 ms): sort one
+    // 32-bit key (start - min) << 8 | row — one shuffle per stage instead of three, and the row
+    // in the low bits breaks ties exactly like (start, row); padding rows sort last
+    uint32_t key = t < len ? (static_cast<uint32_t>(a - bmn) << 8) | t : 0xFFFFFFFFu;
+    for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        uint32_t b;
+        if (j >= 32) {
+          __syncthreads();
+          r[t] = key;
+          __syncthreads();
+          b = r[t ^ j];
+        } else {
+          b = __shfl_xor_sync(0xffffffffu, key, j);
+        }
+        const bool lower = (t & j) == 0, ascending = (t & k) == 0;
+        if ((lower == ascending) == (key > b)) key = b;
+      }
+    }
+    if (t < len) perm[base + t] = static_cast<uint32_t>(base + (key & 0xFFu));
+    return;
   }
   for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
