@@ -239,6 +239,7 @@ def bench_batch(args, world, rank, local, workload):
                 "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
                 "config": {"workload": workload, "traces": args.traces, "distinct_traces": args.distinct,
                            "events_per_step": int(total_events), "workers_per_gpu": args.workers, "executor": args.batch_impl,
+                           "batched_suffix_arrays": args.batch_impl == "native",
                            "parallelism": f"shard{world}", "mined_ok": bool(ok)},
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)

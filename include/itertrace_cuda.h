@@ -391,7 +391,10 @@ int itt_free_parsed(itt_ctx* ctx, itt_parsed_trace* p);
 /* ------------------------------------------------------- L7 orchestration */
 /* itt_analyze_opts.flags: OP_PROFILE fills op_totals / iter_op_totals of every loop result;
  * OP_CELLS also returns the (iteration, op) cell grid (size ~ tokens: large) */
-enum { ITT_ANALYZE_OP_PROFILE = 1u, ITT_ANALYZE_OP_CELLS = 2u };
+enum { ITT_ANALYZE_OP_PROFILE = 1u, ITT_ANALYZE_OP_CELLS = 2u,
+       /* itt_batch_analyze only: the suffix arrays of the traces in flight are built together,
+        * one doubling sequence over their concatenation, instead of one per trace */
+       ITT_ANALYZE_BATCHED_SA = 4u };
 
 typedef struct itt_analyze_opts { /* AnalyzeOptions, pipeline.hpp:18-25 */
   const int64_t* loops;

@@ -156,6 +156,7 @@ class itt_analyze_opts(C.Structure):
 
 ITT_ANALYZE_OP_PROFILE = 1
 ITT_ANALYZE_OP_CELLS = 2
+ITT_ANALYZE_BATCHED_SA = 4  # itt_batch_analyze: suffix arrays of the traces in flight built together
 ITT_OP_PROFILE_AUTO, ITT_OP_PROFILE_SMEM, ITT_OP_PROFILE_SORT = 0, 1, 2
 
 

@@ -61,10 +61,12 @@ def summarize_c(a) -> dict:
     return out
 
 
-def run_shard_native(executor, traces: Sequence, loops: Sequence[int], lo: int, hi: int) -> list:
+def run_shard_native(executor, traces: Sequence, loops: Sequence[int], lo: int, hi: int, batched_sa: bool = True) -> list:
     """traces[lo:hi] through the native executor (cuda.Batch: C++ worker threads, one context
-    each) — the C4 hot path; same summaries as run_shard."""
-    return executor.analyze([traces[i] for i in range(lo, hi)], list(loops), summarize=summarize_c)
+    each) — the C4 hot path; same summaries as run_shard.  batched_sa: the suffix arrays of the
+    traces in flight are built in one doubling sequence (ITT_ANALYZE_BATCHED_SA)."""
+    return executor.analyze([traces[i] for i in range(lo, hi)], list(loops), summarize=summarize_c,
+                            batched_sa=batched_sa)
 
 
 def cuda_processor(device: int = 0) -> Callable:

@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <atomic>
 #include <new>
@@ -998,10 +1000,80 @@ int itt_free_parsed(itt_ctx* ctx, itt_parsed_trace* p) {
 }
 
 // ------------------------------------------------------------------ batch executor (C4)
+// Batched suffix arrays for the executor (ITT_ANALYZE_BATCHED_SA): every analyze in flight reaches
+// its suffix-array stage through itt_analyze_opts.sa_provider; when all of them are waiting there,
+// the last to arrive builds all their suffix arrays in one doubling sequence (build_batched_sa,
+// on its own context) and releases the others.  A trace that ends before that stage (an error)
+// leaves the wave, which may complete it.
+struct BatchSA {
+  struct Req {
+    const int32_t* tok;
+    uint64_t n;
+    int32_t term;
+    uint32_t cap;
+    uint32_t* sa;
+    uint32_t* lcp;
+    int status;
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  int active = 0;
+  bool running = false;
+  std::vector<Req*> pending;
+  uint64_t batches = 0, traces = 0;
+};
+static thread_local Ctx* tl_batch_ctx = nullptr;
+
+// run the pending wave if every trace in flight is waiting for it (caller holds the lock)
+static void batch_sa_maybe_run(BatchSA* b, std::unique_lock<std::mutex>& lk) {
+  while (!b->running && !b->pending.empty() && static_cast<int>(b->pending.size()) == b->active) {
+    b->running = true;
+    std::vector<BatchSA::Req*> reqs;
+    reqs.swap(b->pending);
+    lk.unlock();
+    int st = 0;
+    try {
+      Ctx* c = tl_batch_ctx;
+      if (!c) throw std::runtime_error("batched suffix array: no context on this thread");
+      std::vector<BatchSAItem> items;
+      int32_t vmax = 0;
+      uint32_t cap = 1;
+      for (auto* r : reqs) {
+        items.push_back(BatchSAItem{r->tok, r->n, r->sa, r->lcp});
+        vmax = std::max(vmax, r->term);
+        cap = std::max(cap, r->cap);
+      }
+      radix::Scratch rs;
+      ScanScratch sc;
+      build_batched_sa(c, items, vmax, cap, rs, sc);
+    } catch (const std::exception& e) {
+      st = 1;
+      if (tl_batch_ctx) tl_batch_ctx->last_error = e.what();
+    }
+    lk.lock();
+    for (auto* r : reqs) r->status = st;
+    ++b->batches;
+    b->traces += reqs.size();
+    b->running = false;
+    b->cv.notify_all();
+  }
+}
+
+static int batch_sa_provider(void* user, const int32_t* tok, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa, uint32_t* lcp) {
+  BatchSA* b = static_cast<BatchSA*>(user);
+  BatchSA::Req r{tok, n, term, cap, sa, lcp, -1};
+  std::unique_lock<std::mutex> lk(b->mu);
+  b->pending.push_back(&r);
+  batch_sa_maybe_run(b, lk);
+  b->cv.wait(lk, [&] { return r.status >= 0; });
+  return r.status;
+}
+
 struct itt_batch {
   int device = 0;
   std::vector<itt_ctx*> ctx;
   std::vector<std::string> errors;
+  BatchSA sa;
 };
 
 int itt_batch_create(int device, uint32_t workers, itt_batch** out) {
@@ -1037,13 +1109,32 @@ int itt_batch_analyze(itt_batch* b, const itt_records* traces, uint64_t n, const
   if (!b || (n && (!traces || !opts || !out || !status))) return ITT_E_INVALID_ARGUMENT;
   b->errors.assign(n, std::string());
   std::atomic<uint64_t> next{0};
+  static const int seg_env = [] {  // ITT_BATCH_SEGMENTED=0/1 overrides the flag (A/B runs)
+    const char* e = std::getenv("ITT_BATCH_SEGMENTED");
+    return e && *e ? (*e != '0' ? 1 : 0) : -1;
+  }();
   auto work = [&](itt_ctx* c) {
     cudaSetDevice(b->device);
+    tl_batch_ctx = &c->c;
     for (uint64_t i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
       out[i] = nullptr;
-      status[i] = itt_analyze(c, &traces[i], opts_per_trace ? &opts[i] : opts, &out[i]);
+      itt_analyze_opts o = opts_per_trace ? opts[i] : *opts;
+      const bool batched = (seg_env >= 0 ? seg_env == 1 : (o.flags & ITT_ANALYZE_BATCHED_SA) != 0) && !o.sa_provider;
+      if (batched) {
+        o.sa_provider = batch_sa_provider;
+        o.sa_user = &b->sa;
+        std::lock_guard<std::mutex> lk(b->sa.mu);
+        ++b->sa.active;
+      }
+      status[i] = itt_analyze(c, &traces[i], &o, &out[i]);
       if (status[i] != ITT_OK) b->errors[i] = itt_last_error(c);
+      if (batched) {  // leaving the wave may complete it (a trace that failed before its SA stage)
+        std::unique_lock<std::mutex> lk(b->sa.mu);
+        --b->sa.active;
+        batch_sa_maybe_run(&b->sa, lk);
+      }
     }
+    tl_batch_ctx = nullptr;
   };
   std::vector<std::thread> th;
   for (size_t w = 1; w < b->ctx.size(); ++w) th.emplace_back(work, b->ctx[w]);

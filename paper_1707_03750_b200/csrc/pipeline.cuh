@@ -113,6 +113,17 @@ struct SuffixState {
 void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
                         radix::Scratch& rs, ScanScratch& scan, uint32_t cap = 0xFFFFFFFFu, bool known_alphabet = false);
 
+// Many traces' suffix arrays in one doubling sequence (batched analyze, C4): tokens device
+// int32[n] with ids < vmax; sa / lcp device [n + 1] outputs; LCP capped at cap (>= every L_max+1).
+struct BatchSAItem {
+  const int32_t* tokens;
+  uint64_t n;
+  uint32_t* sa;
+  uint32_t* lcp;
+};
+void build_batched_sa(Ctx* c, const std::vector<BatchSAItem>& items, int32_t vmax, uint32_t cap, radix::Scratch& rs,
+                      ScanScratch& scan);
+
 // ------------------------------------------------------------------ mining (mine.cu)
 struct IntervalState {
   DBuf<uint32_t> cnt;  // count of the interval represented at k (0 = not a representative)

@@ -297,6 +297,56 @@ __global__ void k_lcp_gather(const uint32_t* __restrict__ sa, const uint32_t* __
   if (j < np) lcp[j] = j == 0 ? 0u : plcp[sa[j]];
 }
 
+// ---------------------------------------------------------------- batched suffix arrays (C4)
+struct BatchDevItem {
+  const int32_t* tok;
+  uint64_t n;
+  uint64_t start;  // first position of this trace in the concatenated text
+  uint32_t* sa;    // [n + 1] outputs
+  uint32_t* lcp;
+};
+
+// concatenated text: trace t's tokens, then its separator vmax + t (unique, above every token)
+__global__ void k_batch_concat(const BatchDevItem* __restrict__ items, int32_t vmax, int32_t* __restrict__ text) {
+  const BatchDevItem it = items[blockIdx.y];
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= it.n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    text[it.start + i] = i < it.n ? __ldg(&it.tok[i]) : vmax + static_cast<int32_t>(blockIdx.y);
+}
+
+// trace of each suffix in SA order (for the stable partition by trace)
+__global__ void k_batch_trace_of(const uint32_t* __restrict__ sa, uint64_t np, const uint64_t* __restrict__ starts, uint32_t nb,
+                                 uint32_t* __restrict__ tid, uint32_t* __restrict__ val) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= np) return;
+  const uint32_t p = sa[j];
+  uint32_t lo = 0, hi = nb;  // largest t with starts[t] <= p
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (starts[mid] <= p) lo = mid;
+    else hi = mid;
+  }
+  tid[j] = lo;
+  val[j] = p;
+}
+
+// the first suffix of every trace slice has no predecessor of its own trace
+__global__ void k_batch_phi_heads(const uint32_t* __restrict__ sa, const uint64_t* __restrict__ starts, uint32_t nb,
+                                  uint32_t* __restrict__ phi) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nb) phi[sa[starts[t]]] = kNone;
+}
+
+__global__ void k_batch_out(const BatchDevItem* __restrict__ items, const uint32_t* __restrict__ sa,
+                            const uint32_t* __restrict__ lcp) {
+  const BatchDevItem it = items[blockIdx.y];
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k <= it.n;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    it.sa[k] = sa[it.start + k] - static_cast<uint32_t>(it.start);
+    it.lcp[k] = lcp[it.start + k];
+  }
+}
+
 }  // namespace
 
 void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, SuffixState& s, bool want_lcp,
@@ -452,6 +502,68 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   s.lcp.alloc(c, np);
   launch(c, "lcp_gather", np * 12.0, k_lcp_gather, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, plcp.p, np, s.lcp.p);
   // dlv is released stream-ordered (or lives in the call's arena): no host wait needed
+}
+
+}  // namespace itt
+
+namespace itt {
+
+// Suffix arrays + capped LCP of many traces in one doubling sequence (one sort per
+// round for all resident traces).  The traces are concatenated with distinct separators vmax + t
+// above every token, so each trace's suffixes keep their own relative order (a comparison
+// within trace t is decided at the latest by its unique separator, exactly as by its own
+// terminator) and LCPs of two suffixes of one trace stop at it.  A stable partition of the
+// global suffix array by trace gives every trace its own slice; LCP runs on the partitioned
+// array with each slice's head cut off.  cap >= every trace's L_max + 1 (a larger cap than a
+// trace needs only makes its LCP more exact: mining is unchanged).
+void build_batched_sa(Ctx* c, const std::vector<BatchSAItem>& items, int32_t vmax, uint32_t cap, radix::Scratch& rs,
+                      ScanScratch& scan) {
+  const uint32_t nb = static_cast<uint32_t>(items.size());
+  if (nb == 0) return;
+  std::vector<BatchDevItem> host(nb);
+  std::vector<uint64_t> starts(nb + 1, 0);
+  uint64_t maxn = 0;
+  for (uint32_t t = 0; t < nb; ++t) {
+    host[t] = BatchDevItem{items[t].tokens, items[t].n, starts[t], items[t].sa, items[t].lcp};
+    starts[t + 1] = starts[t] + items[t].n + 1;
+    maxn = std::max(maxn, items[t].n + 1);
+  }
+  const uint64_t np = starts[nb];
+  if (np >= 0xFFFFFFFFull) fail(ITT_E_INVALID_ARGUMENT, "pattern-mining: batch too long for 32-bit suffix indices");
+  DBuf<BatchDevItem> ditems(c, nb);
+  h2d(c, ditems.p, host.data(), nb);
+  DBuf<uint64_t> dstarts(c, nb + 1);
+  h2d(c, dstarts.p, starts.data(), nb + 1);
+  DBuf<int32_t> text(c, np);
+  const dim3 g2(std::min<unsigned>(grid_for(maxn, 256), 64), nb);
+  launch(c, "sa_batch_concat", np * 8.0, k_batch_concat, g2, dim3(256), 0, ditems.p, vmax, text.p);
+  // the last separator is the global terminator
+  SuffixState s;
+  build_suffix_array(c, text.p, np - 1, vmax + static_cast<int32_t>(nb) - 1, s, false, rs, scan, cap, true);
+  text.release();
+  // per-trace slices: stable partition of the suffix array by trace
+  DBuf<uint32_t> k0(c, np), v0(c, np), k1(c, np), v1(c, np);
+  launch(c, "sa_batch_trace", np * 12.0, k_batch_trace_of, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, np, dstarts.p, nb,
+         k0.p, v0.p);
+  const bool alt = radix_sort_pairs<uint32_t>(c, k0.p, v0.p, k1.p, v1.p, np, 0, bits_for(nb > 1 ? nb - 1 : 1), rs, nullptr,
+                                              static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), false);
+  ITT_CUDA(cudaMemcpyAsync(s.sa.p, alt ? v1.p : v0.p, np * 4, cudaMemcpyDeviceToDevice, c->stream));
+  k0.release(), v0.release(), k1.release(), v1.release();
+  // LCP over the partitioned array (sa.cu's phi / capped Kasai / gather), slice heads cut off
+  DBuf<uint32_t> phi(c, np), plcp(c, np);
+  launch(c, "lcp_phi", np * 12.0, k_phi, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, np, phi.p);
+  launch(c, "sa_batch_heads", nb * 8.0, k_batch_phi_heads, dim3(grid_for(nb, 256)), dim3(256), 0, s.sa.p, dstarts.p, nb, phi.p);
+  std::vector<const uint32_t*> lv;
+  for (auto& d : s.levels) lv.push_back(d.p);
+  DBuf<const uint32_t*> dlv(c, lv.size());
+  h2d(c, dlv.p, lv.data(), lv.size());
+  LiftArgs L{s.text.p, np, dlv.p, static_cast<int>(lv.size()), s.h0};
+  const uint64_t chunks = (np + kChunk - 1) / kChunk;
+  launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p, s.cap);
+  s.lcp.alloc(c, np);
+  launch(c, "lcp_gather", np * 12.0, k_lcp_gather, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, plcp.p, np, s.lcp.p);
+  launch(c, "sa_batch_out", np * 16.0, k_batch_out, g2, dim3(256), 0, ditems.p, s.sa.p, s.lcp.p);
+  c->sync();  // the outputs belong to other contexts' calls: complete before they resume
 }
 
 }  // namespace itt

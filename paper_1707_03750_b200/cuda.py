@@ -560,14 +560,16 @@ class Batch:
         lib().itt_batch_launch_count(self.h, C.byref(v))
         return v.value
 
-    def analyze(self, traces, loops, epsilon0=1, k0=-1, main_stream=-1, summarize=None):
+    def analyze(self, traces, loops, epsilon0=1, k0=-1, main_stream=-1, summarize=None, batched_sa=False):
         """Analyze every trace (abi.Records or DeviceRecords); returns per-trace results:
         summarize(itt_analysis) if given (read while the analyses are alive), else
-        (status, pattern_length, pattern_count, iterations) of loop 0; errors as IttError."""
+        (status, pattern_length, pattern_count, iterations) of loop 0; errors as IttError.
+        batched_sa: the suffix arrays of the traces in flight are built in one doubling sequence."""
         n = len(traces)
         recs = (abi.itt_records * max(1, n))(*[t.c() for t in traces])
         lp = (C.c_int64 * max(1, len(loops)))(*loops)
-        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream, 0)
+        opts = abi.itt_analyze_opts(lp, len(loops), epsilon0, k0, main_stream,
+                                    abi.ITT_ANALYZE_BATCHED_SA if batched_sa else 0)
         out = (P(abi.itt_analysis) * max(1, n))()
         st = (C.c_int * max(1, n))()
         rc = lib().itt_batch_analyze(self.h, recs, n, C.byref(opts), 0, out, st)
