@@ -1035,17 +1035,26 @@ static void batch_sa_maybe_run(BatchSA* b, std::unique_lock<std::mutex>& lk) {
     try {
       Ctx* c = tl_batch_ctx;
       if (!c) throw std::runtime_error("batched suffix array: no context on this thread");
-      std::vector<BatchSAItem> items;
-      int32_t vmax = 0;
-      uint32_t cap = 1;
-      for (auto* r : reqs) {
-        items.push_back(BatchSAItem{r->tok, r->n, r->sa, r->lcp});
-        vmax = std::max(vmax, r->term);
-        cap = std::max(cap, r->cap);
+      // one doubling sequence per group of at most kBatchTokens suffixes (bounds 32-bit suffix
+      // indices and the wave's HBM: ~60 B per suffix while the sequence runs)
+      constexpr uint64_t kBatchTokens = 1ull << 28;
+      size_t at = 0;
+      while (at < reqs.size()) {
+        std::vector<BatchSAItem> items;
+        int32_t vmax = 0;
+        uint32_t cap = 1;
+        uint64_t total = 0;
+        while (at < reqs.size() && (items.empty() || total + reqs[at]->n + 1 <= kBatchTokens)) {
+          const auto* r = reqs[at++];
+          items.push_back(BatchSAItem{r->tok, r->n, r->sa, r->lcp});
+          vmax = std::max(vmax, r->term);
+          cap = std::max(cap, r->cap);
+          total += r->n + 1;
+        }
+        radix::Scratch rs;
+        ScanScratch sc;
+        build_batched_sa(c, items, vmax, cap, rs, sc);
       }
-      radix::Scratch rs;
-      ScanScratch sc;
-      build_batched_sa(c, items, vmax, cap, rs, sc);
     } catch (const std::exception& e) {
       st = 1;
       if (tl_batch_ctx) tl_batch_ctx->last_error = e.what();
