@@ -119,6 +119,17 @@ def test_row_order_fast_path_and_fallback(ctx, R):
     rng.shuffle(glob)
     variants["global"] = glob
     variants["ties"] = np.repeat(np.arange(n // 500), 500)[::-1].copy()
+    # blocks spanning >= 2^24 ns take the 64-bit-key bitonic path, narrow ones the packed 32-bit
+    # key: wide and mixed spans (incl. negative starts), locally shuffled
+    wide = np.sort(rng.integers(-(1 << 40), 1 << 40, n))
+    mixed = np.sort(np.concatenate([rng.integers(0, 3000, n // 2), rng.integers(1 << 30, 1 << 36, n - n // 2)]))
+    for nm, arr in (("wide_local", wide), ("mixed_local", mixed)):
+        v = arr.copy()
+        for b in range(0, n, 64):
+            seg = v[b:b + 64].copy()
+            rng.shuffle(seg)
+            v[b:b + 64] = seg
+        variants[nm] = v
     for name, starts in variants.items():
         ops = [(13 if i % 3 else 14, "op%d" % (i % 17) if i % 3 else "[CUDA memcpy HtoD]", int(s), 3, 64, 1e9)
                for i, s in enumerate(starts)]
