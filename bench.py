@@ -459,11 +459,12 @@ def main():
                 roofline["sector_efficiency"] = {"ld_bytes_per_sector_pct": float(f[5]), "st_bytes_per_sector_pct": float(f[6]),
                                                  "l2_hit_pct": float(f[4]), "source": "profiles/r01h_sector_efficiency.csv"}
     # the north star's radix-pass figure: 16 B per key-value pair per onesweep pass
-    if "radix_onesweep" in stats:
-        rs_ = stats["radix_onesweep"]
-        ra = rs_["bytes"] / (rs_["total_ms"] / 1000.0) / 1e9
-        roofline["radix_pass"] = {"achieved": ra, "frac": ra / peak, "passes_per_step": rs_["launches"] / args.profile_steps,
-                                  "us_per_pass": 1000.0 * rs_["total_ms"] / rs_["launches"]}
+    passes = [stats[k] for k in ("radix_onesweep", "radix_onesweep_w10") if k in stats]  # 8- and 10-bit digits
+    if passes:
+        pb, pms, pl = sum(x["bytes"] for x in passes), sum(x["total_ms"] for x in passes), sum(x["launches"] for x in passes)
+        ra = pb / (pms / 1000.0) / 1e9
+        roofline["radix_pass"] = {"achieved": ra, "frac": ra / peak, "passes_per_step": pl / args.profile_steps,
+                                  "us_per_pass": 1000.0 * pms / pl}
     kernel_table = {k: {"ms_per_step": v["total_ms"] / args.profile_steps,
                         "GBps": (v["bytes"] / (v["total_ms"] / 1000.0) / 1e9) if v["total_ms"] > 0 else None}
                     for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])}
