@@ -282,7 +282,12 @@ void sort(Ctx* c, uint64_t* a, uint32_t* b, uint64_t cnt, int bits) {
   DBuf<uint64_t> a1(c, cnt);
   DBuf<uint32_t> b1(c, cnt);
   radix::Scratch rs;
-  const bool alt = radix_sort_pairs<uint64_t>(c, a, b, a1.p, b1.p, cnt, 0, std::max(1, bits), rs);
+  bits = std::max(1, bits);
+  // 10-bit digits when they save a pass (e.g. 42-bit pair keys: 5 passes instead of 6)
+  const bool wide = (bits + radix::kWideBits - 1) / radix::kWideBits < (bits + 7) / 8;
+  const bool alt = wide ? radix_sort_pairs<uint64_t, radix::ArrayLoader<uint64_t>, radix::kWideBits>(c, a, b, a1.p, b1.p, cnt, 0,
+                                                                                                      bits, rs)
+                        : radix_sort_pairs<uint64_t>(c, a, b, a1.p, b1.p, cnt, 0, bits, rs);
   if (alt) {
     ITT_CUDA(cudaMemcpyAsync(a, a1.p, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
     ITT_CUDA(cudaMemcpyAsync(b, b1.p, cnt * 4, cudaMemcpyDeviceToDevice, c->stream));
