@@ -40,6 +40,20 @@ constexpr int kRankItems = 8;  // smaller tiles, 8 CTAs per SM: more look-back c
 constexpr int kMaxPasses = 4;   // ids < 2^32 in 8-bit digits
 constexpr uint32_t kWideGroups = 1u << (2 * radix::kWideBits);  // wide digits for up to 2 passes (G <= 2^20)
 
+// Rank levels are u32, or u16 while the group count allows (periodic traces keep it small): half
+// the bytes for the random scatter of the rank update and the gathers that read it back.  A level
+// is passed as a tagged address: bit 0 set = u16 (device allocations are 256-B aligned).
+constexpr uint64_t kNarrowGroups = 1u << 16;     // ids of a u16 level
+constexpr uint64_t kNarrowTry = 1u << 14;        // try u16 for the next level while G <= this
+__device__ __forceinline__ uint32_t rank_at(uintptr_t lv, uint64_t i) {
+  return (lv & 1u) ? static_cast<uint32_t>(__ldg(reinterpret_cast<const uint16_t*>(lv - 1) + i))
+                   : __ldg(reinterpret_cast<const uint32_t*>(lv) + i);
+}
+__device__ __forceinline__ void rank_put(uintptr_t lv, uint64_t i, uint32_t v) {
+  if (lv & 1u) reinterpret_cast<uint16_t*>(lv - 1)[i] = static_cast<uint16_t>(v);
+  else reinterpret_cast<uint32_t*>(lv)[i] = v;
+}
+
 __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int* out /*min,max,termhits*/) {
   int mn = INT_MAX, mx = INT_MIN, hits = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -83,13 +97,13 @@ __global__ void k_text_keys(const int32_t* __restrict__ tok, uint64_t n, int32_t
 // first radix pass input of a doubling round: E_j and its key rank_{E_j}
 struct EmitLoader {
   const uint32_t* sa;
-  const uint32_t* rank;
+  uintptr_t rank;  // tagged level (rank_at)
   uint64_t np;
   uint32_t h;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t& k, uint32_t& v) const {
     const uint32_t x = __ldcs(&sa[j]);
     const uint32_t i = x >= h ? x - h : static_cast<uint32_t>(x + np - h);
-    k = __ldg(&rank[i]);
+    k = rank_at(rank, i);
     v = i;
   }
 };
@@ -99,8 +113,8 @@ struct EmitLoader {
 // rank_old is null in the init round).  id_j = inclusive count of flags - 1 (decoupled look-back
 // sum scan); rank_new[SA_j] = id_j; hist_next[p][digit_p(id_j)] += 1.
 __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
-                                                            const uint32_t* __restrict__ rank_old, uint32_t h, uint64_t np,
-                                                            uint32_t* __restrict__ rank_new, uint32_t* __restrict__ hist_next,
+                                                            uintptr_t rank_old, uint32_t h, uint64_t np,
+                                                            uintptr_t rank_new, uint32_t* __restrict__ hist_next,
                                                             int passes, uint32_t* __restrict__ gstart,
                                                             uint64_t* status, uint32_t* counter) {
   __shared__ uint32_t s_warp[kRankBlock / 32];
@@ -114,7 +128,7 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
   auto second = [&](uint32_t x) -> uint32_t {
     if (!rank_old) return 0u;
     const uint64_t y = static_cast<uint64_t>(x) + h;
-    return y < np ? __ldg(&rank_old[y]) : kNone;
+    return y < np ? rank_at(rank_old, y) : kNone;
   };
   // phase 1: this thread's SA entries and sorted keys (16-byte loads when the run is whole)
   uint32_t s_idx[kRankItems], kv[kRankItems], r2[kRankItems];
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
     const uint64_t j = base + q;
     if (j < np) {
       const uint32_t id = pre + __popc(fmask & ((2u << q) - 1u)) - 1;
-      rank_new[s_idx[q]] = id;
+      rank_put(rank_new, s_idx[q], id);  // ids beyond a u16 level are caught by the host (G > 2^16)
       // group starts (SA position of each group's first suffix) for the wide-digit histograms
       if (gstart && ((fmask >> q) & 1u) && id < kWideGroups) gstart[id] = static_cast<uint32_t>(j);
 #pragma unroll
@@ -225,7 +239,7 @@ __global__ void k_phi(const uint32_t* __restrict__ sa, uint64_t np, uint32_t* __
 struct LiftArgs {
   const int32_t* text;
   uint64_t np;
-  const uint32_t* const* levels;  // device array of level pointers
+  const uintptr_t* levels;  // device array of tagged level addresses (rank_at)
   int nlev;
   uint32_t h0;
 };
@@ -234,8 +248,8 @@ struct LiftArgs {
 __device__ __forceinline__ uint32_t lcp_lift(const LiftArgs& L, uint64_t a, uint64_t b) {
   uint32_t acc = 0;
   for (int r = L.nlev - 1; r >= 0; --r) {
-    const uint32_t* lv = L.levels[r];
-    if (a < L.np && b < L.np && __ldg(&lv[a]) == __ldg(&lv[b])) {
+    const uintptr_t lv = L.levels[r];
+    if (a < L.np && b < L.np && rank_at(lv, a) == rank_at(lv, b)) {
       const uint32_t hr = L.h0 << r;
       a += hr;
       b += hr;
@@ -258,7 +272,7 @@ __global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* _
   const uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kChunk;
   if (i0 >= L.np) return;
   const uint64_t i1 = min(i0 + kChunk, L.np);
-  const uint32_t* top = L.levels[L.nlev - 1];
+  const uintptr_t top = L.levels[L.nlev - 1];
   uint32_t l = 0;
   bool capped = false;
   for (uint64_t i = i0; i < i1; ++i) {
@@ -269,7 +283,7 @@ __global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* _
       capped = false;
       continue;
     }
-    if (__ldg(&top[i]) == __ldg(&top[p])) {  // same final group: lcp >= h_final >= cap
+    if (rank_at(top, i) == rank_at(top, p)) {  // same final group: lcp >= h_final >= cap
       plcp[i] = cap;
       l = cap - 1;
       capped = true;
@@ -356,6 +370,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   s.n = n;
   s.np = np;
   s.levels.clear();
+  s.level_tags.clear();
   s.rounds = 0;
   // alphabet: codes = value - lo over tokens and the terminator
   int32_t lo = known_alphabet ? 0 : term, hi = term;
@@ -414,36 +429,54 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   hists[0].zero();
   scans[0]->prepare(c, rtiles);
   uint32_t* hist_p = nullptr;  // the histograms the latest rank update produced
-  auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, const uint32_t* rank_old, uint32_t h,
-                         uint32_t* rank_new, bool more) -> uint64_t {
-    ScanScratch& sc = *scans[cur];
-    hist_p = hists[cur].p;
-    launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
-           dim3(kRankBlock), 0, kk, ss, rank_old, h, np, rank_new, hist_p, max_passes, gstart.p, sc.buf.p + 1,
-           reinterpret_cast<uint32_t*>(sc.buf.p));
-    // group count G: the last tile's inclusive word, copied out and waited on by event, so the
-    // next round's scratch zeroing (queued after the copy) runs while the host wakes up
-    ++StageTimer::syncs();
-    uint64_t* word = static_cast<uint64_t*>(c->deferred_block()) + 8;  // [0, 64) holds the order verdict
-    ITT_CUDA(cudaMemcpyAsync(word, sc.buf.p + rtiles, 8, cudaMemcpyDeviceToHost, c->stream));
-    ITT_CUDA(cudaEventRecord(c->deferred_ev, c->stream));
-    if (more) {
-      hists[cur ^ 1].zero();
-      scans[cur ^ 1]->prepare(c, rtiles);
-      radix_prezero_status(c, rs, np, max_passes, 0);  // a wide sort zeroes its own (rare, larger)
+  // one rank update into a new level (u16 when the previous group count suggests the ids fit; if
+  // they do not, the update runs again into a u32 level: its inputs are untouched)
+  auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, uintptr_t rank_old, uint32_t h, bool more,
+                         uint64_t g_prev) -> uint64_t {
+    // only where the arrays outgrow L2 (C2's 40 MB levels stay resident: u16 stores there cost
+    // more than they save); ITT_NARROW_MIN_N overrides the size threshold (tests)
+    const char* ev = std::getenv("ITT_NARROW_MIN_N");
+    const uint64_t min_n = ev && *ev ? std::strtoull(ev, nullptr, 10) : (1ull << 24);
+    bool narrow = g_prev <= kNarrowTry && np >= min_n;
+    for (;;) {
+      s.levels.emplace_back(c, narrow ? (np + 1) / 2 : np);
+      const uintptr_t lvl = reinterpret_cast<uintptr_t>(s.levels.back().p) | (narrow ? 1u : 0u);
+      ScanScratch& sc = *scans[cur];
+      hist_p = hists[cur].p;
+      launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
+             dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, gstart.p, sc.buf.p + 1,
+             reinterpret_cast<uint32_t*>(sc.buf.p));
+      // group count G: the last tile's inclusive word, copied out and waited on by event, so the
+      // next round's scratch zeroing (queued after the copy) runs while the host wakes up
+      ++StageTimer::syncs();
+      uint64_t* word = static_cast<uint64_t*>(c->deferred_block()) + 8;  // [0, 64) holds the order verdict
+      ITT_CUDA(cudaMemcpyAsync(word, sc.buf.p + rtiles, 8, cudaMemcpyDeviceToHost, c->stream));
+      ITT_CUDA(cudaEventRecord(c->deferred_ev, c->stream));
+      if (more) {
+        hists[cur ^ 1].zero();
+        scans[cur ^ 1]->prepare(c, rtiles);
+        radix_prezero_status(c, rs, np, max_passes, 0);  // a wide sort zeroes its own (rare, larger)
+      }
+      ITT_CUDA(cudaEventSynchronize(c->deferred_ev));
+      const uint64_t total = *word & kValMask;
+      if (narrow && total > kNarrowGroups) {  // the ids did not fit 16 bits: redo into u32
+        s.levels.pop_back();
+        hists[cur].zero();
+        sc.prepare(c, rtiles);
+        narrow = false;
+        continue;
+      }
+      s.level_tags.push_back(lvl);
+      cur ^= 1;
+      return total;
     }
-    ITT_CUDA(cudaEventSynchronize(c->deferred_ev));
-    const uint64_t total = *word & kValMask;
-    cur ^= 1;
-    return total;
   };
-  s.levels.emplace_back(c, np);
-  uint64_t g = rank_update(keys, sa, nullptr, 0, s.levels.back().p, s.h0 < cap);
+  uint64_t g = rank_update(keys, sa, 0, 0, s.h0 < cap, 0);
   uint32_t h = s.h0;  // prefix length the newest level separates
   // stop when every suffix is alone, or when the groups already separate `cap` symbols (mining
   // never looks deeper than its L_max; see k_plcp for why the capped LCP stays exact below cap)
   while (g < np && h < cap) {
-    const uint32_t* rank = s.levels.back().p;
+    const uintptr_t rank = s.level_tags.back();
     const int b = bits_for(g - 1);
     const EmitLoader ld{sa, rank, np, h};
     // the SA buffer is read by the first pass, so the sort only writes the other buffers:
@@ -470,8 +503,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     uint32_t* nsa = alt ? f2 : vx;
     uint32_t* other_k = alt ? kx : f1;
     uint32_t* other_v = alt ? vx : f2;
-    s.levels.emplace_back(c, np);
-    g = rank_update(nkeys, nsa, rank, h, s.levels.back().p, static_cast<uint64_t>(h) * 2 < cap);
+    g = rank_update(nkeys, nsa, rank, h, static_cast<uint64_t>(h) * 2 < cap, g);
     ++s.rounds;
     // rotate: new SA / keys; the old SA and the unused pair become free
     spare = sa;
@@ -492,9 +524,8 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   // ---- LCP
   DBuf<uint32_t> phi(c, np), plcp(c, np);
   launch(c, "lcp_phi", np * 12.0, k_phi, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, np, phi.p);
-  std::vector<const uint32_t*> lv;
-  for (auto& d : s.levels) lv.push_back(d.p);
-  DBuf<const uint32_t*> dlv(c, lv.size());
+  const std::vector<uintptr_t>& lv = s.level_tags;
+  DBuf<uintptr_t> dlv(c, lv.size());
   h2d(c, dlv.p, lv.data(), lv.size());
   LiftArgs L{s.text.p, np, dlv.p, static_cast<int>(lv.size()), s.h0};
   const uint64_t chunks = (np + kChunk - 1) / kChunk;
@@ -553,9 +584,8 @@ void build_batched_sa(Ctx* c, const std::vector<BatchSAItem>& items, int32_t vma
   DBuf<uint32_t> phi(c, np), plcp(c, np);
   launch(c, "lcp_phi", np * 12.0, k_phi, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, np, phi.p);
   launch(c, "sa_batch_heads", nb * 8.0, k_batch_phi_heads, dim3(grid_for(nb, 256)), dim3(256), 0, s.sa.p, dstarts.p, nb, phi.p);
-  std::vector<const uint32_t*> lv;
-  for (auto& d : s.levels) lv.push_back(d.p);
-  DBuf<const uint32_t*> dlv(c, lv.size());
+  const std::vector<uintptr_t>& lv = s.level_tags;
+  DBuf<uintptr_t> dlv(c, lv.size());
   h2d(c, dlv.p, lv.data(), lv.size());
   LiftArgs L{s.text.p, np, dlv.p, static_cast<int>(lv.size()), s.h0};
   const uint64_t chunks = (np + kChunk - 1) / kChunk;

@@ -344,3 +344,26 @@ def test_native_batch_executor_matches_single_trace_calls(ctx):
             assert isinstance(g, cuda.IttError) and g.status == e.status and str(g) == str(e)
             continue
         assert g == want
+
+
+def test_narrow_rank_levels(ctx, R):
+    """u16 rank levels (used where the arrays outgrow L2; forced here for small inputs), including
+    the fallback to u32 when a level's group count passes 2^16 (random strings)."""
+    import os
+    rng = np.random.default_rng(77)
+    old = os.environ.get("ITT_NARROW_MIN_N")
+    os.environ["ITT_NARROW_MIN_N"] = "0"
+    try:
+        for n, V in ((3000, 5), (20_000, 3), (150_000, 1000), (90_000, 2)):
+            s = rng.integers(0, V, n).tolist()
+            sa, lcp = ctx.suffix_array(s, V)
+            rsa, rlcp = R.suffix_array(s, V)
+            assert np.array_equal(sa, rsa) and np.array_equal(lcp, rlcp), (n, V)
+        body = rng.integers(0, 40, 97).tolist()
+        tok = np.array((body * 400)[:38_000], np.int32)
+        assert ctx.mine_patterns(tok, 40, [(390, 1)]) == R.mine_patterns(tok, 40, [(390, 1)])
+    finally:
+        if old is None:
+            os.environ.pop("ITT_NARROW_MIN_N", None)
+        else:
+            os.environ["ITT_NARROW_MIN_N"] = old
