@@ -94,28 +94,6 @@ __device__ __forceinline__ bool stage_names(const uint64_t* __restrict__ name_of
 }
 
 // ------------------------------------------------------------------ K1: order
-__global__ void k_order_stats(const int64_t* __restrict__ start, uint64_t n, unsigned long long* out /*min,max,desc*/) {
-  long long mn = LLONG_MAX, mx = LLONG_MIN;
-  unsigned long long desc = 0;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const long long s = start[i];
-    mn = s < mn ? s : mn;
-    mx = s > mx ? s : mx;
-    if (i > 0 && start[i - 1] > s) ++desc;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    desc += __shfl_xor_sync(0xffffffffu, desc, o);
-  }
-  if (lane_id() == 0) {
-    atomicMin(reinterpret_cast<long long*>(&out[0]), mn);
-    atomicMax(reinterpret_cast<long long*>(&out[1]), mx);
-    if (desc) atomicAdd(&out[2], desc);
-  }
-}
-
 // Sort each 256-row block by (start, row) — unique keys because the row breaks ties, so the
 // result is the stable order — and record the block's start range and whether the source order
 // has a descent.  Bitonic network with one row per thread: the 30 stages whose partner is in the

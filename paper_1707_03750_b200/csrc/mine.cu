@@ -32,7 +32,6 @@ constexpr int kAnsvBlock = 256;
 __global__ void __launch_bounds__(kTileA) k_tile_minima(const uint32_t* __restrict__ lcp, uint64_t np,
                                                         uint32_t* __restrict__ premin, uint32_t* __restrict__ sufmin,
                                                         uint32_t* __restrict__ tmin) {
-  __shared__ uint32_t s[kTileA];
   __shared__ uint32_t sw[32];
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTileA;
   const uint64_t j = base + threadIdx.x;
