@@ -77,7 +77,6 @@ __global__ void __launch_bounds__(kTileA) k_tile_minima(const uint32_t* __restri
   __syncthreads();
   if (warp < 31) q = min(q, sw[warp + 1]);
   if (j < np) sufmin[j] = q;
-  (void)s;
 }
 
 // sparse table over tile minima: st[l * nt + t] = min(tmin[t, t + 2^l))
