@@ -431,7 +431,8 @@ class Context:
             n_devices=a.census.n_devices, majority_device=a.census.majority_device,
             dropped=a.census.dropped_records, main_stream=a.main_stream, n_main_streams=a.n_main_streams,
             override_non_main=bool(a.main_stream_override_non_main), n_tokens=a.n_tokens, n_names=a.n_names,
-            name_row=[a.name_row[i] for i in range(a.n_names)], overlapping_kernels=a.overlapping_kernels,
+            name_row=np.ctypeslib.as_array(a.name_row, shape=(a.n_names,)).tolist() if a.n_names else [],
+            overlapping_kernels=a.overlapping_kernels,
             loops=[])
         for k in range(a.n_loops):
             L = a.loops[k]
@@ -443,7 +444,8 @@ class Context:
                 rows = np.zeros((0, 11), np.int64)
             res["loops"].append(dict(
                 iterations_declared=L.iterations_declared, pattern_length=L.pattern_length,
-                pattern_tokens=[L.pattern_tokens[j] for j in range(L.pattern_length)],
+                pattern_tokens=(np.ctypeslib.as_array(L.pattern_tokens, shape=(L.pattern_length,)).tolist()
+                                if L.pattern_length else []),
                 pattern_count=L.pattern_count, epsilon_used=L.epsilon_used, first_token=L.first_token,
                 k0_used=L.k0_used, rows=rows,
                 clamps=(L.clamps.negative_gap_clamps, L.clamps.negative_interval_clamps)))
