@@ -162,6 +162,36 @@ def cpu_reference_run(config: str, iters: int, steps: int, warmup: int):
     return ev, info, sample, times
 
 
+def _c4_ref_worker(seeds):
+    """One host core: the reference (oracle/_ref) analyzing its own C4 traces; returns (events, s)."""
+    from oracle.bindings import ref
+    from paper_1707_03750_b200 import synth
+    R = ref()
+    kw = dict(synth.CONFIGS["C4"])
+    ev, busy = 0, 0.0
+    for sd in seeds:
+        recs, info = synth.generate(**dict(kw, seed=sd))
+        t0 = time.perf_counter()
+        R.analyze(recs, [500], staged=False)
+        busy += time.perf_counter() - t0
+        ev += info["n"]
+    return ev, busy
+
+
+def c4_cpu_baseline(per_core: int = 2):
+    """SURVEY §8d for C4: one reference process per host core over disjoint traces."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    seeds = [[1000 + c * per_core + k for k in range(per_core)] for c in range(cores)]
+    with mp.get_context("spawn").Pool(cores) as p:
+        res = p.map(_c4_ref_worker, seeds)
+    ev = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": ev / wall, "unit": "events/s", "cores": cores, "kind": "reference",
+            "sample": f"{cores} reference processes x {per_core} C4 traces each ({ev} events; busy time of the slowest "
+                      f"process {wall:.2f} s)"}
+
+
 def bench_batch(args, world, rank, local, workload):
     """C4: every rank analyzes its contiguous shard of the batch; no collective on the data path
     (a barrier + max-over-ranks time bracket the timed region).  Strong scaling: the batch size is
@@ -242,6 +272,11 @@ def bench_batch(args, world, rank, local, workload):
                            "batched_suffix_arrays": args.batch_impl == "native",
                            "parallelism": f"shard{world}", "mined_ok": bool(ok)},
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = c4_cpu_baseline()
+            except Exception as e:  # noqa: BLE001 (the reference build is optional on the box)
+                line["cpu_baseline"] = {"unavailable": str(e)[:200]}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
