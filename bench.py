@@ -363,7 +363,7 @@ def main():
                          "NVML queries can stall the driver for milliseconds)")
     ap.add_argument("--traces", type=int, default=8192, help="C4: traces in the batch")
     ap.add_argument("--distinct", type=int, default=256, help="C4: distinct generated traces (batch cycles them)")
-    ap.add_argument("--workers", type=int, default=48, help="C4: concurrent streams (host threads) per GPU")
+    ap.add_argument("--workers", type=int, default=64, help="C4: concurrent streams (host threads) per GPU")
     ap.add_argument("--dist-sa", action="store_true",
                     help="one trace with its suffix array distributed over all ranks (NCCL; C5's multi-GPU path)")
     ap.add_argument("--batch-impl", default="native", choices=["native", "threads"],
