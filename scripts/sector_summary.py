@@ -1,7 +1,8 @@
 """Summarise scripts/sector_profile.sh's ncu CSV into profiles/<tag>_sector_efficiency.csv.
-Usage: python scripts/sector_summary.py gpurun_out/sectors.csv <tag>"""
+Usage: python scripts/sector_summary.py gpurun_out/sectors.csv <tag> [config]"""
 import collections, csv, re, sys
 src, tag = sys.argv[1], sys.argv[2]
+cfg = sys.argv[3] if len(sys.argv) > 3 else "C2"
 rows = list(csv.reader(open(src)))
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hi]
@@ -17,7 +18,7 @@ for r in rows[hi + 1:]:
     if base == "k_onesweep" and re.search(r"\b10\b\s*>|, \(int\)10>|,10>", full):
         base += "_w10"
     agg[base][r[mi]].append((float(r[vi].replace(",", "")), r[ui]))
-out = [f"# {tag}: ncu --metrics (sector efficiency of global loads/stores, L2 hit, DRAM bytes), C2 bench --steps 1, per-launch means",
+out = [f"# {tag}: ncu --metrics (sector efficiency of global loads/stores, L2 hit, DRAM bytes), {cfg} bench --steps 1, per-launch means",
        "kernel,launches,duration_us,dram_MB_per_launch,l2_hit_pct,ld_bytes_per_sector_pct,st_bytes_per_sector_pct"]
 scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
 for k, m in agg.items():
