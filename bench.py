@@ -1,9 +1,9 @@
 #!/usr/bin/env python3
 """bench.py — trace events/sec of the B200 mining pipeline (intern -> SA -> LCP -> repeat ->
-spans -> per-iteration aggregates) on BASELINE.json's configs[1] (C2: 10M-event TF-like
-trace, 50K iterations x 200 ops, 5% memcpy noise, rows locally shuffled).
+spans -> per-iteration aggregates) on the largest single-GPU BASELINE config, C3 (BASELINE.json
+configs[2]: 100M-event TF-like trace, 20K iterations x 5000 ops, V=4096 distinct op names).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference] [--config C2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference] [--config C3]
 
 * value : whole-job events/s with the columns already resident in HBM (device-timed with CUDA
           events on the library's stream; one step = one itt_analyze call = the full path).
@@ -12,7 +12,10 @@ trace, 50K iterations x 200 ops, 5% memcpy noise, rows locally shuffled).
 * roofline : dominant kernel's algorithmic bytes / its CUDA-event launch time (profiled pass).
 * cpu_baseline : the reference itself (oracle/_ref, compiled from the reference headers) on a
           bounded sample of the same workload, 1 host core (the reference is single-threaded).
-Under torchrun each rank runs one replica (C2 does not shard: "replicas only").
+* sa_full : the full suffix array + LCP (itt_suffix_array, cap = infinity) of the same tokens,
+          device-resident, timed beside the step (the step itself builds the capped SA mining needs).
+Under torchrun: C1-C3 run one replica per rank ("replicas only"); C4 shards the
+batch; --dist-sa spreads one trace's suffix array over the ranks.
 """
 from __future__ import annotations
 
@@ -45,7 +48,7 @@ WORKLOADS = {
 }
 # bounded CPU samples (same generator and shape, fewer iterations)
 CPU_SAMPLE_ITERS = {"C1": 100, "C2": 10_000, "C3": 400, "C5": 1_000}
-REF_ARM_ITERS = {"C1": 100, "C2": 2_000, "C3": 100, "C5": 250}  # ~2 s per reference step on one core
+REF_ARM_ITERS = {"C1": 100, "C2": 2_000, "C3": 400, "C5": 250}  # ~1-4 s per reference step on one core
 
 
 def log(*a):
@@ -143,23 +146,37 @@ def make_trace(config: str, iterations: int | None = None):
     return synth.generate_config(config, **kw)
 
 
-def cpu_reference_run(config: str, iters: int, steps: int, warmup: int):
-    """Time the reference (oracle/_ref) on a bounded sample: events/s on 1 core."""
+def cpu_reference_run(config: str, iters: int, steps: int, warmup: int, full_iters: int | None = None):
+    """Time the reference (oracle/_ref: the stock analyze_trace, pipeline.hpp:34-134) on a bounded
+    sample, 1 core.  A step's time is the reference's own work as its CLI would do it after parsing:
+    the (start,row) stable sort (ingest.hpp:396-400) + analyze_trace — not the marshalling of our
+    columns into its AoS records and not the JSON/CSV rendering (the GPU step renders nothing).
+    One extra staged run (the same stage calls with timers) gives the per-stage split, and from it
+    an extrapolation to the full-size trace (labelled as such: linear stages scale with events,
+    the metrics stage with I * H, i.e. quadratically in iterations, metrics.hpp:109-164)."""
     from oracle.bindings import ref
     recs, info = make_trace(config, iters)
     R = ref()
     times = []
     for s in range(warmup + steps):
-        t0 = time.perf_counter()
-        res = R.analyze(recs, [iters], staged=True)
-        dt = time.perf_counter() - t0
+        res = R.analyze(recs, [iters], staged=False)
         if s >= warmup:
-            times.append(dt)
+            times.append((res["times"]["order_ms"] + res["times"]["analyze_ms"]) / 1000.0)
     ev = info["n"] / statistics.mean(times)
-    stage = res["times"]
-    sample = (f"{config}-shaped trace with {iters} iterations ({info['n']} events, {info['n_main']} tokens); "
-              f"reference analyze stages (ms): " + ", ".join(f"{k[:-3]}={v:.0f}" for k, v in stage.items()))
-    return ev, info, sample, times
+    stage = R.analyze(recs, [iters], staged=True)["times"]
+    split = {k[:-3]: round(stage[k], 1) for k in ("order_ms", "filter_census_ms", "intern_ms", "mine_ms", "match_ms",
+                                                  "metrics_ms")}
+    sample = (f"{config}-shaped trace with {iters} iterations ({info['n']} events, {info['n_main']} tokens): stock "
+              f"analyze_trace + the (start,row) sort, 1 core; stage split of one staged run (ms): "
+              + ", ".join(f"{k}={v:.0f}" for k, v in split.items()))
+    extra = {"stage_ms": split}
+    if full_iters and full_iters > iters:
+        f = full_iters / iters
+        lin = sum(v for k, v in split.items() if k != "metrics")
+        extra["extrapolated_full_size_s"] = round((lin * f + split["metrics"] * f * f) / 1000.0, 1)
+        extra["extrapolation"] = (f"EXTRAPOLATED, not measured: {full_iters} iterations = {f:.0f}x the sample; "
+                                  "linear stages x f, metrics x f^2")
+    return ev, info, sample, times, extra
 
 
 def _c4_ref_worker(seeds):
@@ -351,11 +368,12 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--iterations", type=int, default=None,
                     help="override the workload's iteration count (smaller dry runs of C3/C5)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sa-full", action="store_true", help="skip timing the full (uncapped) suffix array")
     ap.add_argument("--no-ingest", action="store_true", help="skip the GPU CSV ingest measurement")
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--clock-ms", type=int, default=200,
@@ -376,12 +394,13 @@ def main():
         if rank != 0:
             return 0
         it = REF_ARM_ITERS[args.config]
-        ev, info, sample, times = cpu_reference_run(args.config, it, args.steps, max(1, args.warmup))
+        ev, info, sample, times, extra = cpu_reference_run(args.config, it, args.steps, max(1, args.warmup), iters)
         line = {"metric": METRIC, "value": ev, "unit": "events/s", "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic", "impl": "reference",
                 "config": {"workload": workload, "sample_iterations": it, "events_per_step": info["n"]},
-                "cpu_baseline": {"value": ev, "unit": "events/s", "cores": 1, "kind": "reference", "sample": sample},
+                "cpu_baseline": {"value": ev, "unit": "events/s", "cores": 1, "kind": "reference", "sample": sample,
+                                 **extra},
                 "e2e": {"value": ev, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
@@ -443,8 +462,16 @@ def main():
     clk = ClockSampler(dev, args.clock_ms).__enter__()
     for _ in range(max(3, args.warmup)):
         res = step_device()
+    # then keep warming for at least 1 s of steps (clocks ramp, caches of the block allocator fill):
+    # a short warm-up at C1/C2 sizes left the first timed region ~10% slower than later ones
+    t_w = time.perf_counter()
+    extra_warmup = 0
+    while time.perf_counter() - t_w < 1.0:
+        res = step_device()
+        extra_warmup += 1
     # correctness guard: the mined period must be the planted body
-    assert res["loops"][0]["pattern_length"] > 0
+    assert res["loops"][0]["pattern_length"] == {"C1": 200, "C2": 200, "C3": 5000, "C5": 2000}[args.config] \
+        or args.iterations
     l0 = ctx.launch_count()
     clk.mark_start()
     ms, res = timed(step_device, args.steps)
@@ -529,21 +556,35 @@ def main():
     # ---- e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off] + \
-            ([] if names_host else [recs.name_bytes]) + ([recs.device] if recs.device is not None else [])
-        registered = []
-        for a in cols:  # pinned for full-speed DMA; pageable if the OS refuses more locked memory
+        fields = ["start_ns", "duration_ns", "size_bytes", "flags", "stream", "name_off"] + \
+            ([] if names_host else ["name_bytes"]) + (["device"] if recs.device is not None else [])
+        registered, staged = [], {}
+        for f in fields:  # pinned for full-speed DMA: registered in place, else staged into cudaHostAlloc memory
+            a = getattr(recs, f)
             try:
                 ctx.register_host(a)
                 registered.append(a)
             except itt.IttError as e:
-                log(f"[rank {rank}] e2e: host column not pinned ({e}); copied from pageable memory")
+                buf = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+                view = buf.numpy().view(a.dtype)
+                view[:] = a
+                staged[f] = (buf, view)
+                log(f"[rank {rank}] e2e: column {f} ({a.nbytes / 1e9:.2f} GB) not registrable ({e}); "
+                    "staged into pinned memory instead")
+        if staged:
+            from paper_1707_03750_b200 import abi as _abi
+            recs_e = _abi.Records(**{f: staged[f][1] if f in staged else getattr(recs, f) for f in
+                                   ("start_ns", "duration_ns", "stream", "name_off", "name_bytes", "size_bytes",
+                                    "flags", "device")}, order=recs.order, keepalive=(recs._keepalive, staged))
+        else:
+            recs_e = recs
+        cols = fields
         if names_host:  # still registered by drecs; streamed again
             from paper_1707_03750_b200 import abi as _abi
-            recs.mem = _abi.MEM_HOST_STREAM_NAMES
+            recs_e.mem = _abi.MEM_HOST_STREAM_NAMES
         try:
             def step_host():
-                return ctx.analyze_raw(recs, [iters])
+                return ctx.analyze_raw(recs_e, [iters])
             step_host()
             ms_e, res_e = timed(step_host, args.steps)
         finally:
@@ -551,8 +592,9 @@ def main():
                 ctx.unregister_host(a)
         d2h = sum(L["rows"].nbytes + 4 * L["pattern_length"] for L in res_e["loops"])
         e2e = {"value": world * n_events / (ms_e / args.steps / 1000.0), "unit": "events/s",
-               "h2d_bytes_per_step": int(recs.nbytes()), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": ms_e / args.steps, "pinned_columns": f"{len(registered)}/{len(cols)}"}
+               "h2d_bytes_per_step": int(recs_e.nbytes()), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": ms_e / args.steps,
+               "pinned_columns": f"{len(registered)} registered + {len(staged)} staged of {len(cols)}"}
         log(f"[rank {rank}] e2e: {e2e['ms_per_step']:.2f} ms/step, {e2e['value'] / 1e9:.3f}G events/s")
 
     # ---- GPU CSV ingest: the same trace as profiler CSV text, parsed by
@@ -590,12 +632,45 @@ def main():
         except Exception as e:  # a failure here must not lose the main measurement
             ingest = {"error": repr(e)}
 
+    # ---- the FULL suffix array + LCP (itt_suffix_array, cap = infinity) of the same tokens, device
+    # resident: the step builds only the capped SA mining needs; this times the rest
+    sa_full = None
+    if not args.no_sa_full and args.config != "C5":
+        try:
+            tok_h, _, names_h = ctx.build_token_sequence(drecs, res["main_stream"])
+            n_tok = int(tok_h.size)
+            dev_t = torch.device("cuda", dev)
+            tok_d = torch.from_numpy(tok_h).to(dev_t)
+            sa_d = torch.empty(n_tok + 1, dtype=torch.int32, device=dev_t)
+            lcp_d = torch.empty(n_tok + 1, dtype=torch.int32, device=dev_t)
+            del tok_h
+            torch.cuda.synchronize(dev)
+
+            def step_sa():
+                ctx.suffix_array_device(tok_d.data_ptr(), n_tok, int(names_h.size), sa_d.data_ptr(), lcp_d.data_ptr())
+            step_sa()
+            ms_sa, _ = timed(step_sa, 3)
+            ctx.set_profiling(True)
+            ctx.reset_stats()
+            step_sa()
+            st_sa = ctx.kernel_stats()
+            ctx.set_profiling(False)
+            rounds = st_sa.get("sa_rank_update", {}).get("launches", 0) - 1
+            sa_full = {"ms": ms_sa / 3, "tokens": n_tok, "suffixes_per_s": (n_tok + 1) / (ms_sa / 3 / 1000.0),
+                       "doubling_rounds": int(rounds),
+                       "kernels_ms": {k: round(v["total_ms"], 3) for k, v in
+                                      sorted(st_sa.items(), key=lambda kv: -kv[1]["total_ms"])[:6]}}
+            del tok_d, sa_d, lcp_d
+            log(f"[rank {rank}] full SA+LCP: {sa_full['ms']:.2f} ms ({rounds} doubling rounds)")
+        except Exception as e:  # noqa: BLE001 (must not lose the main measurement)
+            sa_full = {"error": repr(e)[:300]}
+
     # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            ev, cinfo, sample, _ = cpu_reference_run(args.config, CPU_SAMPLE_ITERS[args.config], 1, 0)
-            cpu = {"value": ev, "unit": "events/s", "cores": 1, "kind": "reference", "sample": sample}
+            ev, cinfo, sample, _, extra = cpu_reference_run(args.config, CPU_SAMPLE_ITERS[args.config], 1, 0, iters)
+            cpu = {"value": ev, "unit": "events/s", "cores": 1, "kind": "reference", "sample": sample, **extra}
         except Exception as e:  # the reference library must be prebuilt in this container
             cpu = {"value": None, "unit": "events/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -604,7 +679,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic", "warmup_extra_steps": extra_warmup,
             "config": {"workload": workload, "events": n_events, "tokens": info["n_main"],
                        "parallelism": f"replicas{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (%.2f GB resident columns)" % (drecs.nbytes / 1e9),
@@ -612,7 +687,7 @@ def main():
                                  "iterations_found": int(L["rows"].shape[0])}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(launches), "kernels": kernel_table, "op_profile": op_profile,
-            "memory": memory, "ingest": ingest,
+            "memory": memory, "ingest": ingest, "sa_full": sa_full,
         }
         print(json.dumps(line), flush=True)
     drecs.free()

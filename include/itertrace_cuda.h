@@ -186,8 +186,16 @@ int itt_radix_sort_pairs_u32(itt_ctx* ctx, uint32_t* keys, uint32_t* vals, uint6
 /* Suffix array + LCP of tokens[0..n) followed by a unique terminator `term`:
  * sa[k] = start of the k-th smallest suffix of tokens+[term] (n+1 entries), lcp[0] = 0,
  * lcp[k] = lcp(sa[k-1], sa[k]).  Equals the leaf order of SuffixTree (suffix_tree.hpp:21-190)
- * in ascending child-key order.  lcp may be NULL.  Host buffers of n+1 entries. */
+ * in ascending child-key order.  lcp may be NULL (then only two rank levels stay resident, so
+ * the SA of ~1B tokens fits one B200).  Buffers of n+1 entries, each in host OR device memory
+ * (told apart through CUDA unified addressing).  n+1 < 2^32 - 1. */
 int itt_suffix_array(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, uint32_t* sa, uint32_t* lcp);
+/* The capped suffix array the mining path builds (mine.hpp:64-67 never looks past L_max; DESIGN
+ * §3.1): suffixes ordered by their first h >= cap symbols (ties of equal cap-prefixes in an
+ * unspecified but deterministic order), lcp[k] = min(lcp(sa[k-1], sa[k]), cap).  cap = 0xFFFFFFFF
+ * is the full suffix array.  Host or device buffers. */
+int itt_suffix_array_capped(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa,
+                            uint32_t* lcp);
 
 typedef struct itt_repeat { /* RepeatCandidate, mine.hpp:31-35 */
   int32_t start;

@@ -15,14 +15,21 @@
 //   mine_pattern              mine.hpp:119-122
 //   mine_patterns_multi       mine.hpp:132-165
 //   approx_match              match.hpp:41-85, :87-91
-//   compute_iteration_metrics metrics.hpp:109-164 (HtoD list = collect_htod_records(trace))
+//   partition_iterations      metrics.hpp:44-55
+//   compute_iteration_metrics metrics.hpp:109-164 (both the reference's 4-parameter form and a
+//                             3-parameter form whose HtoD list is collect_htod_records(trace))
 //   analyze_trace             pipeline.hpp:34-134
+//   parse_trace + analyze_trace, parse_trace + summarize_streams (the CLI's analyze / inspect
+//                             bodies, itertrace_main.cpp:121-149) with the CSV parsed on the GPU:
+//                             analyze_csv_file, inspect_csv_file
 // Device failures (no sm_100 GPU, CUDA errors) throw CudaError, a std::runtime_error — the
 // reference CLI maps those to exit code 1 (itertrace_main.cpp:294-296).  No CPU fallback.
 #pragma once
 
 #include <algorithm>
 #include <cstdlib>
+#include <fstream>
+#include <iterator>
 #include <map>
 #include <memory>
 #include <span>
@@ -234,6 +241,54 @@ inline IterationAnalysis compute_iteration_metrics(const NormalizedTrace& trace,
   return out;
 }
 
+// partition_iterations (metrics.hpp:44-55): the windows' times come from the device aggregate pass
+// (t_start / t_end of every span), so a caller swapping namespaces gets the same vector.
+inline std::vector<IterationWindow> partition_iterations(const NormalizedTrace& trace, const TokenSequence& seq,
+                                                         const std::vector<MatchSpan>& spans) {
+  std::vector<IterationWindow> windows;
+  windows.reserve(spans.size());
+  for (const auto& sp : spans) windows.push_back(IterationWindow{sp, 0, 0});
+  const IterationAnalysis a = itertrace::cuda::compute_iteration_metrics(trace, seq, windows);
+  for (size_t k = 0; k < windows.size(); ++k) {
+    windows[k].t_start = a.iterations[k].t_start;
+    windows[k].t_end = a.iterations[k].t_end;
+  }
+  return windows;
+}
+
+// The reference's 4-parameter form (metrics.hpp:109-112): the HtoD list is the caller's.  When
+// it is collect_htod_records(trace) (what the pipeline passes, pipeline.hpp:93) the trace goes to
+// the device as is; otherwise the device sees the trace with the records' kinds adjusted so that
+// exactly the listed records are MemcpyHtoD (names of unlisted HtoD records neutralised, listed
+// records given an HtoD name) — the token columns are untouched, so the windows are too.
+inline IterationAnalysis compute_iteration_metrics(const NormalizedTrace& trace, const TokenSequence& seq,
+                                                   const std::vector<IterationWindow>& windows,
+                                                   const std::vector<const TraceRecord*>& htod_records) {
+  const size_t n = trace.records.size();
+  std::vector<uint8_t> listed(n, 0);
+  bool same = true;
+  size_t j = 0;
+  for (const TraceRecord* r : htod_records) {
+    if (r < trace.records.data() || r >= trace.records.data() + n)
+      throw Error(ErrorKind::InvalidConfig, "metrics: HtoD record outside the trace");
+    const size_t i = static_cast<size_t>(r - trace.records.data());
+    if (listed[i]) throw Error(ErrorKind::InvalidConfig, "metrics: HtoD record listed twice");
+    listed[i] = 1;
+    while (j < n && kind_of(trace.records[j]) != OpKind::MemcpyHtoD) ++j;
+    same = same && j < n && j == i;
+    ++j;
+  }
+  while (same && j < n && kind_of(trace.records[j]) != OpKind::MemcpyHtoD) ++j;
+  if (same && j >= n) return itertrace::cuda::compute_iteration_metrics(trace, seq, windows);
+  NormalizedTrace adj = trace;
+  for (size_t i = 0; i < n; ++i) {
+    const bool htod = kind_of(adj.records[i]) == OpKind::MemcpyHtoD;
+    if (listed[i] && !htod) adj.records[i].name = "[CUDA memcpy HtoD]";
+    if (!listed[i] && htod) adj.records[i].name = "unlisted-copy";
+  }
+  return itertrace::cuda::compute_iteration_metrics(adj, seq, windows);
+}
+
 // a12, the north star's per-op x per-iteration profile (no reference counterpart; definition
 // in itertrace_cuda.h, itt_op_cell): over the reference's own token sequence and windows.
 struct OpProfile {
@@ -270,14 +325,16 @@ inline OpProfile op_profile(const NormalizedTrace& trace, const TokenSequence& s
   return out;
 }
 
-// analyze_trace (pipeline.hpp:34-134): the device runs filter -> census -> tokens -> SA/LCP ->
-// mining -> matching -> integer aggregates in one call; the host finishes with the reference's
-// own compute_summary / diagnose and assembles warnings in the reference's order.
-inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& trace_label, const AnalyzeOptions& opt) {
+namespace detail {
+
+struct AnalysisHold {
+  itt_ctx* c;
+  void operator()(itt_analysis* x) const { itt_free_analysis(c, x); }  // rows return to the context's pool
+};
+using AnalysisPtr = std::unique_ptr<itt_analysis, AnalysisHold>;
+
+inline AnalysisPtr run_analyze(Context& ctx, const itt_records& rv, const AnalyzeOptions& opt) {
   if (opt.loops.empty()) throw Error(ErrorKind::InvalidConfig, "analyze: at least one iteration count is required");
-  Context& ctx = Context::thread_default();
-  const detail::Columns cols(trace);
-  const itt_records rv = cols.view();
   itt_analyze_opts o{};
   o.loops = opt.loops.data();
   o.n_loops = static_cast<uint32_t>(opt.loops.size());
@@ -286,12 +343,29 @@ inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& tr
   o.main_stream = opt.main_stream ? static_cast<int64_t>(*opt.main_stream) : -1;
   itt_analysis* a = nullptr;
   ctx.check(itt_analyze(ctx.get(), &rv, &o, &a));
-  struct FreeAnalysis {
-    itt_ctx* c;
-    void operator()(itt_analysis* x) const { itt_free_analysis(c, x); }  // rows return to the context's pool
-  };
-  std::unique_ptr<itt_analysis, FreeAnalysis> hold(a, FreeAnalysis{ctx.get()});
+  return AnalysisPtr(a, AnalysisHold{ctx.get()});
+}
 
+inline void fill_streams(const itt_census& c, std::vector<StreamSummary>& streams, std::map<std::uint32_t, StreamClass>& cls) {
+  for (uint32_t i = 0; i < c.n_streams; ++i) {
+    const itt_stream_summary& s = c.streams[i];
+    StreamSummary ss;
+    ss.stream = s.stream;
+    for (int k = 0; k < 6; ++k) ss.counts[static_cast<size_t>(k)] = s.counts[k];
+    ss.first_start = s.first_start;
+    ss.last_end = s.last_end;
+    streams.push_back(ss);
+    cls[s.stream] = static_cast<StreamClass>(s.cls);
+  }
+}
+
+// The host part of analyze_trace (pipeline.hpp:34-134) after the device pipeline: Report fields,
+// the warnings in the reference's order, the reference's own compute_summary / diagnose.
+// label_of(device rank) -> device label; name_of(row) -> name of the record at `row` of the
+// record set itt_analyze ran on.
+template <typename LabelOf, typename NameOf>
+AnalysisResult assemble(const itt_analysis* a, const AnalyzeOptions& opt, const std::string& trace_label,
+                        std::vector<std::string> warnings, LabelOf label_of, NameOf name_of) {
   AnalysisResult result;
   Report& report = result.report;
   report.trace_path = trace_label;
@@ -300,20 +374,11 @@ inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& tr
   report.theta_cpu = opt.theta_cpu;
   report.k0_override = opt.k0;
   report.main_stream_override = opt.main_stream;
-  report.warnings = trace.warnings;
+  report.warnings = std::move(warnings);
   if (a->census.n_devices > 1)  // streams.hpp:198-203
-    report.warnings.push_back("MultiDeviceTrace: kept majority device '" + cols.labels[a->census.majority_device] +
+    report.warnings.push_back("MultiDeviceTrace: kept majority device '" + label_of(a->census.majority_device) +
                               "', dropped " + std::to_string(a->census.dropped_records) + " records from other devices");
-  for (uint32_t i = 0; i < a->census.n_streams; ++i) {
-    const itt_stream_summary& s = a->census.streams[i];
-    StreamSummary ss;
-    ss.stream = s.stream;
-    for (int k = 0; k < 6; ++k) ss.counts[static_cast<size_t>(k)] = s.counts[k];
-    ss.first_start = s.first_start;
-    ss.last_end = s.last_end;
-    report.streams.push_back(ss);
-    report.classes[s.stream] = static_cast<StreamClass>(s.cls);
-  }
+  fill_streams(a->census, report.streams, report.classes);
   report.main_stream = a->main_stream;
   if (opt.main_stream) {
     if (a->main_stream_override_non_main)
@@ -342,10 +407,10 @@ inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& tr
     loop.epsilon_used = L.epsilon_used;
     loop.first_occurrence_token = L.first_token;
     loop.k0_used = L.k0_used;
-    for (int64_t j = 0; j < L.pattern_length; ++j)
-      loop.pattern_names.push_back(trace.records[a->name_row[L.pattern_tokens[j]]].name);
+    for (int64_t j = 0; j < L.pattern_length; ++j) loop.pattern_names.push_back(name_of(a->name_row[L.pattern_tokens[j]]));
     std::vector<IterationMetrics> items;
-    for (uint64_t i = 0; i < L.n_iterations; ++i) items.push_back(detail::to_metrics(L.rows[i], static_cast<int64_t>(i + 1)));
+    items.reserve(L.n_iterations);
+    for (uint64_t i = 0; i < L.n_iterations; ++i) items.push_back(to_metrics(L.rows[i], static_cast<int64_t>(i + 1)));
     if (L.clamps.negative_gap_clamps > 0)
       report.warnings.push_back("NegativeGaps: " + std::to_string(L.clamps.negative_gap_clamps) +
                                 " negative dispatch gaps clamped to zero");
@@ -359,6 +424,94 @@ inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& tr
     result.details.push_back(std::move(items));
   }
   return result;
+}
+
+// itt_parse_csv result, released with the context's allocator
+struct ParsedHold {
+  itt_ctx* c;
+  void operator()(itt_parsed_trace* p) const { itt_free_parsed(c, p); }
+};
+using ParsedPtr = std::unique_ptr<itt_parsed_trace, ParsedHold>;
+
+// parse_trace (ingest.hpp:408-417) with parse_trace_text on the GPU: the file's text crosses to
+// HBM once and the records stay there
+inline ParsedPtr parse_file(Context& ctx, const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(ErrorKind::UnreadableFile, "ingest: cannot open trace file '" + path + "'");
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  itt_parsed_trace* p = nullptr;
+  ctx.check(itt_parse_csv(ctx.get(), text.data(), text.size(), path.c_str(), &p));
+  return ParsedPtr(p, ParsedHold{ctx.get()});
+}
+
+inline IngestReport ingest_report(const itt_parsed_trace& p) {
+  static const char* const kCols[7] = {"Start", "Duration", "Size", "Throughput", "Device", "Stream", "Name"};
+  IngestReport r;
+  r.rows_total = p.rows_total;
+  r.rows_parsed = p.rows_parsed;
+  r.rows_skipped = p.rows_skipped;
+  for (uint64_t i = 0; i < p.n_skips; ++i) r.skip_reasons.emplace_back(p.skip_line[i], p.skip_reason[i]);
+  for (int c = 0; c < 7; ++c)
+    if (p.column[c] >= 0) r.column_map[kCols[c]] = static_cast<size_t>(p.column[c]);
+  return r;
+}
+
+}  // namespace detail
+
+// analyze_trace (pipeline.hpp:34-134): the device runs filter -> census -> tokens -> SA/LCP ->
+// mining -> matching -> integer aggregates in one call; the host finishes with the reference's
+// own compute_summary / diagnose and assembles warnings in the reference's order.
+inline AnalysisResult analyze_trace(NormalizedTrace trace, const std::string& trace_label, const AnalyzeOptions& opt) {
+  if (opt.loops.empty()) throw Error(ErrorKind::InvalidConfig, "analyze: at least one iteration count is required");
+  Context& ctx = Context::thread_default();
+  const detail::Columns cols(trace);
+  const itt_records rv = cols.view();
+  const detail::AnalysisPtr a = detail::run_analyze(ctx, rv, opt);
+  return detail::assemble(
+      a.get(), opt, trace_label, trace.warnings, [&](uint16_t d) { return cols.labels[d]; },
+      [&](uint64_t row) { return trace.records[row].name; });
+}
+
+// The CLI's analyze body (itertrace_main.cpp:121-139, parse_trace + analyze_trace) with the CSV
+// parsed on the GPU (itt_parse_csv) and analyzed where it lies.  Same Report, details, ingest
+// counts, warnings and errors as the reference.
+inline std::pair<AnalysisResult, IngestReport> analyze_csv_file(const std::string& path, const AnalyzeOptions& opt) {
+  if (opt.loops.empty()) throw Error(ErrorKind::InvalidConfig, "analyze: at least one iteration count is required");
+  Context& ctx = Context::thread_default();
+  const detail::ParsedPtr p = detail::parse_file(ctx, path);
+  const detail::AnalysisPtr a = detail::run_analyze(ctx, p->records, opt);
+  // names of the pattern tokens: (offset, bytes) of their rows from the device columns
+  auto name_of = [&](uint64_t row) {
+    uint64_t off[2];
+    ctx.check(itt_memcpy_d2h(ctx.get(), off, p->records.name_off + row, sizeof(off)));
+    std::string name(off[1] - off[0], '\0');
+    if (!name.empty()) ctx.check(itt_memcpy_d2h(ctx.get(), name.data(), p->records.name_bytes + off[0], name.size()));
+    return name;
+  };
+  std::vector<std::string> warnings(p->warnings, p->warnings + p->n_warnings);
+  AnalysisResult r = detail::assemble(
+      a.get(), opt, path, std::move(warnings), [&](uint16_t d) { return std::string(p->device_labels[d]); }, name_of);
+  return {std::move(r), detail::ingest_report(*p)};
+}
+
+// The CLI's inspect body (itertrace_main.cpp:141-149): parse_trace + summarize_streams +
+// classify_streams (no device filter), the parse and the census on the GPU.
+struct InspectResult {
+  std::vector<StreamSummary> streams;
+  std::map<std::uint32_t, StreamClass> classes;
+  IngestReport ingest;
+};
+inline InspectResult inspect_csv_file(const std::string& path) {
+  Context& ctx = Context::thread_default();
+  const detail::ParsedPtr p = detail::parse_file(ctx, path);
+  InspectResult out;
+  out.ingest = detail::ingest_report(*p);
+  if (p->records.n == 0) return out;
+  itt_census c{};
+  ctx.check(itt_summarize_streams(ctx.get(), &p->records, 0, &c));
+  detail::fill_streams(c, out.streams, out.classes);
+  itt_free(ctx.get(), c.streams);
+  return out;
 }
 
 }  // namespace itertrace::cuda

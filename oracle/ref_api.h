@@ -35,6 +35,7 @@ typedef struct ref_loop {
 
 typedef struct ref_stage_times { /* steady_clock milliseconds per stage */
   double order_ms, filter_census_ms, intern_ms, mine_ms, match_ms, metrics_ms, total_ms;
+  double analyze_ms; /* the analyze_trace (or staged) call alone: no AoS marshalling, no rendering */
 } ref_stage_times;
 
 typedef struct ref_analysis {

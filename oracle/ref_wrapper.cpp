@@ -191,8 +191,10 @@ extern "C" int ref_analyze(const itt_records* recs, const itt_analyze_opts* opts
     if (opts->main_stream >= 0) opt.main_stream = static_cast<uint32_t>(opts->main_stream);
     NormalizedTrace trace = to_trace(recs, &out->times.order_ms);
     AnalysisResult res;
+    const auto t_an = std::chrono::steady_clock::now();
     if (staged) res = staged_analyze(std::move(trace), "trace.csv", opt, &out->times);
     else res = analyze_trace(std::move(trace), "trace.csv", opt);
+    out->times.analyze_ms = ms_since(t_an);
     const Report& rep = res.report;
     out->n_streams = static_cast<uint32_t>(rep.streams.size());
     out->streams = static_cast<itt_stream_summary*>(std::calloc(rep.streams.size() + 1, sizeof(itt_stream_summary)));

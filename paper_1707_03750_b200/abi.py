@@ -276,7 +276,8 @@ class ref_parsed(C.Structure):
 
 class ref_stage_times(C.Structure):
     _fields_ = [(k, C.c_double) for k in
-                ("order_ms", "filter_census_ms", "intern_ms", "mine_ms", "match_ms", "metrics_ms", "total_ms")]
+                ("order_ms", "filter_census_ms", "intern_ms", "mine_ms", "match_ms", "metrics_ms", "total_ms",
+                 "analyze_ms")]
 
 
 class ref_analysis(C.Structure):

@@ -23,6 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
                   "-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 CUDA_SO = os.path.join(HERE, "libitertrace_cuda.so")
+CLI_BIN = os.path.join(HERE, "itertrace")  # the reference tool's CLI on the B200 path (tools/itertrace_cli.cpp)
+REF_INC = os.environ.get("ITT_REFERENCE_INCLUDE", "/root/reference/proj/include")
 SYNTH_SO = os.path.join(HERE, "libitt_synth.so")
 
 
@@ -59,8 +61,25 @@ def build(verbose: bool = False, jobs: int = 8) -> None:
     if _newer(SYNTH_SO, [synth_src, os.path.join(ROOT, "include", "itt_synth.h")]):
         _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"), "-o", SYNTH_SO,
               synth_src])
+    # the CLI is built against the reference's headers (the types the drop-in keeps); where they are
+    # absent (the GPU box) the prebuilt binary is used
+    cli_src = os.path.join(HERE, "tools", "itertrace_cli.cpp")
+    shim = os.path.join(ROOT, "include", "itertrace_cuda.hpp")
+    if os.path.isdir(os.path.join(REF_INC, "itertrace")) and _newer(CLI_BIN, [cli_src, shim, CUDA_SO]):
+        _run(["g++", "-O2", "-std=c++20", "-I" + os.path.join(ROOT, "include"), "-I" + REF_INC, "-I" + _json_include(),
+              "-o", CLI_BIN, cli_src, "-L" + HERE, "-litertrace_cuda", "-Wl,-rpath,$ORIGIN"])
     if verbose:
         print(f"built {CUDA_SO} ({len(todo)} objects recompiled)")
+
+
+def _json_include() -> str:
+    """nlohmann/json.hpp (the reference's renderer needs it; not vendored by the reference)."""
+    import site
+    for p in site.getsitepackages():
+        d = os.path.join(p, "include", "cudnn_frontend", "thirdparty", "nlohmann")
+        if os.path.exists(os.path.join(d, "json.hpp")):
+            return d
+    raise RuntimeError("nlohmann/json.hpp not found")
 
 
 if __name__ == "__main__":

@@ -149,6 +149,34 @@ void tokens_to_device(Ctx* c, const int32_t* tokens, uint64_t n, DBuf<int32_t>& 
   h2d(c, d.p, tokens, n);
 }
 
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged;
+}
+
+// itt_suffix_array{,_capped}: inputs and outputs in host or device memory
+void suffix_array_any(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa,
+                      uint32_t* lcp) {
+  DBuf<int32_t> dt;
+  const int32_t* tok = tokens;
+  if (n && !is_device_ptr(tokens)) {
+    tokens_to_device(c, tokens, n, dt);
+    tok = dt.p;
+  }
+  SuffixState s;
+  s.keep_levels = lcp != nullptr;
+  radix::Scratch rs;
+  ScanScratch sc;
+  build_suffix_array(c, tok, n, term, s, lcp != nullptr, rs, sc, cap);
+  ITT_CUDA(cudaMemcpyAsync(sa, s.sa.p, (n + 1) * 4, cudaMemcpyDefault, c->stream));
+  if (lcp) ITT_CUDA(cudaMemcpyAsync(lcp, s.lcp.p, (n + 1) * 4, cudaMemcpyDefault, c->stream));
+  c->sync();
+}
+
 }  // namespace
 
 extern "C" {
@@ -411,14 +439,16 @@ int itt_radix_sort_pairs_u32(itt_ctx* ctx, uint32_t* keys, uint32_t* vals, uint6
 int itt_suffix_array(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, uint32_t* sa, uint32_t* lcp) {
   return guarded(ctx, [&](Ctx* c) {
     if (!sa || (n && !tokens)) fail(ITT_E_INVALID_ARGUMENT, "suffix_array: null argument");
-    DBuf<int32_t> dt;
-    tokens_to_device(c, tokens, n, dt);
-    SuffixState s;
-    radix::Scratch rs;
-    ScanScratch sc;
-    build_suffix_array(c, dt.p, n, term, s, lcp != nullptr, rs, sc);
-    d2h(c, sa, s.sa.p, n + 1);
-    if (lcp) d2h(c, lcp, s.lcp.p, n + 1);
+    suffix_array_any(c, tokens, n, term, 0xFFFFFFFFu, sa, lcp);
+  });
+}
+
+int itt_suffix_array_capped(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa,
+                            uint32_t* lcp) {
+  return guarded(ctx, [&](Ctx* c) {
+    if (!sa || (n && !tokens)) fail(ITT_E_INVALID_ARGUMENT, "suffix_array: null argument");
+    if (cap == 0) fail(ITT_E_INVALID_ARGUMENT, "suffix_array: cap must be positive");
+    suffix_array_any(c, tokens, n, term, cap, sa, lcp);
   });
 }
 

@@ -106,6 +106,7 @@ struct SuffixState {
   int rounds = 0;
   uint32_t h_final = 0;       // prefix length the last level separates
   uint32_t cap = 0xFFFFFFFFu; // LCP values are min(lcp, cap); SA exact up to ties of h_final-prefixes
+  bool keep_levels = true;    // false: only the newest two levels stay allocated (SA without LCP at 1B+)
 };
 // tokens: device int32[n]; term: unique terminator.  cap: only the first `cap` symbols matter
 // (mining with max length L_max needs cap = L_max + 1); 0xFFFFFFFF = full suffix array.

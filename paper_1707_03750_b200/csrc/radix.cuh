@@ -24,9 +24,25 @@ namespace radix {
 constexpr int kRadixBits = 8;  // the default digit width (k_hist, generic sorts)
 constexpr int kBins = 256;
 constexpr int kWideBits = 10;  // the wide digit of the SA rounds
-constexpr uint32_t kStA = 1u << 30;  // aggregate
-constexpr uint32_t kStP = 2u << 30;  // inclusive prefix
-constexpr uint32_t kStMask = (1u << 30) - 1;
+// Look-back status words: 2 flag bits (aggregate / inclusive prefix) above the per-digit count.
+// 32-bit words hold counts below 2^30; sorts of 2^30 or more keys (one digit can then hold 2^30+
+// keys) use 64-bit words (radix_sort_pairs picks them by n).
+template <typename SW>
+struct Status {
+  static constexpr int kShift = static_cast<int>(sizeof(SW)) * 8 - 2;
+  static constexpr SW kA = SW(1) << kShift;  // aggregate
+  static constexpr SW kP = SW(2) << kShift;  // inclusive prefix
+  static constexpr SW kMask = kA - 1;
+  __device__ __forceinline__ static SW load(const SW* p) {
+    if constexpr (sizeof(SW) == 8) return ld_relaxed_u64(p);
+    else return ld_relaxed_u32(p);
+  }
+  __device__ __forceinline__ static void store(SW* p, SW v) {
+    if constexpr (sizeof(SW) == 8) st_relaxed_u64(p, v);
+    else st_relaxed_u32(p, v);
+  }
+};
+constexpr uint64_t kWideStatusN = 1ull << 30;  // sorts of at least this many keys use 64-bit words
 constexpr int kLook = 4;  // look-back window per step (A/B on C2: 1 -> 1.27 ms, 4 and 8 -> 1.16 ms of passes per step)
 
 template <int RB, typename K>
@@ -127,10 +143,11 @@ struct SmemLayout {
   uint32_t tile;
 };
 
-template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB, int RB>
+template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB, int RB, typename SW>
 __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                           uint64_t n, int shift, const uint32_t* __restrict__ digit_hist,
-                                                          uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+                                                          SW* __restrict__ status, uint32_t* __restrict__ counter) {
+  using St = Status<SW>;
   using S_t = SmemLayout<K, BLOCK, ITEMS, RB>;
   constexpr int kTile = S_t::kTile;
   constexpr int kWarps = S_t::kWarps;
@@ -200,7 +217,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
         sum += c;
       }
       cnt[q] = sum;
-      st_relaxed_u32(status + static_cast<uint64_t>(tile) * kDigits + d, (tile == 0 ? kStP : kStA) | sum);
+      St::store(status + static_cast<uint64_t>(tile) * kDigits + d, (tile == 0 ? St::kP : St::kA) | SW(sum));
       csum += sum;
       hsum += hv[q];
     }
@@ -250,22 +267,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
 #pragma unroll
       for (int q = 0; q < DPT; ++q) done[q] = false;
       for (int64_t t = static_cast<int64_t>(tile) - 1;; t -= kLook) {
-        uint32_t sv[DPT][kLook];
+        SW sv[DPT][kLook];
 #pragma unroll
         for (int q = 0; q < DPT; ++q)
 #pragma unroll
           for (int u = 0; u < kLook; ++u)
-            sv[q][u] = (!done[q] && t - u >= 0) ? ld_relaxed_u32(status + static_cast<uint64_t>(t - u) * kDigits + d0 + q) : 0u;
+            sv[q][u] = (!done[q] && t - u >= 0) ? St::load(status + static_cast<uint64_t>(t - u) * kDigits + d0 + q) : SW(0);
         bool all = true;
 #pragma unroll
         for (int q = 0; q < DPT; ++q) {
 #pragma unroll
           for (int u = 0; u < kLook; ++u) {
             if (done[q]) break;
-            uint32_t v = sv[q][u];
-            while ((v >> 30) == 0) v = ld_relaxed_u32(status + static_cast<uint64_t>(t - u) * kDigits + d0 + q);
-            excl[q] += v & kStMask;
-            done[q] = (v >> 30) == 2;
+            SW v = sv[q][u];
+            while ((v >> St::kShift) == 0) v = St::load(status + static_cast<uint64_t>(t - u) * kDigits + d0 + q);
+            excl[q] += static_cast<uint32_t>(v & St::kMask);
+            done[q] = (v >> St::kShift) == 2;
           }
           all = all && done[q];
         }
@@ -273,7 +290,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
       }
 #pragma unroll
       for (int q = 0; q < DPT; ++q)
-        st_relaxed_u32(status + static_cast<uint64_t>(tile) * kDigits + d0 + q, kStP | (excl[q] + cnt[q]));
+        St::store(status + static_cast<uint64_t>(tile) * kDigits + d0 + q, St::kP | SW(excl[q] + cnt[q]));
     }
 #pragma unroll
     for (int q = 0; q < DPT; ++q) S.global_base[d0 + q] = gofs[q] + excl[q];
@@ -303,20 +320,40 @@ constexpr int kCfgBlock[] = {512, 256, 384, 256, 512, 512, 512, 256, 256, 256};
 constexpr int kCfgItems[] = {8, 16, 12, 8, 16, 8, 8, 8, 16, 12};
 int config_index();
 
+// st: this pass's scratch: word 0 = tile counter, then the look-back words (u32 from word 1, or
+// u64 from word 2 when n >= kWideStatusN)
 template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB = 1024 / BLOCK, int RB = kRadixBits>
 void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* dhist, uint32_t* st) {
   constexpr int TILE = BLOCK * ITEMS;
   const size_t smem = sizeof(SmemLayout<K, BLOCK, ITEMS, RB>);
-  auto kern = k_onesweep<K, BLOCK, ITEMS, Loader, MINB, RB>;
-  smem_optin(c, kern, smem);
   const uint64_t tiles = (n + TILE - 1) / TILE;
-  launch(c, RB == kRadixBits ? "radix_onesweep" : "radix_onesweep_w10", static_cast<double>(n) * 2.0 * (sizeof(K) + 4), kern,
-         dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, dhist, st + 1, st);
+  const char* name = RB == kRadixBits ? "radix_onesweep" : "radix_onesweep_w10";
+  const double bytes = static_cast<double>(n) * 2.0 * (sizeof(K) + 4);
+  if (n >= kWideStatusN) {
+    auto kern = k_onesweep<K, BLOCK, ITEMS, Loader, MINB, RB, uint64_t>;
+    smem_optin(c, kern, smem);
+    launch(c, name, bytes, kern, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, dhist,
+           reinterpret_cast<uint64_t*>(st + 2), st);
+  } else {
+    auto kern = k_onesweep<K, BLOCK, ITEMS, Loader, MINB, RB, uint32_t>;
+    smem_optin(c, kern, smem);
+    launch(c, name, bytes, kern, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, dhist, st + 1,
+           st);
+  }
+}
+
+// u32 scratch words one pass of n keys needs (counter + look-back words, see launch_pass)
+inline size_t pass_status_words(uint64_t n, uint64_t tiles, int digits) {
+  return n >= kWideStatusN ? 2 * (tiles * digits + 1) : tiles * digits + 1;
 }
 
 template <typename K, int RB, typename Loader>
 void dispatch_pass(Ctx* c, int cfg, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int shift, const uint32_t* dhist,
                    uint32_t* st) {
+  if (n >= kWideStatusN) {  // 64-bit look-back words: one tile shape only
+    launch_pass<K, 512, 8, Loader, 2, RB>(c, ld, ko, vo, n, shift, dhist, st);
+    return;
+  }
   if constexpr (RB != kRadixBits) {
     launch_pass<K, 512, 8, Loader, 2, RB>(c, ld, ko, vo, n, shift, dhist, st);
   } else {
@@ -346,11 +383,11 @@ inline uint64_t tile_of(int cfg) {
 // anyway), so that sort can pass status_zeroed = true.  Sized for up to passes8 8-bit or passes_w
 // wide passes.
 inline void radix_prezero_status(Ctx* c, radix::Scratch& s, uint64_t n, int passes8, int passes_w) {
-  const int cfg = radix::config_index();
+  const int cfg = n >= radix::kWideStatusN ? 0 : radix::config_index();  // 64-bit words: one tile shape
   const uint64_t t8 = (n + radix::tile_of<radix::kRadixBits>(cfg) - 1) / radix::tile_of<radix::kRadixBits>(cfg);
   const uint64_t tw = (n + radix::tile_of<radix::kWideBits>(cfg) - 1) / radix::tile_of<radix::kWideBits>(cfg);
-  const size_t need = std::max((t8 * (1u << radix::kRadixBits) + 1) * static_cast<size_t>(passes8),
-                               (tw * (1u << radix::kWideBits) + 1) * static_cast<size_t>(passes_w));
+  const size_t need = std::max(radix::pass_status_words(n, t8, 1 << radix::kRadixBits) * static_cast<size_t>(passes8),
+                               radix::pass_status_words(n, tw, 1 << radix::kWideBits) * static_cast<size_t>(passes_w));
   if (s.status.n < need) s.status.alloc(c, need);
   ITT_CUDA(cudaMemsetAsync(s.status.p, 0, need * 4, c->stream));
 }
@@ -369,7 +406,7 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
   constexpr int kD = 1 << RB;
   if (end_bit <= begin_bit) end_bit = begin_bit + 1;
   const int passes = (end_bit - begin_bit + RB - 1) / RB;
-  const int cfg = config_index();
+  const int cfg = n >= kWideStatusN ? 0 : config_index();  // 64-bit look-back words: one tile shape
   const uint64_t tiles = (n + tile_of<RB>(cfg) - 1) / tile_of<RB>(cfg);
   if (n == 0) return false;
   const uint32_t* hist = hist_in;
@@ -399,7 +436,7 @@ bool radix_sort_pairs(Ctx* c, K* keys, uint32_t* vals, K* keys_alt, uint32_t* va
   }
   if (first_loader && (live.empty() || live[0] != 0)) live.insert(live.begin(), 0);  // the loader must run
   if (live.empty()) return false;
-  const size_t per_pass = tiles * kD + 1;
+  const size_t per_pass = pass_status_words(n, tiles, kD);
   if (status_zeroed) {  // the caller zeroed the look-back words ahead of time (radix_prezero_status)
     if (s.status.n < per_pass * live.size()) fail(ITT_E_INVALID_ARGUMENT, "internal: radix status not prepared");
   } else {

@@ -467,6 +467,8 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
         continue;
       }
       s.level_tags.push_back(lvl);
+      // the level before the previous one is read by nothing queued after this launch
+      if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
       cur ^= 1;
       return total;
     }

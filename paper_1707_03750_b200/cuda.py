@@ -73,6 +73,7 @@ def lib() -> C.CDLL:
         "itt_count_interval_overlaps": ([vp, P(abi.itt_records), C.c_uint32, P(C.c_int64)], C.c_int),
         "itt_radix_sort_pairs_u32": ([vp, vp, vp, C.c_uint64, C.c_int, C.c_int, C.c_int], C.c_int),
         "itt_suffix_array": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, P(C.c_uint32), P(C.c_uint32)], C.c_int),
+        "itt_suffix_array_capped": ([vp, vp, C.c_uint64, C.c_int32, C.c_uint32, vp, vp], C.c_int),
         "itt_enumerate_repeats": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, C.c_int64, C.c_int64,
                                    P(P(abi.itt_repeat)), P(C.c_uint64)], C.c_int),
         "itt_mine_patterns": ([vp, P(C.c_int32), C.c_uint64, C.c_int32, P(abi.itt_mining_cfg), C.c_uint32, C.c_int,
@@ -270,6 +271,12 @@ class Context:
         self._check(lib().itt_suffix_array(self.h, _ptr(t, C.c_int32), n, term, _ptr(sa, C.c_uint32),
                                            _ptr(lcp, C.c_uint32) if want_lcp else None))
         return sa, lcp
+
+    def suffix_array_device(self, tokens_ptr: int, n: int, term: int, sa_ptr: int, lcp_ptr: int = 0,
+                            cap: int = 0xFFFFFFFF):
+        """itt_suffix_array_capped on device (or host) addresses; lcp_ptr = 0: no LCP."""
+        self._check(lib().itt_suffix_array_capped(self.h, C.c_void_p(tokens_ptr), n, term, cap, C.c_void_p(sa_ptr),
+                                                  C.c_void_p(lcp_ptr) if lcp_ptr else None))
 
     def enumerate_repeats(self, tokens, term, min_count, max_len):
         t = _i32(tokens)
