@@ -580,6 +580,23 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 __device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Bulk L2 prefetch (cp.async.bulk.prefetch.L2, sm_90+) of [p, p + bytes): the 16-byte aligned
+// interior only.  Streaming kernels whose CTAs each take one tile issue it for the tile the CTA
+// launched one residency wave later will take, so that CTA's loads hit L2 and DRAM stays busy
+// while the resident CTAs rank / scan / look back.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint64_t bytes) {
+  const uint64_t a = (reinterpret_cast<uint64_t>(p) + 15) & ~15ull;
+  const uint64_t e = (reinterpret_cast<uint64_t>(p) + bytes) & ~15ull;
+  if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(e - a)) : "memory");
+}
+// tiles ahead to prefetch: one residency wave (CTAs per SM x SMs); ITT_L2_PREFETCH=0 disables
+inline uint32_t prefetch_distance(int sm_count, int ctas_per_sm) {
+  static const int on = [] {
+    const char* e = std::getenv("ITT_L2_PREFETCH");
+    return e && *e ? std::atoi(e) : 1;
+  }();
+  return on > 0 ? static_cast<uint32_t>(sm_count * ctas_per_sm * on) : 0u;
+}
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -592,4 +609,5 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 namespace itt {
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 }  // namespace itt

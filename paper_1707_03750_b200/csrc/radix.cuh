@@ -59,6 +59,10 @@ struct ArrayLoader {
     k = __ldcs(&keys[i]);  // streaming: evict-first, keeps L2 for the random-access arrays
     v = __ldcs(&vals[i]);
   }
+  __device__ __forceinline__ void prefetch(uint64_t i, uint64_t cnt) const {
+    prefetch_l2(keys + i, cnt * sizeof(K));
+    prefetch_l2(vals + i, cnt * 4);
+  }
 };
 
 // Lanes of the warp holding the same RB-bit digit (valid lanes only among themselves): ballots
@@ -146,7 +150,8 @@ struct SmemLayout {
 template <typename K, int BLOCK, int ITEMS, typename Loader, int MINB, int RB, typename SW>
 __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                           uint64_t n, int shift, const uint32_t* __restrict__ digit_hist,
-                                                          SW* __restrict__ status, uint32_t* __restrict__ counter) {
+                                                          SW* __restrict__ status, uint32_t* __restrict__ counter,
+                                                          uint32_t pf_dist) {
   using St = Status<SW>;
   using S_t = SmemLayout<K, BLOCK, ITEMS, RB>;
   constexpr int kTile = S_t::kTile;
@@ -173,6 +178,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
   __syncthreads();
   const uint32_t tile = S.tile;
   const uint64_t tile_base = static_cast<uint64_t>(tile) * kTile;
+  if (pf_dist && threadIdx.x == 0) {  // the tile the CTA one residency wave later takes
+    const uint64_t pb = tile_base + static_cast<uint64_t>(pf_dist) * kTile;
+    if (pb < n) ld.prefetch(pb, umin64(kTile, n - pb));
+  }
   const uint64_t warp_base = tile_base + static_cast<uint64_t>(warp) * (32 * ITEMS);
 
   K key[ITEMS];
@@ -333,12 +342,12 @@ void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int 
     auto kern = k_onesweep<K, BLOCK, ITEMS, Loader, MINB, RB, uint64_t>;
     smem_optin(c, kern, smem);
     launch(c, name, bytes, kern, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, dhist,
-           reinterpret_cast<uint64_t*>(st + 2), st);
+           reinterpret_cast<uint64_t*>(st + 2), st, prefetch_distance(c->sm_count, MINB));
   } else {
     auto kern = k_onesweep<K, BLOCK, ITEMS, Loader, MINB, RB, uint32_t>;
     smem_optin(c, kern, smem);
     launch(c, name, bytes, kern, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), smem, ld, ko, vo, n, shift, dhist, st + 1,
-           st);
+           st, prefetch_distance(c->sm_count, MINB));
   }
 }
 

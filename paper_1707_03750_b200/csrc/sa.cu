@@ -106,6 +106,7 @@ struct EmitLoader {
     k = rank_at(rank, i);
     v = i;
   }
+  __device__ __forceinline__ void prefetch(uint64_t j, uint64_t cnt) const { prefetch_l2(sa + j, cnt * 4); }
 };
 
 // New dense ids.  flag_j = (key_j, r2_j) != (key_{j-1}, r2_{j-1}) with key = old id of SA_j (the
@@ -116,7 +117,8 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
                                                             uintptr_t rank_old, uint32_t h, uint64_t np,
                                                             uintptr_t rank_new, uint32_t* __restrict__ hist_next,
                                                             int passes, uint32_t* __restrict__ gstart,
-                                                            uint64_t* status, uint32_t* counter) {
+                                                            uint64_t* status, uint32_t* counter, uint32_t pf_dist,
+                                                            uint8_t* __restrict__ heads_out) {
   __shared__ uint32_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_hist[kMaxPasses][256];
@@ -125,6 +127,14 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t base = static_cast<uint64_t>(tile) * (kRankBlock * kRankItems) + static_cast<uint64_t>(threadIdx.x) * kRankItems;
+  if (pf_dist && threadIdx.x == 0) {  // keys + SA of the tile one residency wave later
+    const uint64_t pb = (static_cast<uint64_t>(tile) + pf_dist) * (kRankBlock * kRankItems);
+    if (pb < np) {
+      const uint64_t cnt = umin64(kRankBlock * kRankItems, np - pb);
+      prefetch_l2(keys + pb, cnt * 4);
+      prefetch_l2(sa + pb, cnt * 4);
+    }
+  }
   auto second = [&](uint32_t x) -> uint32_t {
     if (!rank_old) return 0u;
     const uint64_t y = static_cast<uint64_t>(x) + h;
@@ -167,6 +177,7 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
       pr = r2[q];
     }
   }
+  if (heads_out && base < np) heads_out[base / kRankItems] = static_cast<uint8_t>(fmask);  // group heads, SA order
   const uint32_t run = __popc(fmask);
   uint32_t total;
   const uint32_t texcl = block_exclusive_scan<uint32_t, SumOp<uint32_t>, kRankBlock>(run, SumOp<uint32_t>(), &total, s_warp);
@@ -228,6 +239,125 @@ __global__ void k_wide_hist(const uint32_t* __restrict__ gstart, uint64_t g, uin
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kW; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// ---------------------------------------------------------------- refinement rounds
+// A doubling round that finds every group already ordered by its second key needs no sort: the
+// SA stays, groups split where the second key changes.  Traces of training loops reach this state
+// after a few rounds (every group is one rotation class of the loop body; a round only splits off
+// the members whose second half reaches the end of the trace, and they already sit last in their
+// group, in order).  Within a group the members are in text-position order (every sort is stable
+// from the position order of the first one), so the check is: for each non-head j, r2_j >= r2_{j-1}.
+// Levels written by refinement rounds hold the SA position of the group head (u32) instead of a
+// dense id: then a round rewrites only the ranks of suffixes whose group head moved.
+struct HeadPair {  // (last new head + 1, last old head + 1) in two 31-bit halves; positions < 2^31
+  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
+    const uint64_t m = (1ull << 31) - 1;
+    return (umax64(a >> 31, b >> 31) << 31) | umax64(a & m, b & m);
+  }
+  static __device__ __forceinline__ uint64_t identity() { return 0; }
+};
+
+// r2_j = rank_h[SA_j + h] (kNone past the end); new head flags; counts of new groups and inversions
+__global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __restrict__ sa, const uint8_t* __restrict__ heads,
+                                                             uintptr_t rank, uint32_t h, uint64_t np,
+                                                             uint8_t* __restrict__ heads_next,
+                                                             unsigned long long* __restrict__ counts /*[0] groups, [1] inversions*/) {
+  __shared__ uint32_t s_last[kRankBlock / 32];
+  __shared__ unsigned long long s_cnt[2];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+  const uint64_t base = (static_cast<uint64_t>(blockIdx.x) * kRankBlock + threadIdx.x) * kRankItems;
+  auto second = [&](uint32_t x) -> uint32_t {
+    const uint64_t y = static_cast<uint64_t>(x) + h;
+    return y < np ? rank_at(rank, y) : kNone;
+  };
+  uint32_t r2[kRankItems];
+  uint8_t hb = 0;
+  if (base < np) {
+    hb = heads[base / kRankItems];
+    if (base + kRankItems <= np) {
+#pragma unroll
+      for (int q = 0; q < kRankItems; q += 4) {
+        const uint4 a = __ldcs(reinterpret_cast<const uint4*>(sa + base + q));
+        r2[q] = second(a.x), r2[q + 1] = second(a.y), r2[q + 2] = second(a.z), r2[q + 3] = second(a.w);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kRankItems; ++q) r2[q] = base + q < np ? second(sa[base + q]) : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRankItems; ++q) r2[q] = 0u;
+  }
+  // r2 of item base - 1: the previous lane, the previous warp, or (thread 0) one more gather
+  uint32_t prev = __shfl_up_sync(0xffffffffu, r2[kRankItems - 1], 1);
+  if (lane == 31) s_last[warp] = r2[kRankItems - 1];
+  __syncthreads();
+  if (lane == 0) prev = warp > 0 ? s_last[warp - 1] : (base > 0 && base < np ? second(sa[base - 1]) : 0u);
+  uint32_t nh = 0, inv = 0;
+#pragma unroll
+  for (int q = 0; q < kRankItems; ++q) {
+    const uint64_t j = base + q;
+    if (j < np) {
+      const bool head = j == 0 || ((hb >> q) & 1u);
+      if (!head && r2[q] < prev) ++inv;
+      if (head || r2[q] != prev) nh |= 1u << q;
+    }
+    prev = r2[q];
+  }
+  if (base < np) heads_next[base / kRankItems] = static_cast<uint8_t>(nh);
+  uint32_t g = __popc(nh);
+  for (int o = 16; o > 0; o >>= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    inv += __shfl_xor_sync(0xffffffffu, inv, o);
+  }
+  if (lane == 0) {
+    if (g) atomicAdd(&s_cnt[0], static_cast<unsigned long long>(g));
+    if (inv) atomicAdd(&s_cnt[1], static_cast<unsigned long long>(inv));
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+// rank_{2h}[SA_j] = position of j's new group head, written where it differs from the old head
+// (all j when the previous level holds dense ids): a max-scan of (last new head, last old head)
+// over SA order with decoupled look-back
+__global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint8_t* __restrict__ heads_old,
+                                                            const uint8_t* __restrict__ heads_new, uint64_t np,
+                                                            uint32_t* __restrict__ level, int full, uint64_t* status,
+                                                            uint32_t* counter) {
+  __shared__ uint64_t s_warp[kRankBlock / 32];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = static_cast<uint64_t>(tile) * (kRankBlock * kRankItems) + static_cast<uint64_t>(threadIdx.x) * kRankItems;
+  const uint32_t ho = base < np ? heads_old[base / kRankItems] : 0u;
+  const uint32_t hn = base < np ? heads_new[base / kRankItems] : 0u;
+  // this run's last heads (+1; 0 = none)
+  const uint64_t ln = hn ? base + (31 - __clz(hn)) + 1 : 0;
+  const uint64_t lo = ho ? base + (31 - __clz(ho)) + 1 : 0;
+  const HeadPair op;
+  uint64_t total;
+  const uint64_t texcl = block_exclusive_scan<uint64_t, HeadPair, kRankBlock>((ln << 31) | lo, op, &total, s_warp);
+  if (threadIdx.x < 32) {
+    const uint64_t p = tile_lookback<uint64_t, HeadPair>(status, tile, total, op);
+    if (threadIdx.x == 0) s_prefix = p;
+  }
+  __syncthreads();
+  const uint64_t pre = op(s_prefix, texcl);
+  uint64_t cn = pre >> 31, co = pre & ((1ull << 31) - 1);  // last heads before this run (+1)
+#pragma unroll
+  for (int q = 0; q < kRankItems; ++q) {
+    const uint64_t j = base + q;
+    if (j < np) {
+      if ((hn >> q) & 1u) cn = j + 1;
+      if ((ho >> q) & 1u) co = j + 1;
+      if (full || cn != co) level[__ldcs(&sa[j])] = static_cast<uint32_t>(cn - 1);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- LCP
@@ -429,6 +559,10 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   hists[0].zero();
   scans[0]->prepare(c, rtiles);
   uint32_t* hist_p = nullptr;  // the histograms the latest rank update produced
+  // group heads in SA order, one byte per 8 positions: written by every round, read by refinement
+  DBuf<uint8_t> heads[2];
+  for (auto& hb : heads) hb.alloc(c, rtiles * kRankBlock);
+  int hc = 0;
   // one rank update into a new level (u16 when the previous group count suggests the ids fit; if
   // they do not, the update runs again into a u32 level: its inputs are untouched)
   auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, uintptr_t rank_old, uint32_t h, bool more,
@@ -445,7 +579,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       hist_p = hists[cur].p;
       launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
              dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, gstart.p, sc.buf.p + 1,
-             reinterpret_cast<uint32_t*>(sc.buf.p));
+             reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p);
       // group count G: the last tile's inclusive word, copied out and waited on by event, so the
       // next round's scratch zeroing (queued after the copy) runs while the host wakes up
       ++StageTimer::syncs();
@@ -470,16 +604,57 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       // the level before the previous one is read by nothing queued after this launch
       if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
       cur ^= 1;
+      hc ^= 1;
       return total;
     }
   };
   uint64_t g = rank_update(keys, sa, 0, 0, s.h0 < cap, 0);
   uint32_t h = s.h0;  // prefix length the newest level separates
+  bool dense = true;  // the newest level holds dense ids (else group-head positions)
+  static const int refine_mode = [] {  // ITT_SA_REFINE=0: full rounds only (A/B, tests)
+    const char* e = std::getenv("ITT_SA_REFINE");
+    return e && *e ? std::atoi(e) : 1;
+  }();
+  bool try_refine = false;  // decided after each full round from how many groups it added
+  int cooldown = 0;
+  DBuf<unsigned long long> rcount(c, 2);
+  DBuf<uint32_t> head_hist;
+  ScanScratch rscan;
   // stop when every suffix is alone, or when the groups already separate `cap` symbols (mining
   // never looks deeper than its L_max; see k_plcp for why the capped LCP stays exact below cap)
   while (g < np && h < cap) {
     const uintptr_t rank = s.level_tags.back();
-    const int b = bits_for(g - 1);
+    if (try_refine && cooldown == 0) {
+      // ---- refinement round: no sort when every group is already ordered by its second key
+      rcount.zero();
+      launch(c, "sa_refine_detect", np * 9.125, k_refine_detect, dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock), 0, sa,
+             heads[hc].p, rank, h, np, heads[hc ^ 1].p, rcount.p);
+      unsigned long long cnt[2];
+      readback(c, cnt, rcount.p, 2);
+      if (cnt[1] == 0) {
+        s.levels.emplace_back(c, np);
+        uint32_t* lvl = s.levels.back().p;
+        const bool full = dense;  // dense ids: every rank changes representation
+        if (!full) ITT_CUDA(cudaMemcpyAsync(lvl, reinterpret_cast<const uint32_t*>(rank), np * 4, cudaMemcpyDeviceToDevice,
+                                            c->stream));
+        rscan.prepare(c, rtiles);
+        launch(c, "sa_refine_apply", np * (full ? 10.25 : 2.25) + (full ? 0.0 : np * 8.0), k_refine_apply,
+               dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock), 0, sa, heads[hc].p, heads[hc ^ 1].p, np, lvl,
+               full ? 1 : 0, rscan.buf.p + 1, reinterpret_cast<uint32_t*>(rscan.buf.p));
+        s.level_tags.push_back(reinterpret_cast<uintptr_t>(lvl));
+        if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
+        hc ^= 1;
+        dense = false;
+        g = cnt[0];
+        ++s.rounds;
+        if (static_cast<uint64_t>(h) * 2 > 0xFFFFFFFFull) break;
+        h *= 2;
+        continue;
+      }
+      cooldown = 2;  // inversions: sort this round, try again two rounds later
+    }
+    // ---- full round: stable sort of E_j = SA_j - h by rank_h (the E trick) + rank update
+    const int b = dense ? bits_for(g - 1) : bits_for(np - 1);
     const EmitLoader ld{sa, rank, np, h};
     // the SA buffer is read by the first pass, so the sort only writes the other buffers:
     // pass 1: loader(sa) -> (f1, f2); pass 2: (f1, f2) -> (kx, vx); pass 3: -> (f1, f2) ...
@@ -490,23 +665,48 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       const char* e = std::getenv("ITT_NO_WIDE_DIGITS");
       return e && *e && *e != '0';
     }();
-    const bool wide = !no_wide && g <= kWideGroups && (b + radix::kWideBits - 1) / radix::kWideBits < (b + 7) / 8;
+    const bool wide = !no_wide && (!dense || g <= kWideGroups) &&
+                      (b + radix::kWideBits - 1) / radix::kWideBits < (b + 7) / 8;
+    const uint32_t* hist8 = hist_p;
     uint32_t* whist = hist_p + kMaxPasses * 256;
-    if (wide) {
+    if (!dense) {  // keys are head positions: digit histograms straight from the level
+      const int rb = wide ? radix::kWideBits : 8;
+      const int passes = (b + rb - 1) / rb;
+      head_hist.alloc(c, static_cast<size_t>(passes) << rb);
+      head_hist.zero();
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((np + 255) / 256, static_cast<uint64_t>(c->sm_count) * 8));
+      const size_t smem = (static_cast<size_t>(passes) << rb) * 4;
+      if (wide) {
+        smem_optin(c, radix::k_hist<uint32_t, radix::kWideBits>, smem);
+        launch(c, "radix_hist", np * 4.0, radix::k_hist<uint32_t, radix::kWideBits>, dim3(grid), dim3(256), smem,
+               reinterpret_cast<const uint32_t*>(rank), np, 0, passes, head_hist.p);
+        whist = head_hist.p;
+      } else {
+        smem_optin(c, radix::k_hist<uint32_t, 8>, smem);
+        launch(c, "radix_hist", np * 4.0, radix::k_hist<uint32_t, 8>, dim3(grid), dim3(256), smem,
+               reinterpret_cast<const uint32_t*>(rank), np, 0, passes, head_hist.p);
+        hist8 = head_hist.p;
+      }
+    } else if (wide) {
       const int pw = (b + radix::kWideBits - 1) / radix::kWideBits;
       launch(c, "sa_wide_hist", g * 8.0, k_wide_hist, dim3(grid_for(g, 256, c->sm_count * 4)), dim3(256), 0, gstart.p, g, np, pw,
              whist);
     }
     const bool alt = wide ? radix_sort_pairs<uint32_t, EmitLoader, radix::kWideBits>(c, kx, vx, f1, f2, np, 0, b, rs, whist,
                                                                                        &ld, false, false)
-                          : radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist_p, &ld, false,
+                          : radix_sort_pairs<uint32_t, EmitLoader>(c, kx, vx, f1, f2, np, 0, b, rs, hist8, &ld, false,
                                                                    /*status_zeroed=*/true);
     uint32_t* nkeys = alt ? f1 : kx;
     uint32_t* nsa = alt ? f2 : vx;
     uint32_t* other_k = alt ? kx : f1;
     uint32_t* other_v = alt ? vx : f2;
+    const uint64_t g_old = g;
     g = rank_update(nkeys, nsa, rank, h, static_cast<uint64_t>(h) * 2 < cap, g);
+    dense = true;
     ++s.rounds;
+    if (cooldown > 0) --cooldown;
+    // few new groups: the structure has settled (a periodic trace) — try refinement next round
+    try_refine = refine_mode > 0 && np < (1ull << 31) && (g - g_old) * 16 < np;
     // rotate: new SA / keys; the old SA and the unused pair become free
     spare = sa;
     sa = nsa;
