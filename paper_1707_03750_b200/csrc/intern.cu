@@ -44,6 +44,11 @@ __device__ __forceinline__ int kind_from(uint8_t nb, bool has_tp) {
 }
 
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+// low n (< 8) bytes of w, or w
+__device__ __forceinline__ uint64_t low_bytes(uint64_t w, uint32_t n) {
+  return n >= 8 ? w : (w & ((1ull << (8 * n)) - 1ull));
+}
+
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   k ^= k >> 33;
   k *= 0xff51afd7ed558ccdull;
@@ -72,9 +77,8 @@ __device__ __forceinline__ uint64_t hash_name(Get get, uint32_t len, uint64_t se
 
 // Stage the name bytes of rows [g0, g1) into a per-warp shared buffer with 16-byte loads.
 // Returns false when they do not fit (the caller then reads global memory directly).
-__device__ __forceinline__ bool stage_names(const uint64_t* __restrict__ name_off, const uint8_t* __restrict__ bytes,
-                                            uint64_t total, uint64_t g0, uint64_t g1, uint8_t* buf, uint64_t& base) {
-  const uint64_t b0 = name_off[g0], b1 = name_off[g1];
+__device__ __forceinline__ bool stage_names(const uint8_t* __restrict__ bytes, uint64_t total, uint64_t b0, uint64_t b1,
+                                            uint8_t* buf, uint64_t& base) {
   const uint64_t a0 = b0 & ~15ull, a1 = (b1 + 15) & ~15ull;
   if (a1 - a0 > static_cast<uint64_t>(kWarpBuf)) return false;
   const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
@@ -285,22 +289,21 @@ __device__ __forceinline__ bool same_bytes(const A& p, const B& q, uint32_t len)
     if (p.byte(i) != q.byte(i)) return false;
   return true;
 }
-// both runs in shared memory: two streams, one LDS per side per 4 bytes
+// both runs in shared memory: two streams, one LDS per side per 4 bytes, 8 bytes per step; the
+// 0-7 byte tail as one masked 8-byte compare (staging buffers are padded)
 __device__ __forceinline__ bool same_bytes(const SharedBytes& p, const SharedBytes& q, uint32_t len) {
+  SharedStream a(p), b(q);
   uint32_t i = 0;
-  if (len >= 8) {
-    SharedStream a(p), b(q);
-    for (; i + 12 <= len; i += 8) {  // 8 bytes and one branch per step
-      const uint32_t x0 = a.next4(), y0 = b.next4();
-      const uint32_t x1 = a.next4(), y1 = b.next4();
-      if ((x0 ^ y0) | (x1 ^ y1)) return false;
-    }
-    for (; i + 8 <= len; i += 4)
-      if (a.next4() != b.next4()) return false;
+  uint32_t diff = 0;
+  for (; i + 8 <= len; i += 8) {
+    const uint32_t x0 = a.next4(), y0 = b.next4();
+    const uint32_t x1 = a.next4(), y1 = b.next4();
+    diff |= (x0 ^ y0) | (x1 ^ y1);
   }
-  for (; i < len; ++i)
-    if (p.byte(i) != q.byte(i)) return false;
-  return true;
+  const uint32_t x0 = a.next4(), y0 = b.next4();
+  const uint32_t x1 = a.next4(), y1 = b.next4();
+  const uint64_t d = (static_cast<uint64_t>(x0 ^ y0) | (static_cast<uint64_t>(x1 ^ y1) << 32));
+  return diff == 0 && low_bytes(d, len - i) == 0;
 }
 
 struct HashArgs {
@@ -323,21 +326,20 @@ struct HashArgs {
   uint32_t* dev_max;
 };
 
-// 64-bit hash of a name staged in shared memory: 8-byte words from two funnel-shifted aligned
-// loads (the staging buffer is padded, so the word reads stay in bounds)
+// 64-bit hash of a name staged in shared memory: 8-byte words from funnel-shifted aligned loads;
+// the 0-7 byte tail is the next 8 staged bytes masked (the staging buffers are padded, so every
+// read stays in bounds) — no byte loop
 __device__ __forceinline__ uint64_t hash_staged(const SharedBytes& p, uint32_t len, uint64_t seed) {
   uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
+  SharedStream st(p);
   uint32_t i = 0;
-  if (len >= 8) {
-    SharedStream st(p);
-    for (; i + 8 <= len; i += 8) {
-      const uint32_t lo = st.next4();
-      const uint64_t w = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(st.next4()) << 32);
-      h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
-    }
+  for (; i + 8 <= len; i += 8) {
+    const uint32_t lo = st.next4();
+    const uint64_t w = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(st.next4()) << 32);
+    h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
   }
-  uint64_t w = 0;
-  for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(p.byte(i + j)) << (8 * j);
+  const uint32_t lo = st.next4();
+  const uint64_t w = low_bytes(static_cast<uint64_t>(lo) | (static_cast<uint64_t>(st.next4()) << 32), len - i);
   h = rotl64(h ^ (w * 0x87c37b91114253d5ull + len), 31) * 0x4cf5ad432745937full;
   h = fmix64(h);
   return h ? h : 1;  // bit-identical to hash_name (the unstaged path): one name, one hash
@@ -360,15 +362,32 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
   const uint64_t groups = (a.n - a.row0 + 31) / 32;
   const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
   bool bad = false;
-  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp; g < groups; g += gstride) {
+  // name offsets: one load per lane (+ lane 31 the group's end), issued one group ahead
+  auto offsets = [&](uint64_t g, uint64_t& off, uint64_t& nxt) {
+    const uint64_t r0 = a.row0 + g * 32;
+    off = g < groups ? __ldg(&a.name_off[umin64(r0 + lane, a.n)]) : 0;
+    nxt = g < groups && lane == 31 ? __ldg(&a.name_off[umin64(r0 + 32, a.n)]) : 0;
+  };
+  uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
+  uint64_t off_n, end_n;
+  offsets(g, off_n, end_n);
+  for (; g < groups; g += gstride) {
     const uint64_t g0 = a.row0 + g * 32, g1 = min(g0 + 32, a.n);
     const uint64_t row = g0 + lane;
     const bool valid = row < a.n;
+    uint64_t my_off = off_n, my_end = end_n;
+    offsets(g + gstride, off_n, end_n);  // the next group's, in flight while this one is processed
+    {
+      const uint64_t down = __shfl_down_sync(0xffffffffu, my_off, 1);
+      my_end = lane == 31 ? my_end : down;  // name_off[row + 1]
+    }
     uint64_t base = 0;
-    const bool staged = stage_names(a.name_off, a.bytes, a.total, g0, g1, buf, base);
+    const uint64_t b0 = __shfl_sync(0xffffffffu, my_off, 0);
+    const uint64_t b1 = __shfl_sync(0xffffffffu, my_end, static_cast<int>(g1 - g0 - 1));
+    const bool staged = stage_names(a.bytes, a.total, b0, b1, buf, base);
     if (valid) {
-      const uint64_t o = a.name_off[row];
-      const uint32_t len = static_cast<uint32_t>(a.name_off[row + 1] - o);
+      const uint64_t o = my_off;
+      const uint32_t len = static_cast<uint32_t>(my_end - o);
       // separate shared / global paths so the staged case compiles to LDS, not generic loads
       const uint64_t h = staged ? hash_staged(SharedBytes(buf + (o - base)), len, a.seed)
                                 : hash_name([&](uint32_t i) { return a.bytes[o + i]; }, len, a.seed);
@@ -1171,7 +1190,9 @@ void build_dictionary(TraceState& t) {
       HashArgs ha{t.rec.name_off, t.rec.name_bytes, 0,       total,      0,           n,           nullptr,  nullptr,
                   t.rec.device,   t.tkey.p,         cap - 1, seed,       t.slot.p,    t.used.p,    counters.p,
                   dev_counts.p,   dev_max.p};
-      launch(c, "intern_hash", 2.0 * name_bytes + n * 16.0, k_hash_insert, dim3(grid), dim3(kHashBlock), 0, ha);
+      // algorithmic bytes (names once): name bytes + offset (8) + slot (4) + device id (2)
+      launch(c, "intern_hash", static_cast<double>(name_bytes) + n * (t.rec.device ? 14.0 : 12.0), k_hash_insert, dim3(grid),
+             dim3(kHashBlock), 0, ha);
     } else if (n) {
       if (arena.n < arena_cap) arena.alloc(c, arena_cap);
       arena_off.alloc(c, cap);
@@ -1204,7 +1225,7 @@ void build_dictionary(TraceState& t) {
         HashArgs ha{t.rec.name_off, bytes,   lo,       hi,          r0,          r1,          arena.p,  arena_off.p,
                     t.rec.device,   t.tkey.p, cap - 1, seed,        t.slot.p,    t.used.p,    counters.p,
                     dev_counts.p,   dev_max.p};
-        launch(c, "intern_hash", 2.0 * static_cast<double>(bounds[k + 1] - bounds[k]) + (r1 - r0) * 16.0, k_hash_insert,
+        launch(c, "intern_hash", static_cast<double>(bounds[k + 1] - bounds[k]) + (r1 - r0) * (t.rec.device ? 14.0 : 12.0), k_hash_insert,
                dim3(cgrid), dim3(kHashBlock), 0, ha);
         launch(c, "intern_save_reps", 0.0, k_save_reps, dim3(c->sm_count), dim3(128), 0, t.used.p, snap.p, counters.p,
                t.tkey.p, t.rec.name_off, bytes, arena.p, arena_cap, arena_off.p, arena_top.p, counters.p + 3);

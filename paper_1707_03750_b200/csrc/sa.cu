@@ -26,6 +26,7 @@
 // lifting, so periodic traces (Sum LCP ~ n^2/2) stay O(n log n); LCP_j = PLCP[SA_j].
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "pipeline.cuh"
 
@@ -113,12 +114,17 @@ struct EmitLoader {
 // sorted keys) and r2 = old id of SA_j + h (gathered here; none when SA_j + h >= n' or when
 // rank_old is null in the init round).  id_j = inclusive count of flags - 1 (decoupled look-back
 // sum scan); rank_new[SA_j] = id_j; hist_next[p][digit_p(id_j)] += 1.
+// kHeads: rank_new holds the SA position of each group's head instead of a dense id (u32; the
+// scan is a max over head positions and G is counted separately into *gcount) — what refinement
+// rounds continue from without a conversion pass.
+template <bool kHeads>
 __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
                                                             uintptr_t rank_old, uint32_t h, uint64_t np,
                                                             uintptr_t rank_new, uint32_t* __restrict__ hist_next,
                                                             int passes, uint32_t* __restrict__ gstart,
                                                             uint64_t* status, uint32_t* counter, uint32_t pf_dist,
-                                                            uint8_t* __restrict__ heads_out) {
+                                                            uint8_t* __restrict__ heads_out,
+                                                            unsigned long long* __restrict__ gcount) {
   __shared__ uint32_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_hist[kMaxPasses][256];
@@ -178,15 +184,23 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
     }
   }
   if (heads_out && base < np) heads_out[base / kRankItems] = static_cast<uint8_t>(fmask);  // group heads, SA order
-  const uint32_t run = __popc(fmask);
+  using ScanOp = typename std::conditional<kHeads, MaxOp<uint32_t>, SumOp<uint32_t>>::type;
+  // dense: flags in the run; heads: (last head position in the run) + 1, 0 = none
+  const uint32_t run = kHeads ? (fmask ? static_cast<uint32_t>(base) + (31 - __clz(fmask)) + 1 : 0u) : __popc(fmask);
   uint32_t total;
-  const uint32_t texcl = block_exclusive_scan<uint32_t, SumOp<uint32_t>, kRankBlock>(run, SumOp<uint32_t>(), &total, s_warp);
+  const uint32_t texcl = block_exclusive_scan<uint32_t, ScanOp, kRankBlock>(run, ScanOp(), &total, s_warp);
   if (threadIdx.x < 32) {
-    const uint32_t p = tile_lookback<uint32_t, SumOp<uint32_t>>(status, tile, total, SumOp<uint32_t>());
+    const uint32_t p = tile_lookback<uint32_t, ScanOp>(status, tile, total, ScanOp());
     if (threadIdx.x == 0) s_prefix = p;
   }
+  if constexpr (kHeads) {  // G = number of heads
+    uint32_t g = __popc(fmask);
+    for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+    if (lane_id() == 0 && g) atomicAdd(gcount, static_cast<unsigned long long>(g));
+  }
   __syncthreads();
-  const uint32_t pre = s_prefix + texcl;
+  const uint32_t pre = ScanOp()(s_prefix, texcl);
+  uint32_t last_head = pre;  // kHeads: running (last head + 1)
   // ids are non-decreasing across the thread's items: one shared atomic per run of equal digits
   uint32_t cur[kMaxPasses], len[kMaxPasses];
 #pragma unroll
@@ -195,10 +209,16 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
   for (int q = 0; q < kRankItems; ++q) {
     const uint64_t j = base + q;
     if (j < np) {
-      const uint32_t id = pre + __popc(fmask & ((2u << q) - 1u)) - 1;
+      uint32_t id;
+      if constexpr (kHeads) {
+        if ((fmask >> q) & 1u) last_head = static_cast<uint32_t>(j) + 1;
+        id = last_head - 1;
+      } else {
+        id = pre + __popc(fmask & ((2u << q) - 1u)) - 1;
+      }
       rank_put(rank_new, s_idx[q], id);  // ids beyond a u16 level are caught by the host (G > 2^16)
       // group starts (SA position of each group's first suffix) for the wide-digit histograms
-      if (gstart && ((fmask >> q) & 1u) && id < kWideGroups) gstart[id] = static_cast<uint32_t>(j);
+      if (!kHeads && gstart && ((fmask >> q) & 1u) && id < kWideGroups) gstart[id] = static_cast<uint32_t>(j);
 #pragma unroll
       for (int p = 0; p < kMaxPasses; ++p) {
         if (p >= passes) break;
@@ -322,9 +342,11 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __
 
 // rank_{2h}[SA_j] = position of j's new group head, written where it differs from the old head
 // (all j when the previous level holds dense ids): a max-scan of (last new head, last old head)
-// over SA order with decoupled look-back
-__global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint8_t* __restrict__ heads_old,
-                                                            const uint8_t* __restrict__ heads_new, uint64_t np,
+// over SA order with decoupled look-back.  32 positions per thread = one word of each bitmap; SA
+// is read only where a rank is written, so a settled round touches little more than the bitmaps.
+constexpr int kApplyItems = 32;
+__global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads_old,
+                                                            const uint32_t* __restrict__ heads_new, uint64_t np,
                                                             uint32_t* __restrict__ level, int full, uint64_t* status,
                                                             uint32_t* counter) {
   __shared__ uint64_t s_warp[kRankBlock / 32];
@@ -333,9 +355,14 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __r
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint64_t base = static_cast<uint64_t>(tile) * (kRankBlock * kRankItems) + static_cast<uint64_t>(threadIdx.x) * kRankItems;
-  const uint32_t ho = base < np ? heads_old[base / kRankItems] : 0u;
-  const uint32_t hn = base < np ? heads_new[base / kRankItems] : 0u;
+  const uint64_t w = static_cast<uint64_t>(tile) * kRankBlock + threadIdx.x;  // bitmap word
+  const uint64_t base = w * kApplyItems;
+  uint32_t ho = 0, hn = 0;
+  if (base < np) {
+    const uint32_t live = np - base >= kApplyItems ? 0xFFFFFFFFu : (1u << (np - base)) - 1u;  // bytes past np are unset
+    ho = __ldcs(&heads_old[w]) & live;
+    hn = __ldcs(&heads_new[w]) & live;
+  }
   // this run's last heads (+1; 0 = none)
   const uint64_t ln = hn ? base + (31 - __clz(hn)) + 1 : 0;
   const uint64_t lo = ho ? base + (31 - __clz(ho)) + 1 : 0;
@@ -347,16 +374,28 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __r
     if (threadIdx.x == 0) s_prefix = p;
   }
   __syncthreads();
+  if (base >= np) return;
   const uint64_t pre = op(s_prefix, texcl);
   uint64_t cn = pre >> 31, co = pre & ((1ull << 31) - 1);  // last heads before this run (+1)
+  const int cnt = static_cast<int>(umin64(kApplyItems, np - base));
+  if (!full && hn == ho && cn == co) return;  // no head moved in or before this run's groups
+  if (full && cnt == kApplyItems) {  // every rank changes representation: the run's SA in 16-byte loads
 #pragma unroll
-  for (int q = 0; q < kRankItems; ++q) {
-    const uint64_t j = base + q;
-    if (j < np) {
-      if ((hn >> q) & 1u) cn = j + 1;
-      if ((ho >> q) & 1u) co = j + 1;
-      if (full || cn != co) level[__ldcs(&sa[j])] = static_cast<uint32_t>(cn - 1);
+    for (int q4 = 0; q4 < kApplyItems; q4 += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(sa + base + q4);
+      const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((hn >> (q4 + u)) & 1u) cn = base + q4 + u + 1;
+        level[x[u]] = static_cast<uint32_t>(cn - 1);
+      }
     }
+    return;
+  }
+  for (int q = 0; q < cnt; ++q) {
+    if ((hn >> q) & 1u) cn = base + q + 1;
+    if ((ho >> q) & 1u) co = base + q + 1;
+    if (full || cn != co) level[sa[base + q]] = static_cast<uint32_t>(cn - 1);
   }
 }
 
@@ -534,9 +573,15 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   launch(c, "sa_init_keys", np * 16.0, k_text_keys, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, cbits, k,
          s.text.p, ka, va);
   const int init_bits = std::min(32, cbits * k);
-  const bool a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
-                                                 static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr),
-                                                 /*skip_trivial=*/!known_alphabet);
+  // 10-bit digits when they save a pass (a 26-bit key of two 13-bit symbols: 3 passes, not 4)
+  const bool init_wide = (init_bits + radix::kWideBits - 1) / radix::kWideBits < (init_bits + 7) / 8 &&
+                         !std::getenv("ITT_NO_WIDE_DIGITS");
+  const bool a0 = init_wide ? radix_sort_pairs<uint32_t, radix::ArrayLoader<uint32_t>, radix::kWideBits>(
+                                  c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
+                                  static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), !known_alphabet)
+                            : radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
+                                                         static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr),
+                                                         /*skip_trivial=*/!known_alphabet);
   uint32_t* keys = a0 ? kb : ka;
   uint32_t* sa = a0 ? vb : va;
   uint32_t* f1 = a0 ? ka : kb;  // free buffers
@@ -565,26 +610,36 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   int hc = 0;
   // one rank update into a new level (u16 when the previous group count suggests the ids fit; if
   // they do not, the update runs again into a u32 level: its inputs are untouched)
+  DBuf<unsigned long long> gcount(c, 1);
   auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, uintptr_t rank_old, uint32_t h, bool more,
-                         uint64_t g_prev) -> uint64_t {
+                         uint64_t g_prev, bool heads_mode) -> uint64_t {
     // only where the arrays outgrow L2 (C2's 40 MB levels stay resident: u16 stores there cost
     // more than they save); ITT_NARROW_MIN_N overrides the size threshold (tests)
     const char* ev = std::getenv("ITT_NARROW_MIN_N");
     const uint64_t min_n = ev && *ev ? std::strtoull(ev, nullptr, 10) : (1ull << 24);
-    bool narrow = g_prev <= kNarrowTry && np >= min_n;
+    bool narrow = !heads_mode && g_prev <= kNarrowTry && np >= min_n;
     for (;;) {
       s.levels.emplace_back(c, narrow ? (np + 1) / 2 : np);
       const uintptr_t lvl = reinterpret_cast<uintptr_t>(s.levels.back().p) | (narrow ? 1u : 0u);
       ScanScratch& sc = *scans[cur];
       hist_p = hists[cur].p;
-      launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update, dim3(static_cast<unsigned>(rtiles)),
-             dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, gstart.p, sc.buf.p + 1,
-             reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p);
-      // group count G: the last tile's inclusive word, copied out and waited on by event, so the
-      // next round's scratch zeroing (queued after the copy) runs while the host wakes up
+      if (heads_mode) {
+        gcount.zero();
+        launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update<true>, dim3(static_cast<unsigned>(rtiles)),
+               dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, nullptr, sc.buf.p + 1,
+               reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, gcount.p);
+      } else {
+        launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update<false>, dim3(static_cast<unsigned>(rtiles)),
+               dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, gstart.p, sc.buf.p + 1,
+               reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, nullptr);
+      }
+      // group count G: the last tile's inclusive word (dense ids) or the head counter, copied out
+      // and waited on by event, so the next round's scratch zeroing (queued after the copy) runs
+      // while the host wakes up
       ++StageTimer::syncs();
       uint64_t* word = static_cast<uint64_t*>(c->deferred_block()) + 8;  // [0, 64) holds the order verdict
-      ITT_CUDA(cudaMemcpyAsync(word, sc.buf.p + rtiles, 8, cudaMemcpyDeviceToHost, c->stream));
+      ITT_CUDA(cudaMemcpyAsync(word, heads_mode ? reinterpret_cast<const uint64_t*>(gcount.p) : sc.buf.p + rtiles, 8,
+                               cudaMemcpyDeviceToHost, c->stream));
       ITT_CUDA(cudaEventRecord(c->deferred_ev, c->stream));
       if (more) {
         hists[cur ^ 1].zero();
@@ -592,7 +647,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
         radix_prezero_status(c, rs, np, max_passes, 0);  // a wide sort zeroes its own (rare, larger)
       }
       ITT_CUDA(cudaEventSynchronize(c->deferred_ev));
-      const uint64_t total = *word & kValMask;
+      const uint64_t total = heads_mode ? *word : (*word & kValMask);
       if (narrow && total > kNarrowGroups) {  // the ids did not fit 16 bits: redo into u32
         s.levels.pop_back();
         hists[cur].zero();
@@ -608,14 +663,17 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       return total;
     }
   };
-  uint64_t g = rank_update(keys, sa, 0, 0, s.h0 < cap, 0);
-  uint32_t h = s.h0;  // prefix length the newest level separates
-  bool dense = true;  // the newest level holds dense ids (else group-head positions)
   static const int refine_mode = [] {  // ITT_SA_REFINE=0: full rounds only (A/B, tests)
     const char* e = std::getenv("ITT_SA_REFINE");
     return e && *e ? std::atoi(e) : 1;
   }();
-  bool try_refine = false;  // decided after each full round from how many groups it added
+  // the first level holds group heads when refinement may follow: a periodic text (few, large
+  // k-gram groups) then goes straight into refinement rounds with no dense-to-head conversion
+  const bool init_heads = refine_mode > 0 && np < (1ull << 31) && s.h0 < cap;
+  uint64_t g = rank_update(keys, sa, 0, 0, s.h0 < cap, 0, init_heads);
+  uint32_t h = s.h0;  // prefix length the newest level separates
+  bool dense = !init_heads;  // the newest level holds dense ids (else group-head positions)
+  bool try_refine = init_heads && g * 16 < np;  // then decided after each full round from the groups it added
   int cooldown = 0;
   DBuf<unsigned long long> rcount(c, 2);
   DBuf<uint32_t> head_hist;
@@ -632,17 +690,26 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       unsigned long long cnt[2];
       readback(c, cnt, rcount.p, 2);
       if (cnt[1] == 0) {
-        s.levels.emplace_back(c, np);
-        uint32_t* lvl = s.levels.back().p;
         const bool full = dense;  // dense ids: every rank changes representation
-        if (!full) ITT_CUDA(cudaMemcpyAsync(lvl, reinterpret_cast<const uint32_t*>(rank), np * 4, cudaMemcpyDeviceToDevice,
-                                            c->stream));
-        rscan.prepare(c, rtiles);
-        launch(c, "sa_refine_apply", np * (full ? 10.25 : 2.25) + (full ? 0.0 : np * 8.0), k_refine_apply,
-               dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock), 0, sa, heads[hc].p, heads[hc ^ 1].p, np, lvl,
-               full ? 1 : 0, rscan.buf.p + 1, reinterpret_cast<uint32_t*>(rscan.buf.p));
-        s.level_tags.push_back(reinterpret_cast<uintptr_t>(lvl));
-        if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
+        uint32_t* lvl;
+        if (!full && !s.keep_levels) {  // nothing reads the old level again: update it in place
+          lvl = reinterpret_cast<uint32_t*>(rank);
+        } else {
+          s.levels.emplace_back(c, np);
+          lvl = s.levels.back().p;
+          if (!full) ITT_CUDA(cudaMemcpyAsync(lvl, reinterpret_cast<const uint32_t*>(rank), np * 4, cudaMemcpyDeviceToDevice,
+                                              c->stream));
+        }
+        const uint64_t atiles = (np + kRankBlock * kApplyItems - 1) / (kRankBlock * kApplyItems);
+        rscan.prepare(c, atiles);
+        launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply, dim3(static_cast<unsigned>(atiles)),
+               dim3(kRankBlock), 0, sa, reinterpret_cast<const uint32_t*>(heads[hc].p),
+               reinterpret_cast<const uint32_t*>(heads[hc ^ 1].p), np, lvl, full ? 1 : 0, rscan.buf.p + 1,
+               reinterpret_cast<uint32_t*>(rscan.buf.p));
+        if (lvl != reinterpret_cast<uint32_t*>(rank)) {
+          s.level_tags.push_back(reinterpret_cast<uintptr_t>(lvl));
+          if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
+        }
         hc ^= 1;
         dense = false;
         g = cnt[0];
@@ -701,7 +768,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     uint32_t* other_k = alt ? kx : f1;
     uint32_t* other_v = alt ? vx : f2;
     const uint64_t g_old = g;
-    g = rank_update(nkeys, nsa, rank, h, static_cast<uint64_t>(h) * 2 < cap, g);
+    g = rank_update(nkeys, nsa, rank, h, static_cast<uint64_t>(h) * 2 < cap, g, false);
     dense = true;
     ++s.rounds;
     if (cooldown > 0) --cooldown;
