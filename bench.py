@@ -303,17 +303,28 @@ def bench_batch(args, world, rank, local, workload):
 def bench_dist_sa(args, world, rank, local, workload, iters):
     """One trace, suffix array over all ranks (SURVEY §8e C5 path): rank 0 runs itt_analyze on the
     trace with the distributed suffix array plugged in (itt_analyze_opts.sa_provider); every rank
-    builds its share of the SA/LCP (dist_sa.py over NCCL), rank 0 mines / matches / aggregates."""
+    builds its share of the SA/LCP and rank 0 mines / matches / aggregates.  --dist-impl native
+    (default): the C++ driver with NCCL on the library's streams (csrc/dist_driver.cu); python:
+    dist_sa.py over torch.distributed."""
     import torch
     import torch.distributed as dist
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", rank=rank, world_size=world)
-    from paper_1707_03750_b200 import cuda as itt, dist_sa
+    from paper_1707_03750_b200 import cuda as itt, dist_native, dist_sa
     dev = local
     ops_ctx = itt.Context(dev)
-    prov = dist_sa.DistributedSAProvider(dist_sa.TorchExchange(device=torch.device("cuda", dev)), dist_sa.CudaOps(ops_ctx))
+    if args.dist_impl == "native":
+        uid = [dist_native.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = dist_native.Comm.nccl(ops_ctx, world, rank, uid[0])
+        prov = dist_native.Provider(ops_ctx, comm, root=0)
+        kw_of = lambda: dict(native_provider=prov)  # noqa: E731
+    else:
+        prov = dist_sa.DistributedSAProvider(dist_sa.TorchExchange(device=torch.device("cuda", dev)),
+                                             dist_sa.CudaOps(ops_ctx))
+        kw_of = lambda: dict(sa_provider=prov)  # noqa: E731
     if rank != 0:
         prov.serve()
         dist.barrier()
@@ -329,7 +340,7 @@ def bench_dist_sa(args, world, rank, local, workload, iters):
     n_events = info["n"]
 
     def step():
-        return ctx.analyze_raw(drecs, [iters], sa_provider=prov)
+        return ctx.analyze_raw(drecs, [iters], **kw_of())
 
     for _ in range(max(3, args.warmup)):
         res = step()
@@ -347,13 +358,18 @@ def bench_dist_sa(args, world, rank, local, workload, iters):
     e1.synchronize()
     ms_step = e0.elapsed_time(e1) / args.steps
     prov.stop()
-    last = prov.last
+    if args.dist_impl == "native":
+        inf = prov.last_info()
+        rounds, groups, cap = inf.rounds, inf.groups, inf.cap
+    else:
+        rounds, groups, cap = prov.last.rounds, prov.last.groups, prov.last.cap
     line = {"metric": METRIC, "value": n_events / (ms_step / 1000.0), "unit": "events/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": workload + " -- suffix array distributed over the ranks (sample-sort prefix doubling)",
+            "config": {"workload": workload + " -- suffix array distributed over the ranks (sample-sort prefix doubling, "
+                                              f"{args.dist_impl} driver)",
                        "events": n_events, "tokens": res["n_tokens"], "parallelism": f"dist-sa{world}",
-                       "doubling_rounds": last.rounds, "groups": last.groups, "cap": last.cap,
+                       "doubling_rounds": rounds, "groups": groups, "cap": cap,
                        "equal_to_single_gpu_path": bool(same)},
             "gpu_launches": None}
     print(json.dumps(line), flush=True)
@@ -384,6 +400,8 @@ def main():
     ap.add_argument("--workers", type=int, default=64, help="C4: concurrent streams (host threads) per GPU")
     ap.add_argument("--dist-sa", action="store_true",
                     help="one trace with its suffix array distributed over all ranks (NCCL; C5's multi-GPU path)")
+    ap.add_argument("--dist-impl", default="native", choices=["native", "python"],
+                    help="--dist-sa driver: C++ with NCCL on the library streams, or dist_sa.py over torch.distributed")
     ap.add_argument("--batch-impl", default="native", choices=["native", "threads"],
                     help="C4 executor: native C++ worker threads (itt_batch_*) or Python threads")
     args = ap.parse_args()

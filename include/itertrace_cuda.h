@@ -269,6 +269,44 @@ int itt_dsa_kasai(itt_ctx* ctx, const int32_t* text, uint64_t np, uint64_t lo, u
 int itt_dsa_sample(itt_ctx* ctx, const uint64_t* a, const uint32_t* b, uint64_t cnt, uint32_t s, uint64_t* out_a,
                    uint32_t* out_b);
 
+/* The same doubling driven natively (csrc/dist_driver.cu; dist_sa.py is its Python restatement):
+ * the exchanges go through a communicator — NCCL between GPUs (grouped ncclSend/ncclRecv
+ * all-to-alls, ncclAllGather, ncclBroadcast on the context's stream; libnccl is loaded on first
+ * use), or virtual ranks (threads of one process sharing one device: device-to-device copies
+ * behind a barrier, for tests).  One context and one communicator per rank and host thread. */
+typedef struct itt_comm itt_comm;
+int itt_comm_nccl_unique_id(uint8_t* id /* [128] */);
+int itt_comm_create_nccl(itt_ctx* ctx, int nranks, int rank, const uint8_t* id /* [128] */, itt_comm** out);
+int itt_comm_create_local(int nranks, itt_comm** comms /* [nranks] */);
+int itt_comm_abort(itt_comm* comm); /* virtual ranks: release the others after one failed */
+int itt_comm_destroy(itt_comm* comm);
+typedef struct itt_dsa_info {
+  int32_t rounds;      /* doubling rounds after the first sort */
+  int32_t pad_;
+  uint64_t groups;     /* groups of the last level (n+1: a full suffix array) */
+  uint32_t h_final;    /* prefix length the last level separates */
+  uint32_t cap;        /* LCP values are min(lcp, cap); 0xFFFFFFFF when the SA is full */
+} itt_dsa_info;
+/* SPMD over the communicator's ranks: text = tokens + [term] (n+1 int32, DEVICE, replicated,
+ * tokens in [0, term)).  This rank's slice of the suffix array (sorted positions
+ * [kbase, kbase + count)) and, when want_lcp, of the LCP capped at cap (0xFFFFFFFF: full) come back
+ * as device allocations released with itt_device_free.  Same suffix order and node depths as
+ * itt_suffix_array / SuffixTree (suffix_tree.hpp:21-190); n+1 < 2^31 - 1. */
+int itt_dsa_build(itt_ctx* ctx, itt_comm* comm, const int32_t* text, uint64_t n, int32_t term, uint32_t cap, int want_lcp,
+                  uint32_t** sa, uint32_t** lcp, uint64_t* kbase, uint64_t* count, itt_dsa_info* info);
+/* itt_analyze over G ranks: on the root, set itt_analyze_opts.sa_provider = itt_dsa_provide and
+ * sa_user = a provider; the tokens are broadcast, every rank builds its slice, the slices are
+ * gathered into the analyze's buffers.  The other ranks call itt_dsa_serve (returns after the
+ * root's itt_dsa_stop).  ctx: this rank's context for the distributed steps (on the root, not the
+ * one running itt_analyze). */
+typedef struct itt_dsa_provider itt_dsa_provider;
+int itt_dsa_provider_create(itt_ctx* ctx, itt_comm* comm, int root, itt_dsa_provider** out);
+int itt_dsa_provider_destroy(itt_dsa_provider* p);
+int itt_dsa_provide(void* user, const int32_t* tokens, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa, uint32_t* lcp);
+int itt_dsa_serve(itt_dsa_provider* p);
+int itt_dsa_stop(itt_dsa_provider* p);
+int itt_dsa_last_info(itt_dsa_provider* p, itt_dsa_info* info);
+
 /* ------------------------------------------------------- L4 matching (a7) */
 typedef struct itt_span { /* MatchSpan, match.hpp:28-34 */
   int64_t start_token;

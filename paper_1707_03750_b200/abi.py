@@ -127,6 +127,11 @@ class itt_clamps(C.Structure):
 SA_PROVIDER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_uint32, C.c_void_p, C.c_void_p)
 
 
+class itt_dsa_info(C.Structure):  # distributed suffix array (csrc/dist_driver.cu)
+    _fields_ = [("rounds", C.c_int32), ("pad_", C.c_int32), ("groups", C.c_uint64), ("h_final", C.c_uint32),
+                ("cap", C.c_uint32)]
+
+
 class itt_summary(C.Structure):  # SummaryMetrics, metrics.hpp:33-42
     _fields_ = [
         ("avg_interval_ns", C.c_double),

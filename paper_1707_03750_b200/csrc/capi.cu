@@ -26,9 +26,7 @@ int itt::radix::config_index() {
   return cfg;
 }
 
-struct itt_ctx {
-  Ctx c;
-};
+// struct itt_ctx { itt::Ctx c; } lives in pipeline.cuh (dist_driver.cu shares it)
 
 namespace {
 

@@ -194,3 +194,8 @@ void sample(Ctx* c, const uint64_t* a, const uint32_t* b, uint64_t cnt, uint32_t
 }  // namespace dsa
 
 }  // namespace itt
+
+// the C-ABI's opaque context (capi.cu, dist_driver.cu)
+struct itt_ctx {
+  itt::Ctx c;
+};

@@ -91,6 +91,18 @@ def lib() -> C.CDLL:
         "itt_dsa_lcp_requests": ([vp, vp, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, vp, vp], C.c_int),
         "itt_dsa_kasai": ([vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp, C.c_uint32, vp], C.c_int),
         "itt_dsa_sample": ([vp, vp, vp, C.c_uint64, C.c_uint32, vp, vp], C.c_int),
+        "itt_comm_nccl_unique_id": ([vp], C.c_int),
+        "itt_comm_create_nccl": ([vp, C.c_int, C.c_int, vp, P(vp)], C.c_int),
+        "itt_comm_create_local": ([C.c_int, P(vp)], C.c_int),
+        "itt_comm_abort": ([vp], C.c_int),
+        "itt_comm_destroy": ([vp], C.c_int),
+        "itt_dsa_build": ([vp, vp, vp, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, P(vp), P(vp), P(C.c_uint64),
+                           P(C.c_uint64), P(abi.itt_dsa_info)], C.c_int),
+        "itt_dsa_provider_create": ([vp, vp, C.c_int, P(vp)], C.c_int),
+        "itt_dsa_provider_destroy": ([vp], C.c_int),
+        "itt_dsa_serve": ([vp], C.c_int),
+        "itt_dsa_stop": ([vp], C.c_int),
+        "itt_dsa_last_info": ([vp, P(abi.itt_dsa_info)], C.c_int),
         "itt_approx_match": ([vp, P(C.c_int32), C.c_uint64, P(C.c_int32), C.c_uint64, C.c_int64, P(P(abi.itt_span)),
                               P(C.c_uint64)], C.c_int),
         "itt_op_profile": ([vp, P(C.c_int32), P(C.c_int64), P(C.c_int64), P(C.c_uint8), C.c_uint64, C.c_uint32,
@@ -400,7 +412,8 @@ class Context:
         lib().itt_free(self.h, C.cast(rows, C.c_void_p))
         return out, (cl.negative_gap_clamps, cl.negative_interval_clamps)
 
-    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1, op_profile=False, sa_provider=None) -> dict:
+    def analyze_raw(self, recs, loops, epsilon0=1, k0=-1, main_stream=-1, op_profile=False, sa_provider=None,
+                    native_provider=None) -> dict:
         """itt_analyze: device pipeline up to the per-loop integer aggregates.  The per-iteration
         rows (and the a12 op profile: op_profile=True for the per-op / per-iteration totals,
         "cells" for the (iteration, op) grid as well) are zero-copy numpy views of the library's
@@ -425,6 +438,9 @@ class Context:
                     failure.append(e)
                     return 1
             opts.sa_provider = abi.SA_PROVIDER(_cb)
+        if native_provider is not None:  # the C++/NCCL distributed suffix array (dist_native.Provider)
+            opts.sa_provider = C.cast(lib().itt_dsa_provide, abi.SA_PROVIDER)
+            opts.sa_user = native_provider.handle
         out = P(abi.itt_analysis)()
         rc = lib().itt_analyze(self.h, C.byref(c), C.byref(opts), C.byref(out))
         if sa_provider is not None and failure:

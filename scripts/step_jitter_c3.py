@@ -11,11 +11,13 @@ import torch  # noqa: E402
 from paper_1707_03750_b200 import cuda, synth  # noqa: E402
 
 ctx = cuda.Context(0)
-recs, info = synth.generate_config("C3")
+CFG = sys.argv[1] if len(sys.argv) > 1 else "C3"
+IT = {"C2": 50_000, "C3": 20_000}[CFG]
+recs, info = synth.generate_config(CFG)
 d = ctx.upload(recs)
 stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", 0))
 for _ in range(20):
-    ctx.analyze_raw(d, [20_000])
+    ctx.analyze_raw(d, [IT])
 
 
 def block(k=10):
@@ -23,7 +25,7 @@ def block(k=10):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(k):
-        ctx.analyze_raw(d, [20_000])
+        ctx.analyze_raw(d, [IT])
     e1.record(stream)
     e1.synchronize()
     return e0.elapsed_time(e1) / k
@@ -32,8 +34,11 @@ def block(k=10):
 for mode in ("none", "200", "none", "1000", "none", "200"):
     p = None
     if mode != "none":
-        p = subprocess.Popen(["nvidia-smi", "-i", "0", "--query-gpu=timestamp,clocks.sm,clocks_event_reasons.active",
-                              "--format=csv,noheader", "-lms", mode], stdout=subprocess.DEVNULL)
+        q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")  # bench.py's ClockSampler query
+        p = subprocess.Popen(["nvidia-smi", "-i", "0", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", mode],
+                             stdout=subprocess.DEVNULL)
         time.sleep(0.5)
     print(mode, [round(block(), 2) for _ in range(3)], flush=True)
     if p:

@@ -116,18 +116,28 @@ def test_analyze_with_distributed_sa_provider(ctx, P):
         assert got.details_csv(0) == want.details_csv(0)
 
 
-def test_nccl_provider_one_rank_bench():
-    """The NCCL path end to end (torch.distributed over NCCL, TorchExchange, CudaOps, the provider
-    inside itt_analyze) at one rank: bench.py --dist-sa must report results equal to the
-    single-GPU path."""
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+@pytest.mark.parametrize("impl", ["native", "python"])
+def test_nccl_provider_one_rank_bench(impl):
+    """The NCCL path end to end at one rank (torch.distributed rendezvous, the provider inside
+    itt_analyze): the native C++ driver (csrc/dist_driver.cu, ncclSend/Recv on the library
+    stream) and dist_sa.py over torch.distributed; bench.py --dist-sa must report results equal to
+    the single-GPU path."""
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
-                        "--master-addr", "127.0.0.1", "--master-port", "29613", "bench.py", "--dist-sa", "--config", "C1",
-                        "--steps", "2", "--warmup", "1"], cwd=root, capture_output=True, text=True, timeout=600)
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--dist-sa",
+                        "--dist-impl", impl, "--config", "C1", "--steps", "2", "--warmup", "1"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["config"]["equal_to_single_gpu_path"] is True
