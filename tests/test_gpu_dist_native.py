@@ -157,8 +157,11 @@ def test_analyze_with_distributed_sa_over_virtual_ranks(ctx):
     assert dinfo.rounds >= 1
 
 
-def test_nccl_transport_at_one_rank(ctx):
+@pytest.mark.parametrize("force", ["1", "0"])
+def test_nccl_transport_at_one_rank(ctx, force, monkeypatch):
+    """force=1: through the sample-sort rounds and NCCL exchanges; 0: one rank's shortcut."""
     import torch
+    monkeypatch.setenv("ITT_DSA_FORCE_DIST", force)
     uid = dist_native.Comm.unique_id()
     cx = cuda.Context(0)
     comm = dist_native.Comm.nccl(cx, 1, 0, uid)
