@@ -217,9 +217,6 @@ def bench_batch(args, world, rank, local, workload):
 
     import torch
     from paper_1707_03750_b200 import batch, cuda as itt, synth
-    if world > 1:
-        torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl")
     dev = local if world > 1 else 0
     torch.cuda.set_device(dev)
     lo, hi = batch.shard_bounds(args.traces, world, rank)
@@ -294,10 +291,8 @@ def bench_batch(args, world, rank, local, workload):
                 line["cpu_baseline"] = c4_cpu_baseline()
             except Exception as e:  # noqa: BLE001 (the reference build is optional on the box)
                 line["cpu_baseline"] = {"unavailable": str(e)[:200]}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
-    return 0
+        return line
+    return None
 
 
 def bench_dist_sa(args, world, rank, local, workload, iters):
@@ -308,10 +303,7 @@ def bench_dist_sa(args, world, rank, local, workload, iters):
     dist_sa.py over torch.distributed."""
     import torch
     import torch.distributed as dist
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29531")
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", rank=rank, world_size=world)
     from paper_1707_03750_b200 import cuda as itt, dist_native, dist_sa
     dev = local
     ops_ctx = itt.Context(dev)
@@ -328,8 +320,7 @@ def bench_dist_sa(args, world, rank, local, workload, iters):
     if rank != 0:
         prov.serve()
         dist.barrier()
-        dist.destroy_process_group()
-        return 0
+        return None
     ctx = itt.Context(dev)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", dev))
     if args.iterations:
@@ -372,10 +363,8 @@ def bench_dist_sa(args, world, rank, local, workload, iters):
                        "doubling_rounds": rounds, "groups": groups, "cap": cap,
                        "equal_to_single_gpu_path": bool(same)},
             "gpu_launches": None}
-    print(json.dumps(line), flush=True)
     dist.barrier()
-    dist.destroy_process_group()
-    return 0
+    return line
 
 
 def main():
@@ -400,6 +389,11 @@ def main():
     ap.add_argument("--workers", type=int, default=64, help="C4: concurrent streams (host threads) per GPU")
     ap.add_argument("--dist-sa", action="store_true",
                     help="one trace with its suffix array distributed over all ranks (NCCL; C5's multi-GPU path)")
+    ap.add_argument("--sharded-legs", action="store_true", help="add the N>1 sharded legs at N=1 too (tests)")
+    ap.add_argument("--no-sharded-legs", action="store_true",
+                    help="N>1: skip the C4-sharded and distributed-SA measurements added beside the replicas line")
+    ap.add_argument("--dist-config", default="C3", choices=["C1", "C2", "C3", "C5"],
+                    help="N>1: the trace whose suffix array the distributed-SA leg spreads over the ranks")
     ap.add_argument("--dist-impl", default="native", choices=["native", "python"],
                     help="--dist-sa driver: C++ with NCCL on the library streams, or dist_sa.py over torch.distributed")
     ap.add_argument("--batch-impl", default="native", choices=["native", "threads"],
@@ -423,16 +417,47 @@ def main():
         print(json.dumps(line), flush=True)
         return 0
 
-    if args.config == "C4":
-        return bench_batch(args, world, rank, local, workload)
-    if args.dist_sa:
-        return bench_dist_sa(args, world, rank, local, workload, iters)
-
     import torch
-    if world > 1:
-        import torch.distributed as dist
+    # a process group whenever ranks exchange anything: N>1, or the distributed suffix array
+    pg = world > 1 or args.dist_sa or args.sharded_legs
+    if pg:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.distributed.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        if args.config == "C4":
+            line = bench_batch(args, world, rank, local, workload)
+        elif args.dist_sa:
+            line = bench_dist_sa(args, world, rank, local, workload, iters)
+        else:
+            line = bench_single(args, world, rank, local, workload, iters)
+            if (world > 1 or args.sharded_legs) and not args.no_sharded_legs:
+                # the configs that shard across GPUs, measured at this N beside the
+                # replicas line: C4's batch split across ranks (strong scaling, no data-path
+                # collective) and one trace's suffix array distributed over the ranks (NCCL)
+                c4 = argparse.Namespace(**vars(args))
+                c4.steps, c4.warmup, c4.config = max(1, min(args.steps, 3)), 1, "C4"
+                leg_c4 = bench_batch(c4, world, rank, local, WORKLOADS["C4"][0])
+                ds = argparse.Namespace(**vars(args))
+                ds.steps, ds.warmup, ds.config = max(1, min(args.steps, 5)), 1, args.dist_config
+                leg_ds = bench_dist_sa(ds, world, rank, local, WORKLOADS[ds.config][0], WORKLOADS[ds.config][2])
+                if rank == 0:
+                    line["c4_sharded"] = leg_c4
+                    line["dist_sa"] = leg_ds
+        if rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        if pg:
+            torch.distributed.destroy_process_group()
+    return 0
+
+
+def bench_single(args, world, rank, local, workload, iters):
+    """C1/C2/C3/C5: one trace per rank (replicas: a trace's pipeline has no data-path exchange)."""
+    import torch
     from paper_1707_03750_b200 import cuda as itt
 
     dev = local if world > 1 else 0
@@ -707,11 +732,10 @@ def main():
             "gpu_launches": int(launches), "kernels": kernel_table, "op_profile": op_profile,
             "memory": memory, "ingest": ingest, "sa_full": sa_full,
         }
-        print(json.dumps(line), flush=True)
     drecs.free()
-    if world > 1:
-        torch.distributed.destroy_process_group()
-    return 0
+    return line if rank == 0 else None
+
+
 
 
 if __name__ == "__main__":

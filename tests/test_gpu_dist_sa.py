@@ -142,3 +142,23 @@ def test_nccl_provider_one_rank_bench(impl):
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["config"]["equal_to_single_gpu_path"] is True
     assert line["config"]["parallelism"] == "dist-sa1"
+
+
+def test_bench_sharded_legs_one_rank():
+    """bench.py's N>1 line shape at one rank: the replicas line plus the C4-sharded and the
+    distributed-SA legs (the path a multi-GPU SCALE run takes)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--config", "C1",
+                        "--sharded-legs", "--dist-config", "C1", "--traces", "64", "--distinct", "8", "--steps", "2",
+                        "--warmup", "1", "--no-cpu-baseline", "--no-e2e", "--no-ingest", "--no-sa-full"], cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["config"]["mined"]["pattern_length"] == 200
+    assert line["c4_sharded"]["config"]["mined_ok"] is True
+    assert line["dist_sa"]["config"]["equal_to_single_gpu_path"] is True
