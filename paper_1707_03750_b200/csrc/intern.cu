@@ -105,9 +105,41 @@ __device__ __forceinline__ bool stage_names(const uint8_t* __restrict__ bytes, u
 // memory.  Global min/max and the descent flag are folded in k_order_check (no same-address
 // atomics per block).
 constexpr int kOrderBlock = 256;
+
+// Any descent start[i] < start[i-1] in source order?  8 rows per thread (16-byte loads); the block
+// sort and its check run only when one exists (profiler exports of one stream, and the synthetic
+// C3 / C5 traces, arrive in start order: the 256-row bitonic sorts would be pure overhead).
+__global__ void __launch_bounds__(256) k_order_descent(const int64_t* __restrict__ start, uint64_t n,
+                                                       unsigned int* __restrict__ any) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 8;
+  bool d = false;
+  for (uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8; i0 < n; i0 += stride) {
+    long long v[8];
+    if (i0 + 8 <= n) {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        const longlong2 w = __ldcs(reinterpret_cast<const longlong2*>(start + i0 + q));
+        v[q] = w.x, v[q + 1] = w.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = i0 + q < n ? start[i0 + q] : LLONG_MAX;
+    }
+    long long prev = i0 > 0 ? start[i0 - 1] : LLONG_MIN;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      d |= v[q] < prev;
+      prev = v[q];
+    }
+  }
+  if (__any_sync(0xffffffffu, d) && lane_id() == 0) atomicOr(any, 1u);
+}
+
 __global__ void __launch_bounds__(kOrderBlock) k_order_block_sort(const int64_t* __restrict__ start, uint64_t n,
                                                                   uint32_t* __restrict__ perm, int64_t* __restrict__ bmin,
-                                                                  int64_t* __restrict__ bmax, uint8_t* __restrict__ bdesc) {
+                                                                  int64_t* __restrict__ bmax, uint8_t* __restrict__ bdesc,
+                                                                  const unsigned int* __restrict__ any) {
+  if (*any == 0) return;  // already in (start, row) order
   __shared__ long long s[kOrderBlock];
   __shared__ uint32_t r[kOrderBlock];
   __shared__ long long wmn[kOrderBlock / 32], wmx[kOrderBlock / 32];
@@ -185,7 +217,8 @@ __global__ void __launch_bounds__(kOrderBlock) k_order_block_sort(const int64_t*
 // row order).  One set of atomics per CTA.
 __global__ void __launch_bounds__(256) k_order_check(const int64_t* __restrict__ bmin, const int64_t* __restrict__ bmax,
                                                      const uint8_t* __restrict__ bdesc, uint64_t nb,
-                                                     unsigned long long* stats) {
+                                                     unsigned long long* stats, const unsigned int* __restrict__ any) {
+  if (*any == 0) return;  // no descent: stats keep "no descent" (the blocks were not sorted)
   const uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   long long mn = LLONG_MAX, mx = LLONG_MIN;
   unsigned desc = 0, bad = 0;
@@ -1057,10 +1090,14 @@ void order_launch(TraceState& t) {
   t.perm.alloc(c, n);
   DBuf<int64_t> bmin(c, nb), bmax(c, nb);
   DBuf<uint8_t> bdesc(c, nb);
+  DBuf<unsigned int> any(c, 1);
+  any.zero();
+  launch(c, "order_descent", n * 8.0, k_order_descent, dim3(grid_for((n + 7) / 8, 256, c->sm_count * 8)), dim3(256), 0,
+         t.rec.start, n, any.p);
   launch(c, "order_blocks", n * 12.0, k_order_block_sort, dim3(static_cast<unsigned>(nb)), dim3(kOrderBlock), 0, t.rec.start, n,
-         t.perm.p, bmin.p, bmax.p, bdesc.p);
+         t.perm.p, bmin.p, bmax.p, bdesc.p, any.p);
   launch(c, "order_check", nb * 17.0, k_order_check, dim3(grid_for(nb, 256)), dim3(256), 0, bmin.p, bmax.p, bdesc.p, nb,
-         t.order_stats.p);
+         t.order_stats.p, any.p);
   ITT_CUDA(cudaMemcpyAsync(c->deferred_block(), t.order_stats.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
   ITT_CUDA(cudaEventRecord(c->deferred_ev, c->stream));
