@@ -28,6 +28,9 @@ int itt::radix::config_index() {
 
 // struct itt_ctx { itt::Ctx c; } lives in pipeline.cuh (dist_driver.cu shares it)
 
+// why an itt_analyze_opts.sa_provider call failed (set by providers on the calling thread)
+static thread_local std::string tl_provider_error;
+
 namespace {
 
 template <typename F>
@@ -874,8 +877,10 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
         s.sa.alloc(c, n + 1);
         s.lcp.alloc(c, n + 1);
         c->sync();
+        tl_provider_error.clear();
         if (opts->sa_provider(opts->sa_user, s.text.p, n, term, mining_cap(n, cfgs), s.sa.p, s.lcp.p) != 0)
-          fail(ITT_E_CUDA, "pattern-mining: the suffix-array provider failed");
+          fail(ITT_E_CUDA, "pattern-mining: the suffix-array provider failed" +
+                               (tl_provider_error.empty() ? std::string() : ": " + tl_provider_error));
       } else {
         build_suffix_array(c, t.tokens.p, t.n_tok, static_cast<int32_t>(t.n_names), s, true, t.rs, t.scan,
                            mining_cap(t.n_tok, cfgs), /*known_alphabet=*/true);
@@ -1042,6 +1047,7 @@ struct BatchSA {
     uint32_t* sa;
     uint32_t* lcp;
     int status;
+    std::string error;  // the wave build's failure, reported by the waiting trace's own analyze
   };
   std::mutex mu;
   std::condition_variable cv;
@@ -1085,7 +1091,10 @@ static void batch_sa_maybe_run(BatchSA* b, std::unique_lock<std::mutex>& lk) {
       }
     } catch (const std::exception& e) {
       st = 1;
-      if (tl_batch_ctx) tl_batch_ctx->last_error = e.what();
+      // the wave's work may still be queued on the builder's stream: drain it before the waiters
+      // resume (their outputs are in it), and give every waiter the cause
+      if (tl_batch_ctx) cudaStreamSynchronize(tl_batch_ctx->stream);
+      for (auto* r : reqs) r->error = e.what();
     }
     lk.lock();
     for (auto* r : reqs) r->status = st;
@@ -1098,11 +1107,12 @@ static void batch_sa_maybe_run(BatchSA* b, std::unique_lock<std::mutex>& lk) {
 
 static int batch_sa_provider(void* user, const int32_t* tok, uint64_t n, int32_t term, uint32_t cap, uint32_t* sa, uint32_t* lcp) {
   BatchSA* b = static_cast<BatchSA*>(user);
-  BatchSA::Req r{tok, n, term, cap, sa, lcp, -1};
+  BatchSA::Req r{tok, n, term, cap, sa, lcp, -1, {}};
   std::unique_lock<std::mutex> lk(b->mu);
   b->pending.push_back(&r);
   batch_sa_maybe_run(b, lk);
   b->cv.wait(lk, [&] { return r.status >= 0; });
+  if (r.status) tl_provider_error = r.error;
   return r.status;
 }
 
