@@ -22,6 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
                   "-I" + CSRC, "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+NVFLAGS += os.environ.get("ITT_NVCC_EXTRA", "").split()  # A/B builds of kernel variants (e.g. -DITT_HASH_MINB=5)
 CUDA_SO = os.path.join(HERE, "libitertrace_cuda.so")
 CLI_BIN = os.path.join(HERE, "itertrace")  # the reference tool's CLI on the B200 path (tools/itertrace_cli.cpp)
 REF_INC = os.environ.get("ITT_REFERENCE_INCLUDE", "/root/reference/proj/include")

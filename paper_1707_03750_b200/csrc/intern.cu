@@ -24,7 +24,6 @@ namespace itt {
 namespace {
 
 constexpr int kHashBlock = 128;
-constexpr int kRepScratch = 144;  // per-lane staging of the slot representative's name (any name <= 120 B at any alignment)
 constexpr int kWarpBuf = 4096;  // staged name bytes per warp
 constexpr uint32_t kDevSmem = 64;
 constexpr uint32_t kStreamTableCap = 4096;
@@ -43,7 +42,6 @@ __device__ __forceinline__ int kind_from(uint8_t nb, bool has_tp) {
   return has_tp ? ITT_KIND_OTHER : ITT_KIND_KERNEL;
 }
 
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
 // low n (< 8) bytes of w, or w
 __device__ __forceinline__ uint64_t low_bytes(uint64_t w, uint32_t n) {
   return n >= 8 ? w : (w & ((1ull << (8 * n)) - 1ull));
@@ -57,43 +55,59 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   k ^= k >> 33;
   return k;
 }
-// 64-bit hash of a byte string read through `get(i)`
-template <typename Get>
-__device__ __forceinline__ uint64_t hash_name(Get get, uint32_t len, uint64_t seed) {
-  uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
-  uint32_t i = 0;
-  for (; i + 8 <= len; i += 8) {
-    uint64_t w = 0;
+// Name hash: NH (two 32x32->64 products per 16-byte chunk, keys from the seed) summed over the
+// name's 16-byte chunks, then fmix64 with the length.  The sum does not depend on the order the
+// chunks are visited in, so eight lanes hash one name at once (one chunk each, a 3-step shuffle
+// reduction) — coalesced shared-memory reads instead of one lane walking each name.  A new seed
+// draws new keys, so a collision (caught by the byte compare) does not survive a re-run.
+__device__ __forceinline__ uint32_t nh_key(uint64_t seed, uint32_t idx) {
+  return static_cast<uint32_t>(fmix64(seed ^ ((static_cast<uint64_t>(idx) + 1) * 0x9E3779B97F4A7C15ull)));
+}
+__device__ __forceinline__ void nh_keys(uint64_t seed, uint32_t chunk, uint32_t (&k)[4]) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) w |= static_cast<uint64_t>(get(i + j)) << (8 * j);
-    h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
-  }
-  uint64_t w = 0;
-  for (uint32_t j = 0; i + j < len; ++j) w |= static_cast<uint64_t>(get(i + j)) << (8 * j);
-  h = rotl64(h ^ (w * 0x87c37b91114253d5ull + len), 31) * 0x4cf5ad432745937full;
-  h = fmix64(h);
+  for (int i = 0; i < 4; ++i) k[i] = nh_key(seed, chunk * 4 + i);
+}
+__device__ __forceinline__ uint64_t nh_chunk(const uint32_t (&x)[4], const uint32_t (&k)[4]) {
+  return static_cast<uint64_t>(x[0] + k[0]) * (x[1] + k[1]) + static_cast<uint64_t>(x[2] + k[2]) * (x[3] + k[3]);
+}
+__device__ __forceinline__ uint64_t nh_final(uint64_t sum, uint32_t len, uint64_t seed) {
+  const uint64_t h = fmix64(sum ^ seed ^ (static_cast<uint64_t>(len) * 0xC2B2AE3D27D4EB4Full));
   return h ? h : 1;  // 0 marks an empty slot
 }
+// keep the first v (0..16) bytes of a chunk, zero the rest
+__device__ __forceinline__ void mask_chunk(uint32_t (&x)[4], int v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b = v - 4 * i;
+    x[i] = b >= 4 ? x[i] : (b <= 0 ? 0u : x[i] & ((1u << (8 * b)) - 1u));
+  }
+}
 
-// Stage the name bytes of rows [g0, g1) into a per-warp shared buffer with 16-byte loads.
-// Returns false when they do not fit (the caller then reads global memory directly).
-__device__ __forceinline__ bool stage_names(const uint8_t* __restrict__ bytes, uint64_t total, uint64_t b0, uint64_t b1,
+// Stage the name bytes of rows [g0, g1) into a per-warp shared buffer with 16-byte cp.async
+// copies (L2-only: the names are streamed once); the caller commits and waits.  Returns false when
+// they do not fit (the caller then reads global memory directly).
+__device__ __forceinline__ bool stage_issue(const uint8_t* __restrict__ bytes, uint64_t total, uint64_t b0, uint64_t b1,
                                             uint8_t* buf, uint64_t& base) {
   const uint64_t a0 = b0 & ~15ull, a1 = (b1 + 15) & ~15ull;
+  base = a0;
   if (a1 - a0 > static_cast<uint64_t>(kWarpBuf)) return false;
   const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
-  // all 16-byte chunks in flight at once (cp.async, L2-only: the names are streamed once)
-  for (uint64_t o = a0 + lane_id() * 16; o < a1; o += 512) {
-    if (aligned && o + 16 <= total) {
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + (o - a0)));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(bytes + o) : "memory");
-    } else {
-      for (int j = 0; j < 16; ++j) buf[o - a0 + j] = o + j < total ? bytes[o + j] : 0;
+  if (aligned && a1 <= total) {  // every chunk in bounds: 32-bit shared offsets, one cp.async each
+    const uint32_t nch = static_cast<uint32_t>((a1 - a0) >> 4);
+    const uint32_t dst0 = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+    const uint8_t* src0 = bytes + a0;
+    for (uint32_t ch = lane_id(); ch < nch; ch += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + ch * 16), "l"(src0 + ch * 16) : "memory");
+  } else {
+    for (uint64_t o = a0 + lane_id() * 16; o < a1; o += 512) {
+      if (aligned && o + 16 <= total) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + (o - a0)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(bytes + o) : "memory");
+      } else {
+        for (int j = 0; j < 16; ++j) buf[o - a0 + j] = o + j < total ? bytes[o + j] : 0;
+      }
     }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  base = a0;
   return true;
 }
 
@@ -350,6 +364,10 @@ struct HashArgs {
   const uint64_t* arena_off;
   const uint16_t* device;
   uint64_t* tkey;  // (32-bit hash fragment | 1) << 32 | row of the slot's first inserter; 0 = empty
+  uint64_t* tready;  // (128-byte unit of the slot's copy in `copies` + 1) << 32 | name length; 0 = not yet
+  uint8_t* copies;   // representatives' names, 128-byte aligned, zero-padded to whole 16-byte chunks
+  uint64_t copies_cap;
+  unsigned long long* copies_top;
   uint32_t mask;
   uint64_t seed;
   uint32_t* slot_out;
@@ -359,124 +377,343 @@ struct HashArgs {
   uint32_t* dev_max;
 };
 
-// 64-bit hash of a name staged in shared memory: 8-byte words from funnel-shifted aligned loads;
-// the 0-7 byte tail is the next 8 staged bytes masked (the staging buffers are padded, so every
-// read stays in bounds) — no byte loop
-__device__ __forceinline__ uint64_t hash_staged(const SharedBytes& p, uint32_t len, uint64_t seed) {
-  uint64_t h = seed ^ (static_cast<uint64_t>(len) * 0x9E3779B97F4A7C15ull);
-  SharedStream st(p);
-  uint32_t i = 0;
-  for (; i + 8 <= len; i += 8) {
-    const uint32_t lo = st.next4();
-    const uint64_t w = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(st.next4()) << 32);
-    h = rotl64(h ^ (w * 0x87c37b91114253d5ull), 31) * 0x4cf5ad432745937full;
+// name-relative bytes [q, q + 16) of a name staged at shared address `s`: five aligned words,
+// funnel-shifted (the staging buffer is padded, so the fifth word is always in bounds)
+__device__ __forceinline__ void chunk_shared(uint32_t s, uint32_t q, uint32_t (&x)[4]) {
+  const uint32_t a = s + q, w = a & ~3u, sh = (a & 3u) * 8;
+  uint32_t v[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) v[i] = SharedStream::lds(w + 4 * i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = __funnelshift_r(v[i], v[i + 1], sh);
+}
+// the same from global memory, byte by byte (groups too long to stage)
+__device__ __forceinline__ void chunk_global(const uint8_t* p, int v, uint32_t (&x)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (4 * i + j < v) w |= static_cast<uint32_t>(__ldg(p + 4 * i + j)) << (8 * j);
+    x[i] = w;
   }
-  const uint32_t lo = st.next4();
-  const uint64_t w = low_bytes(static_cast<uint64_t>(lo) | (static_cast<uint64_t>(st.next4()) << 32), len - i);
-  h = rotl64(h ^ (w * 0x87c37b91114253d5ull + len), 31) * 0x4cf5ad432745937full;
-  h = fmix64(h);
-  return h ? h : 1;  // bit-identical to hash_name (the unstaged path): one name, one hash
+}
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
 }
 
-// Hash every name (bytes staged per warp in shared memory), find or claim its slot with one 64-bit
-// CAS of (hash fragment, row) — the first inserter's row is the slot representative — then compare
-// every record's bytes with that representative: a mismatch means two different names landed in
-// one slot and raises the collision flag (the host re-runs with another seed), so a hash never
-// decides equality on its own.  Device census: one ballot round per distinct device id in the warp.
-__global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
-  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][kWarpBuf + 16];
-  __shared__ __align__(16) uint8_t s_rep[kHashBlock / 32][32][kRepScratch + 16];
+// One warp per group of 32 consecutive rows.  The group's name bytes are staged into shared
+// memory (one contiguous cp.async range); then
+//   1. hash: sub-warp `sub` (8 lanes) hashes name 4*it + sub in round `it`, one 16-byte chunk per
+//      lane, and the hash moves to the name's own lane;
+//   2. probe (lane per row): find the slot or claim it with one 64-bit CAS of (hash fragment, row);
+//      the claimer also reserves a 16-byte aligned copy of its name in `copies`;
+//   3. verify (sub-warp per name again): a claimer writes its copy and publishes it in tready; any
+//      other row whose slot copy is published compares its chunks (still in registers from step 1
+//      for names up to 128 bytes) with the copy — one coalesced 16-byte load per lane; rows whose
+//      slot copy is not yet published (its claimer is still in flight) compare with the
+//      representative row's own bytes, lane by lane.
+// A byte mismatch means two different names landed in one slot: the collision flag makes the host
+// re-run with another seed, so a hash never decides equality on its own.  Device census: one
+// ballot round per distinct device id in the warp.
+#ifndef ITT_HASH_MINB
+#define ITT_HASH_MINB 4  // 4 CTAs per SM: more warps hide the probe and copy latency (C3: 6.9 -> 5.8 ms)
+#endif
+__global__ void __launch_bounds__(kHashBlock, ITT_HASH_MINB) k_hash_insert(HashArgs a) {
+  // double-buffered names; padded so a lane past its name's end still reads inside the buffer
+  __shared__ __align__(16) uint8_t s_buf[kHashBlock / 32][2][kWarpBuf + 144];
+  __shared__ __align__(16) uint64_t s_part[kHashBlock / 32][8][32];  // per-lane NH partial sums
+  __shared__ uint4 s_mask[17];  // s_mask[v]: keep the first v bytes of a 16-byte chunk
+  __shared__ uint2 s_nm[kHashBlock / 32][32];  // per row of the group: (length, offset) / (mode, copy)
   __shared__ unsigned int s_dev[kDevSmem];
+  __shared__ uint32_t s_devmax;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned sub = lane >> 3, t = lane & 7;
   for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x) s_dev[i] = 0;
+  if (threadIdx.x == 0) s_devmax = 0;
+  uint32_t dev_hi = 0;  // largest device id this thread counted
+  if (threadIdx.x < 17) {
+    uint32_t x[4] = {~0u, ~0u, ~0u, ~0u};
+    mask_chunk(x, static_cast<int>(threadIdx.x));
+    s_mask[threadIdx.x] = make_uint4(x[0], x[1], x[2], x[3]);
+  }
   __syncthreads();
-  uint8_t* buf = s_buf[warp];
   if (a.total == ~0ull) a.total = __ldg(&a.name_off[a.n]);  // resident names: end of the byte buffer
+  uint32_t key0[4];  // NH keys of this lane's chunk in the first 128 bytes of a name
+  nh_keys(a.seed, t, key0);
   const uint64_t groups = (a.n - a.row0 + 31) / 32;
   const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
   bool bad = false;
-  // name offsets: one load per lane (+ lane 31 the group's end), issued one group ahead
+  // name offsets: one load per lane (+ lane 31 the group's end), issued two groups ahead
   auto offsets = [&](uint64_t g, uint64_t& off, uint64_t& nxt) {
     const uint64_t r0 = a.row0 + g * 32;
     off = g < groups ? __ldg(&a.name_off[umin64(r0 + lane, a.n)]) : 0;
     nxt = g < groups && lane == 31 ? __ldg(&a.name_off[umin64(r0 + 32, a.n)]) : 0;
   };
+  // a group's name ends and byte span; its names go into buffer `b` (one group ahead of use)
+  auto stage = [&](uint64_t g, uint64_t off, uint64_t nxt, int b, uint64_t& end, uint64_t& base) -> bool {
+    const uint64_t g0 = a.row0 + g * 32, cnt = umin64(32, a.n - g0);
+    const uint64_t down = __shfl_down_sync(0xffffffffu, off, 1);
+    end = lane == 31 ? nxt : down;  // name_off[row + 1]
+    const uint64_t b0 = __shfl_sync(0xffffffffu, off, 0);
+    const uint64_t b1 = __shfl_sync(0xffffffffu, end, static_cast<int>(cnt - 1));
+    return stage_issue(a.bytes, a.total, b0, b1, s_buf[warp][b], base);
+  };
   uint64_t g = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
-  uint64_t off_n, end_n;
-  offsets(g, off_n, end_n);
+  uint64_t my_off = 0, my_end = 0, cur_base = 0, off_n = 0, end_n = 0;
+  bool cur_staged = false;
+  int cur = 0;
+  if (g < groups) {
+    uint64_t nxt;
+    offsets(g, my_off, nxt);
+    cur_staged = stage(g, my_off, nxt, 0, my_end, cur_base);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  offsets(g + gstride, off_n, end_n);
   for (; g < groups; g += gstride) {
     const uint64_t g0 = a.row0 + g * 32, g1 = min(g0 + 32, a.n);
     const uint64_t row = g0 + lane;
     const bool valid = row < a.n;
-    uint64_t my_off = off_n, my_end = end_n;
-    offsets(g + gstride, off_n, end_n);  // the next group's, in flight while this one is processed
-    {
-      const uint64_t down = __shfl_down_sync(0xffffffffu, my_off, 1);
-      my_end = lane == 31 ? my_end : down;  // name_off[row + 1]
+    // the next group's names into the other buffer while this group is processed
+    uint64_t nx_end = 0, nx_base = 0, nx_off = off_n;
+    bool nx_staged = false;
+    if (g + gstride < groups) nx_staged = stage(g + gstride, off_n, end_n, cur ^ 1, nx_end, nx_base);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    offsets(g + 2 * gstride, off_n, end_n);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    uint8_t* buf = s_buf[warp][cur];
+    const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+    const uint64_t base = cur_base;
+    const bool staged = cur_staged;
+    const uint32_t len = valid ? static_cast<uint32_t>(my_end - my_off) : 0u;
+
+    // ---- 1. hash, 8 lanes per name; each lane's partial sum goes through shared memory, and the
+    // name's own lane adds its eight partials
+    const uint32_t rel = static_cast<uint32_t>(my_off - base);  // staged: the name's offset in buf
+    const bool short_names = __all_sync(0xffffffffu, len <= 128);
+    uint32_t xw[8][4];  // this lane's chunk of the first 128 bytes of name 4*it + sub
+    if (staged && short_names) {  // the common case: one chunk per lane, straight-line code
+      s_nm[warp][lane] = make_uint2(len, rel);
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const uint2 nm = s_nm[warp][4 * it + sub];  // (length, offset in buf) of this sub-warp's name
+        const int vb = static_cast<int>(nm.x) - static_cast<int>(16 * t);  // valid bytes of this lane's chunk
+        uint32_t x[4];
+        chunk_shared(sbuf + nm.y, 16 * t, x);  // in bounds: the buffer is padded past a chunk
+        const uint4 m = s_mask[min(max(vb, 0), 16)];
+        x[0] &= m.x, x[1] &= m.y, x[2] &= m.z, x[3] &= m.w;
+        const uint64_t c = nh_chunk(x, key0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xw[it][i] = x[i];
+        s_part[warp][it][lane] = vb > 0 ? c : 0ull;
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int j = 4 * it + static_cast<int>(sub);
+        const uint32_t lj = __shfl_sync(0xffffffffu, len, j);
+        uint32_t relj = 0;
+        uint64_t oj = 0;
+        if (staged) relj = __shfl_sync(0xffffffffu, rel, j);
+        else oj = __shfl_sync(0xffffffffu, my_off, j);
+        uint64_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xw[it][i] = 0;
+        for (uint32_t q = 16 * t; q < lj; q += 128) {
+          uint32_t x[4];
+          const int v = static_cast<int>(min(16u, lj - q));
+          if (staged) chunk_shared(sbuf + relj, q, x);
+          else chunk_global(a.bytes + oj + q, v, x);
+          const uint4 m = s_mask[v];
+          x[0] &= m.x, x[1] &= m.y, x[2] &= m.z, x[3] &= m.w;
+          if (q < 128) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xw[it][i] = x[i];
+            acc += nh_chunk(x, key0);
+          } else {
+            uint32_t kk[4];
+            nh_keys(a.seed, q / 16, kk);
+            acc += nh_chunk(x, kk);
+          }
+        }
+        s_part[warp][it][lane] = acc;
+      }
     }
-    uint64_t base = 0;
-    const uint64_t b0 = __shfl_sync(0xffffffffu, my_off, 0);
-    const uint64_t b1 = __shfl_sync(0xffffffffu, my_end, static_cast<int>(g1 - g0 - 1));
-    const bool staged = stage_names(a.bytes, a.total, b0, b1, buf, base);
+    __syncwarp();
+    uint64_t my_h;
+    {
+      const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(&s_part[warp][lane >> 2][8 * (lane & 3)]);
+      uint64_t sum = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const ulonglong2 v = pp[i];
+        sum += v.x + v.y;
+      }
+      my_h = nh_final(sum, len, a.seed);
+    }
+    __syncwarp();  // s_part is rewritten by the next group
+    if (a.seed == 0) my_h = 1;  // test hook (ITT_TEST_FORCE_COLLISION): every name in one slot
+    // ---- 2. probe, lane per row
+    uint32_t s = 0, rep = static_cast<uint32_t>(row);
+    uint64_t ready = 0, copy_at = ~0ull;
+    bool claimed = false;
     if (valid) {
-      const uint64_t o = my_off;
-      const uint32_t len = static_cast<uint32_t>(my_end - o);
-      // separate shared / global paths so the staged case compiles to LDS, not generic loads
-      const uint64_t h = staged ? hash_staged(SharedBytes(buf + (o - base)), len, a.seed)
-                                : hash_name([&](uint32_t i) { return a.bytes[o + i]; }, len, a.seed);
-      const uint64_t frag = ((h >> 32) | 1ull) << 32;  // nonzero: 0 marks an empty slot
-      uint32_t s = static_cast<uint32_t>(h) & a.mask, rep = static_cast<uint32_t>(row);
+      const uint64_t frag = ((my_h >> 32) | 1ull) << 32;  // nonzero: 0 marks an empty slot
+      s = static_cast<uint32_t>(my_h) & a.mask;
       for (uint32_t probe = 0;; ++probe) {
         if (probe > a.mask) {
           atomicOr(&a.used_count[1], 1u);
           break;
         }
         uint64_t k = ld_relaxed_u64(&a.tkey[s]);
+        const uint64_t rd = ld_relaxed_u64(&a.tready[s]);  // a published copy is final: read with the key
         if (k == 0) {
-          const unsigned long long mine_key = frag | row;
-          k = atomicCAS(reinterpret_cast<unsigned long long*>(&a.tkey[s]), 0ull, mine_key);
+          k = atomicCAS(reinterpret_cast<unsigned long long*>(&a.tkey[s]), 0ull, frag | row);
           if (k == 0) {  // claimed: this row represents the slot
+            claimed = true;
             a.used[atomicAdd(&a.used_count[0], 1u)] = s;
+            // 128-byte aligned copies: an L1 line never holds bytes of a copy not yet published
+            const uint64_t need = (static_cast<uint64_t>(len) + 127) & ~127ull;
+            const unsigned long long at = atomicAdd(a.copies_top, static_cast<unsigned long long>(need));
+            if (at + need <= a.copies_cap) copy_at = at;  // else the slot keeps no copy (the slow compare)
             break;
           }
         }
         if ((k & 0xFFFFFFFF00000000ull) == frag) {
           rep = static_cast<uint32_t>(k);
+          ready = rd;
           break;
         }
         s = (s + 1) & a.mask;
       }
       a.slot_out[row] = s;
-      if (rep != row) {
-        const uint64_t ro = a.name_off[rep];
-        const uint32_t rlen = static_cast<uint32_t>(a.name_off[rep + 1] - ro);
-        bool same = rlen == len;
-        if (same) {
-          const uint64_t q0 = ro & ~15ull, q1 = (ro + len + 15) & ~15ull;
-          const bool aligned = (reinterpret_cast<uintptr_t>(a.bytes) & 15) == 0;
-          if (rep < a.row0) {  // streamed: the representative's chunk is gone, its bytes are in the arena
-            const GlobalBytes rb(a.arena + a.arena_off[s]);
-            same = staged ? same_bytes(SharedBytes(buf + (o - base)), rb, len) : same_bytes(GlobalBytes(a.bytes + o), rb, len);
-          } else if (staged && rep >= g0 && rep < g1) {
-            same = same_bytes(SharedBytes(buf + (o - base)), SharedBytes(buf + (ro - base)), len);
-          } else if (staged && aligned && q1 - q0 <= kRepScratch && q0 >= a.lo && q1 <= a.total) {
-            // the representative's bytes into this lane's scratch in one round trip (cp.async),
-            // then a shared-to-shared compare instead of a chain of dependent global loads
-            uint8_t* scr = s_rep[warp][lane];
-            for (uint64_t q = q0; q < q1; q += 16) {
-              const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(scr + (q - q0)));
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.bytes + q) : "memory");
+    }
+
+    // ---- 3. verify: 0 nothing, 1 write the slot copy, 2 compare with the copy, 3 slow compare
+    uint32_t mode = 0;
+    uint64_t at = 0;
+    if (valid) {
+      if (claimed) {
+        if (copy_at != ~0ull) mode = 1, at = copy_at;
+      } else if (ready != 0) {
+        if (static_cast<uint32_t>(ready) != len) bad = true;  // different lengths: different names
+        else mode = 2, at = ((ready >> 32) - 1) << 7;
+      } else if (rep != row) {
+        mode = 3;
+      }
+      if (len >= (1u << 30)) mode = mode == 1 ? 0u : (mode == 2 ? 3u : mode);  // keep `pk` exact
+    }
+    // mode and length in one word, the copy's offset in 128-byte units (copies_cap < 2^38 bytes)
+    const uint32_t pk = mode | (len << 2);
+    const uint32_t atu = static_cast<uint32_t>(at >> 7);
+    if (__any_sync(0xffffffffu, mode == 1)) {  // claimers write their copies, then publish them
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int j = 4 * it + static_cast<int>(sub);
+        const uint32_t pj = __shfl_sync(0xffffffffu, pk, j);
+        const uint32_t aj = __shfl_sync(0xffffffffu, atu, j);
+        const uint32_t lj = pj >> 2;
+        uint32_t relj = 0;
+        uint64_t oj = 0;
+        if (staged) relj = __shfl_sync(0xffffffffu, rel, j);
+        else oj = __shfl_sync(0xffffffffu, my_off, j);
+        if ((pj & 3u) == 1u) {
+          for (uint32_t q = 16 * t; q < lj; q += 128) {
+            uint32_t x[4];
+            if (q < 128) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) x[i] = xw[it][i];
+            } else {
+              const int v = static_cast<int>(min(16u, lj - q));
+              if (staged) chunk_shared(sbuf + relj, q, x);
+              else chunk_global(a.bytes + oj + q, v, x);
+              if (v < 16) mask_chunk(x, v);
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            same = same_bytes(SharedBytes(buf + (o - base)), SharedBytes(scr + (ro - q0)), len);
-          } else if (staged) {
-            same = same_bytes(SharedBytes(buf + (o - base)), GlobalBytes(a.bytes + ro), len);
-          } else {
-            same = same_bytes(GlobalBytes(a.bytes + o), GlobalBytes(a.bytes + ro), len);
+            *reinterpret_cast<uint4*>(a.copies + (static_cast<uint64_t>(aj) << 7) + q) = make_uint4(x[0], x[1], x[2], x[3]);
           }
         }
-        if (!same) bad = true;
       }
+      __threadfence();
+      __syncwarp();
+      if (mode == 1) st_relaxed_u64(&a.tready[s], ((static_cast<uint64_t>(atu) + 1) << 32) | len);
+    }
+    if (short_names) {  // every name <= 128 bytes: one chunk per lane, four loads in flight at a time
+      s_nm[warp][lane] = make_uint2(pk, atu);
+      __syncwarp();
+      uint32_t diff = 0;
+#pragma unroll
+      for (int h2 = 0; h2 < 8; h2 += 4) {
+        uint4 y[4];
+        bool use[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint2 nm = s_nm[warp][4 * (h2 + u) + sub];  // (mode | length << 2, copy unit)
+          use[u] = (nm.x & 3u) == 2u && 16 * t < (nm.x >> 2);
+          y[u] = make_uint4(0, 0, 0, 0);
+          if (use[u]) y[u] = *reinterpret_cast<const uint4*>(a.copies + (static_cast<uint64_t>(nm.y) << 7) + 16 * t);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t d = (xw[h2 + u][0] ^ y[u].x) | (xw[h2 + u][1] ^ y[u].y) | (xw[h2 + u][2] ^ y[u].z) |
+                             (xw[h2 + u][3] ^ y[u].w);
+          diff |= use[u] ? d : 0u;
+        }
+      }
+      __syncwarp();  // s_nm is rewritten by the next group
+      if (diff) bad = true;
+    } else {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int j = 4 * it + static_cast<int>(sub);
+        const uint32_t pj = __shfl_sync(0xffffffffu, pk, j);
+        const uint32_t aj = __shfl_sync(0xffffffffu, atu, j);
+        const uint32_t lj = pj >> 2;
+        uint32_t relj = 0;
+        uint64_t oj = 0;
+        if (staged) relj = __shfl_sync(0xffffffffu, rel, j);
+        else oj = __shfl_sync(0xffffffffu, my_off, j);
+        uint32_t diff = 0;
+        if ((pj & 3u) == 2u) {
+          for (uint32_t q = 16 * t; q < lj; q += 128) {
+            uint32_t x[4];
+            if (q < 128) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) x[i] = xw[it][i];
+            } else {
+              const int v = static_cast<int>(min(16u, lj - q));
+              if (staged) chunk_shared(sbuf + relj, q, x);
+              else chunk_global(a.bytes + oj + q, v, x);
+              if (v < 16) mask_chunk(x, v);
+            }
+            const uint4 yy = *reinterpret_cast<const uint4*>(a.copies + (static_cast<uint64_t>(aj) << 7) + q);
+            diff |= (x[0] ^ yy.x) | (x[1] ^ yy.y) | (x[2] ^ yy.z) | (x[3] ^ yy.w);
+          }
+        }
+        if (diff) bad = true;
+      }
+    }
+    if (mode == 3) {  // the slot's copy is not published yet: compare with the representative row
+      const uint64_t o = my_off;
+      const uint64_t ro = a.name_off[rep];
+      const uint32_t rlen = static_cast<uint32_t>(a.name_off[rep + 1] - ro);
+      bool same = rlen == len;
+      if (same) {
+        if (rep < a.row0) {  // streamed: the representative's chunk is gone, its bytes are in the arena
+          const GlobalBytes rb(a.arena + a.arena_off[s]);
+          same = staged ? same_bytes(SharedBytes(buf + (o - base)), rb, len) : same_bytes(GlobalBytes(a.bytes + o), rb, len);
+        } else if (staged && rep >= g0 && rep < g1) {
+          same = same_bytes(SharedBytes(buf + (o - base)), SharedBytes(buf + (ro - base)), len);
+        } else if (staged) {
+          same = same_bytes(SharedBytes(buf + (o - base)), GlobalBytes(a.bytes + ro), len);
+        } else {
+          same = same_bytes(GlobalBytes(a.bytes + o), GlobalBytes(a.bytes + ro), len);
+        }
+      }
+      if (!same) bad = true;
     }
     // device census (filter_majority_device): one ballot round per distinct id in the warp
     if (a.device) {
@@ -488,18 +725,23 @@ __global__ void __launch_bounds__(kHashBlock) k_hash_insert(HashArgs a) {
         if (lane == static_cast<unsigned>(__ffs(m) - 1)) {
           if (d0 < kDevSmem) atomicAdd(&s_dev[d0], static_cast<unsigned>(__popc(m)));
           else atomicAdd(&a.dev_counts[d0], static_cast<unsigned long long>(__popc(m)));
-          atomicMax(a.dev_max, d0);
+          dev_hi = max(dev_hi, d0);
         }
         todo &= ~m;
       }
     }
     __syncwarp();
+    my_off = nx_off, my_end = nx_end, cur_base = nx_base, cur_staged = nx_staged;
+    cur ^= 1;
   }
   if (bad) atomicOr(&a.used_count[2], 1u);
+  if (a.device) atomicMax(&s_devmax, dev_hi);
   __syncthreads();
-  if (a.device)
+  if (a.device) {
     for (unsigned i = threadIdx.x; i < kDevSmem; i += blockDim.x)
       if (s_dev[i]) atomicAdd(&a.dev_counts[i], static_cast<unsigned long long>(s_dev[i]));
+    if (threadIdx.x == 0) atomicMax(a.dev_max, s_devmax);
+  }
 }
 
 // Streamed names: after each chunk, copy the names of the slots it claimed (used[snap..count))
@@ -1159,6 +1401,9 @@ void build_dictionary(TraceState& t) {
   }
   uint32_t bits = 14;
   uint64_t seed = 0x243F6A8885A308D3ull;
+  // test hook: the first attempt puts every name into one slot, so the byte compare must catch the
+  // collisions and the re-run with a real seed must recover
+  if (const char* e = std::getenv("ITT_TEST_FORCE_COLLISION"); e && *e == '1') seed = 0;
   const unsigned groups = static_cast<unsigned>(std::min<uint64_t>((n + 31) / 32, 1ull << 30));
   constexpr unsigned kWarpsPerBlock = kHashBlock / 32;
   const unsigned grid =
@@ -1212,21 +1457,31 @@ void build_dictionary(TraceState& t) {
       ITT_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
     }
   }
+  // 16-byte aligned copies of the slot representatives' names (the fast verify path); a slot
+  // whose copy does not fit is verified against its representative row instead
+  DBuf<uint64_t> tready;
+  DBuf<uint8_t> copies;
+  DBuf<unsigned long long> copies_top(c, 1);
   for (int attempt = 0;; ++attempt) {
     const uint32_t cap = 1u << bits;
     t.tkey.alloc(c, cap);
     t.trep.alloc(c, cap);
     t.tflags.alloc(c, cap);
     t.used.alloc(c, cap);
+    tready.alloc(c, cap);
+    const uint64_t copies_cap = std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1ull << 20, static_cast<uint64_t>(cap) * 256));
+    if (copies.n < copies_cap) copies.alloc(c, copies_cap);
     t.tkey.zero();
+    tready.zero();
+    copies_top.zero();
     t.trep.fill_bytes(0xFF);
     counters.zero();
     dev_max.zero();
     if (t.rec.device) dev_counts.zero();
     if (!streamed) {
-      HashArgs ha{t.rec.name_off, t.rec.name_bytes, 0,       total,      0,           n,           nullptr,  nullptr,
-                  t.rec.device,   t.tkey.p,         cap - 1, seed,       t.slot.p,    t.used.p,    counters.p,
-                  dev_counts.p,   dev_max.p};
+      HashArgs ha{t.rec.name_off, t.rec.name_bytes, 0,         total,        0,          n,         nullptr,
+                  nullptr,        t.rec.device,     t.tkey.p,  tready.p,     copies.p,   copies.n,  copies_top.p,
+                  cap - 1,        seed,             t.slot.p,  t.used.p,     counters.p, dev_counts.p, dev_max.p};
       // algorithmic bytes (names once): name bytes + offset (8) + slot (4) + device id (2)
       launch(c, "intern_hash", static_cast<double>(name_bytes) + n * (t.rec.device ? 14.0 : 12.0), k_hash_insert, dim3(grid),
              dim3(kHashBlock), 0, ha);
@@ -1259,9 +1514,9 @@ void build_dictionary(TraceState& t) {
         const uint64_t cgroups = (r1 - r0 + 31) / 32;
         const unsigned cgrid = static_cast<unsigned>(
             std::max<uint64_t>(1, std::min<uint64_t>((cgroups + kWarpsPerBlock - 1) / kWarpsPerBlock, c->sm_count * 12)));
-        HashArgs ha{t.rec.name_off, bytes,   lo,       hi,          r0,          r1,          arena.p,  arena_off.p,
-                    t.rec.device,   t.tkey.p, cap - 1, seed,        t.slot.p,    t.used.p,    counters.p,
-                    dev_counts.p,   dev_max.p};
+        HashArgs ha{t.rec.name_off, bytes,        lo,       hi,       r0,         r1,       arena.p,
+                    arena_off.p,    t.rec.device, t.tkey.p, tready.p, copies.p,   copies.n, copies_top.p,
+                    cap - 1,        seed,         t.slot.p, t.used.p, counters.p, dev_counts.p, dev_max.p};
         launch(c, "intern_hash", static_cast<double>(bounds[k + 1] - bounds[k]) + (r1 - r0) * (t.rec.device ? 14.0 : 12.0), k_hash_insert,
                dim3(cgrid), dim3(kHashBlock), 0, ha);
         launch(c, "intern_save_reps", 0.0, k_save_reps, dim3(c->sm_count), dim3(128), 0, t.used.p, snap.p, counters.p,
@@ -1285,6 +1540,7 @@ void build_dictionary(TraceState& t) {
     if (cnt[2]) {  // a true 64-bit collision between different names: new seed
       if (attempt >= 3) fail(ITT_E_INVALID_ARGUMENT, "stream-classify: unresolvable name hash collision");
       seed = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+      if (seed == 0) seed = 1;
       continue;
     }
     t.n_used = cnt[0];

@@ -1,0 +1,2 @@
+python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "not c5" 2>&1 | tail -4 > gpurun_out/r02r_tests.log
+python scripts/opprof_c3.py C3 > gpurun_out/r02r_timing.log 2>&1

@@ -173,6 +173,45 @@ def test_long_names_staged_and_unstaged_intern_identically(ctx, R):
     assert np.array_equal(gt, rt) and len(gn) == len(rn) == 15
 
 
+def _adversarial_name_pool(rng):
+    """Names of every length class the dictionary kernel splits on (0, < 16, chunk and 128-byte
+    boundaries, > 128, > 300) and near-duplicates differing in one byte at the first, a chunk-edge,
+    the middle and the last position, or by one extra byte (prefixes)."""
+    pool = [""]
+    for L in (1, 3, 4, 7, 8, 15, 16, 17, 31, 32, 33, 63, 64, 100, 127, 128, 129, 143, 144, 200, 255, 256, 257, 300, 520):
+        base = bytes(rng.integers(33, 127, size=L, dtype=np.uint8)).decode()
+        pool.append(base)
+        pool.append(base + "x")
+        for pos in {0, L // 2, L - 1, 15, 16, 127, 128, 129}:
+            if 0 <= pos < L:
+                ch = "A" if base[pos] != "A" else "B"
+                pool.append(base[:pos] + ch + base[pos + 1:])
+    return sorted(set(pool))
+
+
+@pytest.mark.parametrize("force_collision", [False, True])
+def test_dictionary_adversarial_names(ctx, R, force_collision, monkeypatch):
+    """Exact dictionary on names built to break a hash-only scheme; with ITT_TEST_FORCE_COLLISION
+    every name first lands in ONE slot, so the byte compares (copy, representative row, length)
+    must catch every collision and the re-run must recover."""
+    if force_collision:
+        monkeypatch.setenv("ITT_TEST_FORCE_COLLISION", "1")
+    rng = np.random.default_rng(77)
+    pool = _adversarial_name_pool(rng)
+    longs = [x for x in pool if len(x) > 200]
+    ops, t = [], 0
+    for blk in range(300):
+        # some warp groups only long names (their bytes exceed the staging buffer), the rest mixed
+        src = longs if blk % 5 == 0 else pool
+        for _ in range(32 + int(rng.integers(0, 7))):  # ragged groups: every name alignment occurs
+            ops.append((13, src[int(rng.integers(0, len(src)))], t, 5))
+            t += 7
+    recs = records_from_ops(ops)
+    gt, gri, gn = ctx.build_token_sequence(recs, 13)
+    rt, rri, rn = R.build_token_sequence(recs, 13)
+    assert np.array_equal(gt, rt) and np.array_equal(gri, rri) and len(gn) == len(rn)
+
+
 def test_token_replay_100k(ctx):
     # test_streams.cpp:204-225
     rng = np.random.default_rng(33)
