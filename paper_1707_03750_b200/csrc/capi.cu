@@ -16,12 +16,13 @@
 
 using namespace itt;
 
-// onesweep tile shape (radix.cuh kCfgBlock/kCfgItems); ITT_RADIX_CFG overrides for tuning sweeps
+// onesweep tile shape (radix.cuh kCfgBlock/kCfgItems); ITT_RADIX_CFG overrides for tuning sweeps.
+// Default 256 x 12 at 5 CTAs per SM (C3 radix passes 2.84 -> 2.71 ms/step against 512 x 8).
 int itt::radix::config_index() {
   static int cfg = [] {
     const char* e = std::getenv("ITT_RADIX_CFG");
-    const int v = e ? std::atoi(e) : 0;
-    return (v >= 0 && v < 10) ? v : 0;
+    const int v = e ? std::atoi(e) : 9;
+    return (v >= 0 && v < 10) ? v : 9;
   }();
   return cfg;
 }

@@ -133,6 +133,11 @@ __global__ void __launch_bounds__(256) k_hist(const K* __restrict__ keys, uint64
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
+#ifndef ITT_RADIX_MATCH_OR
+#define ITT_RADIX_MATCH_OR 1
+#endif
+constexpr bool kMatchOr = ITT_RADIX_MATCH_OR != 0;
+
 template <typename K, int BLOCK, int ITEMS, int RB>
 struct SmemLayout {
   static constexpr int kTile = BLOCK * ITEMS;
@@ -141,6 +146,8 @@ struct SmemLayout {
   K keys[kTile];
   uint32_t vals[kTile];
   uint16_t warp_hist[kWarps][kDigits];  // per-warp digit counts, then exclusive offsets across warps
+  static constexpr bool kOr = kMatchOr && RB == 8;  // (10-bit digits: 4 KiB per warp, ballots only)
+  uint32_t match[kOr ? kWarps : 1][kOr ? kDigits : 1];  // per-warp lane masks per digit (kept zero)
   uint32_t local_off[kDigits];
   uint32_t global_base[kDigits];
   uint32_t warp_sum[2][kWarps];  // block scan of (tile count, histogram) per digit owner
@@ -174,6 +181,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
   {
     uint4* wh4 = reinterpret_cast<uint4*>(&S.warp_hist[0][0]);
     for (int i = threadIdx.x; i < kWarps * kDigits * 2 / 16; i += BLOCK) wh4[i] = make_uint4(0, 0, 0, 0);
+    if constexpr (S_t::kOr) {
+      uint4* m4 = reinterpret_cast<uint4*>(&S.match[0][0]);
+      for (int i = threadIdx.x; i < kWarps * kDigits / 4; i += BLOCK) m4[i] = make_uint4(0, 0, 0, 0);
+    }
   }
   __syncthreads();
   const uint32_t tile = S.tile;
@@ -192,18 +203,39 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_onesweep(Loader ld, K* __restri
     const uint64_t i = warp_base + r * 32 + lane;
     if (i < n) ld(i, key[r], val[r]);
   }
-  // ---- stable per-warp ranking
+  // ---- stable per-warp ranking.  Peers (the lanes holding the same digit) come from ballots over
+  // the digit bits that vary in the warp when there are few of them (the group ids of periodic
+  // traces: often none), else from one shared-memory atomic OR of the lane bit into the digit's
+  // word (kMatchOr): one atomic and one load instead of up to RB ballots.
   uint16_t* wh = S.warp_hist[warp];
+  uint32_t* wb = S.match[warp];
 #pragma unroll
   for (int r = 0; r < ITEMS; ++r) {
     const uint64_t i = warp_base + r * 32 + lane;
     const bool valid = i < n;
     const uint32_t d = valid ? digit_of<RB>(key[r], shift) : 0u;
-    const unsigned peers = digit_peers<RB>(d, valid);
+    unsigned peers;
+    bool or_path = false;
+    if constexpr (S_t::kOr) {
+      const unsigned vary = (__reduce_or_sync(0xffffffffu, d) ^ __reduce_and_sync(0xffffffffu, d)) & ((1u << RB) - 1u);
+      or_path = __popc(vary) > 2;
+      if (or_path) {
+        if (valid) atomicOr(&wb[d], 1u << lane);
+        __syncwarp();
+        peers = valid ? wb[d] : 0u;
+      } else {
+        peers = digit_peers<RB>(d, valid);
+      }
+    } else {
+      peers = digit_peers<RB>(d, valid);
+    }
     uint32_t base = 0;
     if (valid) base = wh[d];
     __syncwarp();
-    if (valid && lane == static_cast<unsigned>(__ffs(peers) - 1)) wh[d] = static_cast<uint16_t>(base + __popc(peers));
+    if (valid && lane == static_cast<unsigned>(__ffs(peers) - 1)) {
+      wh[d] = static_cast<uint16_t>(base + __popc(peers));
+      if (or_path) wb[d] = 0u;  // every peer has read the word (the barrier above)
+    }
     __syncwarp();
     rank[r] = base + __popc(peers & lanemask_lt());
   }

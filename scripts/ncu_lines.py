@@ -15,22 +15,30 @@ with tempfile.TemporaryDirectory() as td:
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=td, capture_output=True)
     cub = [f for f in os.listdir(td) if f.endswith(".cubin")][0]
     dis = subprocess.run(["nvdisasm", "-g", os.path.join(td, cub)], capture_output=True, text=True).stdout.splitlines()
-start = next(i for i, l in enumerate(dis) if l.startswith("_Z") and kname in l and l.endswith(":"))
-insts, cur = {}, None
-for l in dis[start + 1:]:
-    if l.startswith(".section") or (l.startswith("_Z") and l.endswith(":")):
-        break
-    m = re.search(r'//## File "([^"]+)", line (\d+)', l)
-    if m:
-        cur = (os.path.basename(m.group(1)), int(m.group(2)))
-        continue
-    m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*)", l)
-    if m:
-        insts[int(m.group(1), 16)] = cur
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 h, data = rows[hi], [r for r in rows[hi + 1:] if len(r) > 5]
+
+
+def parse(start):
+    insts, cur = {}, None
+    for l in dis[start + 1:]:
+        if l.startswith(".section") or (l.startswith("_Z") and l.endswith(":")):
+            break
+        m = re.search(r'//## File "([^"]+)", line (\d+)', l)
+        if m:
+            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            continue
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*)", l)
+        if m:
+            insts[int(m.group(1), 16)] = cur
+    return insts
+
+
+# several instantiations can match the name: take the one whose length equals the profiled SASS
+cands = [parse(i) for i, l in enumerate(dis) if l.startswith("_Z") and kname in l and l.endswith(":")]
+insts = min(cands, key=lambda c: abs(len(c) - len(data)))
 si, ie = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 base = int(data[0][0], 16)
 by = collections.defaultdict(lambda: [0, 0])
