@@ -139,6 +139,10 @@ __device__ __forceinline__ uint64_t first_lt_in_tile(const AnsvArgs& a, uint32_t
   return lo;
 }
 
+// Most positions are decided by their neighbours alone: LCP[k-1] == l (k is not leftmost),
+// or LCP[k-1] < l (the PSE is k-1) with LCP[k+1] < l (the NSV is k+1).  Only the rest search —
+// and the tile builds its shared-memory sparse table only when one of its positions needs it
+// (periodic traces: runs of equal capped LCPs, a few searches per suffix group).
 __global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
   __shared__ uint32_t st[kLogTileA][kTileA];  // st[l][x] = min(LCP[x, x + 2^l)) within the tile
   const uint32_t t = blockIdx.x;
@@ -146,6 +150,35 @@ __global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
   const uint32_t len = static_cast<uint32_t>(umin64(kTileA, a.np - base));
   for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock) st[0][x] = x < len ? a.lcp[base + x] : 0xFFFFFFFFu;
   __syncthreads();
+  bool any_search = false;
+  for (uint32_t x = threadIdx.x; x < len; x += kAnsvBlock) {
+    const uint64_t k = base + x;
+    const uint32_t l = st[0][x];
+    uint32_t cnt = 0, par = 0, lbv = 0;
+    bool search = false;
+    if (k > 0 && l > 0) {
+      const uint32_t lp = x > 0 ? st[0][x - 1] : a.lcp[k - 1];
+      if (lp > l) {
+        search = true;
+      } else if (lp < l) {  // leftmost, PSE = k - 1
+        const uint32_t ln = k + 1 >= a.np ? 0u : (x + 1 < len ? st[0][x + 1] : a.lcp[k + 1]);
+        if (ln < l) {
+          cnt = 2;  // [k - 1, k + 1)
+          par = max(lp, ln);
+          lbv = static_cast<uint32_t>(k - 1);
+        } else {
+          search = true;
+        }
+      }
+    }
+    any_search |= search;
+    if (!search) {
+      a.cnt[k] = cnt;
+      a.par[k] = par;
+      a.lb[k] = lbv;
+    }
+  }
+  if (!__syncthreads_or(any_search)) return;
   for (int l = 1; l < kLogTileA; ++l) {
     const uint32_t half = 1u << (l - 1);
     for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock)
@@ -155,8 +188,17 @@ __global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
   for (uint32_t x = threadIdx.x; x < len; x += kAnsvBlock) {
     const uint64_t k = base + x;
     const uint32_t l = st[0][x];
+    if (k == 0 || l == 0) continue;
+    {  // the positions the first pass decided
+      const uint32_t lp = x > 0 ? st[0][x - 1] : a.lcp[k - 1];
+      if (lp == l) continue;
+      if (lp < l) {
+        const uint32_t ln = k + 1 >= a.np ? 0u : (x + 1 < len ? st[0][x + 1] : a.lcp[k + 1]);
+        if (ln < l) continue;
+      }
+    }
     uint32_t cnt = 0, par = 0, lbv = 0;
-    if (k > 0 && l > 0) {
+    {
       // ---- previous j < k with LCP[j] <= l
       uint32_t pos = x;
 #pragma unroll
