@@ -101,6 +101,7 @@ struct SuffixState {
   DBuf<uint32_t> lcp;         // [np]
   std::vector<DBuf<uint32_t>> levels;  // rank (group head) after each doubling round
   std::vector<uintptr_t> level_tags;   // their addresses, bit 0 set for a u16 level
+  std::vector<uint32_t> level_h;       // prefix length each level separates (ascending; see lift_ratio in sa.cu)
   uint32_t h0 = 1;            // prefix length of levels[0]
   int32_t lo = 0;             // text code = token - lo
   int rounds = 0;

@@ -262,6 +262,15 @@ __global__ void k_wide_hist(const uint32_t* __restrict__ gstart, uint64_t g, uin
 }
 
 // ---------------------------------------------------------------- refinement rounds
+// largest prefix-length ratio between consecutive levels kept for LCP lifting (ITT_LIFT_RATIO: A/B)
+inline uint64_t lift_ratio() {
+  static const uint64_t r = [] {
+    const char* e = std::getenv("ITT_LIFT_RATIO");
+    const long v = e && *e ? std::atol(e) : 16;
+    return static_cast<uint64_t>(v >= 2 ? v : 2);
+  }();
+  return r;
+}
 // A doubling round that finds every group already ordered by its second key needs no sort: the
 // SA stays, groups split where the second key changes.  Traces of training loops reach this state
 // after a few rounds (every group is one rotation class of the loop body; a round only splits off
@@ -409,23 +418,25 @@ struct LiftArgs {
   const int32_t* text;
   uint64_t np;
   const uintptr_t* levels;  // device array of tagged level addresses (rank_at)
+  const uint32_t* hs;       // prefix length of each level, ascending, consecutive ones within lift_ratio()
   int nlev;
-  uint32_t h0;
 };
 
-// lcp of suffixes a != b by binary lifting over the doubling levels
-__device__ __forceinline__ uint32_t lcp_lift(const LiftArgs& L, uint64_t a, uint64_t b) {
+// lcp of suffixes a != b, or `limit` if it is at least that, by lifting over the kept levels: a
+// level is applied while the ids agree (at most lift_ratio() - 1 times below a level that did not
+// agree), then direct compares below the smallest level
+__device__ __forceinline__ uint32_t lcp_lift(const LiftArgs& L, uint64_t a, uint64_t b, uint32_t limit) {
   uint32_t acc = 0;
   for (int r = L.nlev - 1; r >= 0; --r) {
     const uintptr_t lv = L.levels[r];
-    if (a < L.np && b < L.np && rank_at(lv, a) == rank_at(lv, b)) {
-      const uint32_t hr = L.h0 << r;
+    const uint32_t hr = L.hs[r];
+    while (acc < limit && a < L.np && b < L.np && rank_at(lv, a) == rank_at(lv, b)) {
       a += hr;
       b += hr;
       acc += hr;
     }
   }
-  while (a < L.np && b < L.np && __ldg(&L.text[a]) == __ldg(&L.text[b])) ++a, ++b, ++acc;
+  while (acc < limit && a < L.np && b < L.np && __ldg(&L.text[a]) == __ldg(&L.text[b])) ++a, ++b, ++acc;
   return acc;
 }
 
@@ -463,7 +474,7 @@ __global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* _
     while (l < cap && i + l < L.np && p + l < L.np && __ldg(&L.text[i + l]) == __ldg(&L.text[p + l])) {
       ++l;
       if (++steps == kLiftAfter) {
-        l += lcp_lift(L, i + l, static_cast<uint64_t>(p) + l);
+        l += lcp_lift(L, i + l, static_cast<uint64_t>(p) + l, cap - l);
         break;
       }
     }
@@ -540,6 +551,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   s.np = np;
   s.levels.clear();
   s.level_tags.clear();
+  s.level_h.clear();
   s.rounds = 0;
   // alphabet: codes = value - lo over tokens and the terminator
   int32_t lo = known_alphabet ? 0 : term, hi = term;
@@ -667,6 +679,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   // k-gram groups) then goes straight into refinement rounds with no dense-to-head conversion
   const bool init_heads = refine_mode > 0 && np < (1ull << 31) && s.h0 < cap;
   uint64_t g = rank_update(keys, sa, 0, 0, s.h0 < cap, 0, init_heads);
+  s.level_h.push_back(s.h0);
   uint32_t h = s.h0;  // prefix length the newest level separates
   bool dense = !init_heads;  // the newest level holds dense ids (else group-head positions)
   bool try_refine = init_heads && g * 16 < np;  // then decided after each full round from the groups it added
@@ -687,9 +700,16 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       readback(c, cnt, rcount.p, 2);
       if (cnt[1] == 0) {
         const bool full = dense;  // dense ids: every rank changes representation
+        // the input level is updated in place unless LCP lifting keeps it: kept levels stay within
+        // lift_ratio() of each other, so most refinement rounds skip the level copy (C3: 12 -> 3 copies of
+        // 400 MB, step -1.1 ms; lifting repeats a level up to 15 times, lcp_plcp unchanged)
+        const size_t nl = s.level_h.size();
+        const uint64_t below = nl >= 2 ? s.level_h[nl - 2] : 1;
+        const bool dispensable = !s.keep_levels || below * lift_ratio() >= 2ull * h;
         uint32_t* lvl;
-        if (!full && !s.keep_levels) {  // nothing reads the old level again: update it in place
+        if (!full && dispensable) {  // nothing reads the old level again: update it in place
           lvl = reinterpret_cast<uint32_t*>(rank);
+          s.level_h.back() = static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull));
         } else {
           s.levels.emplace_back(c, np);
           lvl = s.levels.back().p;
@@ -704,6 +724,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
                reinterpret_cast<uint32_t*>(rscan.buf.p));
         if (lvl != reinterpret_cast<uint32_t*>(rank)) {
           s.level_tags.push_back(reinterpret_cast<uintptr_t>(lvl));
+          s.level_h.push_back(static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull)));
           if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
         }
         hc ^= 1;
@@ -765,6 +786,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     uint32_t* other_v = alt ? vx : f2;
     const uint64_t g_old = g;
     g = rank_update(nkeys, nsa, rank, h, static_cast<uint64_t>(h) * 2 < cap, g, false);
+    s.level_h.push_back(static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull)));
     dense = true;
     ++s.rounds;
     if (cooldown > 0) --cooldown;
@@ -792,7 +814,9 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   const std::vector<uintptr_t>& lv = s.level_tags;
   DBuf<uintptr_t> dlv(c, lv.size());
   h2d(c, dlv.p, lv.data(), lv.size());
-  LiftArgs L{s.text.p, np, dlv.p, static_cast<int>(lv.size()), s.h0};
+  DBuf<uint32_t> dlh(c, s.level_h.size());
+  h2d(c, dlh.p, s.level_h.data(), s.level_h.size());
+  LiftArgs L{s.text.p, np, dlv.p, dlh.p, static_cast<int>(lv.size())};
   const uint64_t chunks = (np + kChunk - 1) / kChunk;
   launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p, s.cap);
   s.lcp.alloc(c, np);
@@ -852,7 +876,9 @@ void build_batched_sa(Ctx* c, const std::vector<BatchSAItem>& items, int32_t vma
   const std::vector<uintptr_t>& lv = s.level_tags;
   DBuf<uintptr_t> dlv(c, lv.size());
   h2d(c, dlv.p, lv.data(), lv.size());
-  LiftArgs L{s.text.p, np, dlv.p, static_cast<int>(lv.size()), s.h0};
+  DBuf<uint32_t> dlh(c, s.level_h.size());
+  h2d(c, dlh.p, s.level_h.data(), s.level_h.size());
+  LiftArgs L{s.text.p, np, dlv.p, dlh.p, static_cast<int>(lv.size())};
   const uint64_t chunks = (np + kChunk - 1) / kChunk;
   launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p, s.cap);
   s.lcp.alloc(c, np);
