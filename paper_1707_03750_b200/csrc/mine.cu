@@ -465,7 +465,7 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
          wide.p, start.p + 1);
   launch(c, "mine_tied_wide", 0.0, k_tied_wide, dim3(static_cast<unsigned>(c->sm_count) * 4), dim3(256), 0, wide.p, start.p + 1,
          s.sa.p, start.p);
-  constexpr uint32_t kFirstRead = 4096;  // pattern tokens read back with the key; longer ones need a second trip
+  constexpr uint32_t kFirstRead = 16384;  // pattern tokens read back with the key; longer ones need a second trip
   const uint32_t max_out = static_cast<uint32_t>(std::min<int64_t>(max_len, 0xFFFFFFF));
   DBuf<uint32_t> res(c, 6 + static_cast<size_t>(max_out));
   launch(c, "mine_pattern_out", max_out * 8.0, k_pattern_out, dim3(1), dim3(256), 0, bb.p + grid, start.p, s.text.p, s.lo,

@@ -1,7 +1,8 @@
 """Turn a round's ncu launch list + full capture into the committed summaries under profiles/.
-Usage: python scripts/profile_summary.py <launches.csv> <prof.ncu-rep> <tag>"""
+Usage: python scripts/profile_summary.py <launches.csv> <prof.ncu-rep> <tag> [workload, default C3]"""
 import collections, csv, io, json, re, subprocess, sys
 launches, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+workload = sys.argv[4] if len(sys.argv) > 4 else "C3"
 rows = list(csv.reader(open(launches)))
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hi]
@@ -16,7 +17,7 @@ for r in rows[hi + 1:]:
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(v[1] for v in agg.values())
-out = [f"# {tag}: ncu launch list of `python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e` (C2; first 400 launches), gpu__time_duration.sum,",
+out = [f"# {tag}: ncu launch list of `python bench.py --config {workload} --steps 1 --warmup 3 --no-cpu-baseline --no-e2e` (first 400 launches), gpu__time_duration.sum,",
        "# --clock-control none; cold-cache and serialised per launch: compare SHARES, not absolutes",
        "kernel,launches,total_us,share"]
 for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -25,9 +26,14 @@ open(f"profiles/{tag}_launches_summary.csv", "w").write("\n".join(out) + "\n")
 print("\n".join(out[:16]))
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
-hdr = rr[0]
+hdr, units = rr[0], rr[1]
+SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,  # bytes -> MB
+         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}  # durations -> us
 def g(r, k):
-    return float(r[hdr.index(k)]) if k in hdr and r[hdr.index(k)] not in ("", "n/a") else None
+    if k not in hdr or r[hdr.index(k)] in ("", "n/a"):
+        return None
+    i = hdr.index(k)
+    return float(r[i].replace(",", "")) * SCALE.get(units[i], 1.0)
 keys = {"duration_us": "gpu__time_duration.sum", "dram_read_MB": "dram__bytes_read.sum", "dram_write_MB": "dram__bytes_write.sum",
         "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -38,7 +44,8 @@ keys = {"duration_us": "gpu__time_duration.sum", "dram_read_MB": "dram__bytes_re
         "ld_bytes_per_sector_pct": "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
         "st_bytes_per_sector_pct": "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct"}
 names = {"k_onesweep": "radix_onesweep", "k_rank_update": "sa_rank_update", "k_hash_insert": "intern_hash", "k_plcp": "lcp_plcp", "k_compact_local": "compact",
-         "k_ansv": "ansv_intervals", "k_scan": "compact"}
+         "k_ansv": "ansv_intervals", "k_scan": "compact", "k_refine_detect": "sa_refine_detect", "k_refine_apply": "sa_refine_apply",
+         "k_phi": "lcp_phi", "k_lcp_gather": "lcp_gather"}
 per = collections.defaultdict(list)
 for r in rr[2:]:
     full = r[hdr.index("Kernel Name")]
@@ -52,7 +59,7 @@ for r in rr[2:]:
                 key=lambda x: -(x[1] or 0))[:4]
     d["top_stalls"] = {a: b for a, b in st}
     per[nm].append(d)
-summ = {"source": f"{tag}: ncu --set full --clock-control none --import-source on, bench.py C2 (n'=10,000,017)", "workload": "C2",
+summ = {"source": f"{tag}: ncu --set full --clock-control none --import-source on, bench.py --config {workload}", "workload": workload,
         "kernels": {}}
 for nm, lst in per.items():
     avg = {k: sum(x[k] for x in lst) / len(lst) for k in keys if all(x[k] is not None for x in lst)}

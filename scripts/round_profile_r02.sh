@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-2 evidence in one GPU call (repo root, under gpurun): GPU tests, the default bench line (C3),
+# the reference arm, the C2/C4/C5 legs, the ncu launch list of a short C3 run, one --set full capture
+# of the top C3 kernels (each ncu pass only after its command exited 0).
+set -u
+O=gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/r02_tests.log 2>&1; tail -2 $O/r02_tests.log
+timeout 1200 python bench.py > $O/r02_bench_c3.json 2> $O/r02_bench_c3.err; tail -c 300 $O/r02_bench_c3.json
+timeout 900 python bench.py --impl reference > $O/r02_bench_ref.json 2> $O/r02_bench_ref.err
+timeout 900 python bench.py --config C2 --steps 30 > $O/r02_bench_c2.json 2> $O/r02_bench_c2.err
+timeout 900 python bench.py --config C4 --steps 3 > $O/r02_bench_c4.json 2> $O/r02_bench_c4.err
+SHORT="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-ingest --no-sa-full --no-sharded-legs"
+if timeout 600 $SHORT > $O/r02_short.log 2>&1; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/r02_launches.csv $SHORT > $O/r02_ncu_launch.log 2>&1
+  timeout 1800 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_onesweep|k_rank_update|k_hash_insert|k_plcp|k_phi|k_lcp_gather|k_compact_local|k_ansv|k_refine_detect|k_refine_apply" -c 24 \
+    -o $O/r02_full $SHORT > $O/r02_ncu_full.log 2>&1
+  echo "ncu rc=$?"
+fi
+timeout 1200 python bench.py --config C5 --steps 3 --warmup 3 > $O/r02_bench_c5.json 2> $O/r02_bench_c5.err
