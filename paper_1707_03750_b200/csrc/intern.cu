@@ -1044,7 +1044,10 @@ struct CompactF {
 // range, so the tile stages stream / device / kind / slot / start / dur in shared memory with
 // coalesced loads and resolves the permutation there, instead of one scattered global gather
 // per column per record.  Same outputs as CompactF (one packed look-back scan).
-constexpr int kCompactBlock = 256, kCompactItems = 4, kCompactTile = kCompactBlock * kCompactItems;
+#ifndef ITT_COMPACT_ITEMS
+#define ITT_COMPACT_ITEMS 4
+#endif
+constexpr int kCompactBlock = 256, kCompactItems = ITT_COMPACT_ITEMS, kCompactTile = kCompactBlock * kCompactItems;
 static_assert(kCompactTile % 256 == 0, "tiles must be whole order blocks");
 struct CompactLocalSmem {
   int64_t start[kCompactTile];

@@ -351,9 +351,14 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __
 
 // rank_{2h}[SA_j] = position of j's new group head, written where it differs from the old head
 // (all j when the previous level holds dense ids): a max-scan of (last new head, last old head)
-// over SA order with decoupled look-back.  32 positions per thread = one word of each bitmap; SA
-// is read only where a rank is written, so a settled round touches little more than the bitmaps.
-constexpr int kApplyItems = 32;
+// over SA order with decoupled look-back.  kApplyWords words of each bitmap (32 positions each) per
+// thread, so a tile covers 64K positions and the look-back chain is short; SA is read only where a
+// rank is written, so a settled round touches little more than the bitmaps.
+constexpr int kApplyItems = 32;   // positions per bitmap word
+#ifndef ITT_APPLY_WORDS
+#define ITT_APPLY_WORDS 8  // C3: 32 -> 106 -> 39 us per launch for 1, 4, 8 words (16: 41)
+#endif
+constexpr int kApplyWords = ITT_APPLY_WORDS;  // words per thread
 __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads_old,
                                                             const uint32_t* __restrict__ heads_new, uint64_t np,
                                                             uint32_t* __restrict__ level, int full, uint64_t* status,
@@ -364,17 +369,21 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __r
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint64_t w = static_cast<uint64_t>(tile) * kRankBlock + threadIdx.x;  // bitmap word
-  const uint64_t base = w * kApplyItems;
-  uint32_t ho = 0, hn = 0;
-  if (base < np) {
-    const uint32_t live = np - base >= kApplyItems ? 0xFFFFFFFFu : (1u << (np - base)) - 1u;  // bytes past np are unset
-    ho = __ldcs(&heads_old[w]) & live;
-    hn = __ldcs(&heads_new[w]) & live;
+  const uint64_t w0 = (static_cast<uint64_t>(tile) * kRankBlock + threadIdx.x) * kApplyWords;  // first bitmap word
+  uint32_t ho[kApplyWords], hn[kApplyWords];
+  uint64_t ln = 0, lo = 0;  // this thread's last heads (+1; 0 = none)
+#pragma unroll
+  for (int u = 0; u < kApplyWords; ++u) {
+    const uint64_t base = (w0 + u) * kApplyItems;
+    ho[u] = hn[u] = 0;
+    if (base < np) {
+      const uint32_t live = np - base >= kApplyItems ? 0xFFFFFFFFu : (1u << (np - base)) - 1u;  // bits past np are unset
+      ho[u] = __ldcs(&heads_old[w0 + u]) & live;
+      hn[u] = __ldcs(&heads_new[w0 + u]) & live;
+    }
+    if (hn[u]) ln = base + (31 - __clz(hn[u])) + 1;
+    if (ho[u]) lo = base + (31 - __clz(ho[u])) + 1;
   }
-  // this run's last heads (+1; 0 = none)
-  const uint64_t ln = hn ? base + (31 - __clz(hn)) + 1 : 0;
-  const uint64_t lo = ho ? base + (31 - __clz(ho)) + 1 : 0;
   const HeadPair op;
   uint64_t total;
   const uint64_t texcl = block_exclusive_scan<uint64_t, HeadPair, kRankBlock>((ln << 31) | lo, op, &total, s_warp);
@@ -383,30 +392,39 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __r
     if (threadIdx.x == 0) s_prefix = p;
   }
   __syncthreads();
-  if (base >= np) return;
   const uint64_t pre = op(s_prefix, texcl);
   uint64_t cn = pre >> 31, co = pre & ((1ull << 31) - 1);  // last heads before this run (+1)
-  const int cnt = static_cast<int>(umin64(kApplyItems, np - base));
-  if (!full && hn == ho && cn == co) return;  // no head moved in or before this run's groups
-  if (full && cnt == kApplyItems) {  // every rank changes representation: the run's SA in 16-byte loads
 #pragma unroll
-    for (int q4 = 0; q4 < kApplyItems; q4 += 4) {
-      const uint4 v = *reinterpret_cast<const uint4*>(sa + base + q4);
-      const uint32_t x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if ((hn >> (q4 + u)) & 1u) cn = base + q4 + u + 1;
-        level[x[u]] = static_cast<uint32_t>(cn - 1);
-      }
+  for (int u = 0; u < kApplyWords; ++u) {
+    const uint64_t base = (w0 + u) * kApplyItems;
+    if (base >= np) break;
+    const int cnt = static_cast<int>(umin64(kApplyItems, np - base));
+    if (!full && hn[u] == ho[u] && cn == co) {  // no head moved in or before this word's groups
+      if (hn[u]) cn = co = base + (31 - __clz(hn[u])) + 1;
+      continue;
     }
-    return;
-  }
-  for (int q = 0; q < cnt; ++q) {
-    if ((hn >> q) & 1u) cn = base + q + 1;
-    if ((ho >> q) & 1u) co = base + q + 1;
-    if (full || cn != co) level[sa[base + q]] = static_cast<uint32_t>(cn - 1);
+    if (full && cnt == kApplyItems) {  // every rank changes representation: the word's SA in 16-byte loads
+#pragma unroll
+      for (int q4 = 0; q4 < kApplyItems; q4 += 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(sa + base + q4);
+        const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if ((hn[u] >> (q4 + q)) & 1u) cn = base + q4 + q + 1;
+          if ((ho[u] >> (q4 + q)) & 1u) co = base + q4 + q + 1;
+          level[x[q]] = static_cast<uint32_t>(cn - 1);
+        }
+      }
+      continue;
+    }
+    for (int q = 0; q < cnt; ++q) {
+      if ((hn[u] >> q) & 1u) cn = base + q + 1;
+      if ((ho[u] >> q) & 1u) co = base + q + 1;
+      if (full || cn != co) level[sa[base + q]] = static_cast<uint32_t>(cn - 1);
+    }
   }
 }
+
 
 // ---------------------------------------------------------------- LCP
 __global__ void k_phi(const uint32_t* __restrict__ sa, uint64_t np, uint32_t* __restrict__ phi) {
@@ -716,7 +734,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
           if (!full) ITT_CUDA(cudaMemcpyAsync(lvl, reinterpret_cast<const uint32_t*>(rank), np * 4, cudaMemcpyDeviceToDevice,
                                               c->stream));
         }
-        const uint64_t atiles = (np + kRankBlock * kApplyItems - 1) / (kRankBlock * kApplyItems);
+        const uint64_t atiles = (np + kRankBlock * kApplyItems * kApplyWords - 1) / (kRankBlock * kApplyItems * kApplyWords);
         rscan.prepare(c, atiles);
         launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply, dim3(static_cast<unsigned>(atiles)),
                dim3(kRankBlock), 0, sa, reinterpret_cast<const uint32_t*>(heads[hc].p),

@@ -1,0 +1,9 @@
+# A/B of the compaction tile (ITT_COMPACT_ITEMS) at C3 and C2
+for v in ${VARIANTS:-""}; do
+  touch paper_1707_03750_b200/csrc/intern.cu
+  ITT_NVCC_EXTRA="${v//,/ }" python -c "from paper_1707_03750_b200 import build; build.build()" || exit 1
+  echo "== $v" >> gpurun_out/ab_compact.log
+  python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "golden or order or token" 2>&1 | tail -1 >> gpurun_out/ab_compact.log
+  python scripts/kernel_table.py C3 2>&1 | grep -E "kernel sum|compact" >> gpurun_out/ab_compact.log
+  python scripts/kernel_table.py C2 2>&1 | grep -E "kernel sum|compact" >> gpurun_out/ab_compact.log
+done
