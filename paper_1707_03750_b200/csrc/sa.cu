@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __
 // rank is written, so a settled round touches little more than the bitmaps.
 constexpr int kApplyItems = 32;   // positions per bitmap word
 #ifndef ITT_APPLY_WORDS
-#define ITT_APPLY_WORDS 8  // C3: 32 -> 106 -> 39 us per launch for 1, 4, 8 words (16: 41)
+#define ITT_APPLY_WORDS 8  // C3: 106 -> 53 -> 39 us per launch for 1, 4, 8 words (16: 41)
 #endif
 constexpr int kApplyWords = ITT_APPLY_WORDS;  // words per thread
 __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads_old,

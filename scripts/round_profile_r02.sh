@@ -12,9 +12,15 @@ timeout 900 python bench.py --config C4 --steps 3 > $O/r02_bench_c4.json 2> $O/r
 SHORT="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-ingest --no-sa-full --no-sharded-legs"
 if timeout 600 $SHORT > $O/r02_short.log 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/r02_launches.csv $SHORT > $O/r02_ncu_launch.log 2>&1
+  # the full capture stays on the box (tens of MB per kernel); its raw and details pages come back
   timeout 1800 ncu --set full --clock-control none --import-source on \
     -k regex:"k_onesweep|k_rank_update|k_hash_insert|k_plcp|k_phi|k_lcp_gather|k_compact_local|k_ansv|k_refine_detect|k_refine_apply" -c 24 \
-    -o $O/r02_full $SHORT > $O/r02_ncu_full.log 2>&1
+    -o /tmp/r02_full $SHORT > $O/r02_ncu_full.log 2>&1
   echo "ncu rc=$?"
+  ncu -i /tmp/r02_full.ncu-rep --page raw --csv > $O/r02_full_raw.csv 2>/dev/null
+  ncu -i /tmp/r02_full.ncu-rep --page details --csv > $O/r02_full_details.csv 2>/dev/null
+  python scripts/profile_summary.py $O/r02_launches.csv /tmp/r02_full.ncu-rep r02 C3 > $O/r02_profile_summary.log 2>&1
+  cp profiles/ncu_summary.json profiles/r02_launches_summary.csv $O/ 2>/dev/null
+  du -sh $O
 fi
 timeout 1200 python bench.py --config C5 --steps 3 --warmup 3 > $O/r02_bench_c5.json 2> $O/r02_bench_c5.err
