@@ -24,11 +24,13 @@ for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     out.append(f"{k},{c},{t:.1f},{t / tot:.4f}")
 open(f"profiles/{tag}_launches_summary.csv", "w").write("\n".join(out) + "\n")
 print("\n".join(out[:16]))
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+# the capture itself, or its raw page already exported as CSV (the report stays on the GPU box)
+raw = open(rep).read() if rep.endswith(".csv") else subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 hdr, units = rr[0], rr[1]
 SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,  # bytes -> MB
-         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}  # durations -> us
+         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,  # durations -> us
+         "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 def g(r, k):
     if k not in hdr or r[hdr.index(k)] in ("", "n/a"):
         return None
