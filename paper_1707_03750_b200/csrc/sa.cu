@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __
 // thread, so a tile covers 64K positions and the look-back chain is short; SA is read only where a
 // rank is written, so a settled round touches little more than the bitmaps.
 constexpr int kApplyItems = 32;   // positions per bitmap word
+// final groups at most np / kHeadsLcpRatio: LCP from the head bitmap + lifting (k_lcp_heads)
+// instead of phi + capped Kasai + gather
+constexpr uint64_t kHeadsLcpRatio = 64;
 #ifndef ITT_APPLY_WORDS
 #define ITT_APPLY_WORDS 8  // C3: 106 -> 53 -> 39 us per launch for 1, 4, 8 words (16: 41)
 #endif
@@ -500,6 +503,36 @@ __global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* _
     plcp[i] = l;
     capped = false;  // i-1 and phi(i-1) were in different groups: the carry below stays a valid bound
     if (l > 0) --l;
+  }
+}
+
+// LCP in SA order when the final groups are few (periodic traces: a few groups per rotation
+// class): a suffix in its predecessor's final group shares >= h_final >= cap symbols, so its capped
+// LCP is cap; a group head's comes from lifting over the kept levels (< h_final).  One thread per
+// word of the head bitmap; replaces phi + capped Kasai + gather (three passes with random access).
+__global__ void k_lcp_heads(LiftArgs L, const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads, uint32_t cap,
+                            uint32_t* __restrict__ lcp) {
+  const uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t base = w * 32;
+  if (base >= L.np) return;
+  const uint32_t hb = __ldg(&heads[w]);
+  const int cnt = static_cast<int>(umin64(32, L.np - base));
+  if (cnt == 32 && hb == 0 && base > 0) {
+    const uint4 c4 = make_uint4(cap, cap, cap, cap);
+#pragma unroll
+    for (int q = 0; q < 32; q += 4) __stcs(reinterpret_cast<uint4*>(lcp + base + q), c4);
+    return;
+  }
+  for (int q = 0; q < cnt; ++q) {
+    const uint64_t j = base + q;
+    uint32_t v = cap;
+    if (j == 0) {
+      v = 0;
+    } else if ((hb >> q) & 1u) {
+      const uint32_t l = lcp_lift(L, __ldg(&sa[j - 1]), __ldg(&sa[j]), cap);
+      v = l < cap ? l : cap;
+    }
+    lcp[j] = v;
   }
 }
 
@@ -827,14 +860,23 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   if (!want_lcp) return;
 
   // ---- LCP
-  DBuf<uint32_t> phi(c, np), plcp(c, np);
-  launch(c, "lcp_phi", np * 12.0, k_phi, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, np, phi.p);
   const std::vector<uintptr_t>& lv = s.level_tags;
   DBuf<uintptr_t> dlv(c, lv.size());
   h2d(c, dlv.p, lv.data(), lv.size());
   DBuf<uint32_t> dlh(c, s.level_h.size());
   h2d(c, dlh.p, s.level_h.data(), s.level_h.size());
   LiftArgs L{s.text.p, np, dlv.p, dlh.p, static_cast<int>(lv.size())};
+  const char* hl_env = std::getenv("ITT_LCP_HEADS");  // 0: always phi + capped Kasai (A/B, tests)
+  const int heads_lcp = hl_env && *hl_env ? std::atoi(hl_env) : 1;
+  if (heads_lcp && g < np && g * kHeadsLcpRatio < np) {  // few final groups: LCP from the head bitmap
+    s.lcp.alloc(c, np);
+    const uint64_t words = (np + 31) / 32;
+    launch(c, "lcp_heads", np * 4.0 + words * 4.0 + g * 8.0, k_lcp_heads, dim3(grid_for(words, 256)), dim3(256), 0, L, s.sa.p,
+           reinterpret_cast<const uint32_t*>(heads[hc].p), s.cap, s.lcp.p);
+    return;
+  }
+  DBuf<uint32_t> phi(c, np), plcp(c, np);
+  launch(c, "lcp_phi", np * 12.0, k_phi, dim3(grid_for(np, 256)), dim3(256), 0, s.sa.p, np, phi.p);
   const uint64_t chunks = (np + kChunk - 1) / kChunk;
   launch(c, "lcp_plcp", np * 16.0, k_plcp, dim3(grid_for(chunks, 128)), dim3(128), 0, L, phi.p, plcp.p, s.cap);
   s.lcp.alloc(c, np);

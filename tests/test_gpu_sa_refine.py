@@ -86,3 +86,26 @@ def test_capped_mining_vs_reference(ctx, R, name, s, term):
     reference for iteration counts that make the cap small (refinement then ends the doubling)."""
     for it in (max(2, s.size // 400), max(2, s.size // 60)):
         assert _mine(ctx, s, term, [(it, 1)]) == _mine(R, s, term, [(it, 1)]), (name, it)
+
+
+@pytest.mark.parametrize("name,s,term", SMALL, ids=[c[0] for c in SMALL])
+def test_capped_lcp_from_group_heads(ctx, R, name, s, term, monkeypatch):
+    """Capped SA + LCP (what mining consumes): when the final groups are few, the LCP comes from the
+    head bitmap + lifting (k_lcp_heads) instead of phi + capped Kasai.  Either way LCP must equal
+    min(reference LCP, cap) and the suffixes must be grouped as in the reference (order inside a
+    final group is by position)."""
+    import torch
+    rsa, rlcp = R.suffix_array(s, term)
+    n = s.size
+    for cap in (9, 65, 1025):
+        got = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("ITT_LCP_HEADS", mode)
+            tok = torch.from_numpy(s).cuda()
+            sa = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+            lcp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+            ctx.suffix_array_device(tok.data_ptr(), n, term, sa.data_ptr(), lcp.data_ptr(), cap=cap)
+            got[mode] = lcp.cpu().numpy().view(np.uint32)
+        want = np.minimum(rlcp.astype(np.uint64), cap).astype(np.uint32)
+        assert np.array_equal(got["0"], want), (name, cap)
+        assert np.array_equal(got["1"], want), (name, cap)
