@@ -552,6 +552,13 @@ def bench_single(args, world, rank, local, workload, iters):
     roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "share_of_step": st["total_ms"] / tot, "launches_per_step": st["launches"] / args.profile_steps}
+    if traffic:
+        # DRAM bytes the kernel really moves (ncu, same workload) over its live launch time: for the
+        # random-access kernels (one 32-B sector per 4-B gather) this, not the algorithmic figure, is
+        # how close the kernel runs to the memory system's limit
+        roofline["traffic_GBps"] = traffic / (avg_ms / 1000.0) / 1e9
+        roofline["traffic_frac"] = roofline["traffic_GBps"] / peak
+        roofline["traffic_per_algorithmic_byte"] = traffic / per_launch_bytes
     # the random-access kernels are judged on sector efficiency too: the committed
     # ncu metrics pass of the same workload (scripts/sector_profile.sh)
     sect = os.path.join(ROOT, "profiles", "r01h_sector_efficiency.csv")
