@@ -534,7 +534,7 @@ int itt_mine_patterns(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_t t
     ScanScratch sc;
     build_suffix_array(c, dt.p, n, term, s, true, rs, sc, mining_cap(n, cfgs));
     IntervalState iv;
-    lcp_intervals(c, s, iv);
+    lcp_intervals(c, s, iv, mining_cap(n, cfgs) - 1);  // list mode: the candidate intervals only
     const auto res = mine_loops(c, s, iv, cfgs, multi != 0);
     for (const auto& r : res)
       if (r.status) fail(r.status, r.error);
@@ -584,7 +584,7 @@ int itt_mine_patterns_sa(itt_ctx* ctx, const int32_t* tokens, uint64_t n, int32_
     ITT_CUDA(cudaMemcpyAsync(s.sa.p, sa, (n + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
     ITT_CUDA(cudaMemcpyAsync(s.lcp.p, lcp, (n + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
     IntervalState iv;
-    lcp_intervals(c, s, iv);
+    lcp_intervals(c, s, iv, mining_cap(n, cfgs) - 1);  // list mode: the candidate intervals only
     const auto res = mine_loops(c, s, iv, cfgs, multi != 0);
     for (const auto& r : res)
       if (r.status) fail(r.status, r.error);
@@ -891,7 +891,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
     std::vector<MinedPattern> pats;
     {
       StageTimer st(c, "mine");
-      lcp_intervals(c, s, iv);
+      lcp_intervals(c, s, iv, mining_cap(t.n_tok, cfgs) - 1);  // list mode: the candidate intervals only
       pats = mine_loops(c, s, iv, cfgs, multi);
     }
     for (const auto& p : pats)

@@ -116,6 +116,28 @@ struct AnsvArgs {
   uint32_t* cnt;
   uint32_t* par;
   uint32_t* lb;
+  // list mode (mining): only intervals that can be a mining candidate — count >= 2 and
+  // min(LCP, max_len) > parent depth — are appended as (LCP, count, parent, lb); no dense arrays
+  uint4* list;
+  unsigned int* n_list;
+  uint32_t max_len;
+  __device__ __forceinline__ void emit(uint64_t k, uint32_t l, uint32_t c, uint32_t p, uint32_t b) const {
+    if (!list) {
+      cnt[k] = c;
+      par[k] = p;
+      lb[k] = b;
+      return;
+    }
+    const bool want = c >= 2 && min(l, max_len) > p;
+    const unsigned act = __activemask();
+    const unsigned w = __ballot_sync(act, want);  // one atomic per warp
+    if (!w) return;
+    const int leader = __ffs(w) - 1;
+    unsigned base = 0;
+    if (static_cast<int>(lane_id()) == leader) base = atomicAdd(n_list, static_cast<unsigned>(__popc(w)));
+    base = __shfl_sync(act, base, leader);
+    if (want) list[base + __popc(w & lanemask_lt())] = make_uint4(l, c, p, b);
+  }
 };
 
 // last j in tile t with LCP[j] <= thr (the tile's min is known to be <= thr)
@@ -172,11 +194,7 @@ __global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
       }
     }
     any_search |= search;
-    if (!search) {
-      a.cnt[k] = cnt;
-      a.par[k] = par;
-      a.lb[k] = lbv;
-    }
+    if (!search) a.emit(k, l, cnt, par, lbv);
   }
   if (!__syncthreads_or(any_search)) return;
   for (int l = 1; l < kLogTileA; ++l) {
@@ -250,9 +268,7 @@ __global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
         lbv = static_cast<uint32_t>(pse);
       }
     }
-    a.cnt[k] = cnt;
-    a.par[k] = par;
-    a.lb[k] = lbv;
+    a.emit(k, l, cnt, par, lbv);
   }
 }
 
@@ -309,6 +325,42 @@ __global__ void __launch_bounds__(256) k_mine_reduce(MineArgs a, Best* block_bes
   }
 }
 
+// the same over an interval list (lcp_intervals in list mode): entries (LCP, count, parent, lb)
+__device__ __forceinline__ bool candidate_entry(const MineArgs& a, const uint4& e, Best& out) {
+  const int64_t len = imin64(static_cast<int64_t>(e.x), a.max_len);
+  if (len <= static_cast<int64_t>(e.z)) return false;
+  const uint32_t c = e.y;
+  if (static_cast<int64_t>(c) > a.iters) return false;
+  int p = 0;
+  while (p < a.npass && static_cast<int64_t>(c) < a.min_count[p]) ++p;
+  if (p == a.npass) return false;
+  out.hi = (static_cast<unsigned long long>(63 - p) << 32) | static_cast<unsigned long long>(len);
+  out.lo = c;
+  return true;
+}
+__global__ void __launch_bounds__(256) k_mine_reduce_list(MineArgs a, const uint4* __restrict__ list,
+                                                          const unsigned int* __restrict__ n_list, Best* block_best) {
+  Best b{0, 0};
+  const uint64_t nl = *n_list;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nl; i += stride) {
+    Best x;
+    if (candidate_entry(a, list[i], x) && better(x, b)) b = x;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    Best y{__shfl_xor_sync(0xffffffffu, b.hi, o), __shfl_xor_sync(0xffffffffu, b.lo, o)};
+    if (better(y, b)) b = y;
+  }
+  __shared__ Best sw[8];
+  if (lane_id() == 0) sw[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (better(sw[w], b)) b = sw[w];
+    block_best[blockIdx.x] = b;
+  }
+}
+
 __global__ void k_best_final(const Best* bb, uint32_t nb, Best* out) {
   Best b{0, 0};
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
@@ -334,6 +386,30 @@ __global__ void __launch_bounds__(256) k_tied_min_sa(MineArgs a, const uint32_t*
     Best x;
     if (!candidate_key(a, k, x) || x.hi != w.hi || x.lo != w.lo) continue;
     const uint32_t l0 = lb[k], c = a.cnt[k];
+    if (c > kTiedSerial) {
+      const unsigned q = atomicAdd(n_wide, 1u);
+      wide[2 * q] = l0;
+      wide[2 * q + 1] = c;
+      continue;
+    }
+    uint32_t m = 0xFFFFFFFFu;
+    for (uint32_t q = 0; q < c; ++q) m = min(m, sa[l0 + q]);
+    atomicMin(result, m);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_tied_min_sa_list(MineArgs a, const uint4* __restrict__ list,
+                                                          const unsigned int* __restrict__ n_list, const uint32_t* __restrict__ sa,
+                                                          const Best* best, unsigned int* __restrict__ result,
+                                                          uint32_t* __restrict__ wide, unsigned int* __restrict__ n_wide) {
+  const Best w = *best;
+  const uint64_t nl = *n_list;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nl; i += stride) {
+    const uint4 e = list[i];
+    Best x;
+    if (!candidate_entry(a, e, x) || x.hi != w.hi || x.lo != w.lo) continue;
+    const uint32_t l0 = e.w, c = e.y;
     if (c > kTiedSerial) {
       const unsigned q = atomicAdd(n_wide, 1u);
       wide[2 * q] = l0;
@@ -387,7 +463,7 @@ __global__ void k_pattern_out(const Best* __restrict__ best, const unsigned int*
 
 }  // namespace
 
-void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv) {
+void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv, uint32_t list_max_len) {
   const uint64_t np = s.np;
   const uint32_t nt = static_cast<uint32_t>((np + kTileA - 1) / kTileA);
   DBuf<uint32_t> premin(c, np), sufmin(c, np);
@@ -402,10 +478,21 @@ void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv) {
     for (int l = 1; l < tlevels; ++l)
       launch(c, "ansv_sparse", nt * 12.0, k_sparse_level, dim3(grid_for(nt, 256)), dim3(256), 0, tst.p, nt, l);
   }
+  AnsvArgs a{s.lcp.p, premin.p, sufmin.p, tst.p, nt, tlevels, np, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  if (list_max_len) {  // mining: the candidate intervals only (no host sync: the kernels read the count)
+    iv.list.alloc(c, np);
+    iv.n_list.alloc(c, 1);
+    iv.n_list.zero();
+    a.list = iv.list.p;
+    a.n_list = iv.n_list.p;
+    a.max_len = list_max_len;
+    launch(c, "ansv_intervals", np * 4.0, k_ansv, dim3(nt), dim3(kAnsvBlock), 0, a);
+    return;
+  }
   iv.cnt.alloc(c, np);
   iv.par.alloc(c, np);
   iv.lb.alloc(c, np);
-  AnsvArgs a{s.lcp.p, premin.p, sufmin.p, tst.p, nt, tlevels, np, iv.cnt.p, iv.par.p, iv.lb.p};
+  a.cnt = iv.cnt.p, a.par = iv.par.p, a.lb = iv.lb.p;
   launch(c, "ansv_intervals", np * 16.0, k_ansv, dim3(nt), dim3(kAnsvBlock), 0, a);
 }
 
@@ -452,7 +539,10 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
   }
   const unsigned grid = std::min<unsigned>(grid_for(s.np, 256), c->sm_count * 4);
   DBuf<Best> bb(c, grid + 1);
-  launch(c, "mine_reduce", s.np * 12.0, k_mine_reduce, dim3(grid), dim3(256), 0, a, bb.p);
+  if (iv.list.p)
+    launch(c, "mine_reduce", 0.0, k_mine_reduce_list, dim3(grid), dim3(256), 0, a, iv.list.p, iv.n_list.p, bb.p);
+  else
+    launch(c, "mine_reduce", s.np * 12.0, k_mine_reduce, dim3(grid), dim3(256), 0, a, bb.p);
   launch(c, "mine_final", grid * 16.0, k_best_final, dim3(1), dim3(32), 0, bb.p, grid, bb.p + grid);
   // the tie-break kernels run whether or not a candidate exists (no candidate key equals the
   // empty key), so the whole result comes back in one round trip
@@ -461,8 +551,12 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
   ITT_CUDA(cudaMemsetAsync(start.p + 1, 0, 4, c->stream));
   const size_t wide_cap = s.np / (kTiedSerial + 1) + 2;  // disjoint intervals wider than kTiedSerial
   DBuf<uint32_t> wide(c, 2 * wide_cap);
-  launch(c, "mine_tied_min_sa", s.np * 12.0, k_tied_min_sa, dim3(grid), dim3(256), 0, a, iv.lb.p, s.sa.p, bb.p + grid, start.p,
-         wide.p, start.p + 1);
+  if (iv.list.p)
+    launch(c, "mine_tied_min_sa", 0.0, k_tied_min_sa_list, dim3(grid), dim3(256), 0, a, iv.list.p, iv.n_list.p, s.sa.p,
+           bb.p + grid, start.p, wide.p, start.p + 1);
+  else
+    launch(c, "mine_tied_min_sa", s.np * 12.0, k_tied_min_sa, dim3(grid), dim3(256), 0, a, iv.lb.p, s.sa.p, bb.p + grid,
+           start.p, wide.p, start.p + 1);
   launch(c, "mine_tied_wide", 0.0, k_tied_wide, dim3(static_cast<unsigned>(c->sm_count) * 4), dim3(256), 0, wide.p, start.p + 1,
          s.sa.p, start.p);
   constexpr uint32_t kFirstRead = 16384;  // pattern tokens read back with the key; longer ones need a second trip

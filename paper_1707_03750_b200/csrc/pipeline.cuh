@@ -132,8 +132,12 @@ struct IntervalState {
   DBuf<uint32_t> cnt;  // count of the interval represented at k (0 = not a representative)
   DBuf<uint32_t> par;  // parent depth
   DBuf<uint32_t> lb;   // left boundary
+  DBuf<uint4> list;    // list mode: (LCP, count, parent depth, left boundary) of the candidate intervals
+  DBuf<unsigned int> n_list;
 };
-void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv);
+// list_max_len > 0: list mode for mining with repeats cut at list_max_len (the largest L_max of the
+// loops); 0: the dense per-position arrays (enumerate_repeats)
+void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv, uint32_t list_max_len = 0);
 
 struct MinedPattern {
   int status = 0;
