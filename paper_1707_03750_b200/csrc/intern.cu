@@ -153,77 +153,81 @@ __global__ void __launch_bounds__(kOrderBlock) k_order_block_sort(const int64_t*
                                                                   uint32_t* __restrict__ perm, int64_t* __restrict__ bmin,
                                                                   int64_t* __restrict__ bmax, uint8_t* __restrict__ bdesc,
                                                                   const unsigned int* __restrict__ any) {
-  if (*any == 0) return;  // already in (start, row) order
+  if (*any == 0) return;  // already in (start, row) order: one small grid exits at once
   __shared__ long long s[kOrderBlock];
   __shared__ uint32_t r[kOrderBlock];
   __shared__ long long wmn[kOrderBlock / 32], wmx[kOrderBlock / 32];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kOrderBlock;
-  const uint32_t len = static_cast<uint32_t>(umin64(kOrderBlock, n - base));
+  const uint64_t nb = (n + kOrderBlock - 1) / kOrderBlock;
   const uint32_t t = threadIdx.x;
-  long long a = t < len ? __ldcs(&start[base + t]) : LLONG_MAX;  // padding rows sort last
-  uint32_t ra = t;
-  s[t] = a;
-  long long mn = a, mx = t < len ? a : LLONG_MIN;
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  }
-  if (lane_id() == 0) wmn[t >> 5] = mn, wmx[t >> 5] = mx;
-  __syncthreads();
-  // descent in the source order: against the previous row of the block / of the previous block
-  const long long prev = t > 0 ? s[t - 1] : (base > 0 ? start[base - 1] : LLONG_MIN);
-  const int any_desc = __syncthreads_or(t < len && prev > a);
-  long long bmn = wmn[0], bmx = wmx[0];
-  for (int w = 1; w < kOrderBlock / 32; ++w) bmn = min(bmn, wmn[w]), bmx = max(bmx, wmx[w]);
-  if (t == 0) {
-    bmin[blockIdx.x] = bmn;
-    bmax[blockIdx.x] = bmx;
-    bdesc[blockIdx.x] = any_desc ? 1 : 0;
-  }
-  if (static_cast<unsigned long long>(bmx) - static_cast<unsigned long long>(bmn) < (1ull << 24)) {
-    // narrow block (the usual case: 256 consecutive records span far less than 16.7 ms): sort one
-    // 32-bit key (start - min) << 8 | row — one shuffle per stage instead of three, and the row
-    // in the low bits breaks ties exactly like (start, row); padding rows sort last
-    uint32_t key = t < len ? (static_cast<uint32_t>(a - bmn) << 8) | t : 0xFFFFFFFFu;
+  for (uint64_t blk = blockIdx.x; blk < nb; blk += gridDim.x) {  // grid-stride over the 256-row blocks
+    __syncthreads();  // the previous block's shared arrays are consumed
+    const uint64_t base = blk * kOrderBlock;
+    const uint32_t len = static_cast<uint32_t>(umin64(kOrderBlock, n - base));
+    long long a = t < len ? __ldcs(&start[base + t]) : LLONG_MAX;  // padding rows sort last
+    uint32_t ra = t;
+    s[t] = a;
+    long long mn = a, mx = t < len ? a : LLONG_MIN;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane_id() == 0) wmn[t >> 5] = mn, wmx[t >> 5] = mx;
+    __syncthreads();
+    // descent in the source order: against the previous row of the block / of the previous block
+    const long long prev = t > 0 ? s[t - 1] : (base > 0 ? start[base - 1] : LLONG_MIN);
+    const int any_desc = __syncthreads_or(t < len && prev > a);
+    long long bmn = wmn[0], bmx = wmx[0];
+    for (int w = 1; w < kOrderBlock / 32; ++w) bmn = min(bmn, wmn[w]), bmx = max(bmx, wmx[w]);
+    if (t == 0) {
+      bmin[blk] = bmn;
+      bmax[blk] = bmx;
+      bdesc[blk] = any_desc ? 1 : 0;
+    }
+    if (static_cast<unsigned long long>(bmx) - static_cast<unsigned long long>(bmn) < (1ull << 24)) {
+      // narrow block (the usual case: 256 consecutive records span far less than 16.7 ms): sort one
+      // 32-bit key (start - min) << 8 | row — one shuffle per stage instead of three, and the row
+      // in the low bits breaks ties exactly like (start, row); padding rows sort last
+      uint32_t key = t < len ? (static_cast<uint32_t>(a - bmn) << 8) | t : 0xFFFFFFFFu;
+      for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          uint32_t b;
+          if (j >= 32) {
+            __syncthreads();
+            r[t] = key;
+            __syncthreads();
+            b = r[t ^ j];
+          } else {
+            b = __shfl_xor_sync(0xffffffffu, key, j);
+          }
+          const bool lower = (t & j) == 0, ascending = (t & k) == 0;
+          if ((lower == ascending) == (key > b)) key = b;
+        }
+      }
+      if (t < len) perm[base + t] = static_cast<uint32_t>(base + (key & 0xFFu));
+      continue;
+    }
     for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        uint32_t b;
+        long long b;
+        uint32_t rb;
         if (j >= 32) {
           __syncthreads();
-          r[t] = key;
+          s[t] = a;
+          r[t] = ra;
           __syncthreads();
-          b = r[t ^ j];
+          b = s[t ^ j];
+          rb = r[t ^ j];
         } else {
-          b = __shfl_xor_sync(0xffffffffu, key, j);
+          b = __shfl_xor_sync(0xffffffffu, a, j);
+          rb = __shfl_xor_sync(0xffffffffu, ra, j);
         }
+        const bool a_gt_b = a > b || (a == b && ra > rb);
         const bool lower = (t & j) == 0, ascending = (t & k) == 0;
-        if ((lower == ascending) == (key > b)) key = b;
+        if ((lower == ascending) == a_gt_b) a = b, ra = rb;  // lower keeps the min when ascending
       }
     }
-    if (t < len) perm[base + t] = static_cast<uint32_t>(base + (key & 0xFFu));
-    return;
+    if (t < len) perm[base + t] = static_cast<uint32_t>(base + ra);
   }
-  for (uint32_t k = 2; k <= kOrderBlock; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      long long b;
-      uint32_t rb;
-      if (j >= 32) {
-        __syncthreads();
-        s[t] = a;
-        r[t] = ra;
-        __syncthreads();
-        b = s[t ^ j];
-        rb = r[t ^ j];
-      } else {
-        b = __shfl_xor_sync(0xffffffffu, a, j);
-        rb = __shfl_xor_sync(0xffffffffu, ra, j);
-      }
-      const bool a_gt_b = a > b || (a == b && ra > rb);
-      const bool lower = (t & j) == 0, ascending = (t & k) == 0;
-      if ((lower == ascending) == a_gt_b) a = b, ra = rb;  // lower keeps the min when ascending
-    }
-  }
-  if (t < len) perm[base + t] = static_cast<uint32_t>(base + ra);
 }
 
 // Fold the per-block results: stats = [min start, max start, any descent, overlapping block
@@ -1339,8 +1343,9 @@ void order_launch(TraceState& t) {
   any.zero();
   launch(c, "order_descent", n * 8.0, k_order_descent, dim3(grid_for((n + 7) / 8, 256, c->sm_count * 8)), dim3(256), 0,
          t.rec.start, n, any.p);
-  launch(c, "order_blocks", n * 12.0, k_order_block_sort, dim3(static_cast<unsigned>(nb)), dim3(kOrderBlock), 0, t.rec.start, n,
-         t.perm.p, bmin.p, bmax.p, bdesc.p, any.p);
+  launch(c, "order_blocks", n * 12.0, k_order_block_sort,
+         dim3(static_cast<unsigned>(std::min<uint64_t>(nb, static_cast<uint64_t>(c->sm_count) * 32))), dim3(kOrderBlock), 0,
+         t.rec.start, n, t.perm.p, bmin.p, bmax.p, bdesc.p, any.p);
   launch(c, "order_check", nb * 17.0, k_order_check, dim3(grid_for(nb, 256)), dim3(256), 0, bmin.p, bmax.p, bdesc.p, nb,
          t.order_stats.p, any.p);
   ITT_CUDA(cudaMemcpyAsync(c->deferred_block(), t.order_stats.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
