@@ -25,9 +25,31 @@ for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
 open(f"profiles/{tag}_launches_summary.csv", "w").write("\n".join(out) + "\n")
 print("\n".join(out[:16]))
 # the capture itself, or its raw page already exported as CSV (the report stays on the GPU box)
-raw = open(rep).read() if rep.endswith(".csv") else subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(io.StringIO(raw)))
-hdr, units = rr[0], rr[1]
+# several captures may be given comma-separated (raw pages are merged by column name)
+def _rows(one):
+    raw = open(one).read() if one.endswith(".csv") else subprocess.run(["ncu", "-i", one, "--page", "raw", "--csv"],
+                                                                       capture_output=True, text=True).stdout
+    return list(csv.reader(io.StringIO(raw)))
+parts = [_rows(x) for x in rep.split(",")]
+hdr, units = parts[0][0], parts[0][1]
+rr = [hdr, units] + parts[0][2:]
+_S = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6, "nsecond": 1e-3, "usecond": 1.0,
+      "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
+for extra in parts[1:]:
+    eh, eu = extra[0], extra[1]
+    for r in extra[2:]:
+        d = dict(zip(eh, r))
+        du = dict(zip(eh, eu))
+        row = []
+        for k, u0 in zip(hdr, units):
+            v = d.get(k, "")
+            if v and du.get(k) in _S and u0 in _S and du[k] != u0:  # into the first capture's unit
+                try:
+                    v = repr(float(v.replace(",", "")) * _S[du[k]] / _S[u0])
+                except ValueError:
+                    pass
+            row.append(v)
+        rr.append(row)
 SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,  # bytes -> MB
          "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,  # durations -> us
          "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
