@@ -78,6 +78,34 @@ __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32
 
 // codes (tokens - lo, terminator appended at n) and the first k symbols of every suffix packed
 // into 32 bits, in one pass over the tokens
+// The same keys, plus the 8-bit digit histograms of every pass of the init sort (shared-memory
+// counts flushed once per block): the sort then needs no histogram pass over the keys.
+__global__ void __launch_bounds__(256) k_text_keys_hist(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int32_t lo,
+                                                        int bits, int k, int passes, int32_t* __restrict__ text,
+                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                        uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[4 * 256];
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint64_t np = n + 1;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < np; i += stride) {
+    uint32_t key = 0;
+    for (int q = 0; q < k; ++q) {
+      const uint64_t j = i + q;
+      const uint32_t c = j < n ? static_cast<uint32_t>(__ldg(&tok[j]) - lo) : (j == n ? static_cast<uint32_t>(term - lo) : 0u);
+      if (q == 0) text[i] = static_cast<int32_t>(c);
+      key = (key << bits) | c;
+    }
+    __stcs(&keys[i], key);
+    __stcs(&vals[i], static_cast<uint32_t>(i));
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
 __global__ void k_text_keys(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int32_t lo, int bits, int k,
                             int32_t* __restrict__ text, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -633,14 +661,25 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   uint32_t* kb = bufs[2].p;
   uint32_t* vb = bufs[3].p;
   uint32_t* spare = bufs[4].p;
-  launch(c, "sa_init_keys", np * 16.0, k_text_keys, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, cbits, k,
-         s.text.p, ka, va);
   const int init_bits = std::min(32, cbits * k);
   // 8-bit digits: the k-gram codes are spread over the whole key, and a 10-bit pass over them (1024
   // bins) measured 1.12 ms per 100M pairs against 0.82 ms for an 8-bit one — 3 wide passes save nothing
-  const bool a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
-                                             static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr),
-                                             /*skip_trivial=*/!known_alphabet);
+  bool a0;
+  if (known_alphabet) {  // keys and the sort's digit histograms in one pass (no host check of trivial passes)
+    const int passes = (init_bits + 7) / 8;
+    DBuf<uint32_t> ihist(c, static_cast<size_t>(passes) * 256);
+    ihist.zero();
+    launch(c, "sa_init_keys", np * 16.0, k_text_keys_hist, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens, n,
+           term, lo, cbits, k, passes, s.text.p, ka, va, ihist.p);
+    a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p,
+                                    static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), /*skip_trivial=*/false);
+  } else {
+    launch(c, "sa_init_keys", np * 16.0, k_text_keys, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, cbits, k,
+           s.text.p, ka, va);
+    a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, nullptr,
+                                    static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr),
+                                    /*skip_trivial=*/!known_alphabet);
+  }
   uint32_t* keys = a0 ? kb : ka;
   uint32_t* sa = a0 ? vb : va;
   uint32_t* f1 = a0 ? ka : kb;  // free buffers
