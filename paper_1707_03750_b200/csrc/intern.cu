@@ -1043,6 +1043,144 @@ struct CompactF {
   }
 };
 
+// Compaction of rows already in (start, row) order by reduce-then-scan: (1) per-tile counts, (2) one
+// block scans the tile counts, (3) every tile writes at its known offset.  No tile waits on a
+// look-back chain (the single-pass kernel's CTAs sat at the barrier behind warp 0's look-back);
+// the price is a second read of the 5-7 bytes per row that decide main-stream / HtoD.
+constexpr int kRSItems = 8, kRSTile = 256 * kRSItems;
+struct RowSel {  // the selection ballots of one warp's rows (warp-striped: row = wbase + q*32 + lane)
+  unsigned mm[kRSItems], hm[kRSItems];
+  uint8_t kd[kRSItems];
+  __device__ __forceinline__ void load(const CompactF& f, uint64_t wbase) {
+#pragma unroll
+    for (int q = 0; q < kRSItems; ++q) {
+      const uint64_t k = wbase + q * 32 + lane_id();
+      bool m = false, h = false;
+      kd[q] = 0;
+      if (k < f.n) {
+        const uint32_t sm = __ldcs(&f.stream[k]);
+        kd[q] = __ldcs(&f.kind[k]);
+        const bool keep = !(f.filter && __ldcs(&f.device[k]) != f.majority);
+        m = keep && sm == f.main_stream;
+        h = keep && kd[q] == ITT_KIND_HTOD;
+      }
+      mm[q] = __ballot_sync(0xffffffffu, m);
+      hm[q] = __ballot_sync(0xffffffffu, h);
+    }
+  }
+  __device__ __forceinline__ uint64_t packed() const {
+    uint64_t m = 0, h = 0;
+#pragma unroll
+    for (int q = 0; q < kRSItems; ++q) m += __popc(mm[q]), h += __popc(hm[q]);
+    return m | (h << 31);
+  }
+};
+__global__ void __launch_bounds__(256) k_compact_count(CompactF f, uint64_t* __restrict__ tile_counts) {
+  __shared__ uint64_t s_w[8];
+  const unsigned warp = threadIdx.x >> 5;
+  RowSel sel;
+  sel.load(f, static_cast<uint64_t>(blockIdx.x) * kRSTile + warp * (32 * kRSItems));
+  if (lane_id() == 0) s_w[warp] = sel.packed();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < 8; ++w) t += s_w[w];
+    tile_counts[blockIdx.x] = t;
+  }
+}
+// exclusive scan of the tile counts in place, one block walking chunks of 8K counts (8 consecutive
+// per thread, coalesced) with a running carry (C3: 49K tiles, C5: 489K)
+__global__ void __launch_bounds__(1024) k_scan_tile_counts(uint64_t* __restrict__ tc, uint64_t tiles) {
+  __shared__ uint64_t s_warp[32];
+  constexpr int kPer = 8;
+  uint64_t carry = 0;
+  for (uint64_t c0 = 0; c0 < tiles; c0 += 1024 * kPer) {
+    const uint64_t b0 = c0 + static_cast<uint64_t>(threadIdx.x) * kPer;
+    uint64_t v[kPer], run = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      v[q] = b0 + q < tiles ? tc[b0 + q] : 0ull;
+      run += v[q];
+    }
+    uint64_t total;
+    uint64_t acc = carry + block_exclusive_scan<uint64_t, SumOp<uint64_t>, 1024>(run, SumOp<uint64_t>(), &total, s_warp);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      if (b0 + q < tiles) tc[b0 + q] = acc;
+      acc += v[q];
+    }
+    carry += total;
+    __syncthreads();  // s_warp is reused by the next chunk
+  }
+}
+__global__ void __launch_bounds__(256) k_compact_write(CompactF f, const uint64_t* __restrict__ tile_excl) {
+  __shared__ uint64_t s_w[8];
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kRSTile + warp * (32 * kRSItems);
+  RowSel sel;
+  sel.load(f, wbase);
+  // the columns the outputs need (main-stream / HtoD rows only), in flight during the block scan
+  int64_t st[kRSItems], du[kRSItems];
+  uint32_t sl[kRSItems];
+#pragma unroll
+  for (int q = 0; q < kRSItems; ++q) {
+    const uint64_t k = wbase + q * 32 + lane;
+    st[q] = du[q] = 0, sl[q] = 0;
+    if ((sel.mm[q] | sel.hm[q]) >> lane & 1u) {
+      st[q] = __ldcs(&f.start[k]);
+      du[q] = __ldcs(&f.dur[k]);
+    }
+    if (sel.mm[q] >> lane & 1u) sl[q] = __ldcs(&f.slot[k]);
+  }
+  if (lane == 0) s_w[warp] = sel.packed();
+  __syncthreads();
+  uint64_t excl = tile_excl[blockIdx.x];
+  for (unsigned w = 0; w < warp; ++w) excl += s_w[w];
+  uint32_t jm = static_cast<uint32_t>(excl & 0x7FFFFFFFull);
+  uint64_t jh = excl >> 31;
+  const unsigned lt = lanemask_lt();
+  uint32_t tf[kRSItems];
+#pragma unroll
+  for (int q = 0; q < kRSItems; ++q) tf[q] = (sel.mm[q] >> lane & 1u) ? __ldcg(&f.tfirst[sl[q]]) : 0u;
+  unsigned long long emin = ~0ull, emax = 0;
+#pragma unroll
+  for (int q = 0; q < kRSItems; ++q) {
+    const int64_t en = st[q] + du[q];
+    if (sel.mm[q] >> lane & 1u) {
+      const uint32_t j = jm + __popc(sel.mm[q] & lt);
+      f.tok_slot[j] = sl[q];
+      f.tok_start[j] = st[q];
+      f.tok_end[j] = en;
+      f.tok_kind[j] = sel.kd[q];
+      if (f.tok_record) f.tok_record[j] = wbase + q * 32 + lane;
+      if (tf[q] > j) atomicMin(&f.tfirst[sl[q]], j);
+    }
+    if (sel.hm[q] >> lane & 1u) {
+      const uint64_t h = jh + __popc(sel.hm[q] & lt);
+      const uint64_t i = wbase + q * 32 + lane;
+      f.htod_start[h] = st[q];
+      f.htod_end[h] = en;
+      f.htod_size[h] = (f.rflags[i] & ITT_REC_HAS_SIZE) ? f.size[i] : 0;
+      const unsigned long long fe = static_cast<unsigned long long>(en) ^ (1ull << 63);
+      emin = fe < emin ? fe : emin;
+      emax = fe > emax ? fe : emax;
+    }
+    jm += __popc(sel.mm[q]);
+    jh += __popc(sel.hm[q]);
+  }
+  if (__any_sync(0xffffffffu, emax != 0)) {  // HtoD end range: one pair of atomics per warp
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long a = __shfl_xor_sync(0xffffffffu, emin, o), b = __shfl_xor_sync(0xffffffffu, emax, o);
+      emin = a < emin ? a : emin;
+      emax = b > emax ? b : emax;
+    }
+    if (lane == 0) {
+      atomicMin(&f.htod_range[0], emin);
+      atomicMax(&f.htod_range[1], emax);
+    }
+  }
+}
+
 // Compaction when the row order is block-local (rows already sorted, or the 256-row block sort
 // was the whole order): a tile of 2048 sorted positions reads exactly the source rows of the same
 // range, so the tile stages stream / device / kind / slot / start / dur in shared memory with
@@ -1686,7 +1824,21 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
              t.htod_end.p,
              t.htod_size.p,
              t.htod_range.p};
-  if (t.sorted || t.perm_local) {  // block-local order: stage each tile's rows in shared memory
+  static const bool two_pass = [] {  // ITT_COMPACT_RS=0: the single-pass look-back kernel for sorted rows too (A/B)
+    const char* e = std::getenv("ITT_COMPACT_RS");
+    return !(e && *e == '0');
+  }();
+  if (t.sorted && two_pass) {  // rows in order: reduce-then-scan
+    const uint64_t tiles = (n + kRSTile - 1) / kRSTile;
+    if (n) {
+      DBuf<uint64_t> tc(c, tiles);
+      launch(c, "compact_count", n * (t.filtering ? 7.0 : 5.0), k_compact_count, dim3(static_cast<unsigned>(tiles)), dim3(256), 0,
+             f, tc.p);
+      launch(c, "compact_scan", tiles * 16.0, k_scan_tile_counts, dim3(1), dim3(1024), 0, tc.p, tiles);
+      launch(c, "compact", n * (t.filtering ? 7.0 : 5.0) + n_main * 45.0 + n_htod * 48.0, k_compact_write,
+             dim3(static_cast<unsigned>(tiles)), dim3(256), 0, f, tc.p);
+    }
+  } else if (t.sorted || t.perm_local) {  // block-local order: stage each tile's rows in shared memory
     const uint64_t tiles = (n + kCompactTile - 1) / kCompactTile;
     t.scan.prepare(c, tiles);
     const size_t smem = sizeof(CompactLocalSmem);

@@ -28,55 +28,25 @@ constexpr int kTileA = 1024;
 constexpr int kLogTileA = 10;
 constexpr int kAnsvBlock = 256;
 
-// per tile: prefix minima, suffix minima (within the tile) and the tile minimum
+// per tile: the minimum of every 32-position block (bmin) and of the tile (tmin) — what the rare
+// cross-tile searches of k_ansv need, at 1/8 of the bytes prefix and suffix minima per position
+// would take
 __global__ void __launch_bounds__(kTileA) k_tile_minima(const uint32_t* __restrict__ lcp, uint64_t np,
-                                                        uint32_t* __restrict__ premin, uint32_t* __restrict__ sufmin,
-                                                        uint32_t* __restrict__ tmin) {
+                                                        uint32_t* __restrict__ bmin, uint32_t* __restrict__ tmin) {
   __shared__ uint32_t sw[32];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTileA;
-  const uint64_t j = base + threadIdx.x;
-  const uint32_t v = j < np ? lcp[j] : 0xFFFFFFFFu;
-  // inclusive prefix min (warp scan + warp totals)
-  uint32_t p = v;
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * kTileA + threadIdx.x;
+  uint32_t v = j < np ? __ldcs(&lcp[j]) : 0xFFFFFFFFu;
+  v = __reduce_min_sync(0xffffffffu, v);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_up_sync(0xffffffffu, p, o);
-    if (static_cast<int>(lane) >= o) p = min(p, u);
+  if (lane == 0) {
+    bmin[static_cast<uint64_t>(blockIdx.x) * 32 + warp] = v;
+    sw[warp] = v;
   }
-  if (lane == 31) sw[warp] = p;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = sw[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, w, o);
-      if (static_cast<int>(lane) >= o) w = min(w, u);
-    }
-    sw[lane] = w;
+    const uint32_t t = __reduce_min_sync(0xffffffffu, sw[lane]);
+    if (lane == 0) tmin[blockIdx.x] = t;
   }
-  __syncthreads();
-  if (warp > 0) p = min(p, sw[warp - 1]);
-  if (j < np) premin[j] = p;
-  if (threadIdx.x == kTileA - 1) tmin[blockIdx.x] = p;
-  __syncthreads();
-  // inclusive suffix min
-  uint32_t q = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_down_sync(0xffffffffu, q, o);
-    if (static_cast<int>(lane) + o < 32) q = min(q, u);
-  }
-  if (lane == 0) sw[warp] = q;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = sw[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_down_sync(0xffffffffu, w, o);
-      if (static_cast<int>(lane) + o < 32) w = min(w, u);
-    }
-    sw[lane] = w;
-  }
-  __syncthreads();
-  if (warp < 31) q = min(q, sw[warp + 1]);
-  if (j < np) sufmin[j] = q;
 }
 
 // sparse table over tile minima: st[l * nt + t] = min(tmin[t, t + 2^l))
@@ -107,8 +77,7 @@ __global__ void __launch_bounds__(1024) k_sparse_all(uint32_t* st, uint32_t nt, 
 
 struct AnsvArgs {
   const uint32_t* lcp;
-  const uint32_t* premin;
-  const uint32_t* sufmin;
+  const uint32_t* bmin;  // minimum per 32-position block
   const uint32_t* tst;  // tile sparse table
   uint32_t nt;
   int tlevels;
@@ -140,25 +109,24 @@ struct AnsvArgs {
   }
 };
 
-// last j in tile t with LCP[j] <= thr (the tile's min is known to be <= thr)
+// last j in tile t with LCP[j] <= thr (the tile's min is known to be <= thr): the last 32-block
+// whose minimum qualifies, then the last position in it
 __device__ __forceinline__ uint64_t last_le_in_tile(const AnsvArgs& a, uint32_t t, uint32_t thr) {
-  uint64_t lo = static_cast<uint64_t>(t) * kTileA, hi = min(lo + kTileA, a.np) - 1;  // sufmin non-decreasing in j
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi + 1) >> 1;
-    if (a.sufmin[mid] <= thr) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
+  const uint64_t t0 = static_cast<uint64_t>(t) * kTileA;
+  int b = static_cast<int>((umin64(t0 + kTileA, a.np) - 1 - t0) >> 5);
+  while (b > 0 && a.bmin[static_cast<uint64_t>(t) * 32 + b] > thr) --b;
+  uint64_t j = umin64(t0 + (static_cast<uint64_t>(b) + 1) * 32, a.np) - 1;
+  while (a.lcp[j] > thr) --j;
+  return j;
 }
 // first j in tile t with LCP[j] < thr (the tile's min is known to be < thr)
 __device__ __forceinline__ uint64_t first_lt_in_tile(const AnsvArgs& a, uint32_t t, uint32_t thr) {
-  uint64_t lo = static_cast<uint64_t>(t) * kTileA, hi = min(lo + kTileA, a.np) - 1;  // premin non-increasing in j
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (a.premin[mid] < thr) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
+  const uint64_t t0 = static_cast<uint64_t>(t) * kTileA;
+  int b = 0;
+  while (a.bmin[static_cast<uint64_t>(t) * 32 + b] >= thr) ++b;
+  uint64_t j = t0 + static_cast<uint64_t>(b) * 32;
+  while (a.lcp[j] >= thr) ++j;
+  return j;
 }
 
 // Most positions are decided by their neighbours alone: LCP[k-1] == l (k is not leftmost),
@@ -466,11 +434,11 @@ __global__ void k_pattern_out(const Best* __restrict__ best, const unsigned int*
 void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv, uint32_t list_max_len) {
   const uint64_t np = s.np;
   const uint32_t nt = static_cast<uint32_t>((np + kTileA - 1) / kTileA);
-  DBuf<uint32_t> premin(c, np), sufmin(c, np);
+  DBuf<uint32_t> bmin(c, static_cast<size_t>(nt) * 32);
   int tlevels = 1;
   while ((1u << tlevels) <= nt) ++tlevels;
   DBuf<uint32_t> tst(c, static_cast<size_t>(tlevels) * nt);
-  launch(c, "ansv_tile_minima", np * 12.0, k_tile_minima, dim3(nt), dim3(kTileA), 0, s.lcp.p, np, premin.p, sufmin.p, tst.p);
+  launch(c, "ansv_tile_minima", np * 4.0 + nt * 132.0, k_tile_minima, dim3(nt), dim3(kTileA), 0, s.lcp.p, np, bmin.p, tst.p);
   if (nt <= 65536) {
     if (tlevels > 1)
       launch(c, "ansv_sparse", nt * 12.0 * (tlevels - 1), k_sparse_all, dim3(1), dim3(1024), 0, tst.p, nt, tlevels);
@@ -478,7 +446,7 @@ void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv, uint32_t lis
     for (int l = 1; l < tlevels; ++l)
       launch(c, "ansv_sparse", nt * 12.0, k_sparse_level, dim3(grid_for(nt, 256)), dim3(256), 0, tst.p, nt, l);
   }
-  AnsvArgs a{s.lcp.p, premin.p, sufmin.p, tst.p, nt, tlevels, np, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  AnsvArgs a{s.lcp.p, bmin.p, tst.p, nt, tlevels, np, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (list_max_len) {  // mining: the candidate intervals only (no host sync: the kernels read the count)
     iv.list.alloc(c, np);
     iv.n_list.alloc(c, 1);
