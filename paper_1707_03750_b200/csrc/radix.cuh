@@ -146,7 +146,7 @@ struct SmemLayout {
   K keys[kTile];
   uint32_t vals[kTile];
   uint16_t warp_hist[kWarps][kDigits];  // per-warp digit counts, then exclusive offsets across warps
-  static constexpr bool kOr = kMatchOr && RB == 8;  // (10-bit digits: 4 KiB per warp, ballots only)
+  static constexpr bool kOr = kMatchOr && RB <= 9;  // (10-bit digits: 4 KiB per warp, ballots only)
   uint32_t match[kOr ? kWarps : 1][kOr ? kDigits : 1];  // per-warp lane masks per digit (kept zero)
   uint32_t local_off[kDigits];
   uint32_t global_base[kDigits];
@@ -368,7 +368,7 @@ void launch_pass(Ctx* c, const Loader& ld, K* ko, uint32_t* vo, uint64_t n, int 
   constexpr int TILE = BLOCK * ITEMS;
   const size_t smem = sizeof(SmemLayout<K, BLOCK, ITEMS, RB>);
   const uint64_t tiles = (n + TILE - 1) / TILE;
-  const char* name = RB == kRadixBits ? "radix_onesweep" : "radix_onesweep_w10";
+  const char* name = RB <= 9 ? "radix_onesweep" : "radix_onesweep_w10";
   const double bytes = static_cast<double>(n) * 2.0 * (sizeof(K) + 4);
   if (n >= kWideStatusN) {
     auto kern = k_onesweep<K, BLOCK, ITEMS, Loader, MINB, RB, uint64_t>;

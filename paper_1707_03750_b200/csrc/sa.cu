@@ -80,12 +80,14 @@ __global__ void k_token_stats(const int32_t* __restrict__ tok, uint64_t n, int32
 // into 32 bits, in one pass over the tokens
 // The same keys, plus the 8-bit digit histograms of every pass of the init sort (shared-memory
 // counts flushed once per block): the sort then needs no histogram pass over the keys.
+template <int RB>
 __global__ void __launch_bounds__(256) k_text_keys_hist(const int32_t* __restrict__ tok, uint64_t n, int32_t term, int32_t lo,
                                                         int bits, int k, int passes, int32_t* __restrict__ text,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ hist) {
-  __shared__ uint32_t sh[4 * 256];
-  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
+  constexpr int kB = 1 << RB;
+  __shared__ uint32_t sh[(32 / RB + 1) * kB];
+  for (int i = threadIdx.x; i < passes * kB; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const uint64_t np = n + 1;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -99,10 +101,10 @@ __global__ void __launch_bounds__(256) k_text_keys_hist(const int32_t* __restric
     }
     __stcs(&keys[i], key);
     __stcs(&vals[i], static_cast<uint32_t>(i));
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kB + ((key >> (RB * p)) & (kB - 1u))], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+  for (int i = threadIdx.x; i < passes * kB; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
@@ -666,13 +668,23 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   // bins) measured 1.12 ms per 100M pairs against 0.82 ms for an 8-bit one — 3 wide passes save nothing
   bool a0;
   if (known_alphabet) {  // keys and the sort's digit histograms in one pass (no host check of trivial passes)
-    const int passes = (init_bits + 7) / 8;
-    DBuf<uint32_t> ihist(c, static_cast<size_t>(passes) * 256);
+    // 25-27-bit keys (e.g. two 13-bit symbols, V ~ 4K): three 9-bit passes instead of four 8-bit ones
+    const bool nine = init_bits > 24 && init_bits <= 27 && !std::getenv("ITT_NO_NINE_BIT_INIT");
+    const int rb = nine ? 9 : 8;
+    const int passes = (init_bits + rb - 1) / rb;
+    DBuf<uint32_t> ihist(c, static_cast<size_t>(passes) << rb);
     ihist.zero();
-    launch(c, "sa_init_keys", np * 16.0, k_text_keys_hist, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens, n,
-           term, lo, cbits, k, passes, s.text.p, ka, va, ihist.p);
-    a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p,
-                                    static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), /*skip_trivial=*/false);
+    if (nine) {
+      launch(c, "sa_init_keys", np * 16.0, k_text_keys_hist<9>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
+             n, term, lo, cbits, k, passes, s.text.p, ka, va, ihist.p);
+      a0 = radix_sort_pairs<uint32_t, radix::ArrayLoader<uint32_t>, 9>(
+          c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p, static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), false);
+    } else {
+      launch(c, "sa_init_keys", np * 16.0, k_text_keys_hist<8>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
+             n, term, lo, cbits, k, passes, s.text.p, ka, va, ihist.p);
+      a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p,
+                                      static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), /*skip_trivial=*/false);
+    }
   } else {
     launch(c, "sa_init_keys", np * 16.0, k_text_keys, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, cbits, k,
            s.text.p, ka, va);
