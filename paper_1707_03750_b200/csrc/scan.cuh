@@ -153,6 +153,81 @@ struct ScanScratch {
   }
 };
 
+// Reduce-then-scan for large scans: (1) per-tile totals, (2) one block scans them, (3) every tile
+// rescans its items from a known prefix and stores.  Loads run twice (functors' loads are pure),
+// but no CTA waits at a barrier behind a look-back chain — on long scans that wait, not the
+// bytes, set the single-pass kernel's time (C3 compaction: 1.97 -> 1.48 ms).
+template <typename T, typename Op, typename F, int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) k_scan_reduce(F f, uint64_t n, T* __restrict__ tile_vals) {
+  __shared__ T s_w[BLOCK / 32];
+  Op op;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * (BLOCK * ITEMS) + static_cast<uint64_t>(threadIdx.x) * ITEMS;
+  T run = Op::identity();
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k)
+    if (base + k < n) run = op(run, f.load(base + k));
+  run = warp_allreduce(run, op);
+  if (lane_id() == 0) s_w[threadIdx.x >> 5] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T t = s_w[0];
+    for (int w = 1; w < BLOCK / 32; ++w) t = op(t, s_w[w]);
+    tile_vals[blockIdx.x] = t;
+  }
+}
+// exclusive scan of the tile totals in place: one block walking chunks of 8K (coalesced)
+template <typename T, typename Op>
+__global__ void __launch_bounds__(1024) k_scan_tile_totals(T* __restrict__ tv, uint64_t tiles) {
+  __shared__ T s_warp[32];
+  constexpr int kPer = 8;
+  Op op;
+  T carry = Op::identity();
+  for (uint64_t c0 = 0; c0 < tiles; c0 += 1024 * kPer) {
+    const uint64_t b0 = c0 + static_cast<uint64_t>(threadIdx.x) * kPer;
+    T v[kPer], run = Op::identity();
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      v[q] = b0 + q < tiles ? tv[b0 + q] : Op::identity();
+      run = op(run, v[q]);
+    }
+    T total;
+    T acc = op(carry, block_exclusive_scan<T, Op, 1024>(run, op, &total, s_warp));
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      if (b0 + q < tiles) tv[b0 + q] = acc;
+      acc = op(acc, v[q]);
+    }
+    carry = op(carry, total);
+    __syncthreads();
+  }
+}
+// the last tile also writes the inclusive total where ScanScratch::total reads it
+template <typename T, typename Op, typename F, int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) k_scan_apply(F f, uint64_t n, const T* __restrict__ tile_excl, uint64_t* total_word) {
+  __shared__ T s_warp[BLOCK / 32];
+  Op op;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * (BLOCK * ITEMS) + static_cast<uint64_t>(threadIdx.x) * ITEMS;
+  const T prefix = tile_excl[blockIdx.x];
+  T vals[ITEMS];
+  T run = Op::identity();
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    vals[k] = base + k < n ? f.load(base + k) : Op::identity();
+    run = op(run, vals[k]);
+  }
+  T total;
+  T acc = op(prefix, block_exclusive_scan<T, Op, BLOCK>(run, op, &total, s_warp));
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    if (base + k < n) f.store(base + k, acc, vals[k]);
+    acc = op(acc, vals[k]);
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
+    *total_word = kFlagP | (static_cast<uint64_t>(op(prefix, total)) & kValMask);
+}
+
+constexpr uint64_t kScanRsTiles = 4096;  // from this many tiles (8M items) on: reduce-then-scan
+
 template <typename T, typename Op, int BLOCK = 256, int ITEMS = 8, typename F>
 void device_scan(Ctx* c, const char* name, double bytes, F f, uint64_t n, ScanScratch& scratch) {
   if (n == 0) {
@@ -162,6 +237,15 @@ void device_scan(Ctx* c, const char* name, double bytes, F f, uint64_t n, ScanSc
   constexpr uint64_t TILE = BLOCK * ITEMS;
   const uint64_t tiles = (n + TILE - 1) / TILE;
   scratch.prepare(c, tiles);
+  if (tiles >= kScanRsTiles) {  // tile totals in the status words' space ([1, tiles]), the total at [tiles]
+    T* tv = reinterpret_cast<T*>(scratch.buf.p + 1);
+    launch(c, name, bytes * 0.5, k_scan_reduce<T, Op, F, BLOCK, ITEMS>, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), 0, f, n,
+           tv);
+    launch(c, "scan_tiles", tiles * 2.0 * sizeof(T), k_scan_tile_totals<T, Op>, dim3(1), dim3(1024), 0, tv, tiles);
+    launch(c, name, bytes, k_scan_apply<T, Op, F, BLOCK, ITEMS>, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), 0, f, n, tv,
+           scratch.buf.p + tiles);
+    return;
+  }
   uint32_t* counter = reinterpret_cast<uint32_t*>(scratch.buf.p);
   uint64_t* status = scratch.buf.p + 1;
   launch(c, name, bytes, k_scan<T, Op, F, BLOCK, ITEMS>, dim3(static_cast<unsigned>(tiles)), dim3(BLOCK), 0, f, n,
