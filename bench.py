@@ -277,6 +277,49 @@ def bench_batch(args, world, rank, local, workload):
     total_events, ms = float(ev_total[0].item()), float(ev_total[1].item())
     launches = (launch_count() - l0) // max(1, args.steps)
     ok = all(r["loops"][0]["pattern_length"] == 200 and r["loops"][0]["iterations"] == 500 for r in res)
+    # e2e: the same batch from pinned HOST columns (each trace's H2D inside the timed region, the
+    # per-iteration rows back to the host): the executor's own copies, native workers
+    e2e = None
+    if args.batch_impl == "native" and not args.no_e2e:
+        fields = ["start_ns", "duration_ns", "size_bytes", "flags", "stream", "name_off", "name_bytes", "device"]
+        registered = []
+        try:
+            for t in pool_ids:
+                for f in fields:
+                    a = getattr(pool[t][0], f, None)
+                    if a is not None and a.nbytes:
+                        try:
+                            up_ctx.register_host(a)
+                            registered.append(a)
+                        except itt.IttError:
+                            pass  # stays pageable (slower copies, same result)
+            host_traces = [pool[t % args.distinct][0] for t in range(args.traces)]
+
+            def one_pass_host():
+                return batch.run_shard_native(executor, host_traces, [500], lo, hi)
+            one_pass_host()
+            bar()
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record()
+            for _ in range(args.steps):
+                res_h = one_pass_host()
+            torch.cuda.synchronize(dev)
+            h1.record()
+            h1.synchronize()
+            bar()
+            ms_h = torch.tensor([h0.elapsed_time(h1)], device=f"cuda:{dev}")
+            if world > 1:
+                torch.distributed.all_reduce(ms_h, op=torch.distributed.ReduceOp.MAX)
+            ms_h = float(ms_h.item())
+            h2d = sum(host_traces[i].nbytes() for i in range(lo, hi))
+            d2h = sum(sum(L["iterations"] * 88 for L in r["loops"]) for r in res_h)  # itt_iter_row: 11 x i64
+            ok = ok and all(r["loops"][0]["pattern_length"] == 200 for r in res_h)
+            e2e = {"value": total_events / (ms_h / args.steps / 1000.0), "unit": "events/s",
+                   "h2d_bytes_per_step": int(h2d * (world if world > 1 else 1)), "d2h_bytes_per_step": int(d2h),
+                   "ms_per_step": ms_h / args.steps, "pinned_columns": f"{len(registered)} registered"}
+        finally:
+            for a in registered:
+                up_ctx.unregister_host(a)
     if rank == 0:
         line = {"metric": METRIC, "value": total_events / (ms / args.steps / 1000.0), "unit": "events/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -285,7 +328,7 @@ def bench_batch(args, world, rank, local, workload):
                            "events_per_step": int(total_events), "workers_per_gpu": args.workers, "executor": args.batch_impl,
                            "batched_suffix_arrays": args.batch_impl == "native",
                            "parallelism": f"shard{world}", "mined_ok": bool(ok)},
-                "clocks": clk.summary(), "gpu_launches": int(launches)}
+                "clocks": clk.summary(), "gpu_launches": int(launches), "e2e": e2e}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = c4_cpu_baseline()
