@@ -147,6 +147,63 @@ struct EmitLoader {
 // kHeads: rank_new holds the SA position of each group's head instead of a dense id (u32; the
 // scan is a max over head positions and G is counted separately into *gcount) — what refinement
 // rounds continue from without a conversion pass.
+// The first level (k-gram keys, head positions) without the random scatter: while the init rank
+// update walks SA order, each group head enters its (key -> head position) into a small hash
+// table; k_init_fill then writes rank[x] = table[key(x)] in TEXT order — sequential stores
+// instead of one 32-byte sector read-modify-write per suffix.  Only while the distinct k-grams
+// fit the table (periodic traces: thousands); otherwise the scatter (the overflow bit, bit 63 of
+// the group counter, makes the host re-run the update without the table).
+constexpr uint32_t kInitMapBits = 16;  // 64K entries of 8 bytes: L1/L2-resident during the fill
+constexpr int kInitMapProbe = 64;
+__device__ __forceinline__ uint32_t init_map_slot(uint32_t key, uint32_t mask) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(key) * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+}
+// entry = head << 33 | 1 << 32 | key (0 = empty; heads < 2^31 in heads mode)
+__device__ __forceinline__ void init_map_insert(unsigned long long* map, uint32_t mask, uint32_t key, uint32_t val,
+                                                unsigned long long* overflow) {
+  uint32_t sl = init_map_slot(key, mask);
+  const unsigned long long e = (static_cast<unsigned long long>(val) << 33) | (1ull << 32) | key;
+  for (int p = 0; p < kInitMapProbe; ++p) {
+    if (atomicCAS(&map[sl], 0ull, e) == 0ull) return;  // every key is inserted once (at its group's head)
+    sl = (sl + 1) & mask;
+  }
+  atomicOr(overflow, 1ull << 63);
+}
+// 4 positions per thread: one 16-byte store of ranks (u32 levels)
+__global__ void __launch_bounds__(256) k_init_fill(const int32_t* __restrict__ text, uint64_t np, int bits, int k,
+                                                   const unsigned long long* __restrict__ map, uint32_t mask,
+                                                   uint32_t* __restrict__ level) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 4;
+  for (uint64_t x0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; x0 < np; x0 += stride) {
+    uint32_t r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t x = x0 + u;
+      r[u] = 0;
+      if (x >= np) continue;
+      uint32_t key = 0;
+      for (int q = 0; q < k; ++q) {  // the same packing as k_text_keys (text[np - 1] is the terminator code)
+        const uint64_t j = x + q;
+        key = (key << bits) | (j < np ? static_cast<uint32_t>(__ldg(&text[j])) : 0u);
+      }
+      uint32_t sl = init_map_slot(key, mask);
+      const unsigned long long want = (1ull << 32) | key;
+      unsigned long long e = __ldg(&map[sl]);
+      while ((e & 0x1FFFFFFFFull) != want) {
+        sl = (sl + 1) & mask;
+        e = __ldg(&map[sl]);
+      }
+      r[u] = static_cast<uint32_t>(e >> 33);
+    }
+    if (x0 + 4 <= np) {
+      __stcs(reinterpret_cast<uint4*>(level + x0), make_uint4(r[0], r[1], r[2], r[3]));
+    } else {
+      for (int u = 0; u < 4; ++u)
+        if (x0 + u < np) level[x0 + u] = r[u];
+    }
+  }
+}
+
 template <bool kHeads>
 __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
                                                             uintptr_t rank_old, uint32_t h, uint64_t np,
@@ -154,7 +211,8 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
                                                             int passes, uint32_t* __restrict__ gstart,
                                                             uint64_t* status, uint32_t* counter, uint32_t pf_dist,
                                                             uint8_t* __restrict__ heads_out,
-                                                            unsigned long long* __restrict__ gcount) {
+                                                            unsigned long long* __restrict__ gcount,
+                                                            unsigned long long* __restrict__ init_map, uint32_t map_mask) {
   __shared__ uint32_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_hist[kMaxPasses][256];
@@ -246,7 +304,11 @@ __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* _
       } else {
         id = pre + __popc(fmask & ((2u << q) - 1u)) - 1;
       }
-      rank_put(rank_new, s_idx[q], id);  // ids beyond a u16 level are caught by the host (G > 2^16)
+      if (kHeads && init_map) {  // init: key -> head position for the text-order fill (k_init_fill), no scatter
+        if ((fmask >> q) & 1u) init_map_insert(init_map, map_mask, kv[q], id, gcount);
+      } else {
+        rank_put(rank_new, s_idx[q], id);  // ids beyond a u16 level are caught by the host (G > 2^16)
+      }
       // group starts (SA position of each group's first suffix) for the wide-digit histograms
       if (!kHeads && gstart && ((fmask >> q) & 1u) && id < kWideGroups) gstart[id] = static_cast<uint32_t>(j);
 #pragma unroll
@@ -721,6 +783,13 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   // one rank update into a new level (u16 when the previous group count suggests the ids fit; if
   // they do not, the update runs again into a u32 level: its inputs are untouched)
   DBuf<unsigned long long> gcount(c, 1);
+  // the init level by a text-order fill from a (k-gram -> head) table (k_init_fill); ITT_INIT_MAP=0: the scatter
+  bool use_init_map = [] {
+    const char* e = std::getenv("ITT_INIT_MAP");
+    return !(e && *e == '0');
+  }();
+  DBuf<unsigned long long> init_map;
+  const int init_cbits = cbits, init_k = k;
   auto rank_update = [&](const uint32_t* kk, const uint32_t* ss, uintptr_t rank_old, uint32_t h, bool more,
                          uint64_t g_prev, bool heads_mode) -> uint64_t {
     // only where the arrays outgrow L2 (C2's 40 MB levels stay resident: u16 stores there cost
@@ -733,15 +802,21 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
       const uintptr_t lvl = reinterpret_cast<uintptr_t>(s.levels.back().p) | (narrow ? 1u : 0u);
       ScanScratch& sc = *scans[cur];
       hist_p = hists[cur].p;
+      const bool map_init = heads_mode && !rank_old && use_init_map && !narrow;
+      if (map_init) {
+        init_map.alloc(c, size_t{1} << kInitMapBits);
+        init_map.zero();
+      }
       if (heads_mode) {
         gcount.zero();
-        launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update<true>, dim3(static_cast<unsigned>(rtiles)),
-               dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, nullptr, sc.buf.p + 1,
-               reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, gcount.p);
+        launch(c, "sa_rank_update", np * (rank_old ? 20.0 : (map_init ? 8.0 : 12.0)), k_rank_update<true>,
+               dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes,
+               nullptr, sc.buf.p + 1, reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, gcount.p,
+               map_init ? init_map.p : nullptr, (1u << kInitMapBits) - 1);
       } else {
         launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update<false>, dim3(static_cast<unsigned>(rtiles)),
                dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes, gstart.p, sc.buf.p + 1,
-               reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, nullptr);
+               reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, nullptr, nullptr, 0u);
       }
       // group count G: the last tile's inclusive word (dense ids) or the head counter, copied out
       // and waited on by event, so the next round's scratch zeroing (queued after the copy) runs
@@ -757,7 +832,18 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
         radix_prezero_status(c, rs, np, max_passes, 0);  // a wide sort zeroes its own (rare, larger)
       }
       ITT_CUDA(cudaEventSynchronize(c->deferred_ev));
-      const uint64_t total = heads_mode ? *word : (*word & kValMask);
+      uint64_t total = heads_mode ? *word : (*word & kValMask);
+      if (map_init) {
+        if (total >> 63) {  // more distinct k-grams than the table holds: the scatter after all
+          use_init_map = false;
+          s.levels.pop_back();
+          hists[cur].zero();
+          sc.prepare(c, rtiles);
+          continue;
+        }
+        launch(c, "sa_init_fill", np * 8.0, k_init_fill, dim3(grid_for((np + 3) / 4, 256, c->sm_count * 16)), dim3(256), 0,
+               s.text.p, np, init_cbits, init_k, init_map.p, (1u << kInitMapBits) - 1, reinterpret_cast<uint32_t*>(lvl));
+      }
       if (narrow && total > kNarrowGroups) {  // the ids did not fit 16 bits: redo into u32
         s.levels.pop_back();
         hists[cur].zero();

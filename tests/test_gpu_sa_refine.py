@@ -109,3 +109,16 @@ def test_capped_lcp_from_group_heads(ctx, R, name, s, term, monkeypatch):
         want = np.minimum(rlcp.astype(np.uint64), cap).astype(np.uint32)
         assert np.array_equal(got["0"], want), (name, cap)
         assert np.array_equal(got["1"], want), (name, cap)
+
+
+def test_init_level_table_overflow_falls_back_to_scatter(ctx, R):
+    """The first level comes from a (k-gram -> head) table filled in text order when the distinct
+    k-grams fit it (64K entries, at most 64 probes); a random text over a large alphabet has more
+    distinct k-grams than that, so the init update must fall back to the scatter — same SA/LCP."""
+    rng = np.random.default_rng(4242)
+    for n, alpha in ((300_000, 1_000), (150_000, 60_000)):
+        s = rng.integers(0, alpha, n).astype(np.int32)
+        sa, lcp = ctx.suffix_array(s, alpha)
+        rsa, rlcp = R.suffix_array(s, alpha)
+        assert np.array_equal(sa, rsa) and np.array_equal(lcp, rlcp), (n, alpha)
+        assert _mine(ctx, s, alpha, [(50, 1)]) == _mine(R, s, alpha, [(50, 1)])
