@@ -1,9 +1,11 @@
 """Distributed suffix array + capped LCP of one trace over G ranks.
 
 The reference builds one suffix tree on one core (suffix_tree.hpp:21-190, via mine.hpp:38-40).
-On one B200 the capped prefix doubling (sa.cu) covers ~1.5B tokens; beyond that the suffixes are
-block-partitioned by text position across ranks and every doubling round is a global sort of
-(rank_i, rank_{i+h}) keys:
+Limits: one B200 takes fewer than 2^32 - 1 suffixes (32-bit SA entries; the radix look-back
+words are 64-bit from 2^30 keys on), and its 180 GB hold about 1.5B events with streamed names;
+this distributed path takes fewer than 2^31 - 1 suffixes (positions share a u32 with the
+same-group flag of the LCP requests).  The suffixes are block-partitioned by text position
+across ranks and every doubling round is a global sort of (rank_i, rank_{i+h}) keys:
 
   1. halo:    rank_{i+h} for own i comes from the owners of [lo+h, hi+h) — one contiguous slice
               per source rank, one all-to-all;
