@@ -383,11 +383,16 @@ struct HeadPair {  // (last new head + 1, last old head + 1) in two 31-bit halve
 __global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __restrict__ sa, const uint8_t* __restrict__ heads,
                                                              uintptr_t rank, uint32_t h, uint64_t np,
                                                              uint8_t* __restrict__ heads_next,
-                                                             unsigned long long* __restrict__ counts /*[0] groups, [1] inversions*/) {
+                                                             unsigned long long* __restrict__ counts /*[0] groups, [1] inversions*/,
+                                                             unsigned int* __restrict__ abort_flag) {
   __shared__ uint32_t s_last[kRankBlock / 32];
   __shared__ unsigned long long s_cnt[2];
+  __shared__ unsigned int s_abort;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_abort = ld_relaxed_u32(abort_flag);
   if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  if (s_abort) return;  // an earlier round (or block of this one) found inversions: the host redoes it
   const uint64_t base = (static_cast<uint64_t>(blockIdx.x) * kRankBlock + threadIdx.x) * kRankItems;
   auto second = [&](uint32_t x) -> uint32_t {
     const uint64_t y = static_cast<uint64_t>(x) + h;
@@ -439,6 +444,7 @@ __global__ void __launch_bounds__(kRankBlock) k_refine_detect(const uint32_t* __
   }
   __syncthreads();
   if (threadIdx.x < 2 && s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+  if (threadIdx.x == 1 && s_cnt[1]) atomicOr(abort_flag, 1u);  // rounds queued after this one return at once
 }
 
 // rank_{2h}[SA_j] = position of j's new group head, written where it differs from the old head
@@ -457,12 +463,17 @@ constexpr int kApplyWords = ITT_APPLY_WORDS;  // words per thread
 __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads_old,
                                                             const uint32_t* __restrict__ heads_new, uint64_t np,
                                                             uint32_t* __restrict__ level, int full, uint64_t* status,
-                                                            uint32_t* counter) {
+                                                            uint32_t* counter, const unsigned int* __restrict__ abort_flag) {
   __shared__ uint64_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_prefix;
-  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  __shared__ unsigned int s_abort;
+  if (threadIdx.x == 0) {
+    s_abort = ld_relaxed_u32(abort_flag);
+    s_tile = atomicAdd(counter, 1u);
+  }
   __syncthreads();
+  if (s_abort) return;  // this round's detect (or an earlier one) found inversions
   const uint32_t tile = s_tile;
   const uint64_t w0 = (static_cast<uint64_t>(tile) * kRankBlock + threadIdx.x) * kApplyWords;  // first bitmap word
   uint32_t ho[kApplyWords], hn[kApplyWords];
@@ -872,59 +883,122 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   bool dense = !init_heads;  // the newest level holds dense ids (else group-head positions)
   bool try_refine = init_heads && g * 16 < np;  // then decided after each full round from the groups it added
   int cooldown = 0;
-  DBuf<unsigned long long> rcount(c, 2);
+  DBuf<unsigned long long> rcount(c, 4);  // two rounds' (groups, inversions): one round of lookahead
+  DBuf<unsigned int> abort_flag(c, 1);    // set by a detect that counted inversions: later rounds' kernels return
+  abort_flag.zero();
   DBuf<uint32_t> head_hist;
-  ScanScratch rscan;
+  ScanScratch rscan[2];
+  // Refinement rounds run one round ahead of the host: round r+1's kernels are queued before the
+  // host reads round r's verdict (its readback overlaps round r+1 on the device).  A round whose
+  // detect counts inversions sets abort_flag, so everything queued after it returns at once; the
+  // host then restores the state from before that round and sorts it instead.
+  struct Snapshot {
+    int hc;
+    bool dense;
+    uint32_t h;
+    int rounds;
+    size_t n_levels, n_tags;
+    std::vector<uint32_t> level_h;
+  };
+  struct Pending {
+    bool on = false;
+    int slot = 0;
+    Snapshot before;
+  } pend;
+  int rslot = 0;
+  unsigned long long* host_cnt = static_cast<unsigned long long*>(c->deferred_block()) + 16;  // [16, 20): two rounds' counts
+  cudaEvent_t rev[2] = {nullptr, nullptr};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } rev_guard{rev};
+  for (auto& e : rev) ITT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // the pending round's verdict: commit its group count, or undo it and everything after it
+  auto resolve = [&]() -> bool {  // true: the pending round had inversions (state restored)
+    if (!pend.on) return false;
+    pend.on = false;
+    ++StageTimer::syncs();
+    ITT_CUDA(cudaEventSynchronize(rev[pend.slot]));
+    const unsigned long long* cnt = host_cnt + 2 * pend.slot;
+    if (cnt[1] == 0) {
+      g = cnt[0];
+      return false;
+    }
+    const Snapshot& b = pend.before;
+    hc = b.hc, dense = b.dense, h = b.h, s.rounds = b.rounds;
+    s.levels.resize(b.n_levels);
+    s.level_tags.resize(b.n_tags);
+    s.level_h = b.level_h;
+    ITT_CUDA(cudaMemsetAsync(abort_flag.p, 0, 4, c->stream));
+    cooldown = 2;  // inversions: sort this round, try again two rounds later
+    return true;
+  };
   // stop when every suffix is alone, or when the groups already separate `cap` symbols (mining
   // never looks deeper than its L_max; see k_plcp for why the capped LCP stays exact below cap)
-  while (g < np && h < cap) {
-    const uintptr_t rank = s.level_tags.back();
+  for (;;) {
+    if (!(g < np && h < cap)) {
+      if (!pend.on) break;
+      resolve();  // the last speculative round: commit it, or undo it and sort it
+      continue;
+    }
     if (try_refine && cooldown == 0) {
       // ---- refinement round: no sort when every group is already ordered by its second key
-      rcount.zero();
+      const uintptr_t rank = s.level_tags.back();
+      Snapshot before{hc, dense, h, s.rounds, s.levels.size(), s.level_tags.size(), s.level_h};
+      unsigned long long* dcnt = rcount.p + 2 * rslot;
+      ITT_CUDA(cudaMemsetAsync(dcnt, 0, 16, c->stream));
       launch(c, "sa_refine_detect", np * 9.125, k_refine_detect, dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock), 0, sa,
-             heads[hc].p, rank, h, np, heads[hc ^ 1].p, rcount.p);
-      unsigned long long cnt[2];
-      readback(c, cnt, rcount.p, 2);
-      if (cnt[1] == 0) {
-        const bool full = dense;  // dense ids: every rank changes representation
-        // the input level is updated in place unless LCP lifting keeps it: kept levels stay within
-        // lift_ratio() of each other, so most refinement rounds skip the level copy (C3: 12 -> 3 copies of
-        // 400 MB, step -1.1 ms; lifting repeats a level up to 15 times, lcp_plcp unchanged)
-        const size_t nl = s.level_h.size();
-        const uint64_t below = nl >= 2 ? s.level_h[nl - 2] : 1;
-        const bool dispensable = !s.keep_levels || below * lift_ratio() >= 2ull * h;
-        uint32_t* lvl;
-        if (!full && dispensable) {  // nothing reads the old level again: update it in place
-          lvl = reinterpret_cast<uint32_t*>(rank);
-          s.level_h.back() = static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull));
-        } else {
-          s.levels.emplace_back(c, np);
-          lvl = s.levels.back().p;
-          if (!full) ITT_CUDA(cudaMemcpyAsync(lvl, reinterpret_cast<const uint32_t*>(rank), np * 4, cudaMemcpyDeviceToDevice,
-                                              c->stream));
-        }
-        const uint64_t atiles = (np + kRankBlock * kApplyItems * kApplyWords - 1) / (kRankBlock * kApplyItems * kApplyWords);
-        rscan.prepare(c, atiles);
-        launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply, dim3(static_cast<unsigned>(atiles)),
-               dim3(kRankBlock), 0, sa, reinterpret_cast<const uint32_t*>(heads[hc].p),
-               reinterpret_cast<const uint32_t*>(heads[hc ^ 1].p), np, lvl, full ? 1 : 0, rscan.buf.p + 1,
-               reinterpret_cast<uint32_t*>(rscan.buf.p));
-        if (lvl != reinterpret_cast<uint32_t*>(rank)) {
-          s.level_tags.push_back(reinterpret_cast<uintptr_t>(lvl));
-          s.level_h.push_back(static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull)));
-          if (!s.keep_levels && s.levels.size() >= 3) s.levels[s.levels.size() - 3].release();
-        }
-        hc ^= 1;
-        dense = false;
-        g = cnt[0];
-        ++s.rounds;
-        if (static_cast<uint64_t>(h) * 2 > 0xFFFFFFFFull) break;
-        h *= 2;
-        continue;
+             heads[hc].p, rank, h, np, heads[hc ^ 1].p, dcnt, abort_flag.p);
+      const bool full = dense;  // dense ids: every rank changes representation
+      // the input level is updated in place unless LCP lifting keeps it: kept levels stay within
+      // lift_ratio() of each other, so most refinement rounds skip the level copy (C3: 12 -> 3 copies of
+      // 400 MB, step -1.1 ms; lifting repeats a level up to 15 times, lcp_plcp unchanged)
+      const size_t nl = s.level_h.size();
+      const uint64_t below = nl >= 2 ? s.level_h[nl - 2] : 1;
+      const bool dispensable = !s.keep_levels || below * lift_ratio() >= 2ull * h;
+      uint32_t* lvl;
+      if (!full && dispensable) {  // nothing reads the old level again: update it in place
+        lvl = reinterpret_cast<uint32_t*>(rank);
+        s.level_h.back() = static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull));
+      } else {
+        s.levels.emplace_back(c, np);
+        lvl = s.levels.back().p;
+        if (!full) ITT_CUDA(cudaMemcpyAsync(lvl, reinterpret_cast<const uint32_t*>(rank), np * 4, cudaMemcpyDeviceToDevice,
+                                            c->stream));
+        s.level_tags.push_back(reinterpret_cast<uintptr_t>(lvl));
+        s.level_h.push_back(static_cast<uint32_t>(std::min<uint64_t>(2ull * h, 0xFFFFFFFFull)));
+        // (older levels are not released here: an undone round may need them)
       }
-      cooldown = 2;  // inversions: sort this round, try again two rounds later
+      const uint64_t atiles = (np + kRankBlock * kApplyItems * kApplyWords - 1) / (kRankBlock * kApplyItems * kApplyWords);
+      rscan[rslot].prepare(c, atiles);
+      launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply, dim3(static_cast<unsigned>(atiles)),
+             dim3(kRankBlock), 0, sa, reinterpret_cast<const uint32_t*>(heads[hc].p),
+             reinterpret_cast<const uint32_t*>(heads[hc ^ 1].p), np, lvl, full ? 1 : 0, rscan[rslot].buf.p + 1,
+             reinterpret_cast<uint32_t*>(rscan[rslot].buf.p), abort_flag.p);
+      ITT_CUDA(cudaMemcpyAsync(host_cnt + 2 * rslot, dcnt, 16, cudaMemcpyDeviceToHost, c->stream));
+      ITT_CUDA(cudaEventRecord(rev[rslot], c->stream));
+      // this round is queued; now the verdict of the one before it
+      const bool undone = resolve();
+      if (undone) continue;  // state is back before the failed round (this one returned at once on the device)
+      hc ^= 1;
+      dense = false;
+      ++s.rounds;
+      pend.on = true;
+      pend.slot = rslot;
+      pend.before = std::move(before);
+      rslot ^= 1;
+      if (static_cast<uint64_t>(h) * 2 > 0xFFFFFFFFull) {
+        resolve();
+        break;
+      }
+      h *= 2;
+      continue;
     }
+    if (resolve()) continue;  // a full round needs the pending round's verdict (and its exact state)
+    const uintptr_t rank = s.level_tags.back();
     // ---- full round: stable sort of E_j = SA_j - h by rank_h (the E trick) + rank update
     const int b = dense ? bits_for(g - 1) : bits_for(np - 1);
     const EmitLoader ld{sa, rank, np, h};
