@@ -65,6 +65,18 @@ struct ArrayLoader {
   }
 };
 
+// keys from an array, values = their positions (the first pass of a sort whose values are 0..n-1:
+// no value array to write beforehand or read here)
+template <typename K>
+struct IotaLoader {
+  const K* keys;
+  __device__ __forceinline__ void operator()(uint64_t i, K& k, uint32_t& v) const {
+    k = __ldcs(&keys[i]);
+    v = static_cast<uint32_t>(i);
+  }
+  __device__ __forceinline__ void prefetch(uint64_t i, uint64_t cnt) const { prefetch_l2(keys + i, cnt * sizeof(K)); }
+};
+
 // Lanes of the warp holding the same RB-bit digit (valid lanes only among themselves): ballots
 // instead of MATCH.ANY, whose long MIO latency dominated the ranking loop on sm_100a.  Only the
 // digit bits that vary across the warp need a ballot (two warp reductions find them): the keys of

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) k_text_keys_hist(const int32_t* __restric
       key = (key << bits) | c;
     }
     __stcs(&keys[i], key);
-    __stcs(&vals[i], static_cast<uint32_t>(i));
+    if (vals) __stcs(&vals[i], static_cast<uint32_t>(i));  // null: the sort's first pass generates positions
     for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kB + ((key >> (RB * p)) & (kB - 1u))], 1u);
   }
   __syncthreads();
@@ -747,16 +747,17 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     const int passes = (init_bits + rb - 1) / rb;
     DBuf<uint32_t> ihist(c, static_cast<size_t>(passes) << rb);
     ihist.zero();
+    const radix::IotaLoader<uint32_t> iota{ka};  // positions are generated by the first pass
     if (nine) {
-      launch(c, "sa_init_keys", np * 16.0, k_text_keys_hist<9>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
-             n, term, lo, cbits, k, passes, s.text.p, ka, va, ihist.p);
-      a0 = radix_sort_pairs<uint32_t, radix::ArrayLoader<uint32_t>, 9>(
-          c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p, static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), false);
+      launch(c, "sa_init_keys", np * 12.0, k_text_keys_hist<9>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
+             n, term, lo, cbits, k, passes, s.text.p, ka, static_cast<uint32_t*>(nullptr), ihist.p);
+      a0 = radix_sort_pairs<uint32_t, radix::IotaLoader<uint32_t>, 9>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p, &iota,
+                                                                      false);
     } else {
-      launch(c, "sa_init_keys", np * 16.0, k_text_keys_hist<8>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
-             n, term, lo, cbits, k, passes, s.text.p, ka, va, ihist.p);
-      a0 = radix_sort_pairs<uint32_t>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p,
-                                      static_cast<const radix::ArrayLoader<uint32_t>*>(nullptr), /*skip_trivial=*/false);
+      launch(c, "sa_init_keys", np * 12.0, k_text_keys_hist<8>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
+             n, term, lo, cbits, k, passes, s.text.p, ka, static_cast<uint32_t*>(nullptr), ihist.p);
+      a0 = radix_sort_pairs<uint32_t, radix::IotaLoader<uint32_t>>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p, &iota,
+                                                                   /*skip_trivial=*/false);
     }
   } else {
     launch(c, "sa_init_keys", np * 16.0, k_text_keys, dim3(grid_for(np, 256)), dim3(256), 0, tokens, n, term, lo, cbits, k,

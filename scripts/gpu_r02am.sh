@@ -1,0 +1,4 @@
+python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "not c5" 2>&1 | tail -1 > gpurun_out/r02am.log
+python scripts/kernel_table.py C3 2>&1 | grep -E "kernel sum|radix|init" >> gpurun_out/r02am.log
+python scripts/opprof_c3.py C3 2>&1 | head -1 >> gpurun_out/r02am.log
+python scripts/opprof_c3.py C2 2>&1 | head -1 >> gpurun_out/r02am.log
