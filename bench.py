@@ -684,8 +684,10 @@ def bench_single(args, world, rank, local, workload, iters):
             for a in registered:
                 ctx.unregister_host(a)
         d2h = sum(L["rows"].nbytes + 4 * L["pattern_length"] for L in res_e["loops"])
+        # a pinned size column is read in place (HtoD rows only, zero-copy), not copied whole
+        h2d = int(recs_e.nbytes()) - (int(recs.size_bytes.nbytes) if any(a is recs.size_bytes for a in registered) else 0)
         e2e = {"value": world * n_events / (ms_e / args.steps / 1000.0), "unit": "events/s",
-               "h2d_bytes_per_step": int(recs_e.nbytes()), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h),
                "ms_per_step": ms_e / args.steps,
                "pinned_columns": f"{len(registered)} registered + {len(staged)} staged of {len(cols)}"}
         log(f"[rank {rank}] e2e: {e2e['ms_per_step']:.2f} ms/step, {e2e['value'] / 1e9:.3f}G events/s")

@@ -1413,9 +1413,20 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
     d.host_names = r->name_bytes;
     d.stream_chunk = 64ull << 20;
   }
+  // sizes are read only for HtoD records (the compaction's htod_size): from pinned host memory the
+  // kernels read them in place (zero-copy) instead of copying the whole column over PCIe (8 B/record)
+  const int64_t* size_mapped = nullptr;
+  if (n) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, r->size_bytes) == cudaSuccess) {
+      if (pa.type == cudaMemoryTypeHost && pa.devicePointer) size_mapped = static_cast<const int64_t*>(pa.devicePointer);
+    } else {
+      cudaGetLastError();
+    }
+  }
   d.o_start.alloc(c, n);
   d.o_dur.alloc(c, n);
-  d.o_size.alloc(c, n);
+  if (!size_mapped) d.o_size.alloc(c, n);
   d.o_flags.alloc(c, n);
   d.o_stream.alloc(c, n);
   d.o_off.alloc(c, n + 1);
@@ -1431,7 +1442,7 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   }
   h2d_bulk(c, d.o_off.p, r->name_off, (n + 1) * 8, cs);
   h2d_bulk(c, d.o_dur.p, r->duration_ns, n * 8, cs);
-  h2d_bulk(c, d.o_size.p, r->size_bytes, n * 8, cs);
+  if (!size_mapped) h2d_bulk(c, d.o_size.p, r->size_bytes, n * 8, cs);
   h2d_bulk(c, d.o_flags.p, r->flags, n, cs);
   h2d_bulk(c, d.o_stream.p, r->stream, n * 4, cs);
   if (r->device) h2d_bulk(c, d.o_device.p, r->device, n * 2, cs);
@@ -1439,7 +1450,7 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   if (overlap) ITT_CUDA(cudaEventRecord(d.cols_ready, cs));  // the compute stream waits before the dictionary
   d.start = d.o_start.p;
   d.dur = d.o_dur.p;
-  d.size = d.o_size.p;
+  d.size = size_mapped ? size_mapped : d.o_size.p;
   d.flags = d.o_flags.p;
   d.stream = d.o_stream.p;
   d.name_off = d.o_off.p;

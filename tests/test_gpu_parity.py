@@ -336,6 +336,25 @@ def test_device_resident_inputs_match_host_inputs(ctx):
     assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
 
 
+def test_pinned_host_columns_match_device(ctx):
+    """Pinned (registered) host columns: the size column is read in place by the compaction (zero-
+    copy, HtoD rows only) instead of being copied — the per-iteration HtoD bytes must not change."""
+    recs, _ = synth.generate_config("C1", noise_frac=0.05, shuffle_window=64, seed=9)
+    d = ctx.upload(recs)
+    cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off, recs.name_bytes]
+    for a in cols:
+        ctx.register_host(a)
+    try:
+        a = ctx.analyze_raw(recs, [100])
+        b = ctx.analyze_raw(d, [100])
+    finally:
+        for x in cols:
+            ctx.unregister_host(x)
+        d.free()
+    assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
+    assert a["loops"][0]["rows"][:, 7].sum() > 0  # HtoD bytes present: the in-place sizes were read
+
+
 @pytest.mark.parametrize("chunk", [None, "4096", "200000"])
 def test_streamed_host_names_match_copied_names(ctx, chunk, monkeypatch):
     """ITT_MEM_HOST_STREAM_NAMES / ITT_MEM_DEVICE_HOST_NAMES: names streamed through bounded
