@@ -311,7 +311,10 @@ def bench_batch(args, world, rank, local, workload):
             if world > 1:
                 torch.distributed.all_reduce(ms_h, op=torch.distributed.ReduceOp.MAX)
             ms_h = float(ms_h.item())
-            h2d = sum(host_traces[i].nbytes() for i in range(lo, hi))
+            # pinned size columns are read in place (HtoD rows only, zero-copy), not copied whole
+            pinned_ids = {id(a) for a in registered}
+            h2d = sum(host_traces[i].nbytes() - (host_traces[i].size_bytes.nbytes if id(host_traces[i].size_bytes) in pinned_ids
+                                                 else 0) for i in range(lo, hi))
             d2h = sum(sum(L["iterations"] * 88 for L in r["loops"]) for r in res_h)  # itt_iter_row: 11 x i64
             ok = ok and all(r["loops"][0]["pattern_length"] == 200 for r in res_h)
             e2e = {"value": total_events / (ms_h / args.steps / 1000.0), "unit": "events/s",
