@@ -326,6 +326,51 @@ inline void launch(Ctx* c, const char* name, double bytes, void (*k)(KArgs...), 
   k<<<grid, block, smem, c->stream>>>(static_cast<KArgs>(args)...);
 }
 
+// Several small memsets in ONE launch (each cudaMemsetAsync is a GPU operation of its own; small
+// traces are bound by the number of operations, not bytes).  Jobs need 4-byte aligned, 4-byte
+// multiple ranges (pool / arena buffers are); anything else goes through cudaMemsetAsync.
+struct FillJob {
+  void* p;
+  uint64_t words;   // 4-byte words
+  uint32_t value;   // byte value replicated into the word
+};
+constexpr int kMaxFillJobs = 12;
+struct FillBatch {
+  FillJob j[kMaxFillJobs];
+  int n;
+};
+static __global__ void k_fill_many(FillBatch b) {
+  const FillJob& f = b.j[blockIdx.y];
+  uint32_t* w = static_cast<uint32_t*>(f.p);
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < f.words;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    w[i] = f.value;
+}
+struct Fills {
+  Ctx* c;
+  FillBatch b{};
+  uint64_t max_words = 0;
+  explicit Fills(Ctx* ctx) : c(ctx) {}
+  void add(void* p, size_t bytes, int value) {
+    if (!bytes) return;
+    if ((reinterpret_cast<uintptr_t>(p) & 3) || (bytes & 3) || b.n == kMaxFillJobs) {
+      ITT_CUDA(cudaMemsetAsync(p, value, bytes, c->stream));
+      return;
+    }
+    const uint32_t v = static_cast<uint8_t>(value) * 0x01010101u;
+    b.j[b.n++] = FillJob{p, bytes / 4, v};
+    max_words = std::max<uint64_t>(max_words, bytes / 4);
+  }
+  void flush();
+};
+inline void Fills::flush() {
+  if (!b.n) return;
+  const unsigned gx = static_cast<unsigned>(std::min<uint64_t>(64, (max_words + 255) / 256));
+  launch(c, "fill_many", static_cast<double>(max_words) * 4.0, k_fill_many, dim3(std::max(1u, gx), b.n), dim3(256), 0, b);
+  b.n = 0;
+  max_words = 0;
+}
+
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered allocations from the device's default pool (release threshold raised
 // at context creation so memory is recycled across calls instead of returned to the OS).

@@ -973,7 +973,8 @@ __global__ void k_pack_streams(const StreamEntry* __restrict__ table, const uint
   for (uint32_t u = threadIdx.x; u < ns; u += blockDim.x) out[1 + u] = table[list[1 + u]];
 }
 
-__global__ void k_init_stream_table(StreamEntry* t) {
+__global__ void k_init_stream_table(StreamEntry* t, uint32_t* list, uint32_t list_n) {  // + zeroes the list
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < list_n; i += gridDim.x * blockDim.x) list[i] = 0;
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < kStreamTableCap) {
     t[i].key = 0;
@@ -1552,10 +1553,7 @@ void build_dictionary(TraceState& t) {
   DBuf<uint32_t> counters(c, 4);  // used count, overflow, collision, streamed-name arena overflow
   DBuf<unsigned long long> dev_counts;
   DBuf<uint32_t> dev_max(c, 1);
-  if (t.rec.device) {
-    dev_counts.alloc(c, 65536);
-    dev_counts.zero();
-  }
+  if (t.rec.device) dev_counts.alloc(c, 65536);
   uint32_t bits = 14;
   uint64_t seed = 0x243F6A8885A308D3ull;
   // test hook: the first attempt puts every name into one slot, so the byte compare must catch the
@@ -1628,13 +1626,15 @@ void build_dictionary(TraceState& t) {
     tready.alloc(c, cap);
     const uint64_t copies_cap = std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1ull << 20, static_cast<uint64_t>(cap) * 256));
     if (copies.n < copies_cap) copies.alloc(c, copies_cap);
-    t.tkey.zero();
-    tready.zero();
-    copies_top.zero();
-    t.trep.fill_bytes(0xFF);
-    counters.zero();
-    dev_max.zero();
-    if (t.rec.device) dev_counts.zero();
+    Fills fz(c);  // one launch for the table's and counters' initial values
+    fz.add(t.tkey.p, cap * 8, 0);
+    fz.add(tready.p, cap * 8, 0);
+    fz.add(copies_top.p, 8, 0);
+    fz.add(t.trep.p, cap * 4, 0xFF);
+    fz.add(counters.p, 16, 0);
+    fz.add(dev_max.p, 4, 0);
+    if (t.rec.device) fz.add(dev_counts.p, 65536 * 8, 0);
+    fz.flush();
     if (!streamed) {
       HashArgs ha{t.rec.name_off, t.rec.name_bytes, 0,         total,        0,          n,         nullptr,
                   nullptr,        t.rec.device,     t.tkey.p,  tready.p,     copies.p,   copies.n,  copies_top.p,
@@ -1745,8 +1745,8 @@ void stream_census(TraceState& t) {
   const uint64_t n = t.rec.n;
   DBuf<StreamEntry> table(c, kStreamTableCap);
   DBuf<uint32_t> list(c, kStreamTableCap + 1);
-  list.zero();
-  launch(c, "census_init", 0.0, k_init_stream_table, dim3(kStreamTableCap / 256), dim3(256), 0, table.p);
+  launch(c, "census_init", 0.0, k_init_stream_table, dim3(kStreamTableCap / 256), dim3(256), 0, table.p, list.p,
+         kStreamTableCap + 1);
   CensusArgs ca{n, t.rec.stream, t.rec.device, t.filtering ? 1 : 0, t.majority, t.kind.p, t.rec.start, t.rec.dur,
                 table.p, list.p + 1, list.p};
   if (n) {
@@ -1792,7 +1792,8 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
   Ctx* c = t.c;
   const uint64_t n = t.rec.n;
   t.tfirst.alloc(c, t.tkey.n);
-  t.tfirst.fill_bytes(0xFF);
+  Fills fz(c);  // first-appearance sentinels and the HtoD end range's initial (min, max) in one launch
+  fz.add(t.tfirst.p, t.tfirst.n * 4, 0xFF);
   // capacities: count first (cheap readback of the census would do, but the scan itself is exact)
   uint64_t n_main = 0, n_htod = 0;
   for (const auto& s : t.streams) {
@@ -1809,8 +1810,9 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
   t.htod_end.alloc(c, n_htod + 1);
   t.htod_size.alloc(c, n_htod + 1);
   t.htod_range.alloc(c, 2);
-  ITT_CUDA(cudaMemsetAsync(t.htod_range.p, 0xFF, 8, c->stream));
-  ITT_CUDA(cudaMemsetAsync(t.htod_range.p + 1, 0, 8, c->stream));
+  fz.add(t.htod_range.p, 8, 0xFF);
+  fz.add(t.htod_range.p + 1, 8, 0);
+  fz.flush();
   DBuf<uint64_t> tot(c, 1);
   CompactF f{n,
              t.sorted ? nullptr : t.perm.p,

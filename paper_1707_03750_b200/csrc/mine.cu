@@ -515,8 +515,10 @@ MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, con
   // the tie-break kernels run whether or not a candidate exists (no candidate key equals the
   // empty key), so the whole result comes back in one round trip
   DBuf<unsigned int> start(c, 2);
-  start.fill_bytes(0xFF);
-  ITT_CUDA(cudaMemsetAsync(start.p + 1, 0, 4, c->stream));
+  Fills fz(c);  // (min SA = none, wide count = 0) in one launch
+  fz.add(start.p, 4, 0xFF);
+  fz.add(start.p + 1, 4, 0);
+  fz.flush();
   const size_t wide_cap = s.np / (kTiedSerial + 1) + 2;  // disjoint intervals wider than kTiedSerial
   DBuf<uint32_t> wide(c, 2 * wide_cap);
   if (iv.list.p)
