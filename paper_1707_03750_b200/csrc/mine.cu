@@ -28,27 +28,6 @@ constexpr int kTileA = 1024;
 constexpr int kLogTileA = 10;
 constexpr int kAnsvBlock = 256;
 
-// per tile: the minimum of every 32-position block (bmin) and of the tile (tmin) — what the rare
-// cross-tile searches of k_ansv need, at 1/8 of the bytes prefix and suffix minima per position
-// would take
-__global__ void __launch_bounds__(kTileA) k_tile_minima(const uint32_t* __restrict__ lcp, uint64_t np,
-                                                        uint32_t* __restrict__ bmin, uint32_t* __restrict__ tmin) {
-  __shared__ uint32_t sw[32];
-  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * kTileA + threadIdx.x;
-  uint32_t v = j < np ? __ldcs(&lcp[j]) : 0xFFFFFFFFu;
-  v = __reduce_min_sync(0xffffffffu, v);
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    bmin[static_cast<uint64_t>(blockIdx.x) * 32 + warp] = v;
-    sw[warp] = v;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t t = __reduce_min_sync(0xffffffffu, sw[lane]);
-    if (lane == 0) tmin[blockIdx.x] = t;
-  }
-}
-
 // sparse table over tile minima: st[l * nt + t] = min(tmin[t, t + 2^l))
 __global__ void k_sparse_level(uint32_t* st, uint32_t nt, int l) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -130,28 +109,53 @@ __device__ __forceinline__ uint64_t first_lt_in_tile(const AnsvArgs& a, uint32_t
 }
 
 // Most positions are decided by their neighbours alone: LCP[k-1] == l (k is not leftmost),
-// or LCP[k-1] < l (the PSE is k-1) with LCP[k+1] < l (the NSV is k+1).  Only the rest search —
-// and the tile builds its shared-memory sparse table only when one of its positions needs it
-// (periodic traces: runs of equal capped LCPs, a few searches per suffix group).
-__global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
-  __shared__ uint32_t st[kLogTileA][kTileA];  // st[l][x] = min(LCP[x, x + 2^l)) within the tile
+// or LCP[k-1] < l (the PSE is k-1) with LCP[k+1] < l (the NSV is k+1).  Pass 1 (every tile; 4 KiB
+// of shared memory, so many tiles overlap their loads) loads the tile with 16-byte loads, writes
+// its 32-position block minima and its minimum (what the cross-tile searches need; no separate
+// minima pass over the LCP array) and emits every decided position; a tile with undecided ones
+// goes on a list.  Pass 2 runs over the listed tiles only, after the tile sparse table exists.
+__global__ void __launch_bounds__(kAnsvBlock) k_ansv_fast(AnsvArgs a, uint32_t* __restrict__ bmin, uint32_t* __restrict__ tmin,
+                                                          uint32_t* __restrict__ search_tiles, unsigned int* __restrict__ n_search) {
+  __shared__ __align__(16) uint32_t st0[kTileA];
+  __shared__ uint32_t s_w[kAnsvBlock / 32];
   const uint32_t t = blockIdx.x;
   const uint64_t base = static_cast<uint64_t>(t) * kTileA;
   const uint32_t len = static_cast<uint32_t>(umin64(kTileA, a.np - base));
-  for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock) st[0][x] = x < len ? a.lcp[base + x] : 0xFFFFFFFFu;
+  const uint32_t x0 = threadIdx.x * 4;  // 4 consecutive positions per thread
+  uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
+  if (x0 + 4 <= len) {
+    v = __ldcs(reinterpret_cast<const uint4*>(a.lcp + base + x0));
+  } else {
+    if (x0 < len) v.x = a.lcp[base + x0];
+    if (x0 + 1 < len) v.y = a.lcp[base + x0 + 1];
+    if (x0 + 2 < len) v.z = a.lcp[base + x0 + 2];
+  }
+  *reinterpret_cast<uint4*>(&st0[x0]) = v;
+  uint32_t m = min(min(v.x, v.y), min(v.z, v.w));  // 32-position block minima: 8 threads each
+  m = min(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = min(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = min(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  if ((threadIdx.x & 7) == 0) bmin[static_cast<uint64_t>(t) * 32 + (threadIdx.x >> 3)] = m;
+  const uint32_t wm = __reduce_min_sync(0xffffffffu, m);
+  if (lane_id() == 0) s_w[threadIdx.x >> 5] = wm;
   __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tm = s_w[0];
+    for (int w = 1; w < kAnsvBlock / 32; ++w) tm = min(tm, s_w[w]);
+    tmin[t] = tm;
+  }
   bool any_search = false;
   for (uint32_t x = threadIdx.x; x < len; x += kAnsvBlock) {
     const uint64_t k = base + x;
-    const uint32_t l = st[0][x];
+    const uint32_t l = st0[x];
     uint32_t cnt = 0, par = 0, lbv = 0;
     bool search = false;
     if (k > 0 && l > 0) {
-      const uint32_t lp = x > 0 ? st[0][x - 1] : a.lcp[k - 1];
+      const uint32_t lp = x > 0 ? st0[x - 1] : a.lcp[k - 1];
       if (lp > l) {
         search = true;
       } else if (lp < l) {  // leftmost, PSE = k - 1
-        const uint32_t ln = k + 1 >= a.np ? 0u : (x + 1 < len ? st[0][x + 1] : a.lcp[k + 1]);
+        const uint32_t ln = k + 1 >= a.np ? 0u : (x + 1 < len ? st0[x + 1] : a.lcp[k + 1]);
         if (ln < l) {
           cnt = 2;  // [k - 1, k + 1)
           par = max(lp, ln);
@@ -164,79 +168,93 @@ __global__ void __launch_bounds__(kAnsvBlock) k_ansv(AnsvArgs a) {
     any_search |= search;
     if (!search) a.emit(k, l, cnt, par, lbv);
   }
-  if (!__syncthreads_or(any_search)) return;
+  if (__syncthreads_or(any_search) && threadIdx.x == 0) search_tiles[atomicAdd(n_search, 1u)] = t;
+}
+
+__global__ void __launch_bounds__(kAnsvBlock) k_ansv_search(AnsvArgs a, const uint32_t* __restrict__ search_tiles,
+                                                            const unsigned int* __restrict__ n_search) {
+  __shared__ uint32_t st[kLogTileA][kTileA];  // st[l][x] = min(LCP[x, x + 2^l)) within the tile
+  const uint32_t ns = *n_search;
+  for (uint32_t qt = blockIdx.x; qt < ns; qt += gridDim.x) {
+  const uint32_t t = search_tiles[qt];
+  const uint64_t base = static_cast<uint64_t>(t) * kTileA;
+  const uint32_t len = static_cast<uint32_t>(umin64(kTileA, a.np - base));
+  __syncthreads();  // the previous tile's table is consumed
+  for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock) st[0][x] = x < len ? a.lcp[base + x] : 0xFFFFFFFFu;
+  __syncthreads();
   for (int l = 1; l < kLogTileA; ++l) {
     const uint32_t half = 1u << (l - 1);
     for (uint32_t x = threadIdx.x; x < kTileA; x += kAnsvBlock)
       st[l][x] = x + half < kTileA ? min(st[l - 1][x], st[l - 1][x + half]) : st[l - 1][x];
     __syncthreads();
   }
-  for (uint32_t x = threadIdx.x; x < len; x += kAnsvBlock) {
-    const uint64_t k = base + x;
-    const uint32_t l = st[0][x];
-    if (k == 0 || l == 0) continue;
-    {  // the positions the first pass decided
-      const uint32_t lp = x > 0 ? st[0][x - 1] : a.lcp[k - 1];
-      if (lp == l) continue;
-      if (lp < l) {
-        const uint32_t ln = k + 1 >= a.np ? 0u : (x + 1 < len ? st[0][x + 1] : a.lcp[k + 1]);
-        if (ln < l) continue;
-      }
-    }
-    uint32_t cnt = 0, par = 0, lbv = 0;
-    {
-      // ---- previous j < k with LCP[j] <= l
-      uint32_t pos = x;
-#pragma unroll
-      for (int lv = kLogTileA - 1; lv >= 0; --lv) {
-        const uint32_t w = 1u << lv;
-        if (pos >= w && st[lv][pos - w] > l) pos -= w;
-      }
-      uint64_t pse;
-      if (pos > 0) {
-        pse = base + pos - 1;
-      } else {  // cross-tile: last tile before t whose min <= l (tile 0 holds LCP[0] = 0)
-        uint32_t tp = t;
-        for (int lv = a.tlevels - 1; lv >= 0; --lv) {
-          const uint32_t w = 1u << lv;
-          if (tp >= w && a.tst[static_cast<uint64_t>(lv) * a.nt + tp - w] > l) tp -= w;
+    for (uint32_t x = threadIdx.x; x < len; x += kAnsvBlock) {
+      const uint64_t k = base + x;
+      const uint32_t l = st[0][x];
+      if (k == 0 || l == 0) continue;
+      {  // the positions the first pass decided
+        const uint32_t lp = x > 0 ? st[0][x - 1] : a.lcp[k - 1];
+        if (lp == l) continue;
+        if (lp < l) {
+          const uint32_t ln = k + 1 >= a.np ? 0u : (x + 1 < len ? st[0][x + 1] : a.lcp[k + 1]);
+          if (ln < l) continue;
         }
-        pse = last_le_in_tile(a, tp - 1, l);
       }
-      const uint32_t lp = pse - base < kTileA && pse >= base ? st[0][pse - base] : a.lcp[pse];
-      if (lp < l) {  // k is the leftmost position of its interval
-        // ---- next j > k with LCP[j] < l
-        uint32_t q = x + 1;
-#pragma unroll
+      uint32_t cnt = 0, par = 0, lbv = 0;
+      {
+        // ---- previous j < k with LCP[j] <= l
+        uint32_t pos = x;
+  #pragma unroll
         for (int lv = kLogTileA - 1; lv >= 0; --lv) {
           const uint32_t w = 1u << lv;
-          if (q + w <= len && st[lv][q] >= l) q += w;
+          if (pos >= w && st[lv][pos - w] > l) pos -= w;
         }
-        uint64_t nsv;
-        uint32_t ln = 0;
-        if (q < len) {
-          nsv = base + q;
-          ln = st[0][q];
-        } else {
-          uint32_t tn = t + 1;
+        uint64_t pse;
+        if (pos > 0) {
+          pse = base + pos - 1;
+        } else {  // cross-tile: last tile before t whose min <= l (tile 0 holds LCP[0] = 0)
+          uint32_t tp = t;
           for (int lv = a.tlevels - 1; lv >= 0; --lv) {
             const uint32_t w = 1u << lv;
-            if (tn + w <= a.nt && a.tst[static_cast<uint64_t>(lv) * a.nt + tn] >= l) tn += w;
+            if (tp >= w && a.tst[static_cast<uint64_t>(lv) * a.nt + tp - w] > l) tp -= w;
           }
-          if (tn < a.nt) {
-            nsv = first_lt_in_tile(a, tn, l);
-            ln = a.lcp[nsv];
-          } else {
-            nsv = a.np;
-            ln = 0;
-          }
+          pse = last_le_in_tile(a, tp - 1, l);
         }
-        cnt = static_cast<uint32_t>(nsv - pse);
-        par = max(lp, ln);
-        lbv = static_cast<uint32_t>(pse);
+        const uint32_t lp = pse - base < kTileA && pse >= base ? st[0][pse - base] : a.lcp[pse];
+        if (lp < l) {  // k is the leftmost position of its interval
+          // ---- next j > k with LCP[j] < l
+          uint32_t q = x + 1;
+  #pragma unroll
+          for (int lv = kLogTileA - 1; lv >= 0; --lv) {
+            const uint32_t w = 1u << lv;
+            if (q + w <= len && st[lv][q] >= l) q += w;
+          }
+          uint64_t nsv;
+          uint32_t ln = 0;
+          if (q < len) {
+            nsv = base + q;
+            ln = st[0][q];
+          } else {
+            uint32_t tn = t + 1;
+            for (int lv = a.tlevels - 1; lv >= 0; --lv) {
+              const uint32_t w = 1u << lv;
+              if (tn + w <= a.nt && a.tst[static_cast<uint64_t>(lv) * a.nt + tn] >= l) tn += w;
+            }
+            if (tn < a.nt) {
+              nsv = first_lt_in_tile(a, tn, l);
+              ln = a.lcp[nsv];
+            } else {
+              nsv = a.np;
+              ln = 0;
+            }
+          }
+          cnt = static_cast<uint32_t>(nsv - pse);
+          par = max(lp, ln);
+          lbv = static_cast<uint32_t>(pse);
+        }
       }
+      a.emit(k, l, cnt, par, lbv);
     }
-    a.emit(k, l, cnt, par, lbv);
   }
 }
 
@@ -438,7 +456,27 @@ void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv, uint32_t lis
   int tlevels = 1;
   while ((1u << tlevels) <= nt) ++tlevels;
   DBuf<uint32_t> tst(c, static_cast<size_t>(tlevels) * nt);
-  launch(c, "ansv_tile_minima", np * 4.0 + nt * 132.0, k_tile_minima, dim3(nt), dim3(kTileA), 0, s.lcp.p, np, bmin.p, tst.p);
+  DBuf<uint32_t> stiles(c, nt);
+  DBuf<unsigned int> nsearch(c, 1);
+  AnsvArgs a{s.lcp.p, bmin.p, tst.p, nt, tlevels, np, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  Fills fz(c);
+  fz.add(nsearch.p, 4, 0);
+  if (list_max_len) {  // mining: the candidate intervals only (no host sync: the kernels read the count)
+    iv.list.alloc(c, np);
+    iv.n_list.alloc(c, 1);
+    fz.add(iv.n_list.p, 4, 0);
+    a.list = iv.list.p;
+    a.n_list = iv.n_list.p;
+    a.max_len = list_max_len;
+  } else {
+    iv.cnt.alloc(c, np);
+    iv.par.alloc(c, np);
+    iv.lb.alloc(c, np);
+    a.cnt = iv.cnt.p, a.par = iv.par.p, a.lb = iv.lb.p;
+  }
+  fz.flush();
+  launch(c, "ansv_intervals", np * (list_max_len ? 4.0 : 16.0) + nt * 132.0, k_ansv_fast, dim3(nt), dim3(kAnsvBlock), 0, a,
+         bmin.p, tst.p, stiles.p, nsearch.p);
   if (nt <= 65536) {
     if (tlevels > 1)
       launch(c, "ansv_sparse", nt * 12.0 * (tlevels - 1), k_sparse_all, dim3(1), dim3(1024), 0, tst.p, nt, tlevels);
@@ -446,22 +484,8 @@ void lcp_intervals(Ctx* c, const SuffixState& s, IntervalState& iv, uint32_t lis
     for (int l = 1; l < tlevels; ++l)
       launch(c, "ansv_sparse", nt * 12.0, k_sparse_level, dim3(grid_for(nt, 256)), dim3(256), 0, tst.p, nt, l);
   }
-  AnsvArgs a{s.lcp.p, bmin.p, tst.p, nt, tlevels, np, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
-  if (list_max_len) {  // mining: the candidate intervals only (no host sync: the kernels read the count)
-    iv.list.alloc(c, np);
-    iv.n_list.alloc(c, 1);
-    iv.n_list.zero();
-    a.list = iv.list.p;
-    a.n_list = iv.n_list.p;
-    a.max_len = list_max_len;
-    launch(c, "ansv_intervals", np * 4.0, k_ansv, dim3(nt), dim3(kAnsvBlock), 0, a);
-    return;
-  }
-  iv.cnt.alloc(c, np);
-  iv.par.alloc(c, np);
-  iv.lb.alloc(c, np);
-  a.cnt = iv.cnt.p, a.par = iv.par.p, a.lb = iv.lb.p;
-  launch(c, "ansv_intervals", np * 16.0, k_ansv, dim3(nt), dim3(kAnsvBlock), 0, a);
+  launch(c, "ansv_search", 0.0, k_ansv_search, dim3(std::min<uint32_t>(nt, c->sm_count * 5)), dim3(kAnsvBlock), 0, a,
+         stiles.p, nsearch.p);
 }
 
 MinedPattern mine_one(Ctx* c, const SuffixState& s, const IntervalState& iv, const itt_mining_cfg& cfg,
