@@ -1355,10 +1355,20 @@ __global__ void k_first_pairs(const uint32_t* __restrict__ used, uint32_t n_used
   }
 }
 
+// 4 tokens per thread (16-byte loads and stores; both arrays come from the pool, 16-byte aligned)
 __global__ void k_map_tokens(const uint32_t* __restrict__ tok_slot, uint64_t n, const uint32_t* __restrict__ id_of_slot,
                              int32_t* __restrict__ tokens) {
-  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j < n) tokens[j] = static_cast<int32_t>(id_of_slot[tok_slot[j]]);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 4;
+  for (uint64_t j = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; j < n; j += stride) {
+    if (j + 4 <= n) {
+      const uint4 sl = __ldcs(reinterpret_cast<const uint4*>(tok_slot + j));
+      __stcs(reinterpret_cast<int4*>(tokens + j),
+             make_int4(static_cast<int32_t>(__ldg(&id_of_slot[sl.x])), static_cast<int32_t>(__ldg(&id_of_slot[sl.y])),
+                       static_cast<int32_t>(__ldg(&id_of_slot[sl.z])), static_cast<int32_t>(__ldg(&id_of_slot[sl.w]))));
+    } else {
+      for (uint64_t q = j; q < n; ++q) tokens[q] = static_cast<int32_t>(id_of_slot[tok_slot[q]]);
+    }
+  }
 }
 
 __global__ void k_name_rows(const uint32_t* __restrict__ used, uint32_t n_used, const uint32_t* __restrict__ id_of_slot,
@@ -1893,7 +1903,8 @@ void renumber_tokens(TraceState& t) {
     t.n_names = m;
   }
   if (t.n_tok)
-    launch(c, "intern_map", t.n_tok * 8.0, k_map_tokens, dim3(grid_for(t.n_tok, 256)), dim3(256), 0, t.tok_slot.p, t.n_tok,
+    launch(c, "intern_map", t.n_tok * 8.0, k_map_tokens, dim3(grid_for((t.n_tok + 3) / 4, 256, c->sm_count * 16)), dim3(256), 0,
+           t.tok_slot.p, t.n_tok,
            id_of_slot.p, t.tokens.p);
   DBuf<uint64_t> rows(c, t.n_names + 1);
   launch(c, "intern_names", nu * 8.0, k_name_rows, dim3(grid_for(nu, 256)), dim3(256), 0, t.used.p, nu, id_of_slot.p,

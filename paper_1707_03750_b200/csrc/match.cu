@@ -44,11 +44,25 @@ __global__ void k_anchor_eval(const int32_t* __restrict__ tok, uint64_t n, const
       break;
     }
     if (pos >= n) break;  // ran off the sequence before completing (match.hpp:61-64)
-    const uint64_t cnt = umin64(32, umin64(m - j, n - pos));
-    const bool eq = lane < cnt && __ldg(&tok[pos + lane]) == __ldg(&pat[j + lane]);
-    const unsigned mask = __ballot_sync(0xffffffffu, eq);
-    uint64_t f = static_cast<uint64_t>(__ffs(~mask) - 1);  // leading matches
-    if (mask == 0xffffffffu) f = 32;
+    // 128 symbols per step (four 32-symbol ballots, all loads in flight together): the walk over a
+    // matching iteration advances 128 at a time instead of 32
+    const uint64_t cnt = umin64(128, umin64(m - j, n - pos));
+    unsigned mk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t q = lane + 32u * u;
+      mk[u] = __ballot_sync(0xffffffffu, q < cnt && __ldg(&tok[pos + q]) == __ldg(&pat[j + q]));
+    }
+    uint64_t f = 0;  // leading matches
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (mk[u] == 0xffffffffu) {
+        f += 32;
+        continue;
+      }
+      f += static_cast<uint64_t>(__ffs(~mk[u]) - 1);
+      break;
+    }
     if (f > cnt) f = cnt;
     if (f > 0) {
       pos += f;
