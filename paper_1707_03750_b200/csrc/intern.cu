@@ -823,10 +823,10 @@ __global__ void k_kinds_minrow(const uint32_t* __restrict__ slot, const uint8_t*
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   // the caller's flags column may sit at any byte address: quads only when it is 4-byte aligned
   const uint64_t quads = (reinterpret_cast<uintptr_t>(rflags) & 3u) ? 0 : n / 4;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < quads; q += stride) {
+  // two quads per iteration (q, q + stride): both streaming loads are in flight before the
+  // dependent table lookups
+  const auto one = [&](uint64_t q, uint4 sl, uint32_t fl) {
     const uint64_t i = q * 4;
-    const uint4 sl = __ldcs(reinterpret_cast<const uint4*>(slot) + q);
-    const uint32_t fl = __ldcs(reinterpret_cast<const uint32_t*>(rflags) + q);
     const uint32_t s4[4] = {sl.x, sl.y, sl.z, sl.w};
     uint32_t kd = 0;
 #pragma unroll
@@ -836,7 +836,17 @@ __global__ void k_kinds_minrow(const uint32_t* __restrict__ slot, const uint8_t*
       if (__ldca(&trep[s]) > i + u) atomicMin(&trep[s], static_cast<uint32_t>(i + u));
     }
     reinterpret_cast<uint32_t*>(kind)[q] = kd;
+  };
+  uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; q + stride < quads; q += 2 * stride) {
+    const uint4 sa = __ldcs(reinterpret_cast<const uint4*>(slot) + q);
+    const uint4 sb = __ldcs(reinterpret_cast<const uint4*>(slot) + q + stride);
+    const uint32_t fa = __ldcs(reinterpret_cast<const uint32_t*>(rflags) + q);
+    const uint32_t fb = __ldcs(reinterpret_cast<const uint32_t*>(rflags) + q + stride);
+    one(q, sa, fa);
+    one(q + stride, sb, fb);
   }
+  if (q < quads) one(q, __ldcs(reinterpret_cast<const uint4*>(slot) + q), __ldcs(reinterpret_cast<const uint32_t*>(rflags) + q));
   for (uint64_t i = quads * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t s = slot[i];
     kind[i] = static_cast<uint8_t>(kind_from(__ldg(&tflags[s]), (rflags[i] & ITT_REC_HAS_THROUGHPUT) != 0));

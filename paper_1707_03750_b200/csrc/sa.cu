@@ -613,14 +613,27 @@ __global__ void k_plcp(LiftArgs L, const uint32_t* __restrict__ phi, uint32_t* _
 // class): a suffix in its predecessor's final group shares >= h_final >= cap symbols, so its capped
 // LCP is cap; a group head's comes from lifting over the kept levels (< h_final).  One thread per
 // word of the head bitmap; replaces phi + capped Kasai + gather (three passes with random access).
-__global__ void k_lcp_heads(LiftArgs L, const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads, uint32_t cap,
-                            uint32_t* __restrict__ lcp) {
-  const uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_lcp_heads(LiftArgs L, const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads,
+                                                   uint32_t cap, uint32_t* __restrict__ lcp) {
+  // a warp takes 32 consecutive bitmap words (1024 positions): runs without heads are written by the
+  // whole warp in coalesced 512-byte rows; words with heads are finished by their own lane
+  const unsigned lane = lane_id();
+  const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+  const uint64_t wbase = (w - lane) * 32;  // the warp's first position
+  if (wbase >= L.np) return;
   const uint64_t base = w * 32;
-  if (base >= L.np) return;
-  const uint32_t hb = __ldg(&heads[w]);
-  const int cnt = static_cast<int>(umin64(32, L.np - base));
-  if (cnt == 32 && hb == 0 && base > 0) {
+  uint32_t hb = base < L.np ? __ldg(&heads[w]) : 0u;
+  const int cnt = base < L.np ? static_cast<int>(umin64(32, L.np - base)) : 0;
+  if (cnt < 32 && cnt > 0) hb &= (1u << cnt) - 1u;
+  const bool plain = cnt == 32 && hb == 0 && base > 0;  // all 32 positions: LCP = cap
+  const unsigned pm = __ballot_sync(0xffffffffu, plain);
+  if (pm == 0xffffffffu) {  // the whole warp's 1024 positions are plain: coalesced stores
+    const uint4 c4 = make_uint4(cap, cap, cap, cap);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) __stcs(reinterpret_cast<uint4*>(lcp + wbase) + i * 32 + lane, c4);
+    return;
+  }
+  if (plain) {
     const uint4 c4 = make_uint4(cap, cap, cap, cap);
 #pragma unroll
     for (int q = 0; q < 32; q += 4) __stcs(reinterpret_cast<uint4*>(lcp + base + q), c4);
