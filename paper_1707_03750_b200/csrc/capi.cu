@@ -82,12 +82,12 @@ void check_records(const itt_records* r) {
 }
 
 // records -> dictionary -> census (optionally device-filtered)
-void prepare(Ctx* c, TraceState& t, const itt_records* r, bool device_filter) {
+void prepare(Ctx* c, TraceState& t, const itt_records* r, bool device_filter, bool allow_late_dur = false) {
   check_records(r);
   t.c = c;
   {
     StageTimer st(c, "upload");
-    upload_records(c, r, t.rec);
+    upload_records(c, r, t.rec, allow_late_dur);
   }
   {
     StageTimer st(c, "order");
@@ -826,7 +826,7 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       fail(ITT_E_INVALID_CONFIG, "analyze: at least one iteration count is required");
     if (!recs || recs->n == 0) fail(ITT_E_EMPTY_TRACE, "stream-classify: trace has no records");
     TraceState t;
-    prepare(c, t, recs, true);
+    prepare(c, t, recs, true, /*allow_late_dur=*/true);
     // main stream: override or selection (pipeline.hpp:56-73)
     uint32_t main_stream = 0, n_main_streams = 0;
     int32_t override_non_main = 0;
@@ -849,8 +849,10 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       if (t.n_tok == 0)
         fail(ITT_E_EMPTY_MAIN_STREAM, "stream-classify: stream " + std::to_string(main_stream) + " has no records");
       renumber_tokens(t);
-      overlaps = count_overlaps(t);
-      release_rows(t);  // row-level arrays are dead from here: HBM for the suffix array
+      if (!t.rec.dur_host) {
+        overlaps = count_overlaps(t);
+        release_rows(t);  // row-level arrays are dead from here: HBM for the suffix array
+      }  // else the duration column is still crossing PCIe: ends after the suffix array and mining
     }
     // mining over one shared SA / LCP / interval set (pipeline.hpp:81-91)
     std::vector<itt_mining_cfg> cfgs;
@@ -893,6 +895,12 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       StageTimer st(c, "mine");
       lcp_intervals(c, s, iv, mining_cap(t.n_tok, cfgs) - 1);  // list mode: the candidate intervals only
       pats = mine_loops(c, s, iv, cfgs, multi);
+    }
+    if (t.rec.dur_host) {  // late durations: stream ends, token / HtoD ends, then the row arrays go
+      StageTimer st(c, "late-ends");
+      finish_late_durations(t);
+      overlaps = count_overlaps(t);
+      release_rows(t);
     }
     for (const auto& p : pats)
       if (p.status) fail(p.status, p.error);

@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(256) k_stream_census(CensusArgs a) {
     if (valid) {
       const int kd = a.kind[i];
       const int64_t s0 = a.start[i];
-      const int64_t e0 = s0 + a.dur[i];
+      const int64_t e0 = a.dur ? s0 + a.dur[i] : s0;  // no durations yet (late): ends come later
       if (bs == kNone) {  // block table overflow: update the global table directly
         const uint32_t gs = global_stream_slot(a.table, a.list, a.count, key);
         if (gs != kNone) {
@@ -1019,6 +1019,7 @@ struct CompactF {
   int64_t* htod_end;
   int64_t* htod_size;
   unsigned long long* htod_range;
+  int ends_only;  // late durations: only tok_end / htod_end and the HtoD end range (the rest is written)
   __device__ __forceinline__ uint32_t row(uint64_t k) const { return perm ? perm[k] : static_cast<uint32_t>(k); }
   __device__ __forceinline__ uint64_t load(uint64_t k) const {
     const uint32_t i = row(k);
@@ -1139,9 +1140,9 @@ __global__ void __launch_bounds__(256) k_compact_write(CompactF f, const uint64_
     st[q] = du[q] = 0, sl[q] = 0;
     if ((sel.mm[q] | sel.hm[q]) >> lane & 1u) {
       st[q] = __ldcs(&f.start[k]);
-      du[q] = __ldcs(&f.dur[k]);
+      du[q] = f.dur ? __ldcs(&f.dur[k]) : 0;  // null: late durations (the ends pass writes tok_end)
     }
-    if (sel.mm[q] >> lane & 1u) sl[q] = __ldcs(&f.slot[k]);
+    if (!f.ends_only && (sel.mm[q] >> lane & 1u)) sl[q] = __ldcs(&f.slot[k]);
   }
   if (lane == 0) s_w[warp] = sel.packed();
   __syncthreads();
@@ -1152,26 +1153,30 @@ __global__ void __launch_bounds__(256) k_compact_write(CompactF f, const uint64_
   const unsigned lt = lanemask_lt();
   uint32_t tf[kRSItems];
 #pragma unroll
-  for (int q = 0; q < kRSItems; ++q) tf[q] = (sel.mm[q] >> lane & 1u) ? __ldcg(&f.tfirst[sl[q]]) : 0u;
+  for (int q = 0; q < kRSItems; ++q) tf[q] = (!f.ends_only && (sel.mm[q] >> lane & 1u)) ? __ldcg(&f.tfirst[sl[q]]) : 0u;
   unsigned long long emin = ~0ull, emax = 0;
 #pragma unroll
   for (int q = 0; q < kRSItems; ++q) {
     const int64_t en = st[q] + du[q];
     if (sel.mm[q] >> lane & 1u) {
       const uint32_t j = jm + __popc(sel.mm[q] & lt);
-      f.tok_slot[j] = sl[q];
-      f.tok_start[j] = st[q];
       f.tok_end[j] = en;
-      f.tok_kind[j] = sel.kd[q];
-      if (f.tok_record) f.tok_record[j] = wbase + q * 32 + lane;
-      if (tf[q] > j) atomicMin(&f.tfirst[sl[q]], j);
+      if (!f.ends_only) {
+        f.tok_slot[j] = sl[q];
+        f.tok_start[j] = st[q];
+        f.tok_kind[j] = sel.kd[q];
+        if (f.tok_record) f.tok_record[j] = wbase + q * 32 + lane;
+        if (tf[q] > j) atomicMin(&f.tfirst[sl[q]], j);
+      }
     }
     if (sel.hm[q] >> lane & 1u) {
       const uint64_t h = jh + __popc(sel.hm[q] & lt);
       const uint64_t i = wbase + q * 32 + lane;
-      f.htod_start[h] = st[q];
       f.htod_end[h] = en;
-      f.htod_size[h] = (f.rflags[i] & ITT_REC_HAS_SIZE) ? f.size[i] : 0;
+      if (!f.ends_only) {
+        f.htod_start[h] = st[q];
+        f.htod_size[h] = (f.rflags[i] & ITT_REC_HAS_SIZE) ? f.size[i] : 0;
+      }
       const unsigned long long fe = static_cast<unsigned long long>(en) ^ (1ull << 63);
       emin = fe < emin ? fe : emin;
       emax = fe > emax ? fe : emax;
@@ -1403,7 +1408,7 @@ __global__ void k_overlaps(const int64_t* __restrict__ ts, const int64_t* __rest
 }  // namespace
 
 // ------------------------------------------------------------------ host side
-void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
+void upload_records(Ctx* c, const itt_records* r, DevRecords& d, bool allow_late_dur) {
   d.n = r->n;
   d.order = r->order;
   const uint64_t n = r->n;
@@ -1429,7 +1434,9 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   // else); the other columns follow on the copy stream while the order stage runs, and the names
   // are streamed in 64 MiB chunks behind them, each hashed as soon as it lands — the PCIe transfer
   // overlaps the first stages instead of preceding them.
-  const bool overlap = r->mem == ITT_MEM_HOST && nb >= (256ull << 20);
+  uint64_t overlap_min = 256ull << 20;
+  if (const char* e = std::getenv("ITT_TEST_OVERLAP_MIN"); e && *e) overlap_min = std::strtoull(e, nullptr, 10);  // tests
+  const bool overlap = r->mem == ITT_MEM_HOST && nb >= overlap_min;
   if (overlap) {
     d.host_names = r->name_bytes;
     d.stream_chunk = 64ull << 20;
@@ -1441,6 +1448,16 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, r->size_bytes) == cudaSuccess) {
       if (pa.type == cudaMemoryTypeHost && pa.devicePointer) size_mapped = static_cast<const int64_t*>(pa.devicePointer);
+    } else {
+      cudaGetLastError();
+    }
+  }
+  // late durations: a pinned duration column of an analyze goes last over PCIe (after the names),
+  // overlapping the suffix array; only a census end and the token ends need it, later
+  if (overlap && allow_late_dur && n && n <= (1ull << 29)) {  // (larger traces free the rows before the SA)
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, r->duration_ns) == cudaSuccess) {
+      if (pa.type == cudaMemoryTypeHost) d.dur_host = r->duration_ns;
     } else {
       cudaGetLastError();
     }
@@ -1462,7 +1479,7 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
     ITT_CUDA(cudaStreamWaitEvent(cs, d.cols_ready, 0));
   }
   h2d_bulk(c, d.o_off.p, r->name_off, (n + 1) * 8, cs);
-  h2d_bulk(c, d.o_dur.p, r->duration_ns, n * 8, cs);
+  if (!d.dur_host) h2d_bulk(c, d.o_dur.p, r->duration_ns, n * 8, cs);
   if (!size_mapped) h2d_bulk(c, d.o_size.p, r->size_bytes, n * 8, cs);
   h2d_bulk(c, d.o_flags.p, r->flags, n, cs);
   h2d_bulk(c, d.o_stream.p, r->stream, n * 4, cs);
@@ -1477,6 +1494,51 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d) {
   d.name_off = d.o_off.p;
   d.name_bytes = (streamed || overlap) ? nullptr : d.o_names.p;
   d.device = r->device ? d.o_device.p : nullptr;
+}
+
+static std::vector<StreamEntry> census_pass(TraceState& t, const int64_t* dur);
+
+void issue_late_durations(TraceState& t) {
+  DevRecords& d = t.rec;
+  if (!d.dur_host || d.dur_ready) return;
+  Ctx* c = t.c;
+  cudaStream_t cp = c->copier();  // after the columns and names queued on it (the buffer is allocated)
+  ITT_CUDA(cudaEventCreateWithFlags(&d.dur_ready, cudaEventDisableTiming));
+  ITT_CUDA(cudaMemcpyAsync(d.o_dur.p, d.dur_host, d.n * 8, cudaMemcpyHostToDevice, cp));
+  ITT_CUDA(cudaEventRecord(d.dur_ready, cp));
+}
+
+void finish_late_durations(TraceState& t) {
+  DevRecords& d = t.rec;
+  if (!d.dur_host) return;
+  Ctx* c = t.c;
+  issue_late_durations(t);
+  ITT_CUDA(cudaStreamWaitEvent(c->stream, d.dur_ready, 0));
+  d.dur_host = nullptr;
+  const uint64_t n = d.n;
+  if (d.compact_ends_late) {  // the same selection and tile offsets; ends only
+    d.compact_ends_late = false;
+    Fills fz(c);
+    fz.add(t.htod_range.p, 8, 0xFF);
+    fz.add(t.htod_range.p + 1, 8, 0);
+    fz.flush();
+    CompactF f{n, nullptr, d.stream, d.device, t.filtering ? 1 : 0, t.majority, t.main_stream, t.kind.p, nullptr,
+               d.start, d.dur, d.size, d.flags, nullptr, nullptr, t.tok_end.p, nullptr, nullptr, nullptr,
+               nullptr, t.htod_end.p, nullptr, t.htod_range.p, 1};
+    const uint64_t tiles = (n + kRSTile - 1) / kRSTile;
+    launch(c, "compact_ends", n * (t.filtering ? 7.0 : 5.0) + t.n_tok * 24.0 + t.n_htod * 24.0, k_compact_write,
+           dim3(static_cast<unsigned>(tiles)), dim3(256), 0, f, t.compact_tiles.p);
+    t.compact_tiles.release();
+  }
+  if (d.census_ends_late) {  // a second census pass with durations: each stream's last end
+    d.census_ends_late = false;
+    const std::vector<StreamEntry> all = census_pass(t, d.dur);
+    for (size_t u = 1; u < all.size(); ++u) {
+      const uint32_t st = static_cast<uint32_t>(all[u].key - 1);
+      for (auto& o : t.streams)
+        if (o.stream == st) o.last_end = unord64(all[u].max_end);
+    }
+  }
 }
 
 void release_rows(TraceState& t) {
@@ -1685,6 +1747,7 @@ void build_dictionary(TraceState& t) {
         ITT_CUDA(cudaMemcpyAsync(win[b], src, hc - lo, cudaMemcpyHostToDevice, cp));
         if (hi > hc) ITT_CUDA(cudaMemsetAsync(win[b] + (hc - lo), 0, hi - hc, cp));
         ITT_CUDA(cudaEventRecord(copied[b], cp));
+        if (k + 1 == chunks) issue_late_durations(t);  // behind the last names on the copy stream
         ITT_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
         ITT_CUDA(cudaMemcpyAsync(snap.p, counters.p, 4, cudaMemcpyDeviceToDevice, c->stream));
         const uint8_t* bytes = win[b] - lo;  // bytes[o] valid for o in [lo, hi)
@@ -1724,6 +1787,7 @@ void build_dictionary(TraceState& t) {
     t.table_bits = bits;
     break;
   }
+  issue_late_durations(t);  // (a no-op when the last name chunk already queued it)
   if (t.n_used)
     launch(c, "intern_classify", t.n_used * 128.0, k_classify_slots, dim3(grid_for(static_cast<uint64_t>(t.n_used) * 32, 128)),
            dim3(128), 0, t.used.p,
@@ -1760,14 +1824,15 @@ void build_dictionary(TraceState& t) {
   }
 }
 
-void stream_census(TraceState& t) {
+// one census pass over the kept records: the packed used entries (dur null: ends = starts)
+static std::vector<StreamEntry> census_pass(TraceState& t, const int64_t* dur) {
   Ctx* c = t.c;
   const uint64_t n = t.rec.n;
   DBuf<StreamEntry> table(c, kStreamTableCap);
   DBuf<uint32_t> list(c, kStreamTableCap + 1);
   launch(c, "census_init", 0.0, k_init_stream_table, dim3(kStreamTableCap / 256), dim3(256), 0, table.p, list.p,
          kStreamTableCap + 1);
-  CensusArgs ca{n, t.rec.stream, t.rec.device, t.filtering ? 1 : 0, t.majority, t.kind.p, t.rec.start, t.rec.dur,
+  CensusArgs ca{n, t.rec.stream, t.rec.device, t.filtering ? 1 : 0, t.majority, t.kind.p, t.rec.start, dur,
                 table.p, list.p + 1, list.p};
   if (n) {
     const unsigned grid = std::min<unsigned>(grid_for(n, 256), c->sm_count * 8);
@@ -1784,6 +1849,16 @@ void stream_census(TraceState& t) {
     all.resize(ns + 1);
     readback(c, all.data(), packed.p, ns + 1);
   }
+  all.resize(ns + 1);
+  return all;
+}
+
+void stream_census(TraceState& t) {
+  // late durations: the census counts and first starts now, the stream ends after the copy lands
+  const bool late = t.rec.dur_host != nullptr;
+  if (late) t.rec.census_ends_late = true;
+  const std::vector<StreamEntry> all = census_pass(t, late ? nullptr : t.rec.dur);
+  const uint32_t ns = static_cast<uint32_t>(all.size() - 1);
   t.streams.clear();
   for (uint32_t u = 0; u < ns; ++u) {
     const StreamEntry& e = all[1 + u];
@@ -1861,15 +1936,28 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index) {
     const char* e = std::getenv("ITT_COMPACT_RS");
     return !(e && *e == '0');
   }();
-  if (t.sorted && two_pass) {  // rows in order: reduce-then-scan
+  t.main_stream = main_stream;
+  const bool rs_path = t.sorted && two_pass;
+  if (t.rec.dur_host && !t.rec.compact_ends_late) {
+    if (rs_path && n) {  // the ends pass (finish_late_durations) writes tok_end / htod_end later
+      f.dur = nullptr;
+      t.rec.compact_ends_late = true;
+    } else {  // other compaction paths read durations now: wait for the late copy
+      issue_late_durations(t);
+      ITT_CUDA(cudaStreamWaitEvent(c->stream, t.rec.dur_ready, 0));
+    }
+  }
+  if (rs_path) {  // rows in order: reduce-then-scan
     const uint64_t tiles = (n + kRSTile - 1) / kRSTile;
     if (n) {
-      DBuf<uint64_t> tc(c, tiles);
+      t.compact_tiles.alloc(c, tiles);
+      uint64_t* tc = t.compact_tiles.p;
       launch(c, "compact_count", n * (t.filtering ? 7.0 : 5.0), k_compact_count, dim3(static_cast<unsigned>(tiles)), dim3(256), 0,
-             f, tc.p);
-      launch(c, "compact_scan", tiles * 16.0, k_scan_tile_counts, dim3(1), dim3(1024), 0, tc.p, tiles);
-      launch(c, "compact", n * (t.filtering ? 7.0 : 5.0) + n_main * 45.0 + n_htod * 48.0, k_compact_write,
-             dim3(static_cast<unsigned>(tiles)), dim3(256), 0, f, tc.p);
+             f, tc);
+      launch(c, "compact_scan", tiles * 16.0, k_scan_tile_counts, dim3(1), dim3(1024), 0, tc, tiles);
+      launch(c, "compact", n * (t.filtering ? 7.0 : 5.0) + n_main * (f.dur ? 45.0 : 37.0) + n_htod * 48.0, k_compact_write,
+             dim3(static_cast<unsigned>(tiles)), dim3(256), 0, f, tc);
+      if (!t.rec.compact_ends_late) t.compact_tiles.release();
     }
   } else if (t.sorted || t.perm_local) {  // block-local order: stage each tile's rows in shared memory
     const uint64_t tiles = (n + kCompactTile - 1) / kCompactTile;

@@ -26,8 +26,19 @@ struct DevRecords {
   int64_t name_total = -1;               // name_off[n] when known on the host (host columns)
   uint64_t stream_chunk = 0;             // streamed-name chunk bytes (0: default 1 GiB)
   cudaEvent_t cols_ready = nullptr;      // host columns copied on the copy stream (auto-streamed names)
+  // late durations (analyze of large pinned host traces): the duration column crosses PCIe after
+  // the names, while the suffix array is built; the census's stream ends and the token / HtoD ends
+  // are filled in by finish_late_durations before anything reads them
+  const int64_t* dur_host = nullptr;     // pinned source of the late copy (null: no late copy)
+  cudaEvent_t dur_ready = nullptr;       // recorded on the copy stream after the late copy
+  bool census_ends_late = false;         // the census ran without durations: last_end pending
+  bool compact_ends_late = false;        // the compaction ran without durations: tok_end / htod_end pending
   ~DevRecords() {
     if (cols_ready) cudaEventDestroy(cols_ready);
+    if (dur_ready) {  // a late copy still in flight (an error path) must land before o_dur is released
+      cudaEventSynchronize(dur_ready);
+      cudaEventDestroy(dur_ready);
+    }
   }
   int order = ITT_ORDER_UNKNOWN;
   // owned copies when the caller passed host memory
@@ -77,11 +88,13 @@ struct TraceState {
   DBuf<unsigned long long> htod_range;  // [min, max] HtoD end, sign bit flipped (set by compact_main)
   uint32_t n_names = 0;
   std::vector<uint64_t> name_row;  // token id -> source row
+  DBuf<uint64_t> compact_tiles;    // the reduce-then-scan tile offsets, kept for the late ends pass
+  uint32_t main_stream = 0;
   ScanScratch scan;
   radix::Scratch rs;
 };
 
-void upload_records(Ctx* c, const itt_records* r, DevRecords& d);
+void upload_records(Ctx* c, const itt_records* r, DevRecords& d, bool allow_late_dur = false);
 void order_records(TraceState& t);
 void order_launch(TraceState& t);  // order_records in two halves: launches + deferred verdict copy
 void order_finish(TraceState& t);  // reads the verdict (after a later sync), radix fallback if needed
@@ -91,6 +104,8 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index);
 void renumber_tokens(TraceState& t);           // first-appearance ids + token map
 int64_t count_overlaps(TraceState& t);         // count_interval_overlaps on the compacted main stream
 void release_rows(TraceState& t);              // free per-record arrays (and owned column copies) after tokens
+void issue_late_durations(TraceState& t);      // the late duration copy on the copy stream (once)
+void finish_late_durations(TraceState& t);     // wait for it; stream ends, token / HtoD ends
 
 // ------------------------------------------------------------------ suffix array (sa.cu)
 struct SuffixState {

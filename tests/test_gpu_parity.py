@@ -355,6 +355,38 @@ def test_pinned_host_columns_match_device(ctx):
     assert a["loops"][0]["rows"][:, 7].sum() > 0  # HtoD bytes present: the in-place sizes were read
 
 
+@pytest.mark.parametrize("shuffle", [0, 64])
+def test_late_durations_match_device(ctx, shuffle, monkeypatch):
+    """Large pinned host traces send the duration column last over PCIe (after the streamed names)
+    and fill stream ends, token ends and HtoD ends after the suffix array: census (last_end),
+    overlapping kernels, per-iteration rows and the op profile must equal the device-resident
+    call.  ITT_TEST_OVERLAP_MIN lowers the 256 MiB name threshold to this small trace; shuffled
+    rows take the compaction path that waits for the copy instead."""
+    monkeypatch.setenv("ITT_TEST_OVERLAP_MIN", "1")
+    monkeypatch.setenv("ITT_STREAM_CHUNK", "65536")
+    recs, _ = synth.generate_config("C1", noise_frac=0.05, shuffle_window=shuffle, seed=11, minority_frac=0.02)
+    d = ctx.upload(recs)
+    cols = [recs.start_ns, recs.duration_ns, recs.size_bytes, recs.flags, recs.stream, recs.name_off, recs.name_bytes]
+    if recs.device is not None:
+        cols.append(recs.device)
+    for a in cols:
+        ctx.register_host(a)
+    try:
+        a = ctx.analyze_raw(recs, [100], op_profile=True)
+        b = ctx.analyze_raw(d, [100], op_profile=True)
+    finally:
+        for x in cols:
+            ctx.unregister_host(x)
+        d.free()
+    assert a["streams"] == b["streams"]
+    assert a["overlapping_kernels"] == b["overlapping_kernels"]
+    assert a["name_row"] == b["name_row"] and a["dropped"] == b["dropped"]
+    assert a["loops"][0]["pattern_tokens"] == b["loops"][0]["pattern_tokens"]
+    assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
+    assert np.array_equal(a["loops"][0]["op_totals"], b["loops"][0]["op_totals"])
+    assert a["loops"][0]["rows"][:, 7].sum() > 0  # HtoD rows: their ends came from the late pass
+
+
 @pytest.mark.parametrize("chunk", [None, "4096", "200000"])
 def test_streamed_host_names_match_copied_names(ctx, chunk, monkeypatch):
     """ITT_MEM_HOST_STREAM_NAMES / ITT_MEM_DEVICE_HOST_NAMES: names streamed through bounded
