@@ -1090,9 +1090,31 @@ struct RowSel {  // the selection ballots of one warp's rows (warp-striped: row 
 __global__ void __launch_bounds__(256) k_compact_count(CompactF f, uint64_t* __restrict__ tile_counts) {
   __shared__ uint64_t s_w[8];
   const unsigned warp = threadIdx.x >> 5;
-  RowSel sel;
-  sel.load(f, static_cast<uint64_t>(blockIdx.x) * kRSTile + warp * (32 * kRSItems));
-  if (lane_id() == 0) s_w[warp] = sel.packed();
+  const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kRSTile + warp * (32 * kRSItems);
+  uint64_t packed;
+  if (!f.filter && wbase + 32 * kRSItems <= f.n && kRSItems == 8 && (reinterpret_cast<uintptr_t>(f.stream) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(f.kind) & 7) == 0) {
+    // only the totals matter here: 8 consecutive rows per lane, 16-byte stream / 8-byte kind loads
+    const uint64_t r0 = wbase + lane_id() * 8;
+    const uint4 s0 = __ldcs(reinterpret_cast<const uint4*>(f.stream + r0));
+    const uint4 s1 = __ldcs(reinterpret_cast<const uint4*>(f.stream + r0 + 4));
+    const uint2 k8 = __ldcs(reinterpret_cast<const uint2*>(f.kind + r0));
+    const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    uint32_t m = 0, h = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      m += sv[q] == f.main_stream;
+      h += ((q < 4 ? k8.x >> (8 * q) : k8.y >> (8 * (q - 4))) & 0xFFu) == ITT_KIND_HTOD;
+    }
+    m = __reduce_add_sync(0xffffffffu, m);
+    h = __reduce_add_sync(0xffffffffu, h);
+    packed = static_cast<uint64_t>(m) | (static_cast<uint64_t>(h) << 31);
+  } else {
+    RowSel sel;
+    sel.load(f, wbase);
+    packed = sel.packed();
+  }
+  if (lane_id() == 0) s_w[warp] = packed;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint64_t t = 0;
@@ -1129,6 +1151,7 @@ __global__ void __launch_bounds__(256) k_compact_write(CompactF f, const uint64_
   __shared__ uint64_t s_w[8];
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t wbase = static_cast<uint64_t>(blockIdx.x) * kRSTile + warp * (32 * kRSItems);
+  uint64_t excl = __ldg(&tile_excl[blockIdx.x]);  // ready before launch: no round trip after the barrier
   RowSel sel;
   sel.load(f, wbase);
   // the columns the outputs need (main-stream / HtoD rows only), in flight during the block scan
@@ -1144,16 +1167,16 @@ __global__ void __launch_bounds__(256) k_compact_write(CompactF f, const uint64_
     }
     if (!f.ends_only && (sel.mm[q] >> lane & 1u)) sl[q] = __ldcs(&f.slot[k]);
   }
+  // first-appearance filter values in flight across the barrier
+  uint32_t tf[kRSItems];
+#pragma unroll
+  for (int q = 0; q < kRSItems; ++q) tf[q] = (!f.ends_only && (sel.mm[q] >> lane & 1u)) ? __ldcg(&f.tfirst[sl[q]]) : 0u;
   if (lane == 0) s_w[warp] = sel.packed();
   __syncthreads();
-  uint64_t excl = tile_excl[blockIdx.x];
   for (unsigned w = 0; w < warp; ++w) excl += s_w[w];
   uint32_t jm = static_cast<uint32_t>(excl & 0x7FFFFFFFull);
   uint64_t jh = excl >> 31;
   const unsigned lt = lanemask_lt();
-  uint32_t tf[kRSItems];
-#pragma unroll
-  for (int q = 0; q < kRSItems; ++q) tf[q] = (!f.ends_only && (sel.mm[q] >> lane & 1u)) ? __ldcg(&f.tfirst[sl[q]]) : 0u;
   unsigned long long emin = ~0ull, emax = 0;
 #pragma unroll
   for (int q = 0; q < kRSItems; ++q) {

@@ -85,23 +85,61 @@ __global__ void __launch_bounds__(256) k_text_keys_hist(const int32_t* __restric
                                                         int bits, int k, int passes, int32_t* __restrict__ text,
                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                         uint32_t* __restrict__ hist) {
-  constexpr int kB = 1 << RB;
+  // tiles of 1024 positions: the codes (+ k-1 halo) staged in shared memory with 16-byte loads,
+  // four consecutive keys per thread written with 16-byte stores
+  constexpr int kB = 1 << RB, kT = 1024;
   __shared__ uint32_t sh[(32 / RB + 1) * kB];
+  __shared__ __align__(16) uint32_t s_c[kT + 32];
   for (int i = threadIdx.x; i < passes * kB; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
   const uint64_t np = n + 1;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < np; i += stride) {
-    uint32_t key = 0;
-    for (int q = 0; q < k; ++q) {
-      const uint64_t j = i + q;
-      const uint32_t c = j < n ? static_cast<uint32_t>(__ldg(&tok[j]) - lo) : (j == n ? static_cast<uint32_t>(term - lo) : 0u);
-      if (q == 0) text[i] = static_cast<int32_t>(c);
-      key = (key << bits) | c;
+  const auto code = [&](uint64_t j) -> uint32_t {
+    return j < n ? static_cast<uint32_t>(__ldg(&tok[j]) - lo) : (j == n ? static_cast<uint32_t>(term - lo) : 0u);
+  };
+  const bool tok_vec = (reinterpret_cast<uintptr_t>(tok) & 15) == 0;
+  const bool out_vec = ((reinterpret_cast<uintptr_t>(text) | reinterpret_cast<uintptr_t>(keys) |
+                         (vals ? reinterpret_cast<uintptr_t>(vals) : 0)) & 15) == 0;
+  const uint64_t tiles = (np + kT - 1) / kT;
+  for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint64_t base = tile * kT;
+    __syncthreads();  // the previous tile's codes are consumed (and the histogram is zeroed)
+    const uint64_t j0 = base + threadIdx.x * 4;
+    if (tok_vec && j0 + 4 <= n) {
+      const int4 v = __ldcs(reinterpret_cast<const int4*>(tok + j0));
+      *reinterpret_cast<uint4*>(&s_c[threadIdx.x * 4]) =
+          make_uint4(static_cast<uint32_t>(v.x - lo), static_cast<uint32_t>(v.y - lo), static_cast<uint32_t>(v.z - lo),
+                     static_cast<uint32_t>(v.w - lo));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s_c[threadIdx.x * 4 + e] = code(j0 + e);
     }
-    __stcs(&keys[i], key);
-    if (vals) __stcs(&vals[i], static_cast<uint32_t>(i));  // null: the sort's first pass generates positions
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kB + ((key >> (RB * p)) & (kB - 1u))], 1u);
+    if (threadIdx.x < 32) s_c[kT + threadIdx.x] = code(base + kT + threadIdx.x);
+    __syncthreads();
+    uint32_t kv[4], cv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int o = threadIdx.x * 4 + e;
+      uint32_t key = 0;
+      for (int q = 0; q < k; ++q) key = (key << bits) | s_c[o + q];
+      kv[e] = key;
+      cv[e] = s_c[o];
+    }
+    if (out_vec && j0 + 4 <= np) {
+      __stcs(reinterpret_cast<uint4*>(keys + j0), make_uint4(kv[0], kv[1], kv[2], kv[3]));
+      *reinterpret_cast<uint4*>(text + j0) = make_uint4(cv[0], cv[1], cv[2], cv[3]);
+      if (vals) __stcs(reinterpret_cast<uint4*>(vals + j0), make_uint4(j0, j0 + 1, j0 + 2, j0 + 3));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (j0 + e < np) {
+          keys[j0 + e] = kv[e];
+          text[j0 + e] = static_cast<int32_t>(cv[e]);
+          if (vals) vals[j0 + e] = static_cast<uint32_t>(j0 + e);  // null: the sort's first pass generates positions
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (j0 + e < np)
+        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * kB + ((kv[e] >> (RB * p)) & (kB - 1u))], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kB; i += blockDim.x)
@@ -762,12 +800,12 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
     ihist.zero();
     const radix::IotaLoader<uint32_t> iota{ka};  // positions are generated by the first pass
     if (nine) {
-      launch(c, "sa_init_keys", np * 12.0, k_text_keys_hist<9>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
+      launch(c, "sa_init_keys", np * 12.0, k_text_keys_hist<9>, dim3(grid_for((np + 3) / 4, 256, c->sm_count * 8)), dim3(256), 0, tokens,
              n, term, lo, cbits, k, passes, s.text.p, ka, static_cast<uint32_t*>(nullptr), ihist.p);
       a0 = radix_sort_pairs<uint32_t, radix::IotaLoader<uint32_t>, 9>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p, &iota,
                                                                       false);
     } else {
-      launch(c, "sa_init_keys", np * 12.0, k_text_keys_hist<8>, dim3(grid_for(np, 256, c->sm_count * 8)), dim3(256), 0, tokens,
+      launch(c, "sa_init_keys", np * 12.0, k_text_keys_hist<8>, dim3(grid_for((np + 3) / 4, 256, c->sm_count * 8)), dim3(256), 0, tokens,
              n, term, lo, cbits, k, passes, s.text.p, ka, static_cast<uint32_t*>(nullptr), ihist.p);
       a0 = radix_sort_pairs<uint32_t, radix::IotaLoader<uint32_t>>(c, ka, va, kb, vb, np, 0, init_bits, rs, ihist.p, &iota,
                                                                    /*skip_trivial=*/false);
