@@ -852,7 +852,9 @@ int itt_analyze(itt_ctx* ctx, const itt_records* recs, const itt_analyze_opts* o
       if (!t.rec.dur_host) {
         overlaps = count_overlaps(t);
         release_rows(t);  // row-level arrays are dead from here: HBM for the suffix array
-      }  // else the duration column is still crossing PCIe: ends after the suffix array and mining
+      } else {  // the duration column is still crossing PCIe: ends after the suffix array and mining
+        release_rows_but_late(t);
+      }
     }
     // mining over one shared SA / LCP / interval set (pipeline.hpp:81-91)
     std::vector<itt_mining_cfg> cfgs;

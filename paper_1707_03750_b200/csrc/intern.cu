@@ -1459,8 +1459,9 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d, bool allow_late
   // overlaps the first stages instead of preceding them.
   uint64_t overlap_min = 256ull << 20;
   if (const char* e = std::getenv("ITT_TEST_OVERLAP_MIN"); e && *e) overlap_min = std::strtoull(e, nullptr, 10);  // tests
-  const bool overlap = r->mem == ITT_MEM_HOST && nb >= overlap_min;
-  if (overlap) {
+  // (streamed names keep their own chunking; their columns take the same two-stream copy)
+  const bool overlap = (r->mem == ITT_MEM_HOST || r->mem == ITT_MEM_HOST_STREAM_NAMES) && nb >= overlap_min;
+  if (overlap && r->mem == ITT_MEM_HOST) {
     d.host_names = r->name_bytes;
     d.stream_chunk = 64ull << 20;
   }
@@ -1477,7 +1478,7 @@ void upload_records(Ctx* c, const itt_records* r, DevRecords& d, bool allow_late
   }
   // late durations: a pinned duration column of an analyze goes last over PCIe (after the names),
   // overlapping the suffix array; only a census end and the token ends need it, later
-  if (overlap && allow_late_dur && n && n <= (1ull << 29)) {  // (larger traces free the rows before the SA)
+  if (overlap && allow_late_dur && n) {
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, r->duration_ns) == cudaSuccess) {
       if (pa.type == cudaMemoryTypeHost) d.dur_host = r->duration_ns;
@@ -1562,6 +1563,16 @@ void finish_late_durations(TraceState& t) {
         if (o.stream == st) o.last_end = unord64(all[u].max_end);
     }
   }
+}
+
+void release_rows_but_late(TraceState& t) {  // all but what finish_late_durations reads
+  t.perm.release();
+  t.slot.release();
+  t.tok_slot.release();
+  t.tfirst.release();
+  DevRecords& d = t.rec;
+  d.o_size.release(), d.o_flags.release(), d.o_names.release(), d.o_off.release();
+  d.size = nullptr, d.flags = nullptr, d.name_off = nullptr, d.name_bytes = nullptr;
 }
 
 void release_rows(TraceState& t) {

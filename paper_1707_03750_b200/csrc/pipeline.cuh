@@ -104,6 +104,7 @@ void compact_main(TraceState& t, uint32_t main_stream, bool want_record_index);
 void renumber_tokens(TraceState& t);           // first-appearance ids + token map
 int64_t count_overlaps(TraceState& t);         // count_interval_overlaps on the compacted main stream
 void release_rows(TraceState& t);              // free per-record arrays (and owned column copies) after tokens
+void release_rows_but_late(TraceState& t);     // the same, keeping the columns the late ends pass reads
 void issue_late_durations(TraceState& t);      // the late duration copy on the copy stream (once)
 void finish_late_durations(TraceState& t);     // wait for it; stream ends, token / HtoD ends
 

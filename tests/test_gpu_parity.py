@@ -371,19 +371,26 @@ def test_late_durations_match_device(ctx, shuffle, monkeypatch):
         cols.append(recs.device)
     for a in cols:
         ctx.register_host(a)
+    from paper_1707_03750_b200 import abi
     try:
         a = ctx.analyze_raw(recs, [100], op_profile=True)
+        recs.mem = abi.MEM_HOST_STREAM_NAMES  # streamed names: the same two-stream column copy
+        try:
+            s = ctx.analyze_raw(recs, [100], op_profile=True)
+        finally:
+            recs.mem = abi.MEM_HOST
         b = ctx.analyze_raw(d, [100], op_profile=True)
     finally:
         for x in cols:
             ctx.unregister_host(x)
         d.free()
-    assert a["streams"] == b["streams"]
-    assert a["overlapping_kernels"] == b["overlapping_kernels"]
-    assert a["name_row"] == b["name_row"] and a["dropped"] == b["dropped"]
-    assert a["loops"][0]["pattern_tokens"] == b["loops"][0]["pattern_tokens"]
-    assert np.array_equal(a["loops"][0]["rows"], b["loops"][0]["rows"])
-    assert np.array_equal(a["loops"][0]["op_totals"], b["loops"][0]["op_totals"])
+    for x in (a, s):
+        assert x["streams"] == b["streams"]
+        assert x["overlapping_kernels"] == b["overlapping_kernels"]
+        assert x["name_row"] == b["name_row"] and x["dropped"] == b["dropped"]
+        assert x["loops"][0]["pattern_tokens"] == b["loops"][0]["pattern_tokens"]
+        assert np.array_equal(x["loops"][0]["rows"], b["loops"][0]["rows"])
+        assert np.array_equal(x["loops"][0]["op_totals"], b["loops"][0]["op_totals"])
     assert a["loops"][0]["rows"][:, 7].sum() > 0  # HtoD rows: their ends came from the late pass
 
 
