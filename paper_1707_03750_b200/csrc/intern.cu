@@ -909,14 +909,10 @@ __global__ void __launch_bounds__(256) k_stream_census(CensusArgs a) {
   }
   __syncthreads();
   const unsigned lane = lane_id();
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x; b < a.n; b += stride) {
-    const uint64_t i = b + threadIdx.x;
-    bool valid = i < a.n;
-    if (valid && a.filter && a.device[i] != a.majority) valid = false;
-    const uint32_t st = valid ? a.stream[i] : 0u;
+  // one row per lane per round: the stream's block slot by match_any, counts / min start / max end
+  // reduced over the lanes of the same stream
+  const auto row = [&](bool valid, uint32_t st, int kd, int64_t s0, int64_t e0) {
     const unsigned long long key = static_cast<unsigned long long>(st) + 1ull;
-    // per-block slot of this stream
     uint32_t bs = kNone;
     const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : 0ull);
     const int leader = __ffs(peers) - 1;
@@ -936,32 +932,80 @@ __global__ void __launch_bounds__(256) k_stream_census(CensusArgs a) {
       }
     }
     bs = __shfl_sync(0xffffffffu, bs, leader);
-    if (valid) {
-      const int kd = a.kind[i];
-      const int64_t s0 = a.start[i];
-      const int64_t e0 = a.dur ? s0 + a.dur[i] : s0;  // no durations yet (late): ends come later
-      if (bs == kNone) {  // block table overflow: update the global table directly
-        const uint32_t gs = global_stream_slot(a.table, a.list, a.count, key);
-        if (gs != kNone) {
-          atomicAdd(&a.table[gs].counts[kd], 1ull);
-          atomicMin(&a.table[gs].min_start, ord64(s0));
-          atomicMax(&a.table[gs].max_end, ord64(e0));
-        }
-      } else {
-        const unsigned kp = __match_any_sync(peers, static_cast<unsigned>(kd));
-        if (static_cast<int>(lane) == __ffs(kp) - 1) atomicAdd(&s_cnt[bs][kd], static_cast<unsigned>(__popc(kp)));
-        // min start / max end over the stream's lanes: reduce 32-bit halves
-        const unsigned long long us = ord64(s0), ue = ord64(e0);
-        const unsigned hs = __reduce_min_sync(peers, static_cast<unsigned>(us >> 32));
-        const unsigned ls = __reduce_min_sync(peers, static_cast<unsigned>(us >> 32) == hs ? static_cast<unsigned>(us) : ~0u);
-        const unsigned he = __reduce_max_sync(peers, static_cast<unsigned>(ue >> 32));
-        const unsigned le = __reduce_max_sync(peers, static_cast<unsigned>(ue >> 32) == he ? static_cast<unsigned>(ue) : 0u);
-        if (static_cast<int>(lane) == leader) {
-          atomicMin(&s_min[bs], (static_cast<unsigned long long>(hs) << 32) | ls);
-          atomicMax(&s_max[bs], (static_cast<unsigned long long>(he) << 32) | le);
+    if (!valid) return;
+    if (bs == kNone) {  // block table overflow: update the global table directly
+      const uint32_t gs = global_stream_slot(a.table, a.list, a.count, key);
+      if (gs != kNone) {
+        atomicAdd(&a.table[gs].counts[kd], 1ull);
+        atomicMin(&a.table[gs].min_start, ord64(s0));
+        atomicMax(&a.table[gs].max_end, ord64(e0));
+      }
+      return;
+    }
+    const unsigned kp = __match_any_sync(peers, static_cast<unsigned>(kd));
+    if (static_cast<int>(lane) == __ffs(kp) - 1) atomicAdd(&s_cnt[bs][kd], static_cast<unsigned>(__popc(kp)));
+    // min start / max end over the stream's lanes: reduce 32-bit halves
+    const unsigned long long us = ord64(s0), ue = ord64(e0);
+    const unsigned hs = __reduce_min_sync(peers, static_cast<unsigned>(us >> 32));
+    const unsigned ls = __reduce_min_sync(peers, static_cast<unsigned>(us >> 32) == hs ? static_cast<unsigned>(us) : ~0u);
+    const unsigned he = __reduce_max_sync(peers, static_cast<unsigned>(ue >> 32));
+    const unsigned le = __reduce_max_sync(peers, static_cast<unsigned>(ue >> 32) == he ? static_cast<unsigned>(ue) : 0u);
+    if (static_cast<int>(lane) == leader) {
+      atomicMin(&s_min[bs], (static_cast<unsigned long long>(hs) << 32) | ls);
+      atomicMax(&s_max[bs], (static_cast<unsigned long long>(he) << 32) | le);
+    }
+  };
+  // four consecutive rows per thread with 16-byte loads when the columns are aligned
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.stream) | reinterpret_cast<uintptr_t>(a.start) |
+                     (a.dur ? reinterpret_cast<uintptr_t>(a.dur) : 0)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(a.kind) & 3) == 0 &&
+                   (!a.filter || (reinterpret_cast<uintptr_t>(a.device) & 7) == 0);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 4;
+  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x * 4; b < a.n; b += stride) {
+    const uint64_t i0 = b + threadIdx.x * 4;
+    uint32_t st[4] = {0, 0, 0, 0};
+    int kd[4] = {0, 0, 0, 0};
+    int64_t s0[4] = {0, 0, 0, 0}, e0[4] = {0, 0, 0, 0};
+    bool valid[4];
+    if (vec && i0 + 4 <= a.n) {
+      const uint4 sv = __ldcs(reinterpret_cast<const uint4*>(a.stream + i0));
+      const uint32_t kv = __ldcs(reinterpret_cast<const uint32_t*>(a.kind + i0));
+      const longlong2 t0 = __ldcs(reinterpret_cast<const longlong2*>(a.start + i0));
+      const longlong2 t1 = __ldcs(reinterpret_cast<const longlong2*>(a.start + i0 + 2));
+      st[0] = sv.x, st[1] = sv.y, st[2] = sv.z, st[3] = sv.w;
+      s0[0] = t0.x, s0[1] = t0.y, s0[2] = t1.x, s0[3] = t1.y;
+      if (a.dur) {
+        const longlong2 d0 = __ldcs(reinterpret_cast<const longlong2*>(a.dur + i0));
+        const longlong2 d1 = __ldcs(reinterpret_cast<const longlong2*>(a.dur + i0 + 2));
+        e0[0] = s0[0] + d0.x, e0[1] = s0[1] + d0.y, e0[2] = s0[2] + d1.x, e0[3] = s0[3] + d1.y;
+      } else {  // no durations yet (late): ends come later
+#pragma unroll
+        for (int e = 0; e < 4; ++e) e0[e] = s0[e];
+      }
+      uint2 dv = make_uint2(0, 0);
+      if (a.filter) dv = __ldcs(reinterpret_cast<const uint2*>(a.device + i0));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        kd[e] = static_cast<int>((kv >> (8 * e)) & 0xFFu);
+        const uint32_t dev = ((e < 2 ? dv.x : dv.y) >> (16 * (e & 1))) & 0xFFFFu;
+        valid[e] = !(a.filter && dev != a.majority);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t i = i0 + e;
+        valid[e] = i < a.n;
+        if (valid[e] && a.filter && a.device[i] != a.majority) valid[e] = false;
+        if (valid[e]) {
+          st[e] = a.stream[i];
+          kd[e] = a.kind[i];
+          s0[e] = a.start[i];
+          e0[e] = a.dur ? s0[e] + a.dur[i] : s0[e];
         }
       }
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) row(valid[e], valid[e] ? st[e] : 0u, kd[e], s0[e], e0[e]);
   }
   __syncthreads();
   for (unsigned i = threadIdx.x; i < kBlockStreams; i += blockDim.x) {
@@ -1869,7 +1913,7 @@ static std::vector<StreamEntry> census_pass(TraceState& t, const int64_t* dur) {
   CensusArgs ca{n, t.rec.stream, t.rec.device, t.filtering ? 1 : 0, t.majority, t.kind.p, t.rec.start, dur,
                 table.p, list.p + 1, list.p};
   if (n) {
-    const unsigned grid = std::min<unsigned>(grid_for(n, 256), c->sm_count * 8);
+    const unsigned grid = std::min<unsigned>(grid_for((n + 3) / 4, 256), c->sm_count * 8);
     launch(c, "census", n * 23.0, k_stream_census, dim3(grid), dim3(256), 0, ca);
   }
   // one round trip for the usual handful of streams: count + the first kFew packed entries
