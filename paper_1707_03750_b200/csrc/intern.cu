@@ -854,6 +854,47 @@ __global__ void k_kinds_minrow(const uint32_t* __restrict__ slot, const uint8_t*
   }
 }
 
+// The same for dictionaries of up to kKindsSmemCap slots: the slot flags and a per-CTA smallest row
+// per slot in shared memory (random table reads as LDS instead of L1 wavefronts of up to 32 lines),
+// folded into trep once per CTA.  1024-thread CTAs, two per SM.
+constexpr uint32_t kKindsSmemCap = 16384;
+__global__ void __launch_bounds__(1024) k_kinds_minrow_smem(const uint32_t* __restrict__ slot, const uint8_t* __restrict__ rflags,
+                                                           uint64_t n, const uint8_t* __restrict__ tflags, uint32_t cap,
+                                                           uint8_t* __restrict__ kind, uint32_t* trep) {
+  extern __shared__ __align__(16) uint8_t k_sm[];
+  uint32_t* s_rep = reinterpret_cast<uint32_t*>(k_sm);
+  uint8_t* s_fl = k_sm + static_cast<size_t>(cap) * 4;
+  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
+    s_rep[i] = 0xFFFFFFFFu;
+    s_fl[i] = tflags[i];
+  }
+  __syncthreads();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t quads = (reinterpret_cast<uintptr_t>(rflags) & 3u) ? 0 : n / 4;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < quads; q += stride) {
+    const uint64_t i = q * 4;
+    const uint4 sl = __ldcs(reinterpret_cast<const uint4*>(slot) + q);
+    const uint32_t fl = __ldcs(reinterpret_cast<const uint32_t*>(rflags) + q);
+    const uint32_t s4[4] = {sl.x, sl.y, sl.z, sl.w};
+    uint32_t kd = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t s = s4[u];
+      kd |= static_cast<uint32_t>(kind_from(s_fl[s], ((fl >> (8 * u)) & ITT_REC_HAS_THROUGHPUT) != 0)) << (8 * u);
+      if (s_rep[s] > i + u) atomicMin(&s_rep[s], static_cast<uint32_t>(i + u));
+    }
+    reinterpret_cast<uint32_t*>(kind)[q] = kd;
+  }
+  for (uint64_t i = quads * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t s = slot[i];
+    kind[i] = static_cast<uint8_t>(kind_from(s_fl[s], (rflags[i] & ITT_REC_HAS_THROUGHPUT) != 0));
+    if (s_rep[s] > i) atomicMin(&s_rep[s], static_cast<uint32_t>(i));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x)
+    if (s_rep[i] != 0xFFFFFFFFu) atomicMin(&trep[i], s_rep[i]);
+}
+
 // ------------------------------------------------------------------ stream census
 struct StreamEntry {
   unsigned long long key;  // stream + 1 (0 = empty)
@@ -1871,7 +1912,14 @@ void build_dictionary(TraceState& t) {
            dim3(128), 0, t.used.p,
            t.n_used, t.tkey.p, t.rec.name_off, t.rec.name_bytes, streamed ? arena.p : nullptr,
            streamed ? arena_off.p : nullptr, t.tflags.p);
-  if (n) {
+  const uint32_t tcap = 1u << t.table_bits;
+  if (n && tcap <= kKindsSmemCap && n >= (1ull << 20)) {
+    const size_t smem = static_cast<size_t>(tcap) * 5;
+    smem_optin(c, k_kinds_minrow_smem, smem);
+    const unsigned g2 = std::min<unsigned>(grid_for((n + 3) / 4, 1024), c->sm_count * 2);
+    launch(c, "intern_kinds", n * 6.0, k_kinds_minrow_smem, dim3(g2), dim3(1024), smem, t.slot.p, t.rec.flags, n, t.tflags.p,
+           tcap, t.kind.p, t.trep.p);
+  } else if (n) {
     const unsigned g2 = std::min<unsigned>(grid_for(n, 256), c->sm_count * 16);
     launch(c, "intern_kinds", n * 6.0, k_kinds_minrow, dim3(g2), dim3(256), 0, t.slot.p, t.rec.flags, n, t.tflags.p,
            t.kind.p, t.trep.p);
