@@ -242,6 +242,44 @@ __global__ void __launch_bounds__(256) k_init_fill(const int32_t* __restrict__ t
   }
 }
 
+// The init level through the k-gram table needs no scan: a head's rank is its own SA position,
+// the level is filled in text order afterwards (k_init_fill), and head-position levels take their
+// digit histograms from the level itself.  So: heads from adjacent sorted keys, G, table inserts —
+// the sorted keys read once with 16-byte loads, no look-back chain and no SA read.
+__global__ void __launch_bounds__(256) k_init_heads(const uint32_t* __restrict__ keys, uint64_t np,
+                                                    uint8_t* __restrict__ heads_out, unsigned long long* gcount,
+                                                    unsigned long long* init_map, uint32_t map_mask) {
+  static_assert(kRankItems == 8, "one head byte per thread");
+  const uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kRankItems;
+  uint32_t kv[kRankItems];
+  uint32_t fmask = 0;
+  if (base < np) {
+    if (base + kRankItems <= np) {
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(keys + base));
+      const uint4 b = __ldcs(reinterpret_cast<const uint4*>(keys + base + 4));
+      kv[0] = a.x, kv[1] = a.y, kv[2] = a.z, kv[3] = a.w, kv[4] = b.x, kv[5] = b.y, kv[6] = b.z, kv[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kRankItems; ++q) kv[q] = base + q < np ? keys[base + q] : 0u;
+    }
+    uint32_t pk = base > 0 ? keys[base - 1] : 0u;
+#pragma unroll
+    for (int q = 0; q < kRankItems; ++q) {
+      const uint64_t j = base + q;
+      if (j < np && (j == 0 || kv[q] != pk)) fmask |= 1u << q;
+      pk = kv[q];
+    }
+    heads_out[base / kRankItems] = static_cast<uint8_t>(fmask);
+    for (uint32_t m = fmask; m; m &= m - 1) {
+      const int q = __ffs(m) - 1;
+      init_map_insert(init_map, map_mask, kv[q], static_cast<uint32_t>(base + q), gcount);
+    }
+  }
+  uint32_t g = __popc(fmask);
+  g = __reduce_add_sync(0xffffffffu, g);
+  if (lane_id() == 0 && g) atomicAdd(gcount, static_cast<unsigned long long>(g));
+}
+
 template <bool kHeads>
 __global__ void __launch_bounds__(kRankBlock, 8) k_rank_update(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ sa,
                                                             uintptr_t rank_old, uint32_t h, uint64_t np,
@@ -870,9 +908,13 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
         init_map.alloc(c, size_t{1} << kInitMapBits);
         init_map.zero();
       }
-      if (heads_mode) {
+      if (map_init) {
         gcount.zero();
-        launch(c, "sa_rank_update", np * (rank_old ? 20.0 : (map_init ? 8.0 : 12.0)), k_rank_update<true>,
+        launch(c, "sa_rank_update", np * 4.0, k_init_heads, dim3(grid_for((np + kRankItems - 1) / kRankItems, 256)), dim3(256), 0,
+               kk, np, heads[hc ^ 1].p, gcount.p, init_map.p, (1u << kInitMapBits) - 1);
+      } else if (heads_mode) {
+        gcount.zero();
+        launch(c, "sa_rank_update", np * (rank_old ? 20.0 : 12.0), k_rank_update<true>,
                dim3(static_cast<unsigned>(rtiles)), dim3(kRankBlock), 0, kk, ss, rank_old, h, np, lvl, hist_p, max_passes,
                nullptr, sc.buf.p + 1, reinterpret_cast<uint32_t*>(sc.buf.p), 0u, heads[hc ^ 1].p, gcount.p,
                map_init ? init_map.p : nullptr, (1u << kInitMapBits) - 1);
