@@ -536,44 +536,93 @@ constexpr uint64_t kHeadsLcpRatio = 64;
 #define ITT_APPLY_WORDS 8  // C3: 106 -> 53 -> 39 us per launch for 1, 4, 8 words (16: 41)
 #endif
 constexpr int kApplyWords = ITT_APPLY_WORDS;  // words per thread
+// this thread's (last new head + 1, last old head + 1) over its kApplyWords bitmap words
+__device__ __forceinline__ uint64_t apply_run(const uint32_t* __restrict__ heads_old, const uint32_t* __restrict__ heads_new,
+                                              uint64_t np, uint64_t w0, uint32_t (&ho)[kApplyWords], uint32_t (&hn)[kApplyWords]) {
+  uint64_t ln = 0, lo = 0;
+  if (kApplyWords % 4 == 0 && (w0 + kApplyWords) * kApplyItems <= np) {  // whole words: 16-byte loads
+#pragma unroll
+    for (int u = 0; u < kApplyWords; u += 4) {
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(heads_old + w0 + u));
+      const uint4 b = __ldcs(reinterpret_cast<const uint4*>(heads_new + w0 + u));
+      ho[u] = a.x, ho[u + 1] = a.y, ho[u + 2] = a.z, ho[u + 3] = a.w;
+      hn[u] = b.x, hn[u + 1] = b.y, hn[u + 2] = b.z, hn[u + 3] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < kApplyWords; ++u) {
+      const uint64_t base = (w0 + u) * kApplyItems;
+      ho[u] = hn[u] = 0;
+      if (base < np) {
+        const uint32_t live = np - base >= kApplyItems ? 0xFFFFFFFFu : (1u << (np - base)) - 1u;  // bits past np are unset
+        ho[u] = __ldcs(&heads_old[w0 + u]) & live;
+        hn[u] = __ldcs(&heads_new[w0 + u]) & live;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kApplyWords; ++u) {
+    const uint64_t base = (w0 + u) * kApplyItems;
+    if (hn[u]) ln = base + (31 - __clz(hn[u])) + 1;
+    if (ho[u]) lo = base + (31 - __clz(ho[u])) + 1;
+  }
+  return (ln << 31) | lo;
+}
+// reduce-then-scan form of the apply (ITT_APPLY_RS=1; A/B only, the look-back form is faster at C3):
+// per-tile HeadPair totals, one block scans them (k_scan_tile_totals), then k_refine_apply<true>
+__global__ void __launch_bounds__(kRankBlock) k_refine_totals(const uint32_t* __restrict__ heads_old,
+                                                             const uint32_t* __restrict__ heads_new, uint64_t np,
+                                                             uint64_t* __restrict__ tot, const unsigned int* __restrict__ abort_flag) {
+  __shared__ uint64_t s_w[kRankBlock / 32];
+  if (ld_relaxed_u32(abort_flag)) return;
+  uint32_t ho[kApplyWords], hn[kApplyWords];
+  const HeadPair op;
+  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kRankBlock + threadIdx.x) * kApplyWords;
+  uint64_t run = apply_run(heads_old, heads_new, np, w0, ho, hn);
+  for (int o = 16; o > 0; o >>= 1) run = op(run, __shfl_xor_sync(0xffffffffu, run, o));
+  if (lane_id() == 0) s_w[threadIdx.x >> 5] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = s_w[0];
+    for (int w = 1; w < kRankBlock / 32; ++w) t = op(t, s_w[w]);
+    tot[blockIdx.x] = t;
+  }
+}
+template <bool kRS>
 __global__ void __launch_bounds__(kRankBlock) k_refine_apply(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ heads_old,
                                                             const uint32_t* __restrict__ heads_new, uint64_t np,
                                                             uint32_t* __restrict__ level, int full, uint64_t* status,
-                                                            uint32_t* counter, const unsigned int* __restrict__ abort_flag) {
+                                                            uint32_t* counter, const unsigned int* __restrict__ abort_flag,
+                                                            const uint64_t* __restrict__ tile_excl) {
   __shared__ uint64_t s_warp[kRankBlock / 32];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_prefix;
   __shared__ unsigned int s_abort;
   if (threadIdx.x == 0) {
     s_abort = ld_relaxed_u32(abort_flag);
-    s_tile = atomicAdd(counter, 1u);
+    if constexpr (kRS) {
+      s_tile = blockIdx.x;
+      s_prefix = s_abort ? 0 : tile_excl[blockIdx.x];
+    } else {
+      s_tile = atomicAdd(counter, 1u);
+    }
   }
   __syncthreads();
   if (s_abort) return;  // this round's detect (or an earlier one) found inversions
   const uint32_t tile = s_tile;
   const uint64_t w0 = (static_cast<uint64_t>(tile) * kRankBlock + threadIdx.x) * kApplyWords;  // first bitmap word
   uint32_t ho[kApplyWords], hn[kApplyWords];
-  uint64_t ln = 0, lo = 0;  // this thread's last heads (+1; 0 = none)
-#pragma unroll
-  for (int u = 0; u < kApplyWords; ++u) {
-    const uint64_t base = (w0 + u) * kApplyItems;
-    ho[u] = hn[u] = 0;
-    if (base < np) {
-      const uint32_t live = np - base >= kApplyItems ? 0xFFFFFFFFu : (1u << (np - base)) - 1u;  // bits past np are unset
-      ho[u] = __ldcs(&heads_old[w0 + u]) & live;
-      hn[u] = __ldcs(&heads_new[w0 + u]) & live;
-    }
-    if (hn[u]) ln = base + (31 - __clz(hn[u])) + 1;
-    if (ho[u]) lo = base + (31 - __clz(ho[u])) + 1;
-  }
+  const uint64_t run = apply_run(heads_old, heads_new, np, w0, ho, hn);  // this thread's last heads (+1; 0 = none)
   const HeadPair op;
   uint64_t total;
-  const uint64_t texcl = block_exclusive_scan<uint64_t, HeadPair, kRankBlock>((ln << 31) | lo, op, &total, s_warp);
-  if (threadIdx.x < 32) {
-    const uint64_t p = tile_lookback<uint64_t, HeadPair>(status, tile, total, op);
-    if (threadIdx.x == 0) s_prefix = p;
+  const uint64_t texcl = block_exclusive_scan<uint64_t, HeadPair, kRankBlock>(run, op, &total, s_warp);
+  if constexpr (!kRS) {
+    if (threadIdx.x < 32) {
+      const uint64_t p = tile_lookback<uint64_t, HeadPair>(status, tile, total, op);
+      if (threadIdx.x == 0) s_prefix = p;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const uint64_t pre = op(s_prefix, texcl);
   uint64_t cn = pre >> 31, co = pre & ((1ull << 31) - 1);  // last heads before this run (+1)
 #pragma unroll
@@ -982,6 +1031,7 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
   abort_flag.zero();
   DBuf<uint32_t> head_hist;
   ScanScratch rscan[2];
+  DBuf<uint64_t> rtot;  // reduce-then-scan apply: per-tile totals, then their exclusive scan
   // Refinement rounds run one round ahead of the host: round r+1's kernels are queued before the
   // host reads round r's verdict (its readback overlaps round r+1 on the device).  A round whose
   // detect counts inversions sets abort_flag, so everything queued after it returns at once; the
@@ -1067,11 +1117,29 @@ void build_suffix_array(Ctx* c, const int32_t* tokens, uint64_t n, int32_t term,
         // (older levels are not released here: an undone round may need them)
       }
       const uint64_t atiles = (np + kRankBlock * kApplyItems * kApplyWords - 1) / (kRankBlock * kApplyItems * kApplyWords);
-      rscan[rslot].prepare(c, atiles);
-      launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply, dim3(static_cast<unsigned>(atiles)),
-             dim3(kRankBlock), 0, sa, reinterpret_cast<const uint32_t*>(heads[hc].p),
-             reinterpret_cast<const uint32_t*>(heads[hc ^ 1].p), np, lvl, full ? 1 : 0, rscan[rslot].buf.p + 1,
-             reinterpret_cast<uint32_t*>(rscan[rslot].buf.p), abort_flag.p);
+      // ITT_APPLY_RS=1: reduce-then-scan apply (A/B at C3, both with 16-byte bitmap loads: 0.47 ms in three
+      // launches vs 0.375 ms for the look-back kernel, whose chain over ~1.5K tiles is short)
+      static const bool apply_rs = [] {
+        const char* e = std::getenv("ITT_APPLY_RS");
+        return e && *e == '1';
+      }();
+      const uint32_t* h_old = reinterpret_cast<const uint32_t*>(heads[hc].p);
+      const uint32_t* h_new = reinterpret_cast<const uint32_t*>(heads[hc ^ 1].p);
+      if (apply_rs) {  // tile totals, one-block scan, apply from known prefixes (stream order reuses rtot)
+        if (rtot.n < atiles) rtot.alloc(c, atiles);
+        launch(c, "sa_refine_totals", np * 0.25, k_refine_totals, dim3(static_cast<unsigned>(atiles)), dim3(kRankBlock), 0,
+               h_old, h_new, np, rtot.p, abort_flag.p);
+        launch(c, "sa_refine_scan", atiles * 16.0, k_scan_tile_totals<uint64_t, HeadPair>, dim3(1), dim3(1024), 0, rtot.p,
+               atiles);
+        launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply<true>, dim3(static_cast<unsigned>(atiles)),
+               dim3(kRankBlock), 0, sa, h_old, h_new, np, lvl, full ? 1 : 0, static_cast<uint64_t*>(nullptr),
+               static_cast<uint32_t*>(nullptr), abort_flag.p, static_cast<const uint64_t*>(rtot.p));
+      } else {
+        rscan[rslot].prepare(c, atiles);
+        launch(c, "sa_refine_apply", full ? np * 8.25 : np * 0.25, k_refine_apply<false>, dim3(static_cast<unsigned>(atiles)),
+               dim3(kRankBlock), 0, sa, h_old, h_new, np, lvl, full ? 1 : 0, rscan[rslot].buf.p + 1,
+               reinterpret_cast<uint32_t*>(rscan[rslot].buf.p), abort_flag.p, static_cast<const uint64_t*>(nullptr));
+      }
       ITT_CUDA(cudaMemcpyAsync(host_cnt + 2 * rslot, dcnt, 16, cudaMemcpyDeviceToHost, c->stream));
       ITT_CUDA(cudaEventRecord(rev[rslot], c->stream));
       // this round is queued; now the verdict of the one before it
