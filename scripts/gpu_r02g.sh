@@ -1,3 +1,5 @@
-python scripts/step_jitter_c3.py > gpurun_out/r02g_jitter.log 2>&1
-python -m pytest tests/test_gpu_sa_refine.py tests/test_gpu_baseline.py -x -q -p no:cacheprovider -k "not c5" 2>&1 | tail -3 > gpurun_out/r02g_tests.log
-bash scripts/sanitize.sh
+#!/bin/bash
+# final check of the round: the full GPU suite and the default bench line (C3)
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/r02g_tests.log 2>&1; tail -2 gpurun_out/r02g_tests.log
+timeout 1200 python bench.py > gpurun_out/r02g_bench_c3.json 2> gpurun_out/r02g_bench_c3.err; tail -c 400 gpurun_out/r02g_bench_c3.json
